@@ -1,0 +1,139 @@
+/*
+ * c1d.h — C ABI of the B200-native 1D dilated convolution layer (arXiv 2104.08002 hot path).
+ *
+ * Drop-in boundary for the reference's operator API (namespace conv1d in
+ * /root/reference/proj/include/conv1d/conv.hpp). The reference has no FFI of its own: its three
+ * pass entry points are C++ free functions over host std::vector tensors. This header replaces
+ * them with plain-pointer, device-memory entry points; paper_2104_08002_b200/host/conv1d_gpu.cpp
+ * re-implements the exact reference C++ signatures on top of it.
+ *
+ *   c1d_forward          replaces conv1d::conv1d_forward          conv.hpp:42-43, conv.cpp:165-191
+ *   c1d_backward_data    replaces conv1d::conv1d_backward_data    conv.hpp:49-50, conv.cpp:193-227
+ *   c1d_backward_weight  replaces conv1d::conv1d_backward_weight  conv.hpp:56-57, conv.cpp:229-326
+ *   c1d_output_width     replaces conv1d::output_width            conv.hpp:33,   conv.cpp:142-151
+ *   c1d_conv_flops       replaces conv1d::conv_flops              conv.hpp:37,   conv.cpp:161-163
+ *   c1d_round_bf16       replaces conv1d::fp32_to_bf16 over spans bf16.hpp:29-40, conv.cpp:69-73
+ *
+ * Conventions
+ *   - Tensors are NCW with the width axis contiguous (tensor.hpp:13-36): x is (N, C, W_in),
+ *     y / dy is (N, K, Q) with Q = W_in - d*(S-1), dx is (N, C, W_in).
+ *   - Weights are passed in the natural (K, C, S) order (WeightKCS, tensor.hpp:42-56) as FP32;
+ *     the per-pass packing (pack_weights_forward/backward, tensor.cpp:5-41) happens on the device.
+ *     dW is returned in KCS order, FP32.
+ *   - All tensor pointers are DEVICE pointers. Outputs are always FP32 (as in the reference).
+ *   - x / dy storage is FP32 or BF16 (desc.in_dtype). With precision BF16 and FP32 storage the
+ *     inputs and weights are rounded to BF16 (round-to-nearest-even) inside the call, exactly as
+ *     the reference does (conv.cpp:182-183, 218-219, 248-249); products accumulate in FP32.
+ *   - Errors are status codes, one per reference exception class used on this path
+ *     (errors.hpp:8-64); nothing is thrown across the ABI. Validation happens before any launch.
+ *     c1d_last_error_message() returns the human-readable detail for the calling thread.
+ *   - Calls are asynchronous on `stream` and reentrant on disjoint outputs. Results are
+ *     bitwise deterministic run to run (no atomics; fixed-order reductions).
+ *   - Deviation from the reference: BF16 accepts odd C, K and widths (channels are zero-padded
+ *     to tensor-core tile shapes). Set C1D_FLAG_STRICT_BF16_DIMS to get the reference's OddDims
+ *     rejection (conv.cpp:40-57) instead.
+ */
+#ifndef C1D_H_
+#define C1D_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define C1D_API_VERSION 1
+
+#if defined(__GNUC__)
+#define C1D_EXPORT __attribute__((visibility("default")))
+#else
+#define C1D_EXPORT
+#endif
+
+typedef struct CUstream_st* c1d_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum c1d_status {
+    C1D_OK = 0,
+    C1D_ERR_SHAPE_MISMATCH = 1, /* conv1d::ShapeMismatch */
+    C1D_ERR_ODD_DIMS = 2,       /* conv1d::OddDims (only with C1D_FLAG_STRICT_BF16_DIMS) */
+    C1D_ERR_TOO_NARROW = 3,     /* conv1d::TooNarrow */
+    C1D_ERR_INVALID_ARGUMENT = 4,
+    C1D_ERR_WORKSPACE = 5,   /* caller workspace too small */
+    C1D_ERR_UNSUPPORTED = 6, /* requested algo cannot run this shape */
+    C1D_ERR_CUDA = 7,        /* CUDA runtime / launch failure */
+    C1D_ERR_NO_DEVICE = 8    /* no sm_100 device visible */
+} c1d_status;
+
+typedef enum c1d_precision { C1D_PRECISION_FP32 = 0, C1D_PRECISION_BF16 = 1 } c1d_precision;
+typedef enum c1d_dtype { C1D_DTYPE_F32 = 0, C1D_DTYPE_BF16 = 1 } c1d_dtype;
+
+/* Kernel family. AUTO picks the tcgen05 tensor-core kernels whenever the shape allows them and
+ * the direct (FFMA) kernels otherwise. */
+typedef enum c1d_algo {
+    C1D_ALGO_AUTO = 0,
+    C1D_ALGO_DIRECT = 1,  /* CUDA-core FFMA direct convolution, any shape */
+    C1D_ALGO_TCGEN05 = 2, /* tcgen05.mma BF16 tensor-core kernels (TMEM accumulators) */
+    C1D_ALGO_TF32X3 = 3   /* tcgen05 kind::tf32 with 3xTF32 split for FP32 precision */
+} c1d_algo;
+
+typedef enum c1d_pass { C1D_PASS_FORWARD = 0, C1D_PASS_BACKWARD_DATA = 1, C1D_PASS_BACKWARD_WEIGHT = 2 } c1d_pass;
+
+#define C1D_FLAG_STRICT_BF16_DIMS 0x1u
+
+/* Mirrors conv1d::ConvParams (conv.hpp:18-25) plus the tensor sizes the reference reads from
+ * its Tensor3D arguments. */
+typedef struct c1d_desc {
+    int64_t n;         /* batch */
+    int64_t c;         /* input channels */
+    int64_t k;         /* filters */
+    int64_t s;         /* taps */
+    int64_t d;         /* dilation */
+    int64_t w_in;      /* pre-padded input width W_in; Q = W_in - d*(S-1) */
+    int32_t precision; /* c1d_precision */
+    int32_t in_dtype;  /* c1d_dtype of x and dy */
+    int32_t algo;      /* c1d_algo */
+    uint32_t flags;    /* C1D_FLAG_* */
+    int64_t block_w;   /* accepted for API parity; results do not depend on it */
+} c1d_desc;
+
+C1D_EXPORT int c1d_api_version(void);
+C1D_EXPORT const char* c1d_strerror(c1d_status status);
+/* Detail text of the last failing call on this host thread ("" if none). */
+C1D_EXPORT const char* c1d_last_error_message(void);
+
+/* Q = W_in - d*(S-1); C1D_ERR_TOO_NARROW when W_in <= d*(S-1). */
+C1D_EXPORT c1d_status c1d_output_width(const c1d_desc* desc, int64_t* q_out);
+/* 2*N*K*C*S*Q, counted identically for all three passes. -1 on invalid desc. */
+C1D_EXPORT int64_t c1d_conv_flops(const c1d_desc* desc);
+
+/* Device workspace bytes the pass needs (0 if none). Passing workspace == NULL to a pass makes
+ * the library use an internal, lazily grown per-device buffer instead. */
+C1D_EXPORT c1d_status c1d_workspace_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes);
+
+/* Which kernel family the pass will run for this desc (resolves C1D_ALGO_AUTO). */
+C1D_EXPORT c1d_status c1d_selected_algo(const c1d_desc* desc, c1d_pass pass, c1d_algo* algo);
+
+/* y (N,K,Q) = conv(x (N,C,W_in), w (K,C,S)) */
+C1D_EXPORT c1d_status c1d_forward(const c1d_desc* desc, const void* x, const float* w_kcs, float* y, void* workspace,
+                       size_t workspace_bytes, c1d_stream_t stream);
+
+/* dx (N,C,W_in) = gradient w.r.t. the padded input, from dy (N,K,Q) */
+C1D_EXPORT c1d_status c1d_backward_data(const c1d_desc* desc, const void* dy, const float* w_kcs, float* dx,
+                             void* workspace, size_t workspace_bytes, c1d_stream_t stream);
+
+/* dw (K,C,S) = sum_n sum_q x(n,c,q+d*s) dy(n,k,q) */
+C1D_EXPORT c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* dy, float* dw_kcs,
+                               void* workspace, size_t workspace_bytes, c1d_stream_t stream);
+
+/* out[i] = bf16 bits of in[i], round-to-nearest-even, NaN -> quiet NaN (bf16.hpp:29-40). */
+C1D_EXPORT c1d_status c1d_round_bf16(const float* in, uint16_t* out, int64_t count, c1d_stream_t stream);
+
+/* Number of kernels this library has launched since load (instrumentation for benchmarks). */
+C1D_EXPORT uint64_t c1d_launch_count(void);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* C1D_H_ */

@@ -1,0 +1,281 @@
+"""Host-side mirror of the reference operator API (namespace conv1d, proj/include/conv1d/conv.hpp,
+tensor.hpp, errors.hpp) over the B200 C ABI (include/c1d.h).
+
+Same names, argument meaning and error behaviour as the reference:
+
+* ``conv1d_forward(in, w, p)``           conv.hpp:42-43    (NCW input, packed or KCS weights)
+* ``conv1d_backward_data(grad_out, w, p)`` conv.hpp:49-50  (gradient w.r.t. the padded input)
+* ``conv1d_backward_weight(grad_out, in, p)`` conv.hpp:56-57 (returns KCS)
+* ``output_width``, ``conv_shapes``, ``conv_flops``        conv.hpp:31-37
+* ``pack_weights_forward/backward``, ``unpack_weights``    tensor.hpp:77-81
+* exceptions ``ShapeMismatch``, ``OddDims``, ``TooNarrow`` (subclasses of ``Error``) errors.hpp
+
+Tensors are torch CUDA tensors (device memory, any stream); the reference's ``threads``
+argument is accepted and ignored. Inputs may be float32 or bfloat16 storage; outputs are
+float32 as in the reference.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib as L
+
+
+class Precision(enum.IntEnum):
+    Fp32 = 0
+    Bf16 = 1
+
+
+class WeightLayout(enum.IntEnum):
+    ForwardSKC = 0
+    BackwardSCK = 1
+
+
+@dataclass
+class ConvParams:
+    """conv1d::ConvParams (conv.hpp:18-25)."""
+
+    channels: int = 1
+    filters: int = 1
+    taps: int = 1
+    dilation: int = 1
+    precision: Precision = Precision.Fp32
+    block_w: int = 64
+
+
+@dataclass
+class ConvShapes:
+    q: int
+    w_padded: int
+    receptive: int
+
+
+@dataclass
+class PackedWeights:
+    """conv1d::PackedWeights (tensor.hpp:67-75): data is (S, K, C) for ForwardSKC and (S, C, K)
+    with the tap axis reversed for BackwardSCK."""
+
+    layout: WeightLayout
+    s: int
+    k: int
+    c: int
+    data: torch.Tensor
+
+
+# ----------------------------------------------------------------------------- errors (errors.hpp)
+class Error(RuntimeError):
+    pass
+
+
+class ShapeMismatch(Error):
+    pass
+
+
+class OddDims(Error):
+    pass
+
+
+class TooNarrow(Error):
+    pass
+
+
+class UnsupportedShape(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+_STATUS_TO_ERROR = {
+    L.ERR_SHAPE_MISMATCH: ShapeMismatch,
+    L.ERR_ODD_DIMS: OddDims,
+    L.ERR_TOO_NARROW: TooNarrow,
+    L.ERR_UNSUPPORTED: UnsupportedShape,
+    L.ERR_CUDA: CudaError,
+    L.ERR_NO_DEVICE: CudaError,
+}
+
+
+def _check(status: int) -> None:
+    if status == L.OK:
+        return
+    lib = L.lib()
+    msg = lib.c1d_last_error_message().decode() or lib.c1d_strerror(status).decode()
+    raise _STATUS_TO_ERROR.get(status, Error)(msg)
+
+
+_ALGOS = {"auto": L.ALGO_AUTO, "direct": L.ALGO_DIRECT, "tcgen05": L.ALGO_TCGEN05, "tf32x3": L.ALGO_TF32X3}
+ALGO_NAMES = {v: k for k, v in _ALGOS.items()}
+
+
+def make_desc(p: ConvParams, n: int, w_in: int, in_dtype: int = L.DTYPE_F32, algo: str = "auto",
+              strict: bool = False) -> L.Desc:
+    return L.Desc(n=n, c=p.channels, k=p.filters, s=p.taps, d=p.dilation, w_in=w_in, precision=int(p.precision),
+                  in_dtype=in_dtype, algo=_ALGOS[algo], flags=L.FLAG_STRICT_BF16_DIMS if strict else 0,
+                  block_w=p.block_w)
+
+
+# ----------------------------------------------------------------------------- geometry
+def output_width(p: ConvParams, w_padded: int) -> int:
+    q = C.c_int64(0)
+    _check(L.lib().c1d_output_width(C.byref(make_desc(p, 1, w_padded)), C.byref(q)))
+    return q.value
+
+
+def conv_shapes(p: ConvParams, w_padded: int) -> ConvShapes:
+    return ConvShapes(q=output_width(p, w_padded), w_padded=w_padded, receptive=p.dilation * (p.taps - 1))
+
+
+def conv_flops(p: ConvParams, batch: int, q: int) -> int:
+    return 2 * batch * p.filters * p.channels * p.taps * q
+
+
+def same_pad_width(taps: int, dilation: int) -> int:
+    r = dilation * (taps - 1)
+    if r % 2:
+        raise ShapeMismatch(f"same padding needs even d*(S-1), got {r}")
+    return r // 2
+
+
+# ----------------------------------------------------------------------------- weights
+def pack_weights_forward(w_kcs: torch.Tensor) -> PackedWeights:
+    k, c, s = w_kcs.shape
+    return PackedWeights(WeightLayout.ForwardSKC, s, k, c, w_kcs.permute(2, 0, 1).contiguous())
+
+
+def pack_weights_backward(w_kcs: torch.Tensor) -> PackedWeights:
+    k, c, s = w_kcs.shape
+    return PackedWeights(WeightLayout.BackwardSCK, s, k, c, w_kcs.flip(2).permute(2, 1, 0).contiguous())
+
+
+def unpack_weights(pw: PackedWeights) -> torch.Tensor:
+    if pw.layout == WeightLayout.ForwardSKC:
+        return pw.data.permute(1, 2, 0).contiguous()
+    return pw.data.permute(2, 1, 0).flip(2).contiguous()
+
+
+def _weights_kcs(w, p: ConvParams, want: WeightLayout) -> torch.Tensor:
+    if isinstance(w, PackedWeights):
+        if w.layout != want:
+            raise ShapeMismatch("packed weights have the wrong layout for this pass")
+        if (w.c, w.k, w.s) != (p.channels, p.filters, p.taps):
+            raise ShapeMismatch(f"packed weights are S={w.s} K={w.k} C={w.c}, conv params say "
+                                f"S={p.taps} K={p.filters} C={p.channels}")
+        w = unpack_weights(w)
+    if tuple(w.shape) != (p.filters, p.channels, p.taps):
+        raise ShapeMismatch(f"weights are {tuple(w.shape)}, conv params say K={p.filters} C={p.channels} S={p.taps}")
+    return _dev_f32(w)
+
+
+def _dev_f32(t: torch.Tensor) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ShapeMismatch("tensors must live on a CUDA device")
+    return t.to(torch.float32).contiguous()
+
+
+def _dev_input(t: torch.Tensor) -> tuple[torch.Tensor, int]:
+    if not t.is_cuda:
+        raise ShapeMismatch("tensors must live on a CUDA device")
+    if t.dtype == torch.bfloat16:
+        return t.contiguous(), L.DTYPE_BF16
+    return t.to(torch.float32).contiguous(), L.DTYPE_F32
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# ----------------------------------------------------------------------------- passes
+def conv1d_forward(inp: torch.Tensor, w, p: ConvParams, threads: int = 1, *, algo: str = "auto",
+                   strict: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Forward pass (conv.cpp:165-191): out(n,k,q) = sum_c sum_s in(n,c,q+d*s) * w(k,c,s)."""
+    if inp.dim() != 3:
+        raise ShapeMismatch("input must be (N, C, W)")
+    n, c, w_in = inp.shape
+    if c != p.channels:
+        raise ShapeMismatch(f"input has {c} channels, conv expects {p.channels}")
+    wk = _weights_kcs(w, p, WeightLayout.ForwardSKC)
+    x, dt = _dev_input(inp)
+    desc = make_desc(p, n, w_in, dt, algo, strict)
+    q = C.c_int64(0)
+    _check(L.lib().c1d_output_width(C.byref(desc), C.byref(q)))
+    if out is None:
+        out = torch.empty((n, p.filters, q.value), dtype=torch.float32, device=x.device)
+    _check(L.lib().c1d_forward(C.byref(desc), x.data_ptr(), wk.data_ptr(), out.data_ptr(), None, 0, _stream()))
+    return out
+
+
+def conv1d_backward_data(grad_out: torch.Tensor, w, p: ConvParams, threads: int = 1, *, algo: str = "auto",
+                         strict: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Backward-data pass (conv.cpp:193-227): gradient w.r.t. the padded input, width Q + d(S-1)."""
+    if grad_out.dim() != 3:
+        raise ShapeMismatch("grad_out must be (N, K, Q)")
+    n, k, q = grad_out.shape
+    if k != p.filters:
+        raise ShapeMismatch(f"grad_out has {k} channels, conv has K={p.filters}")
+    wk = _weights_kcs(w, p, WeightLayout.BackwardSCK)
+    g, dt = _dev_input(grad_out)
+    w_in = q + p.dilation * (p.taps - 1)
+    desc = make_desc(p, n, w_in, dt, algo, strict)
+    if out is None:
+        out = torch.empty((n, p.channels, w_in), dtype=torch.float32, device=g.device)
+    _check(L.lib().c1d_backward_data(C.byref(desc), g.data_ptr(), wk.data_ptr(), out.data_ptr(), None, 0,
+                                     _stream()))
+    return out
+
+
+def conv1d_backward_weight(grad_out: torch.Tensor, inp: torch.Tensor, p: ConvParams, threads: int = 1, *,
+                           algo: str = "auto", strict: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """Backward-weight pass (conv.cpp:229-326): grad_w(k,c,s) = sum_n sum_q in(n,c,q+d*s) grad_out(n,k,q)."""
+    if grad_out.dim() != 3 or inp.dim() != 3:
+        raise ShapeMismatch("tensors must be rank 3")
+    n, k, q = grad_out.shape
+    n2, c, w_in = inp.shape
+    if n != n2:
+        raise ShapeMismatch("batch sizes differ between input and grad_out")
+    if c != p.channels or k != p.filters:
+        raise ShapeMismatch("channel counts do not match conv params")
+    if w_in != q + p.dilation * (p.taps - 1):
+        raise ShapeMismatch(f"input width {w_in} != Q + d*(S-1) = {q + p.dilation * (p.taps - 1)}")
+    g, dt_g = _dev_input(grad_out)
+    x, dt_x = _dev_input(inp)
+    if dt_g != dt_x:  # one storage dtype per call
+        g, x = g.to(torch.float32), x.to(torch.float32)
+        dt_g = dt_x = L.DTYPE_F32
+    desc = make_desc(p, n, w_in, dt_x, algo, strict)
+    if out is None:
+        out = torch.empty((k, c, p.taps), dtype=torch.float32, device=x.device)
+    _check(L.lib().c1d_backward_weight(C.byref(desc), x.data_ptr(), g.data_ptr(), out.data_ptr(), None, 0,
+                                       _stream()))
+    return out
+
+
+def round_bf16(t: torch.Tensor) -> torch.Tensor:
+    """Reference-exact RNE fp32 -> bf16 (bf16.hpp:29-40) on the device; returns a bfloat16 tensor."""
+    src = _dev_f32(t)
+    out = torch.empty(src.shape, dtype=torch.bfloat16, device=src.device)
+    _check(L.lib().c1d_round_bf16(src.data_ptr(), out.data_ptr(), src.numel(), _stream()))
+    return out
+
+
+def selected_algo(p: ConvParams, n: int, w_in: int, pass_: int, in_dtype: int = L.DTYPE_BF16,
+                  algo: str = "auto") -> str:
+    a = C.c_int(0)
+    _check(L.lib().c1d_selected_algo(C.byref(make_desc(p, n, w_in, in_dtype, algo)), pass_, C.byref(a)))
+    return ALGO_NAMES[a.value]
+
+
+def workspace_size(p: ConvParams, n: int, w_in: int, pass_: int, in_dtype: int = L.DTYPE_BF16,
+                   algo: str = "auto") -> int:
+    b = C.c_size_t(0)
+    _check(L.lib().c1d_workspace_size(C.byref(make_desc(p, n, w_in, in_dtype, algo)), pass_, C.byref(b)))
+    return b.value
+
+
+def launch_count() -> int:
+    return L.lib().c1d_launch_count()

@@ -1,0 +1,378 @@
+// c1d_api.cu — the C ABI (include/c1d.h): validation, workspace, kernel selection, dispatch.
+//
+// Validation mirrors the reference's checks and error classes:
+//   validate_params (positivity, BF16 even dims)  proj/src/conv.cpp:33-50  -> SHAPE_MISMATCH / ODD_DIMS
+//   check_bf16_widths                             proj/src/conv.cpp:52-57  -> ODD_DIMS (strict mode)
+//   output_width / TooNarrow                      proj/src/conv.cpp:142-151
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/c1d.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace c1d {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
+
+int num_sms() {
+    static int sms = [] {
+        int dev = 0, v = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
+    return sms;
+}
+
+namespace {
+
+thread_local std::string t_last_error;
+
+c1d_status fail(c1d_status st, const std::string& msg) {
+    t_last_error = msg;
+    return st;
+}
+
+c1d_status cuda_fail(cudaError_t e, const char* where) {
+    return fail(C1D_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Per-device internal workspace (used when the caller passes workspace == NULL).
+struct DeviceWorkspace {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+};
+std::mutex g_ws_mutex;
+std::vector<DeviceWorkspace> g_ws;
+
+cudaError_t internal_workspace(size_t need, void** out) {
+    *out = nullptr;
+    if (need == 0) return cudaSuccess;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_ws_mutex);
+    if (static_cast<int>(g_ws.size()) <= dev) g_ws.resize(dev + 1);
+    DeviceWorkspace& w = g_ws[dev];
+    if (w.bytes < need) {
+        if (w.ptr) {
+            e = cudaDeviceSynchronize();  // in-flight work may still read the old buffer
+            if (e != cudaSuccess) return e;
+            cudaFree(w.ptr);
+            w.ptr = nullptr;
+            w.bytes = 0;
+        }
+        const size_t grow = need + need / 4;
+        e = cudaMalloc(&w.ptr, grow);
+        if (e != cudaSuccess) return e;
+        w.bytes = grow;
+    }
+    *out = w.ptr;
+    return cudaSuccess;
+}
+
+bool is_bf16(const c1d_desc& d) { return d.precision == C1D_PRECISION_BF16; }
+
+c1d_status validate(const c1d_desc* desc, int64_t* q_out) {
+    if (!desc) return fail(C1D_ERR_INVALID_ARGUMENT, "desc is NULL");
+    const c1d_desc& d = *desc;
+    if (d.c < 1 || d.k < 1 || d.s < 1 || d.d < 1) {
+        return fail(C1D_ERR_SHAPE_MISMATCH, "conv params must be positive: C=" + std::to_string(d.c) +
+                                                " K=" + std::to_string(d.k) + " S=" + std::to_string(d.s) +
+                                                " d=" + std::to_string(d.d));
+    }
+    if (d.n < 0 || d.w_in < 0) return fail(C1D_ERR_SHAPE_MISMATCH, "negative batch or width");
+    if (d.precision != C1D_PRECISION_FP32 && d.precision != C1D_PRECISION_BF16)
+        return fail(C1D_ERR_INVALID_ARGUMENT, "unknown precision");
+    if (d.in_dtype != C1D_DTYPE_F32 && d.in_dtype != C1D_DTYPE_BF16)
+        return fail(C1D_ERR_INVALID_ARGUMENT, "unknown in_dtype");
+    if (d.algo < C1D_ALGO_AUTO || d.algo > C1D_ALGO_TF32X3) return fail(C1D_ERR_INVALID_ARGUMENT, "unknown algo");
+    const int64_t receptive = d.d * (d.s - 1);
+    if (d.w_in <= receptive) {
+        return fail(C1D_ERR_TOO_NARROW, "padded width " + std::to_string(d.w_in) +
+                                            " does not cover the receptive field d*(S-1) = " +
+                                            std::to_string(receptive));
+    }
+    const int64_t q = d.w_in - receptive;
+    if ((d.flags & C1D_FLAG_STRICT_BF16_DIMS) && is_bf16(d)) {
+        if (d.c % 2 != 0 || d.k % 2 != 0)
+            return fail(C1D_ERR_ODD_DIMS, "bf16 conv needs even channels and filters, got C=" + std::to_string(d.c) +
+                                              " K=" + std::to_string(d.k));
+        if (d.block_w > 0 && d.block_w % 2 != 0)
+            return fail(C1D_ERR_ODD_DIMS, "bf16 conv needs an even width tile, got " + std::to_string(d.block_w));
+        if (d.w_in % 2 != 0 || q % 2 != 0)
+            return fail(C1D_ERR_ODD_DIMS, "bf16 conv needs even tensor widths, got input " + std::to_string(d.w_in) +
+                                              ", output " + std::to_string(q));
+    }
+    if (d.n > (int64_t{1} << 31) || d.c * d.s > (int64_t{1} << 31) || d.k * d.s > (int64_t{1} << 31))
+        return fail(C1D_ERR_UNSUPPORTED, "dimensions too large");
+    *q_out = q;
+    return C1D_OK;
+}
+
+ConvGeom fwd_geom(const c1d_desc& d, int64_t q) {
+    return ConvGeom{d.n, d.c, d.w_in, d.k, q, d.s, d.d, 0};
+}
+ConvGeom bwd_geom(const c1d_desc& d, int64_t q) {
+    return ConvGeom{d.n, d.k, q, d.c, d.w_in, d.s, d.d, -d.d * (d.s - 1)};
+}
+
+// Resolve AUTO.
+c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
+    const bool tc_ok = [&] {
+        if (!is_bf16(d)) return false;
+        if (pass == C1D_PASS_FORWARD) return tc_conv_supported(fwd_geom(d, q));
+        if (pass == C1D_PASS_BACKWARD_DATA) return tc_conv_supported(bwd_geom(d, q));
+        return tc_wgrad_supported(d.n, d.c, d.k, d.s, d.d, q);
+    }();
+    if (d.algo == C1D_ALGO_AUTO) return tc_ok ? C1D_ALGO_TCGEN05 : C1D_ALGO_DIRECT;
+    if (d.algo == C1D_ALGO_TCGEN05 && !tc_ok) return static_cast<c1d_algo>(-1);
+    if (d.algo == C1D_ALGO_TF32X3) return static_cast<c1d_algo>(-1);  // not built yet
+    return static_cast<c1d_algo>(d.algo);
+}
+
+size_t align_up(size_t v) { return (v + 255) & ~size_t{255}; }
+
+size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo) {
+    const size_t wbytes = align_up(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+    if (algo == C1D_ALGO_DIRECT) {
+        if (pass == C1D_PASS_BACKWARD_WEIGHT) return align_up(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
+        return wbytes;
+    }
+    // tensor-core paths: BF16 copies of FP32 inputs + kernel workspace
+    const bool conv_in_f32 = d.in_dtype == C1D_DTYPE_F32;
+    if (pass == C1D_PASS_FORWARD) {
+        const ConvGeom g = fwd_geom(d, q);
+        size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
+        if (conv_in_f32) b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
+        return b;
+    }
+    if (pass == C1D_PASS_BACKWARD_DATA) {
+        const ConvGeom g = bwd_geom(d, q);
+        size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
+        if (conv_in_f32) b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        return b;
+    }
+    size_t b = align_up(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, q));
+    if (conv_in_f32)
+        b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in)) +
+             align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+    return b;
+}
+
+struct Bump {
+    char* p;
+    size_t left;
+    template <typename T>
+    T* take(size_t bytes) {
+        bytes = align_up(bytes);
+        if (bytes > left) return nullptr;
+        T* r = reinterpret_cast<T*>(p);
+        p += bytes;
+        left -= bytes;
+        return r;
+    }
+};
+
+c1d_status acquire_workspace(void* user, size_t user_bytes, size_t need, Bump* out) {
+    if (user) {
+        if (user_bytes < need)
+            return fail(C1D_ERR_WORKSPACE, "workspace of " + std::to_string(user_bytes) + " bytes, need " +
+                                               std::to_string(need));
+        *out = Bump{static_cast<char*>(user), user_bytes};
+        return C1D_OK;
+    }
+    void* p = nullptr;
+    cudaError_t e = internal_workspace(need, &p);
+    if (e != cudaSuccess) return cuda_fail(e, "internal workspace");
+    *out = Bump{static_cast<char*>(p), need};
+    return C1D_OK;
+}
+
+c1d_status check_device() {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    int major = 0;
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major < 10) return fail(C1D_ERR_NO_DEVICE, "needs an sm_100 (B200) device");
+    return C1D_OK;
+}
+
+// Conv-shaped pass (forward or backward-data).
+c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const float* w_kcs, float* out,
+                     void* ws, size_t ws_bytes, cudaStream_t stream) {
+    t_last_error.clear();
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const c1d_desc& d = *desc;
+    if (d.n == 0) return C1D_OK;
+    if (!in || !w_kcs || !out) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
+    st = check_device();
+    if (st != C1D_OK) return st;
+    const c1d_algo algo = resolve(d, pass, q);
+    if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    const ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
+    Bump bump{};
+    st = acquire_workspace(ws, ws_bytes, workspace_for(d, pass, q, algo), &bump);
+    if (st != C1D_OK) return st;
+    const bool bf16 = is_bf16(d);
+    float* wg = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+    cudaError_t e = launch_prep_weights(w_kcs, wg, d.k, d.c, d.s,
+                                        pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData, bf16,
+                                        stream);
+    if (e != cudaSuccess) return cuda_fail(e, "prep_weights");
+    if (algo == C1D_ALGO_DIRECT) {
+        e = launch_direct_conv(in, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, wg, out, g, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "direct_conv");
+        return C1D_OK;
+    }
+    const uint16_t* in_b = static_cast<const uint16_t*>(in);
+    if (d.in_dtype == C1D_DTYPE_F32) {
+        const int64_t count = g.n * g.in_ch * g.in_w;
+        uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(count));
+        e = launch_round_bf16(static_cast<const float*>(in), tmp, count, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
+        in_b = tmp;
+    }
+    void* kws = bump.take<char>(tc_conv_workspace_bytes(g));
+    e = launch_tc_conv(in_b, wg, out, g, kws, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
+    return C1D_OK;
+}
+
+}  // namespace
+}  // namespace c1d
+
+using namespace c1d;
+
+extern "C" {
+
+int c1d_api_version(void) { return C1D_API_VERSION; }
+
+const char* c1d_strerror(c1d_status status) {
+    switch (status) {
+        case C1D_OK: return "ok";
+        case C1D_ERR_SHAPE_MISMATCH: return "shape mismatch";
+        case C1D_ERR_ODD_DIMS: return "bf16 conv needs even dimensions";
+        case C1D_ERR_TOO_NARROW: return "input narrower than the receptive field";
+        case C1D_ERR_INVALID_ARGUMENT: return "invalid argument";
+        case C1D_ERR_WORKSPACE: return "workspace too small";
+        case C1D_ERR_UNSUPPORTED: return "unsupported shape for the requested algorithm";
+        case C1D_ERR_CUDA: return "CUDA error";
+        case C1D_ERR_NO_DEVICE: return "no sm_100 device";
+    }
+    return "unknown status";
+}
+
+const char* c1d_last_error_message(void) { return t_last_error.c_str(); }
+
+c1d_status c1d_output_width(const c1d_desc* desc, int64_t* q_out) {
+    t_last_error.clear();
+    if (!q_out) return fail(C1D_ERR_INVALID_ARGUMENT, "q_out is NULL");
+    return validate(desc, q_out);
+}
+
+int64_t c1d_conv_flops(const c1d_desc* desc) {
+    int64_t q = 0;
+    if (validate(desc, &q) != C1D_OK) return -1;
+    return int64_t{2} * desc->n * desc->k * desc->c * desc->s * q;
+}
+
+c1d_status c1d_selected_algo(const c1d_desc* desc, c1d_pass pass, c1d_algo* algo) {
+    t_last_error.clear();
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const c1d_algo a = resolve(*desc, pass, q);
+    if (static_cast<int>(a) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    if (algo) *algo = a;
+    return C1D_OK;
+}
+
+c1d_status c1d_workspace_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes) {
+    t_last_error.clear();
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const c1d_algo a = resolve(*desc, pass, q);
+    if (static_cast<int>(a) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    if (bytes) *bytes = workspace_for(*desc, pass, q, a);
+    return C1D_OK;
+}
+
+c1d_status c1d_forward(const c1d_desc* desc, const void* x, const float* w_kcs, float* y, void* workspace,
+                       size_t workspace_bytes, c1d_stream_t stream) {
+    return conv_pass(desc, C1D_PASS_FORWARD, x, w_kcs, y, workspace, workspace_bytes,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+c1d_status c1d_backward_data(const c1d_desc* desc, const void* dy, const float* w_kcs, float* dx, void* workspace,
+                             size_t workspace_bytes, c1d_stream_t stream) {
+    return conv_pass(desc, C1D_PASS_BACKWARD_DATA, dy, w_kcs, dx, workspace, workspace_bytes,
+                     reinterpret_cast<cudaStream_t>(stream));
+}
+
+c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* dy, float* dw_kcs, void* workspace,
+                               size_t workspace_bytes, c1d_stream_t stream_) {
+    t_last_error.clear();
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const c1d_desc& d = *desc;
+    if (!dw_kcs) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL dw pointer");
+    st = check_device();
+    if (st != C1D_OK) return st;
+    if (d.n == 0) {
+        cudaError_t e = cudaMemsetAsync(dw_kcs, 0, sizeof(float) * static_cast<size_t>(d.k * d.c * d.s), stream);
+        return e == cudaSuccess ? C1D_OK : cuda_fail(e, "memset");
+    }
+    if (!x || !dy) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
+    const c1d_algo algo = resolve(d, C1D_PASS_BACKWARD_WEIGHT, q);
+    if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    Bump bump{};
+    st = acquire_workspace(workspace, workspace_bytes, workspace_for(d, C1D_PASS_BACKWARD_WEIGHT, q, algo), &bump);
+    if (st != C1D_OK) return st;
+    const bool bf16 = is_bf16(d);
+    cudaError_t e;
+    if (algo == C1D_ALGO_DIRECT) {
+        float* part = bump.take<float>(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
+        e = launch_direct_wgrad(x, dy, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, dw_kcs, part, d.n, d.c, d.k,
+                                d.s, d.d, q, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "direct_wgrad");
+        return C1D_OK;
+    }
+    const uint16_t* xb = static_cast<const uint16_t*>(x);
+    const uint16_t* gb = static_cast<const uint16_t*>(dy);
+    if (d.in_dtype == C1D_DTYPE_F32) {
+        uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
+        uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        e = launch_round_bf16(static_cast<const float*>(x), tx, d.n * d.c * d.w_in, stream);
+        if (e == cudaSuccess) e = launch_round_bf16(static_cast<const float*>(dy), tg, d.n * d.k * q, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
+        xb = tx;
+        gb = tg;
+    }
+    void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, q));
+    e = launch_tc_wgrad(xb, gb, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, q, stream);
+    if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad");
+    return C1D_OK;
+}
+
+c1d_status c1d_round_bf16(const float* in, uint16_t* out, int64_t count, c1d_stream_t stream) {
+    t_last_error.clear();
+    if (count < 0 || (count > 0 && (!in || !out))) return fail(C1D_ERR_INVALID_ARGUMENT, "bad round_bf16 arguments");
+    cudaError_t e = launch_round_bf16(in, out, count, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "round_bf16");
+}
+
+uint64_t c1d_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

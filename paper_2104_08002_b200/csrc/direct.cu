@@ -1,0 +1,302 @@
+// direct.cu — CUDA-core (FFMA) direct convolution kernels: the any-shape path.
+//
+// These cover every shape the reference accepts (any C, K, S, d, width; FP32 or BF16 precision)
+// and serve as the FP32 path. The tensor-core kernels (tc_conv.cu, tc_wgrad.cu) take over for
+// the shapes they support. Accumulation is FP32 with FMA; results are deterministic (fixed
+// iteration order, no atomics) and match the reference's naive oracle within its 1e-5 bound.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace c1d {
+
+// ------------------------------------------------------------------------------- weights
+__global__ void prep_weights_kernel(const float* __restrict__ w, float* __restrict__ out, int64_t K, int64_t C,
+                                    int64_t S, int mode, int round) {
+    const int64_t total = K * C * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        float v;
+        if (mode == kWeightsForward) {
+            v = w[e];  // (k, c, s) -> (k, c, s)
+        } else {
+            // out index e = (c, k, s') holds w(k, c, S-1-s')
+            const int64_t sp = e % S;
+            const int64_t kk = (e / S) % K;
+            const int64_t cc = e / (S * K);
+            v = w[(kk * C + cc) * S + (S - 1 - sp)];
+        }
+        out[e] = round ? round_to_bf16(v) : v;
+    }
+}
+
+cudaError_t launch_prep_weights(const float* w_kcs, float* out, int64_t K, int64_t C, int64_t S, int mode,
+                                bool round, cudaStream_t stream) {
+    const int64_t total = K * C * S;
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, threads), 4096));
+    prep_weights_kernel<<<blocks, threads, 0, stream>>>(w_kcs, out, K, C, S, mode, round ? 1 : 0);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------- forward-shaped
+// Block tile: 16 output channels x 256 output columns, 256 threads, each thread a 4x4
+// register tile (4 channels x 4 columns strided by 64). Input channels are staged through
+// shared memory in chunks of 8 together with the halo (taps-1)*dil.
+namespace {
+constexpr int kTO = 16;    // output channels per block
+constexpr int kTX = 256;   // output columns per block
+constexpr int kCC = 8;     // input channels per smem chunk
+}  // namespace
+
+template <typename TIn>
+__global__ void __launch_bounds__(256) direct_conv_kernel(const TIn* __restrict__ in, const float* __restrict__ wg,
+                                                          float* __restrict__ out, ConvGeom g, int round_in) {
+    extern __shared__ float smem[];
+    const int64_t halo = (g.taps - 1) * g.dil;
+    const int64_t span = kTX + halo;
+    float* xs = smem;                   // [kCC][span]
+    float* ws = smem + kCC * span;      // [kTO][kCC][taps]
+    const int tid = threadIdx.x;
+    const int og = tid / 64;            // 4 output-channel groups of 4
+    const int xg = tid % 64;            // column lane
+    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kTX;
+    const int64_t o0 = static_cast<int64_t>(blockIdx.y) * kTO;
+    const int64_t n = blockIdx.z;
+    const TIn* in_n = in + n * g.in_ch * g.in_w;
+
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+
+    for (int64_t c0 = 0; c0 < g.in_ch; c0 += kCC) {
+        __syncthreads();
+        for (int64_t e = tid; e < kCC * span; e += blockDim.x) {
+            const int64_t cc = e / span, xx = e % span;
+            const int64_t c = c0 + cc;
+            const int64_t src = x0 + xx + g.in_off;
+            float v = 0.0f;
+            if (c < g.in_ch && src >= 0 && src < g.in_w) v = load_as_float(in_n, c * g.in_w + src, round_in != 0);
+            xs[e] = v;
+        }
+        for (int64_t e = tid; e < kTO * kCC * g.taps; e += blockDim.x) {
+            const int64_t s = e % g.taps;
+            const int64_t cc = (e / g.taps) % kCC;
+            const int64_t oo = e / (g.taps * kCC);
+            const int64_t o = o0 + oo, c = c0 + cc;
+            ws[e] = (o < g.out_ch && c < g.in_ch) ? wg[(o * g.in_ch + c) * g.taps + s] : 0.0f;
+        }
+        __syncthreads();
+        const int cmax = static_cast<int>(std::min<int64_t>(kCC, g.in_ch - c0));
+        for (int cc = 0; cc < cmax; ++cc) {
+            const float* xr = xs + cc * span + xg;
+            const float* wr = ws + (og * 4) * kCC * g.taps + cc * g.taps;
+            for (int s = 0; s < g.taps; ++s) {
+                float wv[4], xv[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) wv[i] = wr[i * kCC * g.taps + s];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) xv[j] = xr[j * 64 + s * g.dil];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(wv[i], xv[j], acc[i][j]);
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t o = o0 + og * 4 + i;
+        if (o >= g.out_ch) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t x = x0 + xg + 64 * j;
+            if (x < g.out_w) out[(n * g.out_ch + o) * g.out_w + x] = acc[i][j];
+        }
+    }
+}
+
+cudaError_t launch_direct_conv(const void* in, int in_dtype, bool round_in, const float* wg, float* out,
+                               const ConvGeom& g, cudaStream_t stream) {
+    const int64_t span = kTX + (g.taps - 1) * g.dil;
+    const size_t smem = sizeof(float) * static_cast<size_t>(kCC * span + kTO * kCC * g.taps);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    dim3 grid(static_cast<unsigned>(ceil_div(g.out_w, kTX)), static_cast<unsigned>(ceil_div(g.out_ch, kTO)),
+              static_cast<unsigned>(g.n));
+    if (g.n > 65535 || grid.y > 65535) return cudaErrorInvalidValue;
+    cudaError_t e;
+    if (in_dtype == 0) {
+        e = cudaFuncSetAttribute(direct_conv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        direct_conv_kernel<float><<<grid, 256, smem, stream>>>(static_cast<const float*>(in), wg, out, g,
+                                                                round_in ? 1 : 0);
+    } else {
+        e = cudaFuncSetAttribute(direct_conv_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        direct_conv_kernel<uint16_t><<<grid, 256, smem, stream>>>(static_cast<const uint16_t*>(in), wg, out, g, 0);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------- backward weight
+// Split-W partial sums: block (kb, cb, split) owns a 16x16 (filter, channel) tile and a
+// contiguous range of (item, 128-column chunk) work units; each thread owns one (k, c) pair and
+// up to 64 taps in registers. Partials land in workspace[split][k][c][s] and a second kernel
+// sums the splits in ascending order (deterministic; the reference reduces per-item partials
+// in ascending item order, conv.cpp:308-314).
+namespace {
+constexpr int kWT = 16;     // filters / channels per block tile
+constexpr int kWQ = 128;    // columns per chunk
+constexpr int kWS = 64;     // taps held in registers per pass
+}  // namespace
+
+static int64_t wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t q) {
+    const int64_t tiles = ceil_div(k, kWT) * ceil_div(c, kWT);
+    const int64_t units = n * ceil_div(q, kWQ);
+    const int64_t want = std::max<int64_t>(1, (2 * num_sms() + tiles - 1) / tiles);
+    return std::max<int64_t>(1, std::min<int64_t>(want, units));
+}
+
+size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t q) {
+    return sizeof(float) * static_cast<size_t>(wgrad_splits(n, c, k, q) * k * c * s);
+}
+
+template <typename TIn>
+__global__ void __launch_bounds__(256) direct_wgrad_kernel(const TIn* __restrict__ x, const TIn* __restrict__ dy,
+                                                           float* __restrict__ part, int64_t N, int64_t C, int64_t K,
+                                                           int64_t S, int64_t D, int64_t Q, int64_t splits,
+                                                           int round_in) {
+    extern __shared__ float smem[];
+    const int64_t halo = (S - 1) * D;
+    const int64_t span = kWQ + halo;
+    float* xs = smem;                   // [kWT][span]
+    float* gs = smem + kWT * span;      // [kWT][kWQ]
+    const int tid = threadIdx.x;
+    const int kl = tid / kWT, cl = tid % kWT;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kWT, c0 = static_cast<int64_t>(blockIdx.y) * kWT;
+    const int64_t split = blockIdx.z;
+    const int64_t chunks_per_item = ceil_div(Q, kWQ);
+    const int64_t units = N * chunks_per_item;
+    const int64_t u_begin = units * split / splits, u_end = units * (split + 1) / splits;
+    const int64_t W = Q + halo;
+
+    for (int64_t s0 = 0; s0 < S; s0 += kWS) {
+        float acc[kWS];
+#pragma unroll
+        for (int j = 0; j < kWS; ++j) acc[j] = 0.0f;
+        for (int64_t u = u_begin; u < u_end; ++u) {
+            const int64_t n = u / chunks_per_item;
+            const int64_t q0 = (u % chunks_per_item) * kWQ;
+            __syncthreads();
+            for (int64_t e = tid; e < kWT * span; e += blockDim.x) {
+                const int64_t cc = e / span, xx = e % span;
+                const int64_t c = c0 + cc, pos = q0 + xx;
+                xs[e] = (c < C && pos < W) ? load_as_float(x, (n * C + c) * W + pos, round_in != 0) : 0.0f;
+            }
+            for (int64_t e = tid; e < kWT * kWQ; e += blockDim.x) {
+                const int64_t kk = e / kWQ, xx = e % kWQ;
+                const int64_t k = k0 + kk, pos = q0 + xx;
+                gs[e] = (k < K && pos < Q) ? load_as_float(dy, (n * K + k) * Q + pos, round_in != 0) : 0.0f;
+            }
+            __syncthreads();
+            const float* xr = xs + cl * span + s0 * D;
+            const float* gr = gs + kl * kWQ;
+            for (int xx = 0; xx < kWQ; ++xx) {
+                const float gv = gr[xx];
+#pragma unroll
+                for (int j = 0; j < kWS; ++j) {
+                    if (s0 + j < S) acc[j] = fmaf(xr[xx + j * D], gv, acc[j]);
+                }
+            }
+        }
+        const int64_t k = k0 + kl, c = c0 + cl;
+        if (k < K && c < C) {
+            float* dst = part + ((split * K + k) * C + c) * S;
+#pragma unroll
+            for (int j = 0; j < kWS; ++j)
+                if (s0 + j < S) dst[s0 + j] = acc[j];
+        }
+    }
+}
+
+__global__ void reduce_splits_kernel(const float* __restrict__ part, float* __restrict__ out, int64_t count,
+                                     int64_t splits) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+        float v = 0.0f;
+        for (int64_t sp = 0; sp < splits; ++sp) v += part[sp * count + e];
+        out[e] = v;
+    }
+}
+
+cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, bool round_in, float* dw_kcs,
+                                float* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d,
+                                int64_t q, cudaStream_t stream) {
+    const int64_t splits = wgrad_splits(n, c, k, q);
+    const int64_t span = kWQ + (s - 1) * d;
+    const size_t smem = sizeof(float) * static_cast<size_t>(kWT * span + kWT * kWQ);
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    dim3 grid(static_cast<unsigned>(ceil_div(k, kWT)), static_cast<unsigned>(ceil_div(c, kWT)),
+              static_cast<unsigned>(splits));
+    cudaError_t e;
+    if (in_dtype == 0) {
+        e = cudaFuncSetAttribute(direct_wgrad_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        direct_wgrad_kernel<float><<<grid, 256, smem, stream>>>(static_cast<const float*>(x),
+                                                                 static_cast<const float*>(dy), workspace, n, c, k, s,
+                                                                 d, q, splits, round_in ? 1 : 0);
+    } else {
+        e = cudaFuncSetAttribute(direct_wgrad_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        direct_wgrad_kernel<uint16_t><<<grid, 256, smem, stream>>>(static_cast<const uint16_t*>(x),
+                                                                    static_cast<const uint16_t*>(dy), workspace, n, c,
+                                                                    k, s, d, q, splits, 0);
+    }
+    note_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t count = k * c * s;
+    reduce_splits_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 2048)), 256, 0, stream>>>(
+        workspace, dw_kcs, count, splits);
+    note_launch();
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------- bf16 rounding
+__global__ void round_bf16_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4;
+    // vectorised body when 16-byte aligned
+    const bool vec = ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    if (vec) {
+        for (; i + 3 < count; i += stride * 4) {
+            const float4 v = *reinterpret_cast<const float4*>(in + i);
+            uint2 o;
+            o.x = static_cast<uint32_t>(fp32_to_bf16_bits(v.x)) | (static_cast<uint32_t>(fp32_to_bf16_bits(v.y)) << 16);
+            o.y = static_cast<uint32_t>(fp32_to_bf16_bits(v.z)) | (static_cast<uint32_t>(fp32_to_bf16_bits(v.w)) << 16);
+            *reinterpret_cast<uint2*>(out + i) = o;
+        }
+        for (int64_t j = i; j < count && j < i + 4; ++j) out[j] = fp32_to_bf16_bits(in[j]);
+    } else {
+        for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < count; j += stride)
+            out[j] = fp32_to_bf16_bits(in[j]);
+    }
+}
+
+cudaError_t launch_round_bf16(const float* in, uint16_t* out, int64_t count, cudaStream_t stream) {
+    if (count <= 0) return cudaSuccess;
+    const int threads = 256;
+    const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(ceil_div(count, 4), threads), 8 * num_sms()));
+    round_bf16_kernel<<<blocks, threads, 0, stream>>>(in, out, count);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace c1d

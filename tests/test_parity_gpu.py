@@ -1,0 +1,208 @@
+"""GPU parity: the CUDA kernels through the C ABI vs the oracle (C restatement of the reference,
+pinned to the reference's golden vectors). Tolerances are the reference's own
+(norm_rel_error, proj/src/reference.cpp:151-162):
+
+* FP32 precision vs naive oracle: <= 1e-5 (test_conv.cpp:211-217, acceptance.cpp:131)
+* BF16 precision vs oracle on BF16-rounded inputs: <= 1e-5 (products exact, FP32 accumulation)
+* BF16 precision vs the unrounded FP32 oracle: <= 1e-2 (acceptance.cpp:526)
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2104_08002_b200 import conv as cv
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL_ROUNDED = 1e-5
+BF16_TOL_UNROUNDED = 1e-2
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _t(a, dtype=torch.float32):
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
+
+
+def run_passes(x, w, dy, d, precision=cv.Precision.Fp32, algo="auto", bf16_storage=False):
+    k, c, s = w.shape
+    p = cv.ConvParams(c, k, s, d, precision)
+    if bf16_storage:
+        xt, gt = cv.round_bf16(_t(x)), cv.round_bf16(_t(dy))
+    else:
+        xt, gt = _t(x), _t(dy)
+    wt = _t(w)
+    y = cv.conv1d_forward(xt, cv.pack_weights_forward(wt), p, algo=algo)
+    dx = cv.conv1d_backward_data(gt, cv.pack_weights_backward(wt), p, algo=algo)
+    dw = cv.conv1d_backward_weight(gt, xt, p, algo=algo)
+    torch.cuda.synchronize()
+    return y.cpu().numpy(), dx.cpu().numpy(), dw.cpu().numpy()
+
+
+def oracle_passes(x, w, dy, d):
+    s = w.shape[2]
+    return (oracle.naive_forward(x, w, d), oracle.naive_backward_data(dy, w, d),
+            oracle.naive_backward_weight(dy, x, s, d))
+
+
+def assert_close(got, want, tol, what=""):
+    assert got.shape == want.shape, (what, got.shape, want.shape)
+    assert np.all(np.isfinite(got)), what
+    err = oracle.norm_rel_error(got, want)
+    assert err <= tol, f"{what}: norm_rel_error {err:.3g} > {tol}"
+    return err
+
+
+# ----------------------------------------------------------------------------- golden cases
+def _cases(golden):
+    return [(i, tuple(int(v) for v in sh)) for i, sh in enumerate(golden["conv_shapes"])]
+
+
+@pytest.mark.parametrize("algo", ["direct", "auto"])
+def test_golden_fp32(golden, algo):
+    for i, (n, c, k, s, d, q) in _cases(golden):
+        x, w, dy = golden[f"c{i}_x"], golden[f"c{i}_w"], golden[f"c{i}_dy"]
+        got = run_passes(x, w, dy, d, cv.Precision.Fp32, algo)
+        for name, g in zip(("y", "dx", "dw"), got):
+            assert_close(g, golden[f"c{i}_{name}_naive"], FP32_TOL, f"case {i} {name}")
+            # and against the reference's own blocked path
+            assert_close(g, golden[f"c{i}_{name}"], FP32_TOL, f"case {i} {name} vs ref blocked")
+
+
+@pytest.mark.parametrize("algo", ["direct", "auto"])
+@pytest.mark.parametrize("bf16_storage", [False, True])
+def test_golden_bf16(golden, algo, bf16_storage):
+    for i, (n, c, k, s, d, q) in _cases(golden):
+        x, w, dy = golden[f"c{i}_x"], golden[f"c{i}_w"], golden[f"c{i}_dy"]
+        got = run_passes(x, w, dy, d, cv.Precision.Bf16, algo, bf16_storage)
+        xr, wr, dyr = oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy)
+        want_r = oracle_passes(xr, wr, dyr, d)
+        want_u = (golden[f"c{i}_y_naive"], golden[f"c{i}_dx_naive"], golden[f"c{i}_dw_naive"])
+        for j, name in enumerate(("y", "dx", "dw")):
+            assert_close(got[j], want_r[j], BF16_TOL_ROUNDED, f"case {i} {name} vs rounded oracle")
+            assert_close(got[j], want_u[j], BF16_TOL_UNROUNDED, f"case {i} {name} vs fp32 oracle")
+            if f"c{i}_{name}_bf16" in golden:  # the reference's own BF16 path (even dims only)
+                assert_close(got[j], golden[f"c{i}_{name}_bf16"], BF16_TOL_ROUNDED, f"case {i} {name} vs ref bf16")
+
+
+def test_hand_examples_exact():
+    """test_conv.cpp:70-141 known answers, both precisions, every algo."""
+    for prec in (cv.Precision.Fp32, cv.Precision.Bf16):
+        for algo in ("direct", "auto"):
+            x = np.array([[[1, 2, 3, 4, 5]]], np.float32)
+            w = np.array([[[1, 1]]], np.float32)
+            dy = np.ones((1, 1, 3), np.float32)
+            y, dx, dw = run_passes(x, w, dy, 2, prec, algo)
+            assert y.ravel().tolist() == [4, 6, 8]
+            assert dx.ravel().tolist() == [1, 1, 2, 1, 1]
+            assert dw.ravel().tolist() == [6, 12]
+
+
+def test_reference_randomized_sample():
+    """test_conv.cpp:189-219: 25 trials drawn with Rng(50), all passes vs naive at 1e-5."""
+    rng = oracle.Rng(50)
+    ck, ss, ds, qs = [1, 4, 8, 15, 16], [1, 5, 9, 51], [1, 2, 8], [64, 100, 1000]
+    for trial in range(25):
+        c, k = ck[rng.next_below(5)], ck[rng.next_below(5)]
+        s, d, q = ss[rng.next_below(4)], ds[rng.next_below(3)], qs[rng.next_below(3)]
+        n = 1 + rng.next_below(2) * 2
+        w_in = q + d * (s - 1)
+        x = oracle.Rng(1000 + trial).fill_uniform((n, c, w_in))
+        w = oracle.Rng(2000 + trial).fill_uniform((k, c, s))
+        dy = oracle.Rng(3000 + trial).fill_uniform((n, k, q))
+        want = oracle_passes(x, w, dy, d)
+        for algo in ("direct", "auto"):
+            got = run_passes(x, w, dy, d, cv.Precision.Fp32, algo)
+            for j in range(3):
+                assert_close(got[j], want[j], FP32_TOL, f"trial {trial} pass {j} {algo}")
+        got = run_passes(x, w, dy, d, cv.Precision.Bf16, "auto")
+        want_r = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), d)
+        for j in range(3):
+            assert_close(got[j], want_r[j], BF16_TOL_ROUNDED, f"trial {trial} pass {j} bf16")
+
+
+def test_acceptance_grid_sample():
+    """acceptance.cpp:66-135 (criterion 1): random combos from the paper grid, budget 1e8 MACs."""
+    rng = oracle.Rng(101)
+    widths, chans = [1000, 2000], [1, 4, 8, 10, 15, 16, 32, 64]
+    taps, dils = [1, 5, 9, 15, 21, 25, 31, 49, 51], [1, 2, 4, 8, 16]
+    done = 0
+    while done < 40:
+        c, k = chans[rng.next_below(8)], chans[rng.next_below(8)]
+        s, d = taps[rng.next_below(9)], dils[rng.next_below(5)]
+        q = widths[rng.next_below(2)]
+        n = 1 + rng.next_below(4)
+        w_in = q + d * (s - 1)
+        if n * c * k * s * w_in > 100_000_000:
+            continue
+        x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
+        want = oracle_passes(x, w, dy, d)
+        got = run_passes(x, w, dy, d, cv.Precision.Fp32, "auto")
+        for j in range(3):
+            assert_close(got[j], want[j], FP32_TOL, f"combo {done} {(n, c, k, s, d, q)} pass {j}")
+        gotb = run_passes(x, w, dy, d, cv.Precision.Bf16, "auto")
+        want_r = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), d)
+        for j in range(3):
+            assert_close(gotb[j], want_r[j], BF16_TOL_ROUNDED, f"combo {done} bf16 pass {j}")
+        done += 1
+
+
+def test_bitwise_determinism():
+    """acceptance.cpp:383-416 (criterion 5): reruns are bitwise identical."""
+    rng = oracle.Rng(505)
+    x, w, dy = rng.fill_uniform((4, 16, 256 + 8 * 50)), rng.fill_uniform((16, 16, 51)), rng.fill_uniform((4, 16, 256))
+    for prec in (cv.Precision.Fp32, cv.Precision.Bf16):
+        a = run_passes(x, w, dy, 8, prec)
+        b = run_passes(x, w, dy, 8, prec)
+        for u, v in zip(a, b):
+            assert u.tobytes() == v.tobytes()
+
+
+def test_edge_shapes():
+    rng = oracle.Rng(9)
+    shapes = [(1, 1, 1, 1, 1, 1), (2, 3, 5, 7, 3, 1), (1, 2, 2, 1, 1, 17), (3, 5, 7, 4, 5, 33),
+              (1, 17, 9, 51, 8, 7), (2, 64, 64, 3, 16, 130), (1, 130, 3, 2, 1, 50)]
+    for (n, c, k, s, d, q) in shapes:
+        w_in = q + d * (s - 1)
+        x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
+        want = oracle_passes(x, w, dy, d)
+        for prec in (cv.Precision.Fp32, cv.Precision.Bf16):
+            got = run_passes(x, w, dy, d, prec)
+            if prec == cv.Precision.Bf16:
+                want = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), d)
+            for j in range(3):
+                assert_close(got[j], want[j], FP32_TOL, f"{(n, c, k, s, d, q)} {prec} pass {j}")
+
+
+def test_empty_batch_and_errors():
+    p = cv.ConvParams(2, 3, 2, 1)
+    x = torch.zeros((0, 2, 16), device="cuda")
+    w = torch.ones((3, 2, 2), device="cuda")
+    assert cv.conv1d_forward(x, w, p).shape == (0, 3, 15)
+    dw = cv.conv1d_backward_weight(torch.zeros((0, 3, 15), device="cuda"), x, p)
+    assert torch.count_nonzero(dw) == 0
+    x1 = torch.ones((1, 2, 16), device="cuda")
+    with pytest.raises(cv.ShapeMismatch):  # backward layout handed to the forward entry point
+        cv.conv1d_forward(x1, cv.pack_weights_backward(w), p)
+    with pytest.raises(cv.ShapeMismatch):  # channel mismatch
+        cv.conv1d_forward(x1, w, cv.ConvParams(4, 3, 2, 1))
+    with pytest.raises(cv.ShapeMismatch):  # inconsistent width for backward weight
+        cv.conv1d_backward_weight(torch.ones((1, 3, 10), device="cuda"), x1, cv.ConvParams(2, 3, 2, 2))
+    with pytest.raises(cv.TooNarrow):
+        cv.conv1d_forward(torch.ones((1, 2, 4), device="cuda"), torch.ones((3, 2, 5), device="cuda"),
+                          cv.ConvParams(2, 3, 5, 1))
+    with pytest.raises(cv.OddDims):
+        cv.conv1d_forward(torch.ones((1, 3, 16), device="cuda"), torch.ones((4, 3, 5), device="cuda"),
+                          cv.ConvParams(3, 4, 5, 2, cv.Precision.Bf16), strict=True)
+
+
+def test_round_bf16_matches_reference_bits(golden):
+    vals = golden["bf16_in"]
+    got = cv.round_bf16(_t(vals)).view(torch.int16).cpu().numpy().view(np.uint16)
+    np.testing.assert_array_equal(got, golden["bf16_bits"])
