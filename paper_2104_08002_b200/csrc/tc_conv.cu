@@ -30,6 +30,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -46,7 +48,6 @@ constexpr int kTileQ = 128;      // output columns per tile (MMA M)
 constexpr int kSegQ = 256;       // TMA box width in elements
 constexpr int kTapsPerBlock = 16;
 constexpr int kMaxStages = 6;
-constexpr int kMaxSlots = 32;
 constexpr int kThreads = 256;
 constexpr uint32_t kTmemCols = 512;
 
@@ -74,6 +75,7 @@ struct KParams {
     Plan pl;
     const uint16_t* bimg;  // this filter group's B image: [in_ch][ntot*16] bf16
     float* out;
+    unsigned long long* prof;  // optional per-CTA cycle counters (C1D_PROFILE=1), else nullptr
 };
 
 bool make_plan(const ConvGeom& g, Plan* pl) {
@@ -86,11 +88,8 @@ bool make_plan(const ConvGeom& g, Plan* pl) {
     p.g = static_cast<int>(ceil_div(g.taps, kTapsPerBlock));
     p.r = static_cast<int>(kTmemCols) / p.kp;
     p.ntot = p.g * p.kp;
-    if (p.ntot > static_cast<int>(kTmemCols) / 2 && p.kp == 64) {
-        if (p.g > 4) return false;
-    }
-    if (p.g + 1 > p.r) return false;
-    p.t = std::min(4, p.r - p.g);
+    if (p.ntot > 256) return false;  // one MMA covers all tap blocks of a tile
+    p.t = std::min(8, p.r - (p.g - 1));  // linear TMEM: T + G - 1 slots
     if (p.t < 1) return false;
     p.n_seg = static_cast<int>(ceil_div(p.t * kTileQ + 8 * (kTapsPerBlock - 1), kSegQ));
     p.xw = p.n_seg * kSegQ;
@@ -113,7 +112,7 @@ bool make_plan(const ConvGeom& g, Plan* pl) {
 }
 
 // ---------------------------------------------------------------------------- B image packing
-// img[kg][c][row][r] in the K-major SWIZZLE_NONE core-matrix order:
+// img[kg][c][row][r] (row = b*KP + o, b = G-1-tap block) in the K-major SWIZZLE_NONE core-matrix order:
 //   element (row, r) at (row/8)*128 + (r/8)*64 + (row%8)*8 + (r%8)   (SBO 256 B, LBO 128 B)
 __global__ void pack_bimg_kernel(const float* __restrict__ wg, uint16_t* __restrict__ img, int64_t out_ch,
                                  int64_t in_ch, int64_t taps, int kp, int g, int kgroups) {
@@ -125,7 +124,9 @@ __global__ void pack_bimg_kernel(const float* __restrict__ wg, uint16_t* __restr
         const int64_t row = (e / kTapsPerBlock) % ntot;
         const int64_t c = (e / per_chan) % in_ch;
         const int64_t kg = e / (per_chan * in_ch);
-        const int64_t blk = row / kp, o = kg * kp + row % kp, s = blk * kTapsPerBlock + r;
+        // B row block b holds tap block G-1-b: input tile i0+t then writes output slot t+b, i.e.
+        // column (t+b)*KP, because tap block g of tile p lands on output tile p-g.
+        const int64_t blk = row / kp, o = kg * kp + row % kp, s = (g - 1 - blk) * kTapsPerBlock + r;
         float v = 0.0f;
         if (o < out_ch && s < taps) v = wg[(o * in_ch + c) * taps + s];
         const int64_t off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
@@ -135,13 +136,20 @@ __global__ void pack_bimg_kernel(const float* __restrict__ wg, uint16_t* __restr
 
 // ---------------------------------------------------------------------------- schedule
 // Each CTA owns output tiles [b, e) of the flattened (item, tile) list. For each item segment
-// (n, j0..j1) it processes input tiles j0 .. j1+G-1 in super-tiles of up to T tiles. Positions
-// are consecutive across segments and start at G-1 (positions 0..G-2 are warm-up phantoms).
+// (n, j0..j1) it walks input tiles j0 .. j1+G-1 in super-tiles of up to T tiles. Input tile
+// i0+t of a super-tile writes output tiles i0+t-G+1 .. i0+t, which live at TMEM slots t..t+G-1
+// (slot j <-> output i0-(G-1)+j, KP columns per slot): every MMA is one contiguous N = G*KP run.
 struct Cursor {
     int64_t cur, end;         // flattened output-tile cursor
     int64_t n, j0, j1;        // current segment
     int64_t i;                // next input tile in the segment
     bool valid;
+};
+
+struct Super {
+    int64_t n, i0, j0, j1;
+    int tcur;
+    bool last_in_segment;
 };
 
 __device__ __forceinline__ bool next_segment(Cursor& c, int64_t J) {
@@ -155,23 +163,23 @@ __device__ __forceinline__ bool next_segment(Cursor& c, int64_t J) {
     return true;
 }
 
-// Returns the number of input tiles in the next super-tile (0 = done) and its first tile index.
-__device__ __forceinline__ int next_super(Cursor& c, int64_t J, int G, int T, int64_t* n_out, int64_t* i_out,
-                                          int64_t* j1_out) {
-    if (!c.valid) return 0;
+__device__ __forceinline__ bool next_super(Cursor& c, int64_t J, int G, int T, Super* s) {
+    if (!c.valid) return false;
     if (c.i > c.j1 + G - 1) {
         if (!next_segment(c, J)) {
             c.valid = false;
-            return 0;
+            return false;
         }
     }
     const int64_t remain = c.j1 + G - 1 - c.i + 1;
-    const int tcur = static_cast<int>(imin64(T, remain));
-    *n_out = c.n;
-    *i_out = c.i;
-    *j1_out = c.j1;
-    c.i += tcur;
-    return tcur;
+    s->tcur = static_cast<int>(imin64(T, remain));
+    s->n = c.n;
+    s->i0 = c.i;
+    s->j0 = c.j0;
+    s->j1 = c.j1;
+    c.i += s->tcur;
+    s->last_in_segment = c.i > c.j1 + G - 1;
+    return true;
 }
 
 __device__ __forceinline__ Cursor make_cursor(const KParams& p) {
@@ -184,17 +192,11 @@ __device__ __forceinline__ Cursor make_cursor(const KParams& p) {
     return c;
 }
 
-__device__ __forceinline__ uint32_t slot_col(int64_t x, int R, int KP) {
-    int64_t m = (-x) % R;
-    if (m < 0) m += R;
-    return static_cast<uint32_t>(m * KP);
-}
-
 __global__ void __launch_bounds__(kThreads, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t stage_full[kMaxStages], stage_empty[kMaxStages];
-    __shared__ uint64_t slot_full[kMaxSlots], slot_empty[kMaxSlots];
+    __shared__ uint64_t tmem_full, tmem_empty;
     __shared__ uint32_t tmem_base_s;
 
     const Plan& pl = p.pl;
@@ -202,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* xs_base = smem;
     uint8_t* ws_base = smem + static_cast<size_t>(pl.stages) * pl.x_stage_bytes;
-    const int G = pl.g, T = pl.t, R = pl.r, KP = pl.kp;
+    const int G = pl.g, T = pl.t, KP = pl.kp;
     const int64_t J = p.tiles_per_item;
     const int n_chunks = static_cast<int>(ceil_div(p.in_ch, pl.cc));
 
@@ -211,10 +213,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&stage_full[s], 1);
             mbar_init(&stage_empty[s], 1);
         }
-        for (int s = 0; s < R; ++s) {
-            mbar_init(&slot_full[s], 1);
-            mbar_init(&slot_empty[s], 4);  // one arrival per epilogue warp
-        }
+        mbar_init(&tmem_full, 1);
+        mbar_init(&tmem_empty, 4);  // one arrival per epilogue warp
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base_s);
@@ -227,24 +227,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------------ TMA producer
         if (lane == 0) {
             prefetch_tmap(&tmap);
+            long long t_wait = 0;
+            const long long t_begin = clock64();
             Cursor cur = make_cursor(p);
             int stage = 0;
             uint32_t phase = 0;
-            int64_t n, i0, j1;
-            int tcur;
-            while ((tcur = next_super(cur, J, G, T, &n, &i0, &j1)) > 0) {
-                const int32_t x_start = static_cast<int32_t>(i0 * kTileQ + p.in_off);
+            Super su;
+            while (next_super(cur, J, G, T, &su)) {
+                const int32_t x_start = static_cast<int32_t>(su.i0 * kTileQ + p.in_off);
+                const int nseg = static_cast<int>(ceil_div(su.tcur * kTileQ + 8 * (kTapsPerBlock - 1), kSegQ));
                 for (int ch = 0; ch < n_chunks; ++ch) {
                     const int c0 = ch * pl.cc;
                     const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - c0));
+                    const long long tw0 = clock64();
                     mbar_wait(smem_u32(&stage_empty[stage]), phase ^ 1);
+                    t_wait += clock64() - tw0;
                     const uint32_t full = smem_u32(&stage_full[stage]);
-                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (pl.n_seg * kSegQ * 2 + pl.b_chan_bytes);
+                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (nseg * kSegQ * 2 + pl.b_chan_bytes);
                     mbar_arrive_expect_tx(full, bytes);
                     const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
                     for (int c = 0; c < ccn; ++c) {
-                        const int32_t row = static_cast<int32_t>(n * p.in_ch + c0 + c);
-                        for (int sg = 0; sg < pl.n_seg; ++sg)
+                        const int32_t row = static_cast<int32_t>(su.n * p.in_ch + c0 + c);
+                        for (int sg = 0; sg < nseg; ++sg)
                             tma_load_2d(xs + static_cast<uint32_t>((c * pl.xw + sg * kSegQ) * 2), &tmap,
                                         x_start + sg * kSegQ, row, full);
                     }
@@ -257,144 +261,118 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            if (p.prof) {
+                p.prof[blockIdx.x * 8 + 0] = t_wait;
+                p.prof[blockIdx.x * 8 + 1] = clock64() - t_begin;
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
-            Cursor cur = make_cursor(p);
-            int stage = 0;
-            uint32_t phase = 0;
-            int64_t pos = G - 1;         // position of the next input tile
-            int64_t completed = -1;      // highest committed output position
-            int64_t n, i0, j1;
-            int tcur;
-            // warm-up phantom positions 0..G-2 are touched first by input tile G-1
-            for (int64_t x = 0; x < G - 1; ++x) mbar_wait(smem_u32(&slot_empty[x % R]), 0);
-            while ((tcur = next_super(cur, J, G, T, &n, &i0, &j1)) > 0) {
-                for (int t = 0; t < tcur; ++t) {
-                    const int64_t x = pos + t;
-                    mbar_wait(smem_u32(&slot_empty[x % R]), static_cast<uint32_t>((x / R) & 1));
-                }
+        // The whole warp walks the schedule (warp-uniform control flow keeps descriptors in
+        // uniform registers); one elected lane issues each tcgen05 instruction.
+        long long t_full = 0, t_tmem = 0;
+        const long long t_begin = clock64();
+        Cursor cur = make_cursor(p);
+        int stage = 0;
+        uint32_t phase = 0, tphase = 0;
+        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(G * KP), kFmtBF16, 1, 0);
+        Super su;
+        while (next_super(cur, J, G, T, &su)) {
+            const long long ts0 = clock64();
+            mbar_wait(smem_u32(&tmem_empty), tphase);
+            tphase ^= 1;
+            t_tmem += clock64() - ts0;
+            tc_fence_after();
+            for (int ch = 0; ch < n_chunks; ++ch) {
+                const int c0 = ch * pl.cc;
+                const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - c0));
+                const long long tf0 = clock64();
+                mbar_wait(smem_u32(&stage_full[stage]), phase);
+                t_full += clock64() - tf0;
                 tc_fence_after();
-                // MMA runs of this super-tile (identical for every channel): contiguous TMEM
-                // column ranges of output blocks, split where the slot ring wraps.
-                uint32_t rcol[4][2], rboff[4][2], ridesc[4][2];
-                int nr[4];
-                for (int t = 0; t < tcur; ++t) {
-                    const int64_t x = pos + t;
-                    int gblk = 0, k = 0;
-                    while (gblk < G) {
-                        const uint32_t col = slot_col(x - gblk, R, KP);
-                        int run = 1;
-                        while (gblk + run < G && slot_col(x - gblk - run, R, KP) == col + run * KP &&
-                               (run + 1) * KP <= 256)
-                            ++run;
-                        rcol[t][k] = col;
-                        rboff[t][k] = static_cast<uint32_t>((gblk * KP / 8) * 256);
-                        ridesc[t][k] = make_idesc(128, static_cast<uint32_t>(run * KP), kFmtBF16, 1, 0);
-                        ++k;
-                        gblk += run;
-                    }
-                    nr[t] = k;
-                }
-                for (int ch = 0; ch < n_chunks; ++ch) {
-                    const int c0 = ch * pl.cc;
-                    const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - c0));
-                    mbar_wait(smem_u32(&stage_full[stage]), phase);
-                    tc_fence_after();
-                    const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
-                    const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
-                    const uint64_t a0 = make_smem_desc(xs, 128, 16, kLayoutNone);
-                    const uint64_t b0 = make_smem_desc(wsm, 128, 256, kLayoutNone);
-                    for (int c = 0; c < ccn; ++c) {
-                        const uint32_t bchan = static_cast<uint32_t>(c) * pl.b_chan_bytes;
-                        const uint32_t achan = static_cast<uint32_t>(c * pl.xw * 2);
-                        for (int t = 0; t < tcur; ++t) {
-                            const uint64_t adesc = desc_advance(a0, achan + static_cast<uint32_t>(t * kTileQ * 2));
-                            for (int k = 0; k < nr[t]; ++k)
-                                mma_bf16_ss(tmem + rcol[t][k], adesc, desc_advance(b0, bchan + rboff[t][k]),
-                                            ridesc[t][k], 1);
-                        }
-                    }
-                    mma_commit(smem_u32(&stage_empty[stage]));
-                    if (++stage == pl.stages) {
-                        stage = 0;
-                        phase ^= 1;
+                const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
+                const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
+                const uint64_t a0 = make_smem_desc(xs, 128, 16, kLayoutNone);
+                const uint64_t b0 = make_smem_desc(wsm, 128, 256, kLayoutNone);
+                for (int c = 0; c < ccn; ++c) {
+                    const uint64_t bdesc = desc_advance(b0, static_cast<uint32_t>(c) * pl.b_chan_bytes);
+                    const uint64_t achan = desc_advance(a0, static_cast<uint32_t>(c * pl.xw * 2));
+                    for (int t = 0; t < su.tcur; ++t) {
+                        const uint64_t adesc = desc_advance(achan, static_cast<uint32_t>(t * kTileQ * 2));
+                        if (elect_one()) mma_bf16_ss(tmem + static_cast<uint32_t>(t * KP), adesc, bdesc, idesc, 1);
+                        __syncwarp();
                     }
                 }
-                pos += tcur;
-                const int64_t done_upto = pos - 1 - (G - 1);
-                for (int64_t x = completed + 1; x <= done_upto; ++x) mma_commit(smem_u32(&slot_full[x % R]));
-                completed = (completed > done_upto ? completed : done_upto);
+                if (elect_one()) mma_commit(smem_u32(&stage_empty[stage]));
+                __syncwarp();
+                if (++stage == pl.stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
+            if (elect_one()) mma_commit(smem_u32(&tmem_full));
+            __syncwarp();
+        }
+        if (p.prof && lane == 0) {
+            p.prof[blockIdx.x * 8 + 2] = t_full;
+            p.prof[blockIdx.x * 8 + 3] = t_tmem;
+            p.prof[blockIdx.x * 8 + 4] = clock64() - t_begin;
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------------ epilogue
         const int quarter = warp - 4;  // TMEM lanes 32*quarter .. +31
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-        // zero every slot once, then hand them out
-        {
-            uint32_t z[16];
+        uint32_t z[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j) z[j] = 0;
-            for (uint32_t col = 0; col < kTmemCols; col += 16) tmem_st16(lane_base + col, z);
+        for (int j = 0; j < 16; ++j) z[j] = 0;
+        for (uint32_t col = 0; col < kTmemCols; col += 16) tmem_st16(lane_base + col, z);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+        Cursor cur = make_cursor(p);
+        uint32_t tphase = 0;
+        Super su;
+        const int slots = static_cast<int>(kTmemCols) / KP;
+        while (next_super(cur, J, G, T, &su)) {
+            mbar_wait(smem_u32(&tmem_full), tphase);
+            tphase ^= 1;
+            tc_fence_after();
+            // 1. store the completed outputs (slots 0..tcur-1)
+            for (int j = 0; j < su.tcur; ++j) {
+                const int64_t o = su.i0 - (G - 1) + j;
+                if (o < su.j0 || o > su.j1) continue;  // phantom (warm-up / beyond the segment)
+                const int64_t q = o * kTileQ + quarter * 32 + lane;
+                for (int kb = 0; kb < KP; kb += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(lane_base + static_cast<uint32_t>(j * KP + kb), v);
+                    tmem_ld_wait();
+                    if (q < p.out_w) {
+                        float* dst = p.out + (su.n * p.out_ch + p.k_begin + kb) * p.out_w + q;
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj)
+                            if (p.k_begin + kb + jj < p.out_ch) dst[static_cast<int64_t>(jj) * p.out_w] = __uint_as_float(v[jj]);
+                    }
+                }
+            }
+            // 2. carry the partial outputs (slots tcur..tcur+G-2) down to slots 0..G-2
+            if (!su.last_in_segment) {
+                for (int j = 0; j < G - 1; ++j) {
+                    for (int kb = 0; kb < KP; kb += 16) {
+                        uint32_t v[16];
+                        tmem_ld16(lane_base + static_cast<uint32_t>((su.tcur + j) * KP + kb), v);
+                        tmem_ld_wait();
+                        tmem_st16(lane_base + static_cast<uint32_t>(j * KP + kb), v);
+                    }
+                }
+            }
+            // 3. zero the slots the next super-tile accumulates from scratch
+            for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < static_cast<uint32_t>(slots * KP); col += 16)
+                tmem_st16(lane_base + col, z);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0)
-                for (int s = 0; s < R; ++s) mbar_arrive(smem_u32(&slot_empty[s]));
-        }
-        Cursor cur = make_cursor(p);
-        // ring of what sits at recent positions: real output? (n, tile)
-        int64_t ring_n[kMaxSlots];
-        int64_t ring_j[kMaxSlots];
-        bool ring_real[kMaxSlots];
-        (void)ring_n;
-        int64_t pos = G - 1;
-        for (int x = 0; x < G - 1; ++x) ring_real[x % kMaxSlots] = false;
-        int64_t n, i0, j1;
-        int tcur;
-        int64_t drained = 0;
-        while ((tcur = next_super(cur, J, G, T, &n, &i0, &j1)) > 0) {
-            for (int t = 0; t < tcur; ++t) {
-                const int64_t x = pos + t;
-                ring_n[x % kMaxSlots] = n;
-                ring_j[x % kMaxSlots] = i0 + t;
-                ring_real[x % kMaxSlots] = (i0 + t) <= j1;
-            }
-            pos += tcur;
-            const int64_t done_upto = pos - 1 - (G - 1);
-            for (; drained <= done_upto; ++drained) {
-                const int64_t x = drained;
-                mbar_wait(smem_u32(&slot_full[x % R]), static_cast<uint32_t>((x / R) & 1));
-                tc_fence_after();
-                const uint32_t col = slot_col(x, R, KP);
-                const int sl = static_cast<int>(x % kMaxSlots);
-                if (ring_real[sl]) {
-                    const int64_t nn = ring_n[sl];
-                    const int64_t q = ring_j[sl] * kTileQ + quarter * 32 + lane;
-                    for (int kb = 0; kb < KP; kb += 16) {
-                        uint32_t v[16];
-                        tmem_ld16(lane_base + col + kb, v);
-                        tmem_ld_wait();
-                        if (q < p.out_w) {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                const int64_t o = p.k_begin + kb + j;
-                                if (o < p.out_ch) p.out[(nn * p.out_ch + o) * p.out_w + q] = __uint_as_float(v[j]);
-                            }
-                        }
-                    }
-                }
-                uint32_t z[16];
-#pragma unroll
-                for (int j = 0; j < 16; ++j) z[j] = 0;
-                for (int kb = 0; kb < KP; kb += 16) tmem_st16(lane_base + col + kb, z);
-                tmem_st_wait();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&slot_empty[x % R]));
-            }
+            if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
         }
     }
     tc_fence_before();
@@ -468,6 +446,11 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     kp.pl = pl;
     kp.out = out;
     const int grid = static_cast<int>(std::min<int64_t>(num_sms(), kp.total_tiles));
+    static const bool profile = getenv("C1D_PROFILE") != nullptr;
+    if (profile) {
+        cudaMalloc(&kp.prof, sizeof(unsigned long long) * 8 * grid);
+        cudaMemset(kp.prof, 0, sizeof(unsigned long long) * 8 * grid);
+    }
     for (int kg = 0; kg < pl.kgroups; ++kg) {
         kp.k_begin = kg * pl.kp;
         kp.bimg = img + static_cast<size_t>(kg) * g.in_ch * (pl.b_chan_bytes / 2);
@@ -475,6 +458,16 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         note_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
+    }
+    if (profile) {
+        std::vector<unsigned long long> h(8 * grid);
+        cudaMemcpy(h.data(), kp.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+        double a[8] = {0};
+        for (int b = 0; b < grid; ++b)
+            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[b * 8 + i]) / grid;
+        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f (cycles, CTA avg)\n",
+                a[0], a[1], a[2], a[3], a[4]);
+        cudaFree(kp.prof);
     }
     return cudaSuccess;
 }

@@ -27,7 +27,7 @@ static float bf2f(uint16_t b) { uint32_t u = (uint32_t)b << 16; float f; memcpy(
 //       1 = TS A (tmem) x B K-major none
 //       2 = SS A K-major none (K=64, 4 steps) x B K-major SW128
 struct Params {
-    int mode, n, a_swap, b_swap, reps, ts_pack_hi_first, nacc;
+    int mode, n, a_swap, b_swap, reps, ts_pack_hi_first, nacc, vary, dcol, split;
 };
 
 __global__ void __launch_bounds__(128, 1) probe_kernel(Params p, const uint16_t* gx, const uint16_t* gw,
@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Params p, const uint16_t*
     if (tid == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
     // ---- fill smem
     if (p.mode == 0) {
-        for (int i = tid; i < 512; i += 128) reinterpret_cast<uint16_t*>(sx)[i] = gx[i];
+        for (int i = tid; i < 1024; i += 128) reinterpret_cast<uint16_t*>(sx)[i] = gx[i & 511];
     } else if (p.mode == 2) {
         // A K-major interleave: 128 rows x 64 k; addr = (m/8)*1024 + (k/8)*128 + (m%8)*16 + (k%8)*2
         for (int i = tid; i < 128 * 64; i += 128) {
@@ -107,8 +107,27 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Params p, const uint16_t*
         }
         t0 = clock64();
         const uint32_t nstep = (uint32_t)p.n;
+        uint32_t vi = 0;
         auto issue = [&](uint32_t dcol, uint32_t accf) {
-            if (p.mode == 0) mma_bf16_ss(dcol, adesc, bdesc, idesc, accf);
+            if (p.mode == 0) {
+                if (p.split) {
+                    vi = (vi + 1) & 3;
+                    const uint64_t ad = desc_advance(adesc, vi * 256);
+                    const uint32_t n1 = (uint32_t)p.split, n2 = 256 - n1;
+                    if (p.split > 0 && p.vary == 2) {
+                        mma_bf16_ss_afill(tbase + p.dcol, ad, bdesc, make_idesc(128, n1, kFmtBF16, 1, 0), accf);
+                        mma_bf16_ss_alastuse(tbase + p.dcol + n1, ad, desc_advance(bdesc, n1 * 32), make_idesc(128, n2, kFmtBF16, 1, 0), accf);
+                    } else {
+                        mma_bf16_ss(tbase + p.dcol, ad, bdesc, make_idesc(128, n1, kFmtBF16, 1, 0), accf);
+                        mma_bf16_ss(tbase + p.dcol + n1, ad, desc_advance(bdesc, n1 * 32), make_idesc(128, n2, kFmtBF16, 1, 0), accf);
+                    }
+                } else if (p.vary) {
+                    vi = (vi + 1) & 3;
+                    mma_bf16_ss(dcol + p.dcol, desc_advance(adesc, vi * 256), desc_advance(bdesc, (vi & 1) * 8192), idesc, accf);
+                } else {
+                    mma_bf16_ss(dcol + p.dcol, adesc, bdesc, idesc, accf);
+                }
+            }
             else if (p.mode == 1) mma_bf16_ts(dcol, tA, bdesc, idesc, accf);
             else {
 #pragma unroll
@@ -134,7 +153,7 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Params p, const uint16_t*
     // read D: 128 lanes x n cols
     for (int c0 = 0; c0 < p.n; c0 += 16) {
         uint32_t r[16];
-        tmem_ld16(tbase + ((uint32_t)(warp * 32) << 16) + c0, r);
+        tmem_ld16(tbase + ((uint32_t)(warp * 32) << 16) + ((c0 + (uint32_t)p.dcol) & 511), r);
         tmem_ld_wait();
         for (int j = 0; j < 16; ++j) gd[tid * 256 + c0 + j] = __uint_as_float(r[j]);
     }
@@ -185,24 +204,31 @@ int main() {
                maxerr <= 1e-3 * fmax(1.0, maxref) ? "OK" : "MISMATCH", (double)cyc / nmma);
     };
     // correctness (reps = 1)
-    run({0, 64, 0, 0, 1, 0, 1}, "SS rowtap A(LBO=128,SBO=16) B(LBO=128,SBO=256)");
-    run({0, 64, 1, 0, 1, 0, 1}, "SS rowtap A(LBO=16,SBO=128) B(LBO=128,SBO=256)");
-    run({0, 64, 0, 1, 1, 0, 1}, "SS rowtap A(LBO=128,SBO=16) B(LBO=256,SBO=128)");
-    run({0, 64, 1, 1, 1, 0, 1}, "SS rowtap A(LBO=16,SBO=128) B(LBO=256,SBO=128)");
-    run({1, 64, 0, 0, 1, 0, 1}, "TS A(lo=even) B(LBO=128,SBO=256)");
-    run({1, 64, 0, 0, 1, 1, 1}, "TS A(lo=odd)  B(LBO=128,SBO=256)");
-    run({1, 64, 0, 1, 1, 0, 1}, "TS A(lo=even) B(LBO=256,SBO=128)");
-    run({2, 64, 0, 0, 1, 0, 1}, "SS Kmaj A(LBO=128,SBO=1024) B SW128");
-    run({2, 64, 1, 0, 1, 0, 1}, "SS Kmaj A(LBO=1024,SBO=128) B SW128");
-    run({2, 256, 0, 0, 1, 0, 1}, "SS Kmaj A(LBO=128,SBO=1024) B SW128");
+    run({0, 64, 0, 0, 1, 0, 1, 0, 0, 0}, "SS rowtap A(LBO=128,SBO=16) B(LBO=128,SBO=256)");
+    run({0, 64, 1, 0, 1, 0, 1, 0, 0, 0}, "SS rowtap A(LBO=16,SBO=128) B(LBO=128,SBO=256)");
+    run({0, 64, 0, 1, 1, 0, 1, 0, 0, 0}, "SS rowtap A(LBO=128,SBO=16) B(LBO=256,SBO=128)");
+    run({0, 64, 1, 1, 1, 0, 1, 0, 0, 0}, "SS rowtap A(LBO=16,SBO=128) B(LBO=256,SBO=128)");
+    run({1, 64, 0, 0, 1, 0, 1, 0, 0, 0}, "TS A(lo=even) B(LBO=128,SBO=256)");
+    run({1, 64, 0, 0, 1, 1, 1, 0, 0, 0}, "TS A(lo=odd)  B(LBO=128,SBO=256)");
+    run({1, 64, 0, 1, 1, 0, 1, 0, 0, 0}, "TS A(lo=even) B(LBO=256,SBO=128)");
+    run({2, 64, 0, 0, 1, 0, 1, 0, 0, 0}, "SS Kmaj A(LBO=128,SBO=1024) B SW128");
+    run({2, 64, 1, 0, 1, 0, 1, 0, 0, 0}, "SS Kmaj A(LBO=1024,SBO=128) B SW128");
+    run({2, 256, 0, 0, 1, 0, 1, 0, 0, 0}, "SS Kmaj A(LBO=128,SBO=1024) B SW128");
     // throughput (values are garbage-scaled by reps but we only time)
     char nm[128];
+    run({0, 256, 0, 0, 1, 0, 1, 0, 0, 0}, "WRAP test dcol=0");
+    run({0, 256, 0, 0, 1, 0, 1, 0, 256, 0}, "WRAP test dcol=256");
+    run({0, 256, 0, 0, 1, 0, 1, 0, 448, 0}, "WRAP test dcol=448 (wraps past 512)");
+    for (int dc : {0, 64, 128, 192, 256}) { snprintf(nm, 128, "TPUT SS rowtap VARY N=256 dcol=%d", dc); run({0, 256, 0, 0, 2048, 0, 1, 1, dc, 0}, nm); }
+    for (int sp : {64, 128, 192}) { snprintf(nm, 128, "TPUT split %d+%d plain", sp, 256 - sp); run({0, 256, 0, 0, 2048, 0, 1, 1, 0, sp}, nm); }
+    for (int sp : {64, 128, 192}) { snprintf(nm, 128, "TPUT split %d+%d collector", sp, 256 - sp); run({0, 256, 0, 0, 2048, 0, 1, 2, 0, sp}, nm); }
+    for (int sp : {64, 128, 192}) { snprintf(nm, 128, "TPUT split %d+%d plain dcol64", sp, 256 - sp); run({0, 256, 0, 0, 2048, 0, 1, 1, 64, sp}, nm); }
     for (int na : {1, 2, 4})
-        for (int n : {64, 128, 192, 256}) if (n * na <= 512) { snprintf(nm, 128, "TPUT SS rowtap nacc=%d", na); run({0, n, 0, 0, 2048, 0, na}, nm); }
+        for (int n : {64, 128, 192, 256}) if (n * na <= 512) { snprintf(nm, 128, "TPUT SS rowtap nacc=%d", na); run({0, n, 0, 0, 2048, 0, na, 0, 0, 0}, nm); }
     for (int na : {1, 2, 4, 7})
-        for (int n : {64, 128, 256}) if (n * na <= 480) { snprintf(nm, 128, "TPUT TS nacc=%d", na); run({1, n, 0, 0, 2048, 0, na}, nm); }
+        for (int n : {64, 128, 256}) if (n * na <= 480) { snprintf(nm, 128, "TPUT TS nacc=%d", na); run({1, n, 0, 0, 2048, 0, na, 0, 0, 0}, nm); }
     for (int na : {1, 2, 4})
-        for (int n : {64, 128, 256}) if (n * na <= 512) { snprintf(nm, 128, "TPUT SS Kmaj/SW128 nacc=%d", na); run({2, n, 0, 0, 512, 0, na}, nm); }
+        for (int n : {64, 128, 256}) if (n * na <= 512) { snprintf(nm, 128, "TPUT SS Kmaj/SW128 nacc=%d", na); run({2, n, 0, 0, 512, 0, na, 0, 0, 0}, nm); }
     printf("done\n");
     return 0;
 }
