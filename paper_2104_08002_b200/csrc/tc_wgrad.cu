@@ -1,10 +1,351 @@
-// tc_wgrad.cu — placeholder, replaced by the tcgen05 backward-weight kernel.
+// tc_wgrad.cu — tcgen05 (sm_100a) BF16 backward-weight for dilation 8.
+//
+//   dW[k][c][s] = sum_n sum_q X[n][c][q + 8s] * dY[n][k][q]
+//
+// Implicit GEMM with K = q (16 columns per MMA), M = 128 rows = T taps x CP channels
+// (CP = C rounded up to a power of two >= 8, T = 128/CP), N = KP filters (K rounded up to 16):
+//   A[(t,c)][kk] = X[c][q + 8(s0 + t)]     B[k][kk] = dY[k][q]     D[(t,c)][k] += A.B^T
+// The X window sits in shared memory in a "q-chunk major" layout,
+//   byte(c, q) = (q/8)*CP*16 + c*16 + (q%8)*2,
+// produced directly by a 4-D TMA box (8 columns x CP channels x chunks). In that layout one tap
+// (8 columns) is exactly CP*16 bytes = CP/8 core-matrix row groups, so the T tap-shifted copies
+// of the window that form A's rows are just consecutive row groups at a uniform 128 B stride:
+// no copies are made, and a different tap group is only a different start address. dY arrives
+// as a 128B-swizzled K-major TMA box. Each CTA accumulates G tap groups (G*KP TMEM columns)
+// over a contiguous range of (item, 16-column step) work; partials of the CTAs sharing a tap
+// range are summed in a fixed order by a second kernel (deterministic; the reference sums
+// per-item partials in ascending order, proj/src/conv.cpp:308-314).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
 #include "kernels.h"
+#include "sm100.cuh"
+
 namespace c1d {
-bool tc_wgrad_supported(int64_t, int64_t, int64_t, int64_t, int64_t, int64_t) { return false; }
-size_t tc_wgrad_workspace_bytes(int64_t, int64_t, int64_t, int64_t, int64_t, int64_t) { return 0; }
-cudaError_t launch_tc_wgrad(const uint16_t*, const uint16_t*, float*, void*, int64_t, int64_t, int64_t, int64_t,
-                            int64_t, int64_t, cudaStream_t) {
-    return cudaErrorNotSupported;
+namespace {
+
+using namespace sm100;
+
+constexpr int kThreads = 256;
+constexpr int kKS = 4;          // MMA K-steps (16 columns each) per pipeline stage
+constexpr int kStageQ = 16 * kKS;
+constexpr int kMaxStages = 4;
+constexpr uint32_t kTmemCols = 512;
+
+struct WPlan {
+    int cp, t, kp;
+    int groups_total;   // ceil(S / T)
+    int roles;          // CTA roles (tap-group ranges)
+    int gmax;           // groups per role (max)
+    int splits;         // CTAs per role
+    int x_chunks;       // q-chunks (8 columns) per X stage window
+    uint32_t x_bytes, y_bytes, stage_bytes;
+    int stages;
+    size_t smem_bytes;
+};
+
+__host__ __device__ inline int64_t imin(int64_t a, int64_t b) { return a < b ? a : b; }
+
+bool make_wplan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, WPlan* out) {
+    if (d != 8 || q % 8 != 0 || q < 8) return false;
+    if (c > 128 || k > 256) return false;
+    if (n * c >= (int64_t{1} << 31) || n * k >= (int64_t{1} << 31)) return false;
+    WPlan p{};
+    p.cp = 8;
+    while (p.cp < c) p.cp *= 2;
+    p.t = 128 / p.cp;
+    p.kp = static_cast<int>(ceil_div(k, 16) * 16);
+    p.groups_total = static_cast<int>(ceil_div(s, p.t));
+    const int gcap = static_cast<int>(kTmemCols) / p.kp;
+    if (gcap < 1) return false;
+    p.roles = static_cast<int>(ceil_div(p.groups_total, gcap));
+    p.gmax = static_cast<int>(ceil_div(p.groups_total, p.roles));
+    p.splits = std::max(1, num_sms() / p.roles);
+    // X window per stage: kStageQ new columns + the tap span of one role's groups + K overrun
+    p.x_chunks = kStageQ / 8 + p.gmax * p.t + 1;
+    if (p.x_chunks > 256) return false;
+    p.x_bytes = static_cast<uint32_t>(p.x_chunks * p.cp * 16);
+    p.y_bytes = static_cast<uint32_t>(p.kp * kStageQ * 2);
+    const uint32_t xb = (p.x_bytes + 1023) & ~1023u;
+    p.stage_bytes = xb + p.y_bytes;
+    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / p.stage_bytes));
+    if (p.stages < 2) return false;
+    p.x_bytes = xb;
+    p.smem_bytes = static_cast<size_t>(p.stages) * p.stage_bytes + 1024;
+    *out = p;
+    return true;
 }
+
+struct WParams {
+    int64_t n_items, c, k, s, q, w_in;
+    int64_t steps_per_item, total_steps;  // 16-column K-steps
+    WPlan pl;
+    float* part;  // [role-split][k][c][s]  (only this role's taps are written)
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_wgrad_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                    const WParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ uint64_t acc_done;
+    __shared__ uint32_t tmem_base_s;
+
+    const WPlan& pl = p.pl;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    const int role = blockIdx.x / pl.splits;
+    const int split = blockIdx.x % pl.splits;
+    const int g_begin = role * pl.gmax;
+    const int g_count = static_cast<int>(imin(pl.gmax, pl.groups_total - g_begin));
+    const int tap0 = g_begin * pl.t;  // first tap of this role
+    // this CTA's K-steps: [kb, ke) of the flattened (item, step) space
+    const int64_t kb = p.total_steps * split / pl.splits;
+    const int64_t ke = p.total_steps * (split + 1) / pl.splits;
+    const int64_t n_stages_total = [&] {
+        // stages never straddle items: count per item segment
+        int64_t cnt = 0, cur = kb;
+        while (cur < ke) {
+            const int64_t item_end = (cur / p.steps_per_item + 1) * p.steps_per_item;
+            const int64_t seg_end = imin(ke, item_end);
+            cnt += ceil_div(seg_end - cur, kKS);
+            cur = seg_end;
+        }
+        return cnt;
+    }();
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < pl.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&acc_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base_s);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+
+    if (warp == 0) {
+        if (lane == 0 && g_count > 0) {
+            prefetch_tmap(&xmap);
+            prefetch_tmap(&ymap);
+            int stage = 0;
+            uint32_t phase = 0;
+            int64_t cur = kb;
+            while (cur < ke) {
+                const int64_t item = cur / p.steps_per_item;
+                const int64_t item_end = (item + 1) * p.steps_per_item;
+                const int64_t seg_end = imin(ke, item_end);
+                for (int64_t st = cur; st < seg_end; st += kKS) {
+                    const int64_t q0 = (st - item * p.steps_per_item) * 16;  // first column of the stage
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.x_chunks * pl.cp * 16) + pl.y_bytes);
+                    uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
+                    // X window: q-chunks starting at (q0/8 + tap0), box (8, CP, x_chunks, 1)
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(sbase)),
+                        "l"(&xmap), "r"(0), "r"(0), "r"(static_cast<int32_t>(q0 / 8 + tap0)),
+                        "r"(static_cast<int32_t>(item)), "r"(fb)
+                        : "memory");
+                    // dY box (64 columns, KP filters, 1 item), 128B swizzle
+                    tma_load_3d(smem_u32(sbase + pl.x_bytes), &ymap, static_cast<int32_t>(q0), 0,
+                                static_cast<int32_t>(item), fb);
+                    if (++stage == pl.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                cur = seg_end;
+            }
+        }
+    } else if (warp == 1) {
+        if (g_count > 0) {
+            const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.kp), kFmtBF16, 0, 0);
+            int stage = 0;
+            uint32_t phase = 0;
+            bool first = true;
+            int64_t cur = kb;
+            while (cur < ke) {
+                const int64_t item = cur / p.steps_per_item;
+                const int64_t item_end = (item + 1) * p.steps_per_item;
+                const int64_t seg_end = imin(ke, item_end);
+                for (int64_t st = cur; st < seg_end; st += kKS) {
+                    const int nks = static_cast<int>(imin(kKS, seg_end - st));
+                    mbar_wait(smem_u32(&full[stage]), phase);
+                    tc_fence_after();
+                    uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
+                    const uint64_t a0 = make_smem_desc(smem_u32(sbase), static_cast<uint32_t>(pl.cp * 16), 128,
+                                                       kLayoutNone);
+                    const uint64_t b0 = make_smem_desc(smem_u32(sbase + pl.x_bytes), 16, 1024, kLayoutSw128);
+                    for (int ks = 0; ks < nks; ++ks) {
+                        const uint64_t bdesc = desc_advance(b0, static_cast<uint32_t>(ks * 32));
+                        for (int g = 0; g < g_count; ++g) {
+                            // group g starts g*T taps later = g*T q-chunks; K-step ks = 2 chunks
+                            const uint64_t adesc =
+                                desc_advance(a0, static_cast<uint32_t>((g * pl.t + 2 * ks) * pl.cp * 16));
+                            if (elect_one())
+                                mma_bf16_ss(tmem + static_cast<uint32_t>(g * pl.kp), adesc, bdesc, idesc,
+                                            first ? 0u : 1u);
+                            __syncwarp();
+                        }
+                        first = false;
+                    }
+                    if (elect_one()) mma_commit(smem_u32(&empty[stage]));
+                    __syncwarp();
+                    if (++stage == pl.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                cur = seg_end;
+            }
+            if (elect_one()) mma_commit(smem_u32(&acc_done));
+            __syncwarp();
+        }
+    } else if (warp >= 4) {
+        // epilogue: D rows (t, c) x columns (g, k) -> partial[role-split][k][c][tap]
+        if (g_count > 0) {
+            const int quarter = warp - 4;
+            const int row = quarter * 32 + lane;
+            const int t = row / pl.cp, c = row % pl.cp;
+            const bool have = n_stages_total > 0;
+            if (have) {
+                mbar_wait(smem_u32(&acc_done), 0);
+                tc_fence_after();
+            }
+            float* dst = p.part + static_cast<int64_t>(blockIdx.x) * p.k * p.c * p.s;
+            for (int g = 0; g < g_count; ++g) {
+                const int64_t tap = tap0 + static_cast<int64_t>(g) * pl.t + t;
+                for (int kb2 = 0; kb2 < pl.kp; kb2 += 16) {
+                    uint32_t v[16];
+                    if (have) {
+                        tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) +
+                                      static_cast<uint32_t>(g * pl.kp + kb2), v);
+                        tmem_ld_wait();
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = 0;
+                    }
+                    if (c < p.c && tap < p.s) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int64_t kk = kb2 + j;
+                            if (kk < p.k) dst[(kk * p.c + c) * p.s + tap] = __uint_as_float(v[j]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
+}
+
+// dw[k][c][s] = sum over the splits of the role owning tap s, in ascending split order.
+__global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw, int64_t K, int64_t C,
+                                    int64_t S, int t, int gmax, int splits) {
+    const int64_t count = K * C * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e % S;
+        const int role = static_cast<int>(s / (static_cast<int64_t>(gmax) * t));
+        const float* src = part + static_cast<int64_t>(role) * splits * count + e;
+        float v = 0.0f;
+        for (int sp = 0; sp < splits; ++sp) v += src[static_cast<int64_t>(sp) * count];
+        dw[e] = v;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+}  // namespace
+
+bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    WPlan p;
+    return make_wplan(n, c, k, s, d, q, &p);
+}
+
+size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    WPlan p;
+    if (!make_wplan(n, c, k, s, d, q, &p)) return 0;
+    return sizeof(float) * static_cast<size_t>(p.roles) * p.splits * static_cast<size_t>(k * c * s);
+}
+
+cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace,
+                            int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream) {
+    WPlan pl;
+    if (!make_wplan(n, c, k, s, d, q, &pl)) return cudaErrorNotSupported;
+    auto encode = encode_fn();
+    if (!encode) return cudaErrorNotSupported;
+    const int64_t w_in = q + d * (s - 1);
+    CUtensorMap xmap, ymap;
+    {
+        // X as (qi=8, c, q-chunk, n): element (qi, c, qc, n) at n*C*W + c*W + qc*8 + qi
+        const cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w_in / 8),
+                                    static_cast<cuuint64_t>(n)};
+        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(w_in) * 2, 16,
+                                       static_cast<cuuint64_t>(c * w_in) * 2};
+        const cuuint32_t box[4] = {8, static_cast<cuuint32_t>(pl.cp), static_cast<cuuint32_t>(pl.x_chunks), 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        CUresult r = encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(x_bf16), dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(q), static_cast<cuuint64_t>(k),
+                                    static_cast<cuuint64_t>(n)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(q) * 2, static_cast<cuuint64_t>(k * q) * 2};
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(kStageQ), static_cast<cuuint32_t>(pl.kp), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        CUresult r = encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(dy_bf16), dims, strides,
+                            box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(pl.smem_bytes));
+    if (e != cudaSuccess) return e;
+    WParams wp{};
+    wp.n_items = n;
+    wp.c = c;
+    wp.k = k;
+    wp.s = s;
+    wp.q = q;
+    wp.w_in = w_in;
+    wp.steps_per_item = ceil_div(q, 16);
+    wp.total_steps = n * wp.steps_per_item;
+    wp.pl = pl;
+    wp.part = static_cast<float*>(workspace);
+    tc_wgrad_kernel<<<pl.roles * pl.splits, kThreads, pl.smem_bytes, stream>>>(xmap, ymap, wp);
+    note_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t count = k * c * s;
+    wgrad_reduce_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 4096)), 256, 0, stream>>>(
+        wp.part, dw_kcs, k, c, s, pl.t, pl.gmax, pl.splits);
+    note_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace c1d
