@@ -20,6 +20,8 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -31,13 +33,13 @@ namespace {
 using namespace sm100;
 
 constexpr int kThreads = 256;
-constexpr int kKS = 4;          // MMA K-steps (16 columns each) per pipeline stage
-constexpr int kStageQ = 16 * kKS;
 constexpr int kMaxStages = 4;
 constexpr uint32_t kTmemCols = 512;
 
 struct WPlan {
     int cp, t, kp;
+    int ks;             // MMA K-steps (16 columns each) per pipeline stage (multiple of 4)
+    int stage_q;        // columns per stage = 16 * ks
     int groups_total;   // ceil(S / T)
     int roles;          // CTA roles (tap-group ranges)
     int gmax;           // groups per role (max)
@@ -65,15 +67,25 @@ bool make_wplan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q
     p.roles = static_cast<int>(ceil_div(p.groups_total, gcap));
     p.gmax = static_cast<int>(ceil_div(p.groups_total, p.roles));
     p.splits = std::max(1, num_sms() / p.roles);
-    // X window per stage: kStageQ new columns + the tap span of one role's groups + K overrun
-    p.x_chunks = kStageQ / 8 + p.gmax * p.t + 1;
-    if (p.x_chunks > 256) return false;
-    p.x_bytes = static_cast<uint32_t>(p.x_chunks * p.cp * 16);
-    p.y_bytes = static_cast<uint32_t>(p.kp * kStageQ * 2);
+    // X window per stage: stage_q new columns + the tap span of one role's groups + K overrun.
+    // Bigger stages amortise the tap-span overlap that every stage re-fetches.
+    bool ok = false;
+    for (int ks = 16; ks >= 4; ks -= 4) {
+        p.ks = ks;
+        p.stage_q = 16 * ks;
+        p.x_chunks = p.stage_q / 8 + p.gmax * p.t + 1;
+        if (p.x_chunks > 256) continue;
+        p.x_bytes = static_cast<uint32_t>(p.x_chunks * p.cp * 16);
+        p.y_bytes = static_cast<uint32_t>(p.kp * p.stage_q * 2);
+        const uint32_t xb = (p.x_bytes + 1023) & ~1023u;
+        p.stage_bytes = xb + p.y_bytes;
+        p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / p.stage_bytes));
+        if (p.stages < 2) continue;
+        ok = true;
+        break;
+    }
+    if (!ok) return false;
     const uint32_t xb = (p.x_bytes + 1023) & ~1023u;
-    p.stage_bytes = xb + p.y_bytes;
-    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / p.stage_bytes));
-    if (p.stages < 2) return false;
     p.x_bytes = xb;
     p.smem_bytes = static_cast<size_t>(p.stages) * p.stage_bytes + 1024;
     *out = p;
@@ -85,6 +97,7 @@ struct WParams {
     int64_t steps_per_item, total_steps;  // 16-column K-steps
     WPlan pl;
     float* part;  // [role-split][k][c][s]  (only this role's taps are written)
+    unsigned long long* prof;  // optional per-CTA cycle counters (C1D_PROFILE=1)
 };
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -112,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (cur < ke) {
             const int64_t item_end = (cur / p.steps_per_item + 1) * p.steps_per_item;
             const int64_t seg_end = imin(ke, item_end);
-            cnt += ceil_div(seg_end - cur, kKS);
+            cnt += ceil_div(seg_end - cur, pl.ks);
             cur = seg_end;
         }
         return cnt;
@@ -136,6 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0 && g_count > 0) {
             prefetch_tmap(&xmap);
             prefetch_tmap(&ymap);
+            long long t_wait = 0;
+            const long long t_begin = clock64();
             int stage = 0;
             uint32_t phase = 0;
             int64_t cur = kb;
@@ -143,9 +158,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t item = cur / p.steps_per_item;
                 const int64_t item_end = (item + 1) * p.steps_per_item;
                 const int64_t seg_end = imin(ke, item_end);
-                for (int64_t st = cur; st < seg_end; st += kKS) {
+                for (int64_t st = cur; st < seg_end; st += pl.ks) {
                     const int64_t q0 = (st - item * p.steps_per_item) * 16;  // first column of the stage
+                    const long long tw = clock64();
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    t_wait += clock64() - tw;
                     const uint32_t fb = smem_u32(&full[stage]);
                     mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.x_chunks * pl.cp * 16) + pl.y_bytes);
                     uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
@@ -156,9 +173,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         "l"(&xmap), "r"(0), "r"(0), "r"(static_cast<int32_t>(q0 / 8 + tap0)),
                         "r"(static_cast<int32_t>(item)), "r"(fb)
                         : "memory");
-                    // dY box (64 columns, KP filters, 1 item), 128B swizzle
-                    tma_load_3d(smem_u32(sbase + pl.x_bytes), &ymap, static_cast<int32_t>(q0), 0,
-                                static_cast<int32_t>(item), fb);
+                    // dY boxes (64 columns, KP filters, 1 item), 128B swizzle, one per 4 K-steps
+                    for (int b = 0; b < pl.ks / 4; ++b)
+                        tma_load_3d(smem_u32(sbase + pl.x_bytes + static_cast<uint32_t>(b * pl.kp * 128)), &ymap,
+                                    static_cast<int32_t>(q0 + 64 * b), 0, static_cast<int32_t>(item), fb);
                     if (++stage == pl.stages) {
                         stage = 0;
                         phase ^= 1;
@@ -166,10 +184,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 cur = seg_end;
             }
+            if (p.prof) {
+                p.prof[blockIdx.x * 8 + 0] = t_wait;
+                p.prof[blockIdx.x * 8 + 1] = clock64() - t_begin;
+            }
         }
     } else if (warp == 1) {
         if (g_count > 0) {
             const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.kp), kFmtBF16, 0, 0);
+            long long t_full = 0;
+            const long long t_begin = clock64();
             int stage = 0;
             uint32_t phase = 0;
             bool first = true;
@@ -178,16 +202,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int64_t item = cur / p.steps_per_item;
                 const int64_t item_end = (item + 1) * p.steps_per_item;
                 const int64_t seg_end = imin(ke, item_end);
-                for (int64_t st = cur; st < seg_end; st += kKS) {
-                    const int nks = static_cast<int>(imin(kKS, seg_end - st));
+                for (int64_t st = cur; st < seg_end; st += pl.ks) {
+                    const int nks = static_cast<int>(imin(pl.ks, seg_end - st));
+                    const long long tf = clock64();
                     mbar_wait(smem_u32(&full[stage]), phase);
+                    t_full += clock64() - tf;
                     tc_fence_after();
                     uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
                     const uint64_t a0 = make_smem_desc(smem_u32(sbase), static_cast<uint32_t>(pl.cp * 16), 128,
                                                        kLayoutNone);
                     const uint64_t b0 = make_smem_desc(smem_u32(sbase + pl.x_bytes), 16, 1024, kLayoutSw128);
                     for (int ks = 0; ks < nks; ++ks) {
-                        const uint64_t bdesc = desc_advance(b0, static_cast<uint32_t>(ks * 32));
+                        const uint64_t bdesc =
+                            desc_advance(b0, static_cast<uint32_t>((ks / 4) * pl.kp * 128 + (ks % 4) * 32));
                         for (int g = 0; g < g_count; ++g) {
                             // group g starts g*T taps later = g*T q-chunks; K-step ks = 2 chunks
                             const uint64_t adesc =
@@ -210,6 +237,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (elect_one()) mma_commit(smem_u32(&acc_done));
             __syncwarp();
+            if (p.prof && lane == 0) {
+                p.prof[blockIdx.x * 8 + 2] = t_full;
+                p.prof[blockIdx.x * 8 + 4] = clock64() - t_begin;
+            }
         }
     } else if (warp >= 4) {
         // epilogue: D rows (t, c) x columns (g, k) -> partial[role-split][k][c][tap]
@@ -316,7 +347,7 @@ cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, flo
         const cuuint64_t dims[3] = {static_cast<cuuint64_t>(q), static_cast<cuuint64_t>(k),
                                     static_cast<cuuint64_t>(n)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(q) * 2, static_cast<cuuint64_t>(k * q) * 2};
-        const cuuint32_t box[3] = {static_cast<cuuint32_t>(kStageQ), static_cast<cuuint32_t>(pl.kp), 1};
+        const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(pl.kp), 1};
         const cuuint32_t estr[3] = {1, 1, 1};
         CUresult r = encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(dy_bf16), dims, strides,
                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -337,10 +368,26 @@ cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, flo
     wp.total_steps = n * wp.steps_per_item;
     wp.pl = pl;
     wp.part = static_cast<float*>(workspace);
-    tc_wgrad_kernel<<<pl.roles * pl.splits, kThreads, pl.smem_bytes, stream>>>(xmap, ymap, wp);
+    const int grid = pl.roles * pl.splits;
+    static const bool profile = getenv("C1D_PROFILE") != nullptr;
+    if (profile) {
+        cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * grid);
+        cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * grid);
+    }
+    tc_wgrad_kernel<<<grid, kThreads, pl.smem_bytes, stream>>>(xmap, ymap, wp);
     note_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    if (profile) {
+        std::vector<unsigned long long> h(8 * grid);
+        cudaMemcpy(h.data(), wp.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+        double a[8] = {0};
+        for (int b = 0; b < grid; ++b)
+            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[b * 8 + i]) / grid;
+        fprintf(stderr, "[tc_wgrad prof] ks=%d stages=%d x_chunks=%d | producer wait_empty %.0f / total %.0f | mma wait_full %.0f total %.0f\n",
+                pl.ks, pl.stages, pl.x_chunks, a[0], a[1], a[2], a[4]);
+        cudaFree(wp.prof);
+    }
     const int64_t count = k * c * s;
     wgrad_reduce_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 4096)), 256, 0, stream>>>(
         wp.part, dw_kcs, k, c, s, pl.t, pl.gmax, pl.splits);
