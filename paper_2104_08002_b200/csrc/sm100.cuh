@@ -205,6 +205,22 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar_saddr, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Polling wait with nanosleep backoff, for warps that wait a long time (epilogue, idle roles):
+// keeps them from stealing issue slots from the MMA-issuing warp on the same SM sub-partition.
+__device__ __forceinline__ bool mbar_try(uint32_t bar_saddr, uint32_t parity) {
+    uint32_t ok = 0;
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}\n"
+        : "=r"(ok)
+        : "r"(bar_saddr), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint32_t bar_saddr, uint32_t parity, uint32_t ns = 256) {
+    while (!mbar_try(bar_saddr, parity)) __nanosleep(ns);
+}
 __device__ __forceinline__ void mbar_arrive(uint32_t bar_saddr) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar_saddr) : "memory");
 }

@@ -294,15 +294,22 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                 const uint64_t a0 = make_smem_desc(xs, 128, 16, kLayoutNone);
                 const uint64_t b0 = make_smem_desc(wsm, 128, 256, kLayoutNone);
-                for (int c = 0; c < ccn; ++c) {
-                    const uint64_t bdesc = desc_advance(b0, static_cast<uint32_t>(c) * pl.b_chan_bytes);
-                    const uint64_t achan = desc_advance(a0, static_cast<uint32_t>(c * pl.xw * 2));
-                    for (int t = 0; t < su.tcur; ++t) {
-                        const uint64_t adesc = desc_advance(achan, static_cast<uint32_t>(t * kTileQ * 2));
-                        if (elect_one()) mma_bf16_ss(tmem + static_cast<uint32_t>(t * KP), adesc, bdesc, idesc, 1);
-                        __syncwarp();
+                if (elect_one()) {
+                    uint64_t bdesc = b0;
+                    uint64_t achan = a0;
+                    for (int c = 0; c < ccn; ++c) {
+                        uint64_t adesc = achan;
+                        uint32_t dcol = tmem;
+                        for (int t = 0; t < su.tcur; ++t) {
+                            mma_bf16_ss(dcol, adesc, bdesc, idesc, 1);
+                            adesc = desc_advance(adesc, static_cast<uint32_t>(kTileQ * 2));
+                            dcol += static_cast<uint32_t>(KP);
+                        }
+                        bdesc = desc_advance(bdesc, pl.b_chan_bytes);
+                        achan = desc_advance(achan, static_cast<uint32_t>(pl.xw * 2));
                     }
                 }
+                __syncwarp();
                 if (elect_one()) mma_commit(smem_u32(&stage_empty[stage]));
                 __syncwarp();
                 if (++stage == pl.stages) {
@@ -335,7 +342,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         Super su;
         const int slots = static_cast<int>(kTmemCols) / KP;
         while (next_super(cur, J, G, T, &su)) {
-            mbar_wait(smem_u32(&tmem_full), tphase);
+            mbar_wait_sleep(smem_u32(&tmem_full), tphase, 256);
             tphase ^= 1;
             tc_fence_after();
             // 1. store the completed outputs (slots 0..tcur-1)

@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int t = row / pl.cp, c = row % pl.cp;
             const bool have = n_stages_total > 0;
             if (have) {
-                mbar_wait(smem_u32(&acc_done), 0);
+                mbar_wait_sleep(smem_u32(&acc_done), 0, 1000);
                 tc_fence_after();
             }
             float* dst = p.part + static_cast<int64_t>(blockIdx.x) * p.k * p.c * p.s;
@@ -297,6 +297,304 @@ __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __res
     }
 }
 
+// ============================================================================ v3
+// Backward-weight with the tensor core's B operand reused by consecutive MMAs:
+//   M = 128 rows = T taps x CP channels (CP = C rounded up to a power of two >= 16, T = 128/CP):
+//        A[(t, c)][kk] = X[c][q + 8*(s0 + t)]         q-chunk-major X window (see v1)
+//   N = P x KPw rows (KPw = K rounded up to a power of two >= 16, P <= 256/KPw copies):
+//        B[(p', k)][kk] = dY[k][q - Bq*(P-1-p')]      copy p' shifted by Bq = 8*T columns
+//   D[(t,c)][(p',k)] = sum_q' X[c][q' + 8*(s0 + t + T*(P-1-p'))] dY[k][q']  -> T*P taps per MMA.
+// The P copies of dY are P consecutive Bq-column TMA boxes (K-major, 2*Bq-byte swizzle, or the
+// plain core-matrix layout for Bq = 8), so the copy shift is a uniform row-group stride: nothing
+// is loaded twice. Each CTA accumulates up to 512/N tap groups; all groups of a K-step use the
+// same B (dY) and differ only in A's start address (the tap offset). The X window arrives by a
+// 4-D TMA box straight into the q-chunk-major layout.
+namespace {
+
+struct W2Plan {
+    int cp, t, kpw, p, bq, n;
+    uint32_t swz;            // UMMA layout type for the dY operand
+    int taps_per_group, groups_total, gpc, roles;
+    int role_groups[64];
+    int role_cta_begin[65];
+    int ks, stage_q, x_chunks, nbox;
+    uint32_t box_bytes, x_bytes, y_bytes, stage_bytes;
+    int stages;
+    size_t smem_bytes;
+    int grid;
+};
+
+bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out) {
+    if (d != 8 || q % 8 != 0 || q < 16) return false;
+    if (c > 128 || k > 128) return false;
+    if (n * c >= (int64_t{1} << 31) || n * k >= (int64_t{1} << 31)) return false;
+    W2Plan p{};
+    p.cp = 16;
+    while (p.cp < c) p.cp *= 2;
+    p.t = 128 / p.cp;
+    p.kpw = 16;
+    while (p.kpw < k) p.kpw *= 2;
+    p.p = std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t)));
+    p.n = p.p * p.kpw;
+    p.bq = 8 * p.t;
+    if (p.bq > 64) return false;
+    p.swz = p.bq == 64 ? kLayoutSw128 : (p.bq == 32 ? kLayoutSw64 : (p.bq == 16 ? kLayoutSw32 : kLayoutNone));
+    p.taps_per_group = p.t * p.p;
+    p.groups_total = static_cast<int>(ceil_div(s, p.taps_per_group));
+    p.gpc = std::max(1, static_cast<int>(kTmemCols) / p.n);
+    if (p.gpc > 8) p.gpc = 8;
+    if (p.gpc > p.groups_total) p.gpc = p.groups_total;
+    p.roles = static_cast<int>(ceil_div(p.groups_total, p.gpc));
+    if (p.roles > 64) return false;
+    const int sms = num_sms();
+    if (p.roles > sms) return false;
+    int assigned = 0;
+    for (int r = 0; r < p.roles; ++r) p.role_groups[r] = std::min(p.gpc, p.groups_total - p.gpc * r);
+    p.role_cta_begin[0] = 0;
+    // Every role streams the same X/dY data per K-step (the data path, not the MMA count, bounds
+    // the per-step time), so the CTAs are split evenly across roles.
+    for (int r = 0; r < p.roles; ++r) {
+        const int64_t want = static_cast<int64_t>(sms) * (r + 1) / p.roles;
+        int end = static_cast<int>(std::max<int64_t>(want, assigned + 1));
+        if (r == p.roles - 1) end = std::max(sms, assigned + 1);
+        p.role_cta_begin[r + 1] = end;
+        assigned = end;
+    }
+    p.grid = assigned;
+    p.box_bytes = static_cast<uint32_t>(p.kpw * 2 * p.bq);
+    bool ok = false;
+    for (int ks = 16; ks >= 4; ks -= 4) {
+        p.ks = ks;
+        p.stage_q = 16 * ks;
+        if (p.stage_q % p.bq) continue;
+        // X chunks read: stage + tap span of the role's groups (+T-1 rows, +1 K-chunk)
+        p.x_chunks = p.stage_q / 8 + p.gpc * p.taps_per_group + p.t + 1;
+        if (p.x_chunks > 256) continue;
+        p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
+        p.x_bytes = (static_cast<uint32_t>(p.x_chunks * p.cp * 16) + 1023) & ~1023u;
+        p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
+        p.stage_bytes = p.x_bytes + p.y_bytes;
+        p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / p.stage_bytes));
+        if (p.stages < 3) continue;
+        ok = true;
+        break;
+    }
+    if (!ok) return false;
+    p.smem_bytes = static_cast<size_t>(p.stages) * p.stage_bytes + 1024;
+    *out = p;
+    return true;
+}
+
+struct W2Params {
+    int64_t n_items, c, k, s, q, w_in;
+    int64_t steps_per_item, total_steps;
+    W2Plan pl;
+    float* part;        // [cta][k][c][s]
+    unsigned long long* prof;
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    tc_wgrad2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+                     const W2Params p) {
+    extern __shared__ uint8_t smem_raw[];
+    __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ uint64_t acc_done;
+    __shared__ uint32_t tmem_base_s;
+
+    const W2Plan& pl = p.pl;
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    int role = 0;
+    while (role + 1 < pl.roles && static_cast<int>(blockIdx.x) >= pl.role_cta_begin[role + 1]) ++role;
+    const int split = blockIdx.x - pl.role_cta_begin[role];
+    const int splits = pl.role_cta_begin[role + 1] - pl.role_cta_begin[role];
+    const int g_count = pl.role_groups[role];
+    const int tap0 = pl.gpc * role * pl.taps_per_group;
+    const int64_t kb = p.total_steps * split / splits;
+    const int64_t ke = p.total_steps * (split + 1) / splits;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < pl.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&acc_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base_s);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+    const int64_t back = static_cast<int64_t>(pl.p - 1) * pl.bq;  // dY history columns per stage
+
+    if (warp == 0) {
+        if (lane == 0) {
+            prefetch_tmap(&xmap);
+            prefetch_tmap(&ymap);
+            long long tw_sum = 0;
+            const long long tb = clock64();
+            int stage = 0;
+            uint32_t phase = 0;
+            int64_t cur = kb;
+            while (cur < ke) {
+                const int64_t item = cur / p.steps_per_item;
+                const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
+                for (int64_t st = cur; st < seg_end; st += pl.ks) {
+                    const int64_t q0 = (st - item * p.steps_per_item) * 16;
+                    const long long tw = clock64();
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    tw_sum += clock64() - tw;
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.x_chunks * pl.cp * 16) +
+                                                  static_cast<uint32_t>(pl.nbox) * pl.box_bytes);
+                    uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
+                    // X window, q-chunk-major: 4-D box (8 columns, CP channels, x_chunks chunks, 1 item)
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(sbase)),
+                        "l"(&xmap), "r"(0), "r"(0), "r"(static_cast<int32_t>(q0 / 8 + tap0)),
+                        "r"(static_cast<int32_t>(item)), "r"(fb)
+                        : "memory");
+                    for (int b = 0; b < pl.nbox; ++b)
+                        tma_load_3d(smem_u32(sbase + pl.x_bytes + static_cast<uint32_t>(b) * pl.box_bytes), &ymap,
+                                    static_cast<int32_t>(q0 - back + static_cast<int64_t>(b) * pl.bq), 0,
+                                    static_cast<int32_t>(item), fb);
+                    if (++stage == pl.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                cur = seg_end;
+            }
+            if (p.prof) {
+                p.prof[blockIdx.x * 8 + 0] = tw_sum;
+                p.prof[blockIdx.x * 8 + 1] = clock64() - tb;
+            }
+        }
+    } else if (warp == 1) {
+        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.n), kFmtBF16, 0, 0);
+        // B (dY) descriptor: swizzled K-major rows of 2*Bq bytes (8-row atoms), or for Bq = 8 the
+        // plain core-matrix layout with K-chunks one box apart.
+        const uint32_t b_sbo = pl.bq == 8 ? 128u : 16u * static_cast<uint32_t>(pl.bq);
+        const uint32_t b_lbo = pl.bq == 8 ? pl.box_bytes : 16u;
+        long long tf_sum = 0;
+        const long long tb = clock64();
+        int stage = 0;
+        uint32_t phase = 0;
+        bool first = true;
+        int64_t cur = kb;
+        while (cur < ke) {
+            const int64_t item = cur / p.steps_per_item;
+            const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
+            for (int64_t st = cur; st < seg_end; st += pl.ks) {
+                const int nks = static_cast<int>(imin(pl.ks, seg_end - st));
+                const long long tf = clock64();
+                mbar_wait(smem_u32(&full[stage]), phase);
+                tf_sum += clock64() - tf;
+                tc_fence_after();
+                uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
+                const uint64_t ax0 = make_smem_desc(smem_u32(sbase), static_cast<uint32_t>(pl.cp * 16), 128, kLayoutNone);
+                const uint64_t by0 = make_smem_desc(smem_u32(sbase + pl.x_bytes), b_lbo, b_sbo, pl.swz);
+                // One elected lane issues the whole stage; descriptors advance incrementally
+                // (no divisions, no per-MMA reconvergence).
+                if (elect_one()) {
+                    uint64_t adesc = ax0;
+                    const uint32_t a_step = static_cast<uint32_t>(2 * pl.cp * 16);          // one K-step
+                    const uint32_t g_step = static_cast<uint32_t>(pl.taps_per_group * pl.cp * 16);
+                    const int per_box = pl.bq / 16;                                         // K-steps per dY box
+                    uint64_t bbox = by0;
+                    int inbox = 0;
+                    for (int ks = 0; ks < nks; ++ks) {
+                        const uint64_t bdesc = desc_advance(bbox, static_cast<uint32_t>(inbox * 32));
+                        uint64_t ag = adesc;
+                        uint32_t dcol = tmem;
+                        for (int g = 0; g < g_count; ++g) {
+                            mma_bf16_ss(dcol, ag, bdesc, idesc, first ? 0u : 1u);
+                            ag = desc_advance(ag, g_step);
+                            dcol += static_cast<uint32_t>(pl.n);
+                        }
+                        first = false;
+                        adesc = desc_advance(adesc, a_step);
+                        if (per_box == 0) {  // Bq = 8: a K-step spans 16/Bq boxes
+                            bbox = desc_advance(bbox, pl.box_bytes * static_cast<uint32_t>(16 / pl.bq));
+                        } else if (++inbox == per_box) {
+                            inbox = 0;
+                            bbox = desc_advance(bbox, pl.box_bytes);
+                        }
+                    }
+                }
+                __syncwarp();
+                first = false;
+                if (elect_one()) mma_commit(smem_u32(&empty[stage]));
+                __syncwarp();
+                if (++stage == pl.stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            cur = seg_end;
+        }
+        if (elect_one()) mma_commit(smem_u32(&acc_done));
+        __syncwarp();
+        if (p.prof && lane == 0) {
+            p.prof[blockIdx.x * 8 + 2] = tf_sum;
+            p.prof[blockIdx.x * 8 + 4] = clock64() - tb;
+        }
+    } else if (warp >= 4) {
+        // ---- epilogue: D rows (t, c) x columns (p', k) -> partial[cta][k][c][tap]
+        const int quarter = warp - 4;
+        const int row = quarter * 32 + lane;
+        const int t = row / pl.cp, c = row % pl.cp;
+        const bool have = kb < ke;
+        if (have) {
+            mbar_wait_sleep(smem_u32(&acc_done), 0, 1000);
+            tc_fence_after();
+        }
+        float* dst = p.part + static_cast<int64_t>(blockIdx.x) * p.k * p.c * p.s;
+        for (int g = 0; g < g_count; ++g) {
+            const int64_t sgrp = tap0 + static_cast<int64_t>(g) * pl.taps_per_group + t;
+            for (int cb = 0; cb < pl.n; cb += 16) {
+                uint32_t v[16];
+                if (have) {
+                    tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(g * pl.n + cb), v);
+                    tmem_ld_wait();
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = 0;
+                }
+                if (c < p.c) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = cb + j;
+                        const int pp = col / pl.kpw, kk = col % pl.kpw;
+                        const int64_t tap = sgrp + static_cast<int64_t>(pl.t) * (pl.p - 1 - pp);
+                        if (kk < p.k && tap < p.s) dst[(static_cast<int64_t>(kk) * p.c + c) * p.s + tap] = __uint_as_float(v[j]);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
+}
+
+__global__ void wgrad2_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw, int64_t K, int64_t C,
+                                     int64_t S, const W2Plan pl) {
+    const int64_t count = K * C * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e % S;
+        const int role = static_cast<int>(s / (static_cast<int64_t>(pl.gpc) * pl.taps_per_group));
+        float v = 0.0f;
+        for (int b = pl.role_cta_begin[role]; b < pl.role_cta_begin[role + 1]; ++b) v += part[static_cast<int64_t>(b) * count + e];
+        dw[e] = v;
+    }
+}
+
+}  // namespace
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
         void* f = nullptr;
@@ -311,12 +609,100 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 }  // namespace
 
+namespace {
+cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace, int64_t n,
+                      int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, const W2Plan& pl, cudaStream_t stream) {
+    auto encode = encode_fn();
+    if (!encode) return cudaErrorNotSupported;
+    const int64_t w_in = q + d * (s - 1);
+    CUtensorMap xmap, ymap;
+    {
+        const cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w_in / 8),
+                                    static_cast<cuuint64_t>(n)};
+        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(w_in) * 2, 16, static_cast<cuuint64_t>(c * w_in) * 2};
+        const cuuint32_t box[4] = {8, static_cast<cuuint32_t>(pl.cp), static_cast<cuuint32_t>(pl.x_chunks), 1};
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        if (encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(x_bf16), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    {
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(q), static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(q) * 2, static_cast<cuuint64_t>(k * q) * 2};
+        const cuuint32_t box[3] = {static_cast<cuuint32_t>(pl.bq), static_cast<cuuint32_t>(pl.kpw), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        const CUtensorMapSwizzle sw =
+            pl.bq == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                        : (pl.bq == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : (pl.bq == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                                                   : CU_TENSOR_MAP_SWIZZLE_NONE));
+        if (encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(dy_bf16), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
+    cudaError_t e = cudaFuncSetAttribute(tc_wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(pl.smem_bytes));
+    if (e != cudaSuccess) return e;
+    W2Params wp{};
+    wp.n_items = n;
+    wp.c = c;
+    wp.k = k;
+    wp.s = s;
+    wp.q = q;
+    wp.w_in = w_in;
+    // reduction columns q in [0, Q + (P-1)*Bq): copy p' reaches (P-1-p')*Bq columns back
+    wp.steps_per_item = ceil_div(q + static_cast<int64_t>(pl.p - 1) * pl.bq, 16);
+    wp.total_steps = n * wp.steps_per_item;
+    wp.pl = pl;
+    wp.part = static_cast<float*>(workspace);
+    static const bool profile = getenv("C1D_PROFILE") != nullptr;
+    if (profile) {
+        cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * pl.grid);
+        cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * pl.grid);
+    }
+    tc_wgrad2_kernel<<<pl.grid, kThreads, pl.smem_bytes, stream>>>(xmap, ymap, wp);
+    note_launch();
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (profile) {
+        std::vector<unsigned long long> h(8 * pl.grid);
+        cudaMemcpy(h.data(), wp.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+        double acc[8] = {0};
+        for (int bb = 0; bb < pl.grid; ++bb)
+            for (int i2 = 0; i2 < 8; ++i2) acc[i2] += static_cast<double>(h[bb * 8 + i2]) / pl.grid;
+        fprintf(stderr, "[tc_wgrad3 prof] T=%d P=%d N=%d gpc=%d roles=%d ks=%d stages=%d x_chunks=%d nbox=%d | "
+                "producer wait_empty %.0f / total %.0f | mma wait_full %.0f total %.0f\n",
+                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.x_chunks, pl.nbox, acc[0], acc[1], acc[2], acc[4]);
+        for (int r = 0; r < pl.roles; ++r) {
+            unsigned long long mx = 0, wf = 0;
+            for (int bb = pl.role_cta_begin[r]; bb < pl.role_cta_begin[r + 1]; ++bb) {
+                mx = std::max(mx, h[bb * 8 + 4]);
+                wf = std::max(wf, h[bb * 8 + 2]);
+            }
+            fprintf(stderr, "   role %d: ctas %d groups %d  max total %llu  max wait_full %llu\n", r,
+                    pl.role_cta_begin[r + 1] - pl.role_cta_begin[r], pl.role_groups[r], mx, wf);
+        }
+        cudaFree(wp.prof);
+    }
+    const int64_t count = k * c * s;
+    wgrad2_reduce_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 4096)), 256, 0, stream>>>(
+        wp.part, dw_kcs, k, c, s, pl);
+    note_launch();
+    return cudaGetLastError();
+}
+}  // namespace
+
 bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
     WPlan p;
-    return make_wplan(n, c, k, s, d, q, &p);
+    W2Plan p2;
+    return make_w2plan(n, c, k, s, d, q, &p2) || make_wplan(n, c, k, s, d, q, &p);
 }
 
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    if (make_w2plan(n, c, k, s, d, q, &p2))
+        return sizeof(float) * static_cast<size_t>(p2.grid) * static_cast<size_t>(k * c * s);
     WPlan p;
     if (!make_wplan(n, c, k, s, d, q, &p)) return 0;
     return sizeof(float) * static_cast<size_t>(p.roles) * p.splits * static_cast<size_t>(k * c * s);
@@ -324,6 +710,10 @@ size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int6
 
 cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace,
                             int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream) {
+    {
+        W2Plan p2;
+        if (make_w2plan(n, c, k, s, d, q, &p2)) return launch_v2(x_bf16, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream);
+    }
     WPlan pl;
     if (!make_wplan(n, c, k, s, d, q, &pl)) return cudaErrorNotSupported;
     auto encode = encode_fn();

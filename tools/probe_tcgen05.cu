@@ -52,6 +52,17 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Params p, const uint16_t*
             *reinterpret_cast<uint16_t*>(sx + off) = ga[i];
         }
     }
+    if (p.mode == 3) {
+        // A K-major SW64: 128 rows x 32 k, row = 64 B, 8-row atoms of 512 B, 16B chunk XOR (row%8)>>1... write generic pattern
+        for (int i = tid; i < 128 * 32; i += 128) {
+            int m = i / 32, k = i % 32;
+            int chunk = (k / 8) ^ ((m % 8) >> 1);  // SW64: XOR 16B-chunk index (2 bits) with row bits
+            int off = (m / 8) * 512 + (m % 8) * 64 + chunk * 16 + (k % 8) * 2;
+            *reinterpret_cast<uint16_t*>(sx + off) = ga[(m * 32 + k) % (128 * 64)];
+        }
+        // B: 256 rows, K = 16; interleave; fill a 16 KB region with a pattern (timing only)
+        for (int i = tid; i < 8192; i += 128) reinterpret_cast<uint16_t*>(sb)[i] = gw[i % (256 * 64)];
+    }
     if (p.mode == 0 || p.mode == 1) {
         // B K-major interleave: n rows x 16 k; addr = (n/8)*256 + (k/8)*128 + (n%8)*16 + (k%8)*2
         for (int i = tid; i < p.n * 16; i += 128) {
@@ -100,16 +111,23 @@ __global__ void __launch_bounds__(128, 1) probe_kernel(Params p, const uint16_t*
         } else if (p.mode == 1) {
             idesc = make_idesc(128, p.n, kFmtBF16, 0, 0);
             bdesc = p.b_swap ? make_smem_desc(sba, 256, 128, kLayoutNone) : make_smem_desc(sba, 128, 256, kLayoutNone);
-        } else {
+        } else if (p.mode == 2) {
             idesc = make_idesc(128, p.n, kFmtBF16, 0, 0);
             adesc = p.a_swap ? make_smem_desc(sxa, 1024, 128, kLayoutNone) : make_smem_desc(sxa, 128, 1024, kLayoutNone);
             bdesc = make_smem_desc(sba, 16, 1024, kLayoutSw128);
+        } else {
+            idesc = make_idesc(128, p.n, kFmtBF16, 0, 0);
+            adesc = make_smem_desc(sxa, 16, 512, kLayoutSw64);
+            bdesc = p.a_swap ? make_smem_desc(sba, 1024, 128, kLayoutNone) : make_smem_desc(sba, 128, 256, kLayoutNone);
         }
         t0 = clock64();
         const uint32_t nstep = (uint32_t)p.n;
         uint32_t vi = 0;
         auto issue = [&](uint32_t dcol, uint32_t accf) {
-            if (p.mode == 0) {
+            if (p.mode == 3) {
+                vi = (vi + 1) & 3;
+                mma_bf16_ss(dcol, desc_advance(adesc, (vi & 1) * 32), desc_advance(bdesc, p.vary ? vi * 2048 : 0), idesc, accf);
+            } else if (p.mode == 0) {
                 if (p.split) {
                     vi = (vi + 1) & 3;
                     const uint64_t ad = desc_advance(adesc, vi * 256);
@@ -216,9 +234,11 @@ int main() {
     run({2, 256, 0, 0, 1, 0, 1, 0, 0, 0}, "SS Kmaj A(LBO=128,SBO=1024) B SW128");
     // throughput (values are garbage-scaled by reps but we only time)
     char nm[128];
-    run({0, 256, 0, 0, 1, 0, 1, 0, 0, 0}, "WRAP test dcol=0");
-    run({0, 256, 0, 0, 1, 0, 1, 0, 256, 0}, "WRAP test dcol=256");
-    run({0, 256, 0, 0, 1, 0, 1, 0, 448, 0}, "WRAP test dcol=448 (wraps past 512)");
+    run({3, 256, 0, 0, 2048, 0, 1, 0, 0, 0}, "TPUT3 A SW64, B interleave std, fixed");
+    run({3, 256, 0, 0, 2048, 0, 1, 1, 0, 0}, "TPUT3 A SW64, B interleave std, vary");
+    run({3, 256, 1, 0, 2048, 0, 1, 0, 0, 0}, "TPUT3 A SW64, B interleave overlap, fixed");
+    run({3, 256, 1, 0, 2048, 0, 1, 1, 0, 0}, "TPUT3 A SW64, B interleave overlap, vary");
+    run({3, 256, 1, 0, 2048, 0, 2, 1, 0, 0}, "TPUT3 A SW64, B overlap, vary, nacc2");
     for (int dc : {0, 64, 128, 192, 256}) { snprintf(nm, 128, "TPUT SS rowtap VARY N=256 dcol=%d", dc); run({0, 256, 0, 0, 2048, 0, 1, 1, dc, 0}, nm); }
     for (int sp : {64, 128, 192}) { snprintf(nm, 128, "TPUT split %d+%d plain", sp, 256 - sp); run({0, 256, 0, 0, 2048, 0, 1, 1, 0, sp}, nm); }
     for (int sp : {64, 128, 192}) { snprintf(nm, 128, "TPUT split %d+%d collector", sp, 256 - sp); run({0, 256, 0, 0, 2048, 0, 1, 2, 0, sp}, nm); }
