@@ -206,3 +206,20 @@ def test_round_bf16_matches_reference_bits(golden):
     vals = golden["bf16_in"]
     got = cv.round_bf16(_t(vals)).view(torch.int16).cpu().numpy().view(np.uint16)
     np.testing.assert_array_equal(got, golden["bf16_bits"])
+
+
+def test_reference_acceptance_binary_on_gpu_backend():
+    """The reference's unmodified proj/tests/acceptance.cpp linked against the B200 backend
+    (paper_2104_08002_b200/host/conv1d_gpu.cpp replaces conv.cpp; built by oracle/Makefile into
+    oracle/_ref/acceptance_gpu). Criteria 1 (220 random combos vs naive at 1e-5), 3 (finite
+    differences incl. a 2-block net), 5 (bitwise determinism) and 7 (BF16 + OddDims) must pass.
+    Criterion 6's 4-thread-scaling clause is a CPU property the GPU path does not have."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "acceptance_gpu")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/acceptance_gpu not built (needs /root/reference at build time)")
+    for crit in ("1", "3", "5", "7"):
+        out = subprocess.run([exe, crit], capture_output=True, text=True, timeout=300)
+        assert out.returncode == 0 and f"criterion {crit} PASS" in out.stdout, out.stdout + out.stderr
