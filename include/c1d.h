@@ -74,7 +74,8 @@ typedef enum c1d_algo {
     C1D_ALGO_AUTO = 0,
     C1D_ALGO_DIRECT = 1,  /* CUDA-core FFMA direct convolution, any shape */
     C1D_ALGO_TCGEN05 = 2, /* tcgen05.mma BF16 tensor-core kernels (TMEM accumulators) */
-    C1D_ALGO_TF32X3 = 3   /* tcgen05 kind::tf32 with 3xTF32 split for FP32 precision */
+    C1D_ALGO_BF16X3 = 3   /* FP32 precision on the tcgen05 kernels: operands split into bf16 hi+lo
+                             parts (3 partial products per term, FP32 accumulation in TMEM) */
 } c1d_algo;
 
 typedef enum c1d_pass { C1D_PASS_FORWARD = 0, C1D_PASS_BACKWARD_DATA = 1, C1D_PASS_BACKWARD_WEIGHT = 2 } c1d_pass;

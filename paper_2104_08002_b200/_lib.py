@@ -15,7 +15,7 @@ HEADER_PATH = os.path.join(ROOT, "include", "c1d.h")
 OK, ERR_SHAPE_MISMATCH, ERR_ODD_DIMS, ERR_TOO_NARROW, ERR_INVALID_ARGUMENT, ERR_WORKSPACE, ERR_UNSUPPORTED, \
     ERR_CUDA, ERR_NO_DEVICE = range(9)
 PASS_FORWARD, PASS_BACKWARD_DATA, PASS_BACKWARD_WEIGHT = 0, 1, 2
-ALGO_AUTO, ALGO_DIRECT, ALGO_TCGEN05, ALGO_TF32X3 = 0, 1, 2, 3
+ALGO_AUTO, ALGO_DIRECT, ALGO_TCGEN05, ALGO_BF16X3 = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16 = 0, 1
 FLAG_STRICT_BF16_DIMS = 0x1
 

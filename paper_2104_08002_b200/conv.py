@@ -109,7 +109,7 @@ def _check(status: int) -> None:
     raise _STATUS_TO_ERROR.get(status, Error)(msg)
 
 
-_ALGOS = {"auto": L.ALGO_AUTO, "direct": L.ALGO_DIRECT, "tcgen05": L.ALGO_TCGEN05, "tf32x3": L.ALGO_TF32X3}
+_ALGOS = {"auto": L.ALGO_AUTO, "direct": L.ALGO_DIRECT, "tcgen05": L.ALGO_TCGEN05, "bf16x3": L.ALGO_BF16X3}
 ALGO_NAMES = {v: k for k, v in _ALGOS.items()}
 
 

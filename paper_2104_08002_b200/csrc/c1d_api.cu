@@ -91,7 +91,7 @@ c1d_status validate(const c1d_desc* desc, int64_t* q_out) {
         return fail(C1D_ERR_INVALID_ARGUMENT, "unknown precision");
     if (d.in_dtype != C1D_DTYPE_F32 && d.in_dtype != C1D_DTYPE_BF16)
         return fail(C1D_ERR_INVALID_ARGUMENT, "unknown in_dtype");
-    if (d.algo < C1D_ALGO_AUTO || d.algo > C1D_ALGO_TF32X3) return fail(C1D_ERR_INVALID_ARGUMENT, "unknown algo");
+    if (d.algo < C1D_ALGO_AUTO || d.algo > C1D_ALGO_BF16X3) return fail(C1D_ERR_INVALID_ARGUMENT, "unknown algo");
     const int64_t receptive = d.d * (d.s - 1);
     if (d.w_in <= receptive) {
         return fail(C1D_ERR_TOO_NARROW, "padded width " + std::to_string(d.w_in) +
@@ -122,6 +122,15 @@ ConvGeom bwd_geom(const c1d_desc& d, int64_t q) {
     return ConvGeom{d.n, d.k, q, d.c, d.w_in, d.s, d.d, -d.d * (d.s - 1)};
 }
 
+// Geometry of the split (BF16X3) problems: fwd/bwd-d carry 4x the input channels
+// ([hi | lo | hi | lo] against weights [hi | hi | lo | lo]), bwd-w runs on 2C channels x 2K filters.
+ConvGeom split_geom(const c1d_desc& d, int64_t q, c1d_pass pass) {
+    ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
+    g.in_ch *= 4;
+    return g;
+}
+int64_t split_main_ch(const c1d_desc& d, c1d_pass pass) { return pass == C1D_PASS_FORWARD ? d.c : d.k; }
+
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     const bool tc_ok = [&] {
@@ -130,9 +139,23 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         if (pass == C1D_PASS_BACKWARD_DATA) return tc_conv_supported(bwd_geom(d, q));
         return tc_wgrad_supported(d.n, d.c, d.k, d.s, d.d, q);
     }();
-    if (d.algo == C1D_ALGO_AUTO) return tc_ok ? C1D_ALGO_TCGEN05 : C1D_ALGO_DIRECT;
+    const bool split_ok = [&] {
+        if (is_bf16(d) || d.in_dtype != C1D_DTYPE_F32) return false;
+        if (pass == C1D_PASS_BACKWARD_WEIGHT) return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q);
+        // Error model: each product carries <= 2*2^-18 relative representation error (dropped
+        // residuals of the two-level split), and the tensor core's FP32 accumulation adds
+        // ~1.5e-9 norm-relative per accumulated main-term product (measured); the correction
+        // terms accumulate in their own TMEM region, so only the C_in*S main products form the
+        // long chain. Keep C_in*S <= kMaxSplitTerms (<= ~6e-6 + 7.6e-6 worst case, 1e-5 bound);
+        // longer reductions run on FFMA.
+        constexpr int64_t kMaxSplitTerms = 3300;
+        const int64_t cin = pass == C1D_PASS_FORWARD ? d.c : d.k;
+        if (cin * d.s > kMaxSplitTerms) return false;
+        return tc_conv_supported(split_geom(d, q, pass), split_main_ch(d, pass));
+    }();
+    if (d.algo == C1D_ALGO_AUTO) return tc_ok ? C1D_ALGO_TCGEN05 : (split_ok ? C1D_ALGO_BF16X3 : C1D_ALGO_DIRECT);
     if (d.algo == C1D_ALGO_TCGEN05 && !tc_ok) return static_cast<c1d_algo>(-1);
-    if (d.algo == C1D_ALGO_TF32X3) return static_cast<c1d_algo>(-1);  // not built yet
+    if (d.algo == C1D_ALGO_BF16X3 && !split_ok) return static_cast<c1d_algo>(-1);
     return static_cast<c1d_algo>(d.algo);
 }
 
@@ -140,6 +163,15 @@ size_t align_up(size_t v) { return (v + 255) & ~size_t{255}; }
 
 size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo) {
     const size_t wbytes = align_up(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+    if (algo == C1D_ALGO_BF16X3) {
+        if (pass == C1D_PASS_BACKWARD_WEIGHT)
+            return align_up(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * d.w_in)) +
+                   align_up(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.k * q)) + 4 * wbytes +
+                   align_up(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q));
+        const ConvGeom g = split_geom(d, q, pass);
+        return align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * g.in_w)) + 8 * wbytes +
+               align_up(tc_conv_workspace_bytes(g, split_main_ch(d, pass)));
+    }
     if (algo == C1D_ALGO_DIRECT) {
         if (pass == C1D_PASS_BACKWARD_WEIGHT) return align_up(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
         return wbytes;
@@ -222,6 +254,30 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     Bump bump{};
     st = acquire_workspace(ws, ws_bytes, workspace_for(d, pass, q, algo), &bump);
     if (st != C1D_OK) return st;
+    if (algo == C1D_ALGO_BF16X3) {
+        // FP32 via split BF16 operands (split.cu): input channel blocks [hi | lo | hi | lo] against
+        // weight blocks [hi | hi | lo | lo]; block 0 (hi*hi) accumulates in its own TMEM region.
+        const ConvGeom gs = split_geom(d, q, pass);
+        const int64_t main_ch = split_main_ch(d, pass);
+        uint16_t* in4 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(gs.n * gs.in_ch * gs.in_w));
+        float* w4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+        float* wg4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+        cudaError_t e = launch_split_channels(static_cast<const float*>(in), in4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "split_channels");
+        if (pass == C1D_PASS_FORWARD) {
+            e = launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 1, 4, 0xCu, stream);  // c-blocks hi,hi,lo,lo
+            if (e == cudaSuccess) e = launch_prep_weights(w4, wg4, d.k, 4 * d.c, d.s, kWeightsForward, false, stream);
+        } else {
+            e = launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 4, 1, 0xCu, stream);  // k-blocks hi,hi,lo,lo
+            if (e == cudaSuccess)
+                e = launch_prep_weights(w4, wg4, 4 * d.k, d.c, d.s, kWeightsBackwardData, false, stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "split_weights");
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gs, main_ch));
+        e = launch_tc_conv(in4, wg4, out, gs, kws, stream, main_ch);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_conv (bf16x3)");
+        return C1D_OK;
+    }
     const bool bf16 = is_bf16(d);
     float* wg = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
     cudaError_t e = launch_prep_weights(w_kcs, wg, d.k, d.c, d.s,
@@ -342,6 +398,21 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     if (st != C1D_OK) return st;
     const bool bf16 = is_bf16(d);
     cudaError_t e;
+    if (algo == C1D_ALGO_BF16X3) {
+        // FP32 via split BF16 operands: x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the four
+        // (k-block, c-block) tiles of the 2K x 2C gradient are summed.
+        uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * d.w_in));
+        uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.k * q));
+        float* dw4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+        e = launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, 0x2u, stream);
+        if (e == cudaSuccess) e = launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, 0x2u, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "split_channels");
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q));
+        e = launch_tc_wgrad(x2, g2, dw4, kws, d.n, 2 * d.c, 2 * d.k, d.s, d.d, q, stream);
+        if (e == cudaSuccess) e = launch_sum_split_blocks(dw4, dw_kcs, d.k, d.c, d.s, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (bf16x3)");
+        return C1D_OK;
+    }
     if (algo == C1D_ALGO_DIRECT) {
         float* part = bump.take<float>(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
         e = launch_direct_wgrad(x, dy, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, dw_kcs, part, d.n, d.c, d.k,

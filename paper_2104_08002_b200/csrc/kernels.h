@@ -41,15 +41,25 @@ cudaError_t launch_round_bf16(const float* in, uint16_t* out, int64_t count, cud
 // Row-tap BF16 tensor-core convolution for dilation 8 (fwd and bwd-data). Returns
 // cudaErrorNotSupported when the shape is outside its envelope.
 struct TcConvPlan;
-bool tc_conv_supported(const ConvGeom& g);
-size_t tc_conv_workspace_bytes(const ConvGeom& g);
+// main_ch > 0 (split-FP32 mode): input channels >= main_ch accumulate into a second TMEM region
+// that the epilogue adds to the first, so the long accumulation chain only carries the main term.
+bool tc_conv_supported(const ConvGeom& g, int64_t main_ch = 0);
+size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch = 0);
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g,
-                           void* workspace, cudaStream_t stream);
+                           void* workspace, cudaStream_t stream, int64_t main_ch = 0);
 
 bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace,
                             int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream);
+
+// FP32-on-tensor-core operand splitting (split.cu)
+cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
+                                  unsigned pattern, cudaStream_t stream);
+cudaError_t launch_split_weights(const float* w, float* out, int64_t K, int64_t C, int64_t S, int kr, int cr,
+                                 unsigned sel, cudaStream_t stream);
+cudaError_t launch_sum_split_blocks(const float* dw4, float* dw, int64_t K, int64_t C, int64_t S,
+                                    cudaStream_t stream);
 
 int num_sms();
 

@@ -1,0 +1,100 @@
+// split.cu — FP32 precision on the BF16 tensor-core kernels by operand splitting.
+//
+// Every FP32 value v is written as v = hi + lo + e with hi = bf16(v), lo = bf16(v - hi) (both
+// round-to-nearest-even), |e| <= 2^-18 |v|. A product w*x is then
+//   w_hi*x_hi + w_hi*x_lo + w_lo*x_hi  (+ w_lo*x_lo)
+// with every partial product exact in the tensor core's FP32 accumulator. The split is expressed
+// as extra channels so the tcgen05 kernels do all the work:
+//   forward / backward-data:  x' = [x_hi | x_lo | x_hi | x_lo] (4C channels),
+//                             w' = [w_hi | w_hi | w_lo | w_lo]; channel block 0 (hi*hi) accumulates
+//                             in its own TMEM region, the three correction blocks in a second one
+//   backward-weight:          x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the 2K x 2C
+//                             weight gradient's four blocks are summed (hi*hi + hi*lo + lo*hi + lo*lo).
+// Error per product is <= 2*2^-18 relative (the two split residuals), plus the tensor core's
+// FP32 accumulation error on the main chain; c1d_api.cu gates the path so the total stays inside
+// the reference's 1e-5 FP32 bound.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace c1d {
+
+// in: [N][C][W] fp32 -> out: [N][R*C][W] bf16 bits, channel block b of `pattern` (bit b: 0 = hi,
+// 1 = lo) for b < R.
+__global__ void split_channels_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n,
+                                      int64_t c, int64_t w, int reps, unsigned pattern) {
+    const int64_t total = n * c * w;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t x = e % w;
+        const int64_t ch = (e / w) % c;
+        const int64_t item = e / (w * c);
+        const float v = in[e];
+        const uint16_t hi = fp32_to_bf16_bits(v);
+        const uint16_t lo = fp32_to_bf16_bits(v - bf16_bits_to_fp32(hi));
+        for (int r = 0; r < reps; ++r) {
+            const uint16_t val = ((pattern >> r) & 1u) ? lo : hi;
+            out[((item * reps + r) * c + ch) * w + x] = val;
+        }
+    }
+}
+
+// Weights KCS fp32 [K][C][S] -> expanded KCS fp32 [K*kr][C*cr][S] whose entries are the bf16 hi or
+// lo parts (exactly representable), selected per (k-block, c-block) by `sel` (bit kb*cr + cb).
+__global__ void split_weights_kernel(const float* __restrict__ w, float* __restrict__ out, int64_t K, int64_t C,
+                                     int64_t S, int kr, int cr, unsigned sel) {
+    const int64_t total = K * kr * C * cr * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e % S;
+        const int64_t cc = (e / S) % (C * cr);
+        const int64_t kk = e / (S * C * cr);
+        const int64_t cb = cc / C, c = cc % C, kb = kk / K, k = kk % K;
+        const float v = w[(k * C + c) * S + s];
+        const uint16_t hi = fp32_to_bf16_bits(v);
+        const float hif = bf16_bits_to_fp32(hi);
+        const float lof = bf16_bits_to_fp32(fp32_to_bf16_bits(v - hif));
+        out[e] = ((sel >> (kb * cr + cb)) & 1u) ? lof : hif;
+    }
+}
+
+// dw[k][c][s] = sum over the 2x2 (k-block, c-block) tiles of dw4[(kb*K + k)][(cb*C + c)][s]
+__global__ void sum_split_blocks_kernel(const float* __restrict__ dw4, float* __restrict__ dw, int64_t K, int64_t C,
+                                        int64_t S) {
+    const int64_t total = K * C * S;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = e % S, c = (e / S) % C, k = e / (S * C);
+        // fixed order: small terms first
+        const float ll = dw4[((K + k) * 2 * C + (C + c)) * S + s];
+        const float lh = dw4[((K + k) * 2 * C + c) * S + s];
+        const float hl = dw4[(k * 2 * C + (C + c)) * S + s];
+        const float hh = dw4[(k * 2 * C + c) * S + s];
+        dw[e] = hh + (hl + (lh + ll));
+    }
+}
+
+static unsigned blocks_for(int64_t total) {
+    return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 16 * num_sms())));
+}
+
+cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
+                                  unsigned pattern, cudaStream_t stream) {
+    split_channels_kernel<<<blocks_for(n * c * w), 256, 0, stream>>>(in, out, n, c, w, reps, pattern);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_weights(const float* w, float* out, int64_t K, int64_t C, int64_t S, int kr, int cr,
+                                 unsigned sel, cudaStream_t stream) {
+    split_weights_kernel<<<blocks_for(K * kr * C * cr * S), 256, 0, stream>>>(w, out, K, C, S, kr, cr, sel);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum_split_blocks(const float* dw4, float* dw, int64_t K, int64_t C, int64_t S,
+                                    cudaStream_t stream) {
+    sum_split_blocks_kernel<<<blocks_for(K * C * S), 256, 0, stream>>>(dw4, dw, K, C, S);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace c1d

@@ -66,6 +66,7 @@ struct Plan {
     uint32_t w_stage_bytes;
     size_t smem_bytes;
     int kgroups;     // filter groups of kp
+    uint32_t acc2;   // TMEM column offset of the second accumulator region (0 = none)
 };
 
 struct KParams {
@@ -74,11 +75,12 @@ struct KParams {
     int taps, k_begin;
     Plan pl;
     const uint16_t* bimg;  // this filter group's B image: [in_ch][ntot*16] bf16
+    int64_t main_ch;       // channels < main_ch -> region 0, others -> region acc2 (split FP32)
     float* out;
     unsigned long long* prof;  // optional per-CTA cycle counters (C1D_PROFILE=1), else nullptr
 };
 
-bool make_plan(const ConvGeom& g, Plan* pl) {
+bool make_plan(const ConvGeom& g, Plan* pl, bool two_regions = false) {
     if (g.dil != 8) return false;
     if (g.in_w % 8 != 0 || g.in_w < 8) return false;  // TMA global stride must be a multiple of 16 B
     if (g.n * g.in_ch >= (int64_t{1} << 31) || g.in_w >= (int64_t{1} << 31)) return false;
@@ -90,6 +92,11 @@ bool make_plan(const ConvGeom& g, Plan* pl) {
     p.ntot = p.g * p.kp;
     if (p.ntot > 256) return false;  // one MMA covers all tap blocks of a tile
     p.t = std::min(8, p.r - (p.g - 1));  // linear TMEM: T + G - 1 slots
+    p.acc2 = 0;
+    if (two_regions) {  // two accumulator regions of 256 columns each
+        p.t = std::min(p.t, 256 / p.kp - (p.g - 1));
+        p.acc2 = 256;
+    }
     if (p.t < 1) return false;
     p.n_seg = static_cast<int>(ceil_div(p.t * kTileQ + 8 * (kTapsPerBlock - 1), kSegQ));
     p.xw = p.n_seg * kSegQ;
@@ -299,7 +306,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint64_t achan = a0;
                     for (int c = 0; c < ccn; ++c) {
                         uint64_t adesc = achan;
-                        uint32_t dcol = tmem;
+                        uint32_t dcol = tmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u);
                         for (int t = 0; t < su.tcur; ++t) {
                             mma_bf16_ss(dcol, adesc, bdesc, idesc, 1);
                             adesc = desc_advance(adesc, static_cast<uint32_t>(kTileQ * 2));
@@ -354,6 +361,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint32_t v[16];
                     tmem_ld16(lane_base + static_cast<uint32_t>(j * KP + kb), v);
                     tmem_ld_wait();
+                    if (pl.acc2) {  // main term + the correction terms' separate accumulator
+                        uint32_t v2[16];
+                        tmem_ld16(lane_base + pl.acc2 + static_cast<uint32_t>(j * KP + kb), v2);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(v2[jj]));
+                    }
                     if (q < p.out_w) {
                         float* dst = p.out + (su.n * p.out_ch + p.k_begin + kb) * p.out_w + q;
 #pragma unroll
@@ -364,18 +378,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             // 2. carry the partial outputs (slots tcur..tcur+G-2) down to slots 0..G-2
             if (!su.last_in_segment) {
-                for (int j = 0; j < G - 1; ++j) {
-                    for (int kb = 0; kb < KP; kb += 16) {
-                        uint32_t v[16];
-                        tmem_ld16(lane_base + static_cast<uint32_t>((su.tcur + j) * KP + kb), v);
-                        tmem_ld_wait();
-                        tmem_st16(lane_base + static_cast<uint32_t>(j * KP + kb), v);
+                for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u)) {
+                    for (int j = 0; j < G - 1; ++j) {
+                        for (int kb = 0; kb < KP; kb += 16) {
+                            uint32_t v[16];
+                            tmem_ld16(lane_base + reg + static_cast<uint32_t>((su.tcur + j) * KP + kb), v);
+                            tmem_ld_wait();
+                            tmem_st16(lane_base + reg + static_cast<uint32_t>(j * KP + kb), v);
+                        }
                     }
                 }
             }
             // 3. zero the slots the next super-tile accumulates from scratch
-            for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < static_cast<uint32_t>(slots * KP); col += 16)
-                tmem_st16(lane_base + col, z);
+            const uint32_t region_cols = pl.acc2 ? pl.acc2 : static_cast<uint32_t>(slots * KP);
+            for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u))
+                for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < region_cols; col += 16)
+                    tmem_st16(lane_base + reg + col, z);
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
@@ -402,21 +420,21 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 }  // namespace
 
-bool tc_conv_supported(const ConvGeom& g) {
+bool tc_conv_supported(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
-    return make_plan(g, &pl);
+    return make_plan(g, &pl, main_ch > 0);
 }
 
-size_t tc_conv_workspace_bytes(const ConvGeom& g) {
+size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
-    if (!make_plan(g, &pl)) return 0;
+    if (!make_plan(g, &pl, main_ch > 0)) return 0;
     return static_cast<size_t>(pl.kgroups) * static_cast<size_t>(g.in_ch) * pl.b_chan_bytes;
 }
 
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g, void* workspace,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, int64_t main_ch) {
     Plan pl;
-    if (!make_plan(g, &pl)) return cudaErrorNotSupported;
+    if (!make_plan(g, &pl, main_ch > 0)) return cudaErrorNotSupported;
     auto encode = get_encode_fn();
     if (!encode) return cudaErrorNotSupported;
     uint16_t* img = static_cast<uint16_t*>(workspace);
@@ -450,6 +468,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     kp.tiles_per_item = ceil_div(g.out_w, kTileQ);
     kp.total_tiles = g.n * kp.tiles_per_item;
     kp.taps = static_cast<int>(g.taps);
+    kp.main_ch = main_ch > 0 ? main_ch : g.in_ch;
     kp.pl = pl;
     kp.out = out;
     const int grid = static_cast<int>(std::min<int64_t>(num_sms(), kp.total_tiles));

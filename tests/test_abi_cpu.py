@@ -73,9 +73,15 @@ def test_strict_bf16_odd_dims_mirror_reference():
 
 def test_algo_selection_host_side():
     a = C.c_int()
-    # FP32 precision runs the direct kernels
+    # FP32 precision at d=8 runs the split-BF16 tensor path, elsewhere the direct kernels
     assert L.lib().c1d_selected_algo(C.byref(_desc(c=15, k=15, s=51, d=8, w_in=60400)), 0, C.byref(a)) == L.OK
+    assert a.value == L.ALGO_BF16X3
+    assert L.lib().c1d_selected_algo(C.byref(_desc(c=15, k=15, s=51, d=3, w_in=60150)), 0, C.byref(a)) == L.OK
     assert a.value == L.ALGO_DIRECT
+    # BF16 precision at d=8 runs tcgen05
+    assert L.lib().c1d_selected_algo(C.byref(_desc(c=64, k=64, s=51, d=8, w_in=60400, precision=1)), 2,
+                                     C.byref(a)) == L.OK
+    assert a.value == L.ALGO_TCGEN05
     # forced direct is always allowed
     assert L.lib().c1d_selected_algo(C.byref(_desc(precision=1, algo=L.ALGO_DIRECT)), 2, C.byref(a)) == L.OK
     assert a.value == L.ALGO_DIRECT

@@ -66,6 +66,7 @@ def _cases(golden):
 
 @pytest.mark.parametrize("algo", ["direct", "auto"])
 def test_golden_fp32(golden, algo):
+    """FP32 precision: the direct FFMA kernels and AUTO (split-BF16 tensor path where d=8)."""
     for i, (n, c, k, s, d, q) in _cases(golden):
         x, w, dy = golden[f"c{i}_x"], golden[f"c{i}_w"], golden[f"c{i}_dy"]
         got = run_passes(x, w, dy, d, cv.Precision.Fp32, algo)
