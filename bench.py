@@ -17,6 +17,11 @@ Multi-GPU (torchrun, one rank per GPU): every rank runs the full per-GPU batch (
 and the dW of all ranks is summed with one NCCL all-reduce per step (the data-parallel exchange).
 
 `--impl reference` runs only the reference CPU path (rank 0) and prints its line.
+
+`--workload network` measures BASELINE config 5 instead: the residual 1D CNN training step
+(input layer 1->15, 5 residual blocks x 3 convs C=K=15 S=51 d=8, two 1-tap heads, MSE+BCE loss,
+SGD) at global batch 64 split across the ranks (64/N items per GPU, one NCCL all-reduce of the
+173,162-float gradient bucket per step). value = conv FLOP/s of the whole job (3 passes per layer).
 """
 from __future__ import annotations
 
@@ -345,6 +350,116 @@ def main_arm(args):
     return 0
 
 
+def network_arm(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2104_08002_b200 import conv as cv
+    from paper_2104_08002_b200.network import ResidualNet, train_step
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    global_batch, width = 64, 60000
+    if global_batch % world:
+        raise SystemExit("global batch 64 must divide by the GPU count")
+    per = global_batch // world
+    net = ResidualNet(blocks=5, convs_per_block=3, hidden=15, taps=51, dilation=8,
+                      precision=cv.Precision.Bf16, seed=1, device=dev)
+    pad = net.pad()
+    g = torch.Generator(device=dev).manual_seed(20260822 + rank)
+    x = torch.poisson(torch.full((per, 1, width + 2 * pad), 2.0, device=dev), generator=g)
+    target = torch.poisson(torch.full((per, 1, width), 2.0, device=dev), generator=g)
+    labels = (torch.rand((per, 1, width), device=dev, generator=g) < 0.1).float()
+    stream = torch.cuda.current_stream(dev)
+    from paper_2104_08002_b200 import _lib as L
+
+    lib = L.lib()
+
+    def step():
+        loss = train_step(net, x, target, labels)
+        net.sgd_step(1e-3)
+        return loss
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.c1d_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        loss = step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = lib.c1d_launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = t.item()
+    flops_job = net.conv_flops(global_batch, width)
+    value = flops_job / (ms * 1e-3) / 1e12
+    # e2e: H2D of this rank's batch (pinned) + D2H of the loss each step
+    hx, ht, hl = (torch.empty(a.shape, pin_memory=True) for a in (x, target, labels))
+    hx.copy_(x)
+    ht.copy_(target)
+    hl.copy_(labels)
+    hloss = torch.empty((), dtype=torch.float64, pin_memory=True)
+
+    def step_e2e():
+        x.copy_(hx, non_blocking=True)
+        target.copy_(ht, non_blocking=True)
+        labels.copy_(hl, non_blocking=True)
+        hloss.copy_(step(), non_blocking=True)
+
+    step_e2e()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n_e2e = max(1, min(args.steps, 5))
+    f0.record(stream)
+    for _ in range(n_e2e):
+        step_e2e()
+    f1.record(stream)
+    torch.cuda.synchronize()
+    te = torch.tensor([f0.elapsed_time(f1) / n_e2e], device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": METRIC + " (config-5 network step)", "value": value, "unit": "TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic Poisson(2) inputs/targets, Bernoulli(0.1) labels, seeded init",
+            "config": {"workload": "BASELINE config 5: residual 1D CNN training step (input 1->15, 5 blocks x 3 "
+                                   "convs C=K=15 S=51 d=8 same-pad ReLU skip, 2 heads S=1), global batch 64, "
+                                   "width 60000 (+200 pad/side), MSE+BCE, SGD",
+                       "global_batch": global_batch, "per_gpu_batch": per, "width": width,
+                       "parallelism": f"dp{world} (NCCL all-reduce of one 173,162-float gradient bucket)",
+                       "flops_per_step": flops_job, "params": net.num_parameters()},
+            "steps_per_s": 1e3 / ms, "loss": float(loss),
+            "e2e": {"value": flops_job / (te.item() * 1e-3) / 1e12, "unit": "TFLOP/s",
+                    "h2d_bytes_per_step": (hx.numel() + ht.numel() + hl.numel()) * 4, "d2h_bytes_per_step": 8,
+                    "ms_per_step": te.item()},
+            "gpu_launches": int(launches), "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -352,9 +467,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="layer", choices=["layer", "network"])
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)
+    if args.workload == "network":
+        return network_arm(args)
     return main_arm(args)
 
 

@@ -164,6 +164,7 @@ static int64_t wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t q) {
 }
 
 size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t q) {
+    if (k * c * s <= 16) return sizeof(float) * static_cast<size_t>(592 * k * c * s);
     return sizeof(float) * static_cast<size_t>(wgrad_splits(n, c, k, q) * k * c * s);
 }
 
@@ -234,9 +235,73 @@ __global__ void reduce_splits_kernel(const float* __restrict__ part, float* __re
     }
 }
 
+// Tiny gradients (K*C*S <= 16, e.g. the 1-filter, 1-tap heads of the config-5 network): each
+// output is a dot product over all N*Q columns. Threads stride over columns (coalesced), keep all
+// outputs in registers, and every block writes one partial per output; a fixed-order pass sums
+// the blocks (deterministic).
+constexpr int kSmallOut = 16;
+constexpr int kSmallBlocks = 592;  // 4 waves of 148 SMs
+
+template <typename TIn>
+__global__ void __launch_bounds__(256) small_wgrad_kernel(const TIn* __restrict__ x, const TIn* __restrict__ dy,
+                                                          float* __restrict__ part, int64_t N, int64_t C, int64_t K,
+                                                          int64_t S, int64_t D, int64_t Q, int round_in) {
+    const int O = static_cast<int>(K * C * S);
+    const int64_t W = Q + (S - 1) * D;
+    float acc[kSmallOut];
+#pragma unroll
+    for (int o = 0; o < kSmallOut; ++o) acc[o] = 0.0f;
+    const int64_t total = N * Q;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t n = e / Q, qq = e % Q;
+#pragma unroll
+        for (int o = 0; o < kSmallOut; ++o) {
+            if (o < O) {
+                const int64_t ss = o % S, cc = (o / S) % C, kk = o / (S * C);
+                const float g = load_as_float(dy, (n * K + kk) * Q + qq, round_in != 0);
+                const float xv = load_as_float(x, (n * C + cc) * W + qq + ss * D, round_in != 0);
+                acc[o] = fmaf(xv, g, acc[o]);
+            }
+        }
+    }
+    __shared__ float red[kSmallOut][8];
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#pragma unroll
+    for (int o = 0; o < kSmallOut; ++o) {
+        float v = acc[o];
+        for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+        if (lane == 0) red[o][warp] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < O) {
+        float v = 0.0f;
+        for (int w = 0; w < 8; ++w) v += red[threadIdx.x][w];
+        part[static_cast<int64_t>(blockIdx.x) * O + threadIdx.x] = v;
+    }
+}
+
 cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, bool round_in, float* dw_kcs,
                                 float* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d,
                                 int64_t q, cudaStream_t stream) {
+    if (k * c * s <= kSmallOut) {
+        if (in_dtype == 0)
+            small_wgrad_kernel<float><<<kSmallBlocks, 256, 0, stream>>>(static_cast<const float*>(x),
+                                                                      static_cast<const float*>(dy), workspace, n, c,
+                                                                      k, s, d, q, round_in ? 1 : 0);
+        else
+            small_wgrad_kernel<uint16_t><<<kSmallBlocks, 256, 0, stream>>>(static_cast<const uint16_t*>(x),
+                                                                         static_cast<const uint16_t*>(dy), workspace,
+                                                                         n, c, k, s, d, q, 0);
+        note_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        // part is [block][o] with o in KCS order; sum blocks in ascending order
+        const int64_t count = k * c * s;
+        // reuse reduce_splits_kernel: it expects part[split * count + e]
+        reduce_splits_kernel<<<1, 32, 0, stream>>>(workspace, dw_kcs, count, kSmallBlocks);
+        note_launch();
+        return cudaGetLastError();
+    }
     const int64_t splits = wgrad_splits(n, c, k, q);
     const int64_t span = kWQ + (s - 1) * d;
     const size_t smem = sizeof(float) * static_cast<size_t>(kWT * span + kWT * kWQ);
