@@ -8,7 +8,7 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libc1d.so")
+LIB_PATH = os.environ.get("C1D_LIB_PATH") or os.path.join(HERE, "libc1d.so")  # override: dev A/B only
 HEADER_PATH = os.path.join(ROOT, "include", "c1d.h")
 
 # status codes (c1d_status)

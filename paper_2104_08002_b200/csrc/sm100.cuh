@@ -230,6 +230,19 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar_saddr, uint32
                  : "memory");
 }
 
+// ---- 16-byte LDGSTS copies (LSU path; completion by commit/wait groups) --------------
+// Copies 16 bytes global -> shared, or writes 16 zero bytes when !valid (src-size 0).
+__device__ __forceinline__ void cp_async16_zfill(uint32_t dst_saddr, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_saddr), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int kPending>
+__device__ __forceinline__ void cp_async_wait_group() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(kPending) : "memory");
+}
+
 // ---- bulk copies (TMA engine) --------------------------------------------------
 // 1-D bulk copy global -> shared, completes `bytes` of tx on the mbarrier.
 __device__ __forceinline__ void bulk_g2s(uint32_t dst_saddr, const void* src, uint32_t bytes,

@@ -35,6 +35,8 @@ using namespace sm100;
 constexpr int kThreads = 256;
 constexpr int kMaxStages = 4;
 constexpr uint32_t kTmemCols = 512;
+constexpr int kLoaderThreads = 128;
+constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage  // v3: warps 4-7 load X before running the epilogue
 
 struct WPlan {
     int cp, t, kp;
@@ -322,6 +324,11 @@ struct W2Plan {
     int stages;
     size_t smem_bytes;
     int grid;
+    // X ring (q-chunk-major, chunks of 8 columns x CP channels): `span` chunks of tap overlap
+    // carried between consecutive stages, `kch` new chunks per stage, `xb` mirrored chunks
+    int xb, span, kch, ring;
+    uint32_t chunk_bytes, ring_bytes;
+    int copies;  // accumulator copies per group (power of two)
 };
 
 bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out) {
@@ -343,6 +350,7 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     p.groups_total = static_cast<int>(ceil_div(s, p.taps_per_group));
     p.gpc = std::max(1, static_cast<int>(kTmemCols) / p.n);
     if (p.gpc > 8) p.gpc = 8;
+    if (p.n > static_cast<int>(kTmemCols)) return false;
     if (p.gpc > p.groups_total) p.gpc = p.groups_total;
     p.roles = static_cast<int>(ceil_div(p.groups_total, p.gpc));
     if (p.roles > 64) return false;
@@ -362,25 +370,40 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     }
     p.grid = assigned;
     p.box_bytes = static_cast<uint32_t>(p.kpw * 2 * p.bq);
+    // Accumulator copies: MMAs into one accumulator serialise on a ~128-cycle chain, so when a
+    // K-step's MMAs (gpc x N/2 cycles) are shorter than that, consecutive K-steps rotate over R
+    // copies (summed by the epilogue).
+    p.copies = 1;
+    while (p.copies < 4 && p.gpc * p.n * p.copies < 256 && p.gpc * p.n * p.copies * 2 <= static_cast<int>(kTmemCols))
+        p.copies *= 2;
+    // X lives in a ring: every stage loads only its new chunks; the window's tap span is reused.
+    // Safety (a stage slot is refilled only after that slot's MMAs completed):
+    //   ring >= 2*span + (stages + 1)*kch   (incl. a full window at every item change)
+    // Ring positions [0, xb) are mirrored past the end, xb = the furthest chunk one stage's MMAs
+    // reach beyond the stage's first chunk, so a stage never wraps.
+    p.ks = kW2Ks;
+    p.stage_q = 16 * p.ks;
+    p.kch = 2 * p.ks;
+    p.xb = 2 * (p.ks - 1) + (p.gpc - 1) * p.taps_per_group + p.t + 1;
+    p.chunk_bytes = static_cast<uint32_t>(p.cp * 16);
+    p.span = static_cast<int>(ceil_div(p.gpc * p.taps_per_group + p.t + 1, 4) * 4);
+    p.x_chunks = p.kch + p.span;
+    p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
+    p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
+    p.stage_bytes = p.y_bytes;
     bool ok = false;
-    for (int ks = 16; ks >= 4; ks -= 4) {
-        p.ks = ks;
-        p.stage_q = 16 * ks;
-        if (p.stage_q % p.bq) continue;
-        // X chunks read: stage + tap span of the role's groups (+T-1 rows, +1 K-chunk)
-        p.x_chunks = p.stage_q / 8 + p.gpc * p.taps_per_group + p.t + 1;
-        if (p.x_chunks > 256) continue;
-        p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
-        p.x_bytes = (static_cast<uint32_t>(p.x_chunks * p.cp * 16) + 1023) & ~1023u;
-        p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
-        p.stage_bytes = p.x_bytes + p.y_bytes;
-        p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / p.stage_bytes));
-        if (p.stages < 3) continue;
-        ok = true;
-        break;
+    for (int st = kMaxStages; st >= 3; --st) {
+        p.stages = st;
+        p.ring = static_cast<int>(ceil_div(2 * p.span + (st + 1) * p.kch, 4) * 4);
+        p.ring_bytes = ((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u;
+        if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes <= 200 * 1024) {
+            ok = true;
+            break;
+        }
     }
     if (!ok) return false;
-    p.smem_bytes = static_cast<size_t>(p.stages) * p.stage_bytes + 1024;
+    p.x_bytes = p.ring_bytes;
+    p.smem_bytes = p.ring_bytes + static_cast<size_t>(p.stages) * p.stage_bytes + 1024;
     *out = p;
     return true;
 }
@@ -389,13 +412,43 @@ struct W2Params {
     int64_t n_items, c, k, s, q, w_in;
     int64_t steps_per_item, total_steps;
     W2Plan pl;
+    const uint16_t* x;  // [n][c][w_in] bf16
     float* part;        // [cta][k][c][s]
     unsigned long long* prof;
 };
 
+// One full stage of MMAs, straight-line: K-step ks (copy (k0 + ks) mod R) x G tap groups.
+template <int G>
+__device__ __forceinline__ void w2_issue_stage(uint32_t tmem, uint64_t a_st, uint64_t b_st, uint32_t idesc,
+                                               uint32_t a_ks, uint32_t a_g, const uint32_t (&boff)[kW2Ks],
+                                               uint32_t copy_stride, uint32_t cmask, int n, int k0) {
+#pragma unroll
+    for (int ks = 0; ks < kW2Ks; ++ks) {
+        const uint64_t b = desc_advance(b_st, boff[ks]);
+        const uint32_t d0 = tmem + (static_cast<uint32_t>(k0 + ks) & cmask) * copy_stride;
+#pragma unroll
+        for (int g = 0; g < G; ++g)
+            mma_bf16_ss(d0 + static_cast<uint32_t>(g * n), desc_advance(a_st, ks * a_ks + g * a_g), b, idesc, 1u);
+    }
+}
+// Partial / first stages and large group counts: same MMAs, runtime bounds, first-use flags.
+__device__ __forceinline__ void w2_issue_generic(uint32_t tmem, uint64_t a_st, uint64_t b_st, uint32_t idesc,
+                                                 uint32_t a_ks, uint32_t a_g, const uint32_t (&boff)[kW2Ks],
+                                                 uint32_t copy_stride, uint32_t cmask, int n, int k0, int nks,
+                                                 int g_count, int copies) {
+#pragma unroll 1
+    for (int ks = 0; ks < nks; ++ks) {
+        const uint64_t b = desc_advance(b_st, boff[ks]);
+        const uint32_t d0 = tmem + (static_cast<uint32_t>(k0 + ks) & cmask) * copy_stride;
+        const uint32_t acc = (k0 + ks) >= copies ? 1u : 0u;
+#pragma unroll 1
+        for (int g = 0; g < g_count; ++g)
+            mma_bf16_ss(d0 + static_cast<uint32_t>(g * n), desc_advance(a_st, ks * a_ks + g * a_g), b, idesc, acc);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_wgrad2_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
-                     const W2Params p) {
+    tc_wgrad2_kernel(const __grid_constant__ CUtensorMap ymap, const W2Params p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
     __shared__ uint64_t acc_done;
@@ -415,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < pl.stages; ++s) {
-            mbar_init(&full[s], 1);
+            mbar_init(&full[s], 1 + kLoaderThreads);  // dY TMA (tx bytes) + every X loader thread
             mbar_init(&empty[s], 1);
         }
         mbar_init(&acc_done, 1);
@@ -430,7 +483,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {
-            prefetch_tmap(&xmap);
             prefetch_tmap(&ymap);
             long long tw_sum = 0;
             const long long tb = clock64();
@@ -446,18 +498,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     tw_sum += clock64() - tw;
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.x_chunks * pl.cp * 16) +
-                                                  static_cast<uint32_t>(pl.nbox) * pl.box_bytes);
-                    uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
-                    // X window, q-chunk-major: 4-D box (8 columns, CP channels, x_chunks chunks, 1 item)
-                    asm volatile(
-                        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-                        "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(sbase)),
-                        "l"(&xmap), "r"(0), "r"(0), "r"(static_cast<int32_t>(q0 / 8 + tap0)),
-                        "r"(static_cast<int32_t>(item)), "r"(fb)
-                        : "memory");
+                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.nbox) * pl.box_bytes);
+                    uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
                     for (int b = 0; b < pl.nbox; ++b)
-                        tma_load_3d(smem_u32(sbase + pl.x_bytes + static_cast<uint32_t>(b) * pl.box_bytes), &ymap,
+                        tma_load_3d(smem_u32(sbase + static_cast<uint32_t>(b) * pl.box_bytes), &ymap,
                                     static_cast<int32_t>(q0 - back + static_cast<int64_t>(b) * pl.bq), 0,
                                     static_cast<int32_t>(item), fb);
                     if (++stage == pl.stages) {
@@ -482,50 +526,73 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long tb = clock64();
         int stage = 0;
         uint32_t phase = 0;
-        bool first = true;
+        // per-K-step B (dY) offsets: Bq = 8 -> a K-step spans two boxes; else 16/Bq K-steps per box
+        uint32_t boff[kW2Ks];
+#pragma unroll
+        for (int ks = 0; ks < kW2Ks; ++ks) {
+            if (pl.bq == 8) {
+                boff[ks] = static_cast<uint32_t>(ks) * 2u * pl.box_bytes;
+            } else {
+                const int per_box = pl.bq / 16;
+                boff[ks] = static_cast<uint32_t>(ks / per_box) * pl.box_bytes + static_cast<uint32_t>(ks % per_box) * 32u;
+            }
+        }
+        const uint32_t a_ks = 2u * pl.chunk_bytes;
+        const uint32_t a_g = static_cast<uint32_t>(pl.taps_per_group) * pl.chunk_bytes;
+        const uint32_t copy_stride = static_cast<uint32_t>(pl.gpc * pl.n);
+        const uint32_t cmask = static_cast<uint32_t>(pl.copies - 1);
+        int kdone = 0;  // K-steps issued so far (accumulator copy rotation)
+        int v_pos = 0, seg_pos = 0;  // ring position of the next chunk / of the segment's first chunk
+        int64_t seg_lo = 0;
         int64_t cur = kb;
         while (cur < ke) {
             const int64_t item = cur / p.steps_per_item;
             const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
+            bool seg_first = true;
             for (int64_t st = cur; st < seg_end; st += pl.ks) {
                 const int nks = static_cast<int>(imin(pl.ks, seg_end - st));
+                const int64_t q0 = (st - item * p.steps_per_item) * 16;
+                const int64_t lo = q0 / 8 + tap0;
+                if (seg_first) {  // mirror the loaders' ring bookkeeping
+                    seg_pos = v_pos;
+                    seg_lo = lo;
+                    v_pos += pl.span + pl.kch;
+                    seg_first = false;
+                } else {
+                    v_pos += pl.kch;
+                }
+                if (v_pos >= pl.ring) v_pos -= pl.ring;
                 const long long tf = clock64();
                 mbar_wait(smem_u32(&full[stage]), phase);
                 tf_sum += clock64() - tf;
                 tc_fence_after();
-                uint8_t* sbase = smem + static_cast<size_t>(stage) * pl.stage_bytes;
-                const uint64_t ax0 = make_smem_desc(smem_u32(sbase), static_cast<uint32_t>(pl.cp * 16), 128, kLayoutNone);
-                const uint64_t by0 = make_smem_desc(smem_u32(sbase + pl.x_bytes), b_lbo, b_sbo, pl.swz);
-                // One elected lane issues the whole stage; descriptors advance incrementally
-                // (no divisions, no per-MMA reconvergence).
+                uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
+                // A (X) of K-step ks, group g starts at chunk lo + 2ks + g*tpg: ring position
+                int stage_pos = seg_pos + static_cast<int>((lo - seg_lo) % pl.ring);
+                if (stage_pos >= pl.ring) stage_pos -= pl.ring;
+                const uint64_t ax0 = make_smem_desc(smem_u32(smem), static_cast<uint32_t>(pl.cp * 16), 128, kLayoutNone);
+                const uint64_t by0 = make_smem_desc(smem_u32(sbase), b_lbo, b_sbo, pl.swz);
+                // One elected lane issues the whole stage. The ring mirror keeps every address of
+                // the stage wrap-free, so a full stage is a straight-line run of MMAs.
                 if (elect_one()) {
-                    uint64_t adesc = ax0;
-                    const uint32_t a_step = static_cast<uint32_t>(2 * pl.cp * 16);          // one K-step
-                    const uint32_t g_step = static_cast<uint32_t>(pl.taps_per_group * pl.cp * 16);
-                    const int per_box = pl.bq / 16;                                         // K-steps per dY box
-                    uint64_t bbox = by0;
-                    int inbox = 0;
-                    for (int ks = 0; ks < nks; ++ks) {
-                        const uint64_t bdesc = desc_advance(bbox, static_cast<uint32_t>(inbox * 32));
-                        uint64_t ag = adesc;
-                        uint32_t dcol = tmem;
-                        for (int g = 0; g < g_count; ++g) {
-                            mma_bf16_ss(dcol, ag, bdesc, idesc, first ? 0u : 1u);
-                            ag = desc_advance(ag, g_step);
-                            dcol += static_cast<uint32_t>(pl.n);
+                    const uint64_t a_st = desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
+                    if (nks == kW2Ks && kdone >= pl.copies) {
+                        switch (g_count) {
+                            case 1: w2_issue_stage<1>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
+                            case 2: w2_issue_stage<2>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
+                            case 3: w2_issue_stage<3>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
+                            case 4: w2_issue_stage<4>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
+                            default:
+                                w2_issue_generic(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone,
+                                                 kW2Ks, g_count, pl.copies);
                         }
-                        first = false;
-                        adesc = desc_advance(adesc, a_step);
-                        if (per_box == 0) {  // Bq = 8: a K-step spans 16/Bq boxes
-                            bbox = desc_advance(bbox, pl.box_bytes * static_cast<uint32_t>(16 / pl.bq));
-                        } else if (++inbox == per_box) {
-                            inbox = 0;
-                            bbox = desc_advance(bbox, pl.box_bytes);
-                        }
+                    } else {
+                        w2_issue_generic(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone, nks,
+                                         g_count, pl.copies);
                     }
                 }
+                kdone += nks;
                 __syncwarp();
-                first = false;
                 if (elect_one()) mma_commit(smem_u32(&empty[stage]));
                 __syncwarp();
                 if (++stage == pl.stages) {
@@ -542,6 +609,67 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.prof[blockIdx.x * 8 + 4] = clock64() - tb;
         }
     } else if (warp >= 4) {
+        // ---- X loaders (warps 4-7 until the accumulators are ready): 16-byte cp.async pieces
+        // straight from the [n][c][w] rows into the q-chunk-major ring. A warp moves 8 channels x
+        // 4 chunks: 64 contiguous bytes per channel row in global, one 128-byte smem row per chunk.
+        // (TMA moves 16-byte-wide boxes at ~16 B/clk/SM, below what the MMAs consume.)
+        {
+            const int lt = threadIdx.x - 128;
+            const int c_lo = lt & 7, j_lo = (lt >> 3) & 3;
+            const int cgroups = pl.cp / 8;
+            const uint32_t ring_s = smem_u32(smem);
+            int stage = 0, pending = -1;
+            uint32_t phase = 0;
+            int v_pos = 0;  // ring position of the next chunk loaded
+            int64_t cur = kb;
+            while (cur < ke) {
+                const int64_t item = cur / p.steps_per_item;
+                const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
+                const uint16_t* xi = p.x + item * p.c * p.w_in;
+                bool seg_first = true;
+                int64_t next_chunk = 0;
+                for (int64_t st = cur; st < seg_end; st += pl.ks) {
+                    const int64_t q0 = (st - item * p.steps_per_item) * 16;
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    const int64_t first_chunk = seg_first ? q0 / 8 + tap0 : next_chunk;
+                    const int nchunks = seg_first ? pl.span + pl.kch : pl.kch;
+                    seg_first = false;
+                    next_chunk = first_chunk + nchunks;
+                    for (int e = lt; e < nchunks * pl.cp; e += kLoaderThreads) {
+                        const int r = e >> 5;
+                        const int c = (r % cgroups) * 8 + c_lo;
+                        const int jl = (r / cgroups) * 4 + j_lo;
+                        const int64_t j = first_chunk + jl;
+                        int pos = v_pos + jl;
+                        if (pos >= pl.ring) pos -= pl.ring;
+                        const bool valid = c < p.c && j * 8 < p.w_in;
+                        const uint16_t* src = valid ? xi + static_cast<int64_t>(c) * p.w_in + j * 8 : p.x;
+                        const uint32_t dst = ring_s + static_cast<uint32_t>(pos) * pl.chunk_bytes + static_cast<uint32_t>(c) * 16u;
+                        cp_async16_zfill(dst, src, valid);
+                        if (pos < pl.xb) cp_async16_zfill(dst + static_cast<uint32_t>(pl.ring) * pl.chunk_bytes, src, valid);
+                    }
+                    cp_async_commit();
+                    v_pos += nchunks;
+                    if (v_pos >= pl.ring) v_pos -= pl.ring;
+                    if (pending >= 0) {  // the previous stage's pieces have landed: publish them
+                        cp_async_wait_group<1>();
+                        fence_async_smem();
+                        mbar_arrive(smem_u32(&full[pending]));
+                    }
+                    pending = stage;
+                    if (++stage == pl.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                cur = seg_end;
+            }
+            if (pending >= 0) {
+                cp_async_wait_group<0>();
+                fence_async_smem();
+                mbar_arrive(smem_u32(&full[pending]));
+            }
+        }
         // ---- epilogue: D rows (t, c) x columns (p', k) -> partial[cta][k][c][tap]
         const int quarter = warp - 4;
         const int row = quarter * 32 + lane;
@@ -557,8 +685,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int cb = 0; cb < pl.n; cb += 16) {
                 uint32_t v[16];
                 if (have) {
-                    tmem_ld16(tmem + (static_cast<uint32_t>(quarter * 32) << 16) + static_cast<uint32_t>(g * pl.n + cb), v);
+                    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+                    tmem_ld16(lane_base + static_cast<uint32_t>(g * pl.n + cb), v);
                     tmem_ld_wait();
+                    // copies this CTA actually wrote (a CTA with fewer K-steps than copies leaves
+                    // the rest uninitialised); fixed order: copy 0 + 1 + ...
+                    const int used = static_cast<int>(imin(pl.copies, ke - kb));
+                    for (int r = 1; r < used; ++r) {
+                        uint32_t u[16];
+                        tmem_ld16(lane_base + static_cast<uint32_t>((r * pl.gpc + g) * pl.n + cb), u);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(u[j]));
+                    }
                 } else {
 #pragma unroll
                     for (int j = 0; j < 16; ++j) v[j] = 0;
@@ -615,18 +754,8 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
     auto encode = encode_fn();
     if (!encode) return cudaErrorNotSupported;
     const int64_t w_in = q + d * (s - 1);
-    CUtensorMap xmap, ymap;
-    {
-        const cuuint64_t dims[4] = {8, static_cast<cuuint64_t>(c), static_cast<cuuint64_t>(w_in / 8),
-                                    static_cast<cuuint64_t>(n)};
-        const cuuint64_t strides[3] = {static_cast<cuuint64_t>(w_in) * 2, 16, static_cast<cuuint64_t>(c * w_in) * 2};
-        const cuuint32_t box[4] = {8, static_cast<cuuint32_t>(pl.cp), static_cast<cuuint32_t>(pl.x_chunks), 1};
-        const cuuint32_t estr[4] = {1, 1, 1, 1};
-        if (encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(x_bf16), dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-            return cudaErrorInvalidValue;
-    }
+    CUtensorMap ymap;
+    if ((reinterpret_cast<uintptr_t>(x_bf16) & 15u) || (w_in % 8)) return cudaErrorInvalidValue;
     {
         const cuuint64_t dims[3] = {static_cast<cuuint64_t>(q), static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(q) * 2, static_cast<cuuint64_t>(k * q) * 2};
@@ -655,13 +784,14 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
     wp.steps_per_item = ceil_div(q + static_cast<int64_t>(pl.p - 1) * pl.bq, 16);
     wp.total_steps = n * wp.steps_per_item;
     wp.pl = pl;
+    wp.x = x_bf16;
     wp.part = static_cast<float*>(workspace);
     static const bool profile = getenv("C1D_PROFILE") != nullptr;
     if (profile) {
         cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * pl.grid);
         cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * pl.grid);
     }
-    tc_wgrad2_kernel<<<pl.grid, kThreads, pl.smem_bytes, stream>>>(xmap, ymap, wp);
+    tc_wgrad2_kernel<<<pl.grid, kThreads, pl.smem_bytes, stream>>>(ymap, wp);
     note_launch();
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -671,9 +801,9 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         double acc[8] = {0};
         for (int bb = 0; bb < pl.grid; ++bb)
             for (int i2 = 0; i2 < 8; ++i2) acc[i2] += static_cast<double>(h[bb * 8 + i2]) / pl.grid;
-        fprintf(stderr, "[tc_wgrad3 prof] T=%d P=%d N=%d gpc=%d roles=%d ks=%d stages=%d x_chunks=%d nbox=%d | "
+        fprintf(stderr, "[tc_wgrad3 prof] T=%d P=%d N=%d gpc=%d roles=%d ks=%d stages=%d span=%d ring=%d nbox=%d copies=%d xb=%d | "
                 "producer wait_empty %.0f / total %.0f | mma wait_full %.0f total %.0f\n",
-                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.x_chunks, pl.nbox, acc[0], acc[1], acc[2], acc[4]);
+                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.span, pl.ring, pl.nbox, pl.copies, pl.xb, acc[0], acc[1], acc[2], acc[4]);
         for (int r = 0; r < pl.roles; ++r) {
             unsigned long long mx = 0, wf = 0;
             for (int bb = pl.role_cta_begin[r]; bb < pl.role_cta_begin[r + 1]; ++bb) {

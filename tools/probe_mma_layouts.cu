@@ -1,0 +1,128 @@
+// probe_mma_layouts.cu — tcgen05.mma (kind::f16, M=128, cta_group::1) issue throughput for the
+// smem operand layouts the conv kernels use (dev tooling, not product code). Operand contents are
+// zeros: only the cycles per MMA are measured, on all SMs at once (one CTA per SM).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "../paper_2104_08002_b200/csrc/sm100.cuh"
+
+using namespace c1d::sm100;
+
+#define CK(x)                                                           \
+    do {                                                                \
+        cudaError_t e = (x);                                            \
+        if (e != cudaSuccess) {                                         \
+            printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); \
+            exit(1);                                                    \
+        }                                                               \
+    } while (0)
+
+struct Cfg {
+    const char* name;
+    uint32_t a_lbo, a_sbo, a_layout, a_mn;  // A descriptor
+    uint32_t b_lbo, b_sbo, b_layout;        // B descriptor (K-major)
+    uint32_t n;
+    uint32_t a_step, b_step;  // start-address advance per K-step (bytes), wraps in a 64 KB window
+    int nacc;                 // accumulators per K-step (different A start, same B)
+    uint32_t g_step;          // A start offset between accumulators
+    int unroll;               // issue 8 K-steps straight-line (no address wrap)
+};
+
+__global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long* cyc) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_s;
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x / 32 == 0) tmem_alloc<512>(&tmem_s);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x / 32 == 0 && elect_one()) {
+        const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 80 * 1024);
+        const uint32_t idesc = make_idesc(128, c.n, kFmtBF16, c.a_mn, 0);
+        const uint64_t a0 = make_smem_desc(sa, c.a_lbo, c.a_sbo, c.a_layout);
+        const uint64_t b0 = make_smem_desc(sb, c.b_lbo, c.b_sbo, c.b_layout);
+        const long long t0 = clock64();
+        uint32_t ao = 0, bo = 0;
+        if (c.unroll) {
+            for (int k = 0; k < ksteps; k += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll 1
+                    for (int g = 0; g < c.nacc; ++g)
+                        mma_bf16_ss(tmem_s + g * c.n, desc_advance(a0, u * c.a_step + g * c.g_step),
+                                    desc_advance(b0, u * c.b_step), idesc, 1u);
+            }
+        } else
+        for (int k = 0; k < ksteps; ++k) {
+#pragma unroll 1
+            for (int g = 0; g < c.nacc; ++g)
+                mma_bf16_ss(tmem_s + g * c.n, desc_advance(a0, ao + g * c.g_step), desc_advance(b0, bo), idesc,
+                            k > 0 ? 1u : 0u);
+            ao += c.a_step;
+            if (ao >= 32768) ao -= 32768;
+            bo += c.b_step;
+            if (bo >= 32768) bo -= 32768;
+        }
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        cyc[blockIdx.x] = clock64() - t0;
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x / 32 == 0) tmem_dealloc<512>(tmem_s);
+}
+
+int main() {
+    const Cfg cfgs[] = {
+        // wgrad v3, CP=64: A K-major none (core matrices: 8 channels x 16 B; K-chunks 1 KB apart)
+        {"wgrad A Kmaj none LBO1024 SBO128 | B SW32 (N=256)", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256,
+         2048, 2048, 2, 8192},
+        {"same, 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 1, 0},
+        {"wgrad A | B SW128 (N=256)", 1024, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 256, 2048, 32, 2, 8192},
+        {"A Kmaj none LBO128 SBO256 | B SW32", 128, 256, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 2, 8192},
+        {"A SW128 | B SW128 (GEMM)", 16, 1024, kLayoutSw128, 0, 16, 1024, kLayoutSw128, 256, 32, 32, 2, 16384},
+        {"A SW32 | B SW32", 16, 256, kLayoutSw32, 0, 16, 256, kLayoutSw32, 256, 4096, 2048, 2, 8192},
+        {"fwd row-tap A MN none LBO128 SBO16 | B Kmaj none", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512,
+         8192, 1, 0},
+        {"UNROLLED same, 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 1, 0, 1},
+        {"UNROLLED wgrad 2 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 2, 8192, 1},
+        {"UNROLLED N=112 1 acc", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 1},
+        {"UNROLLED N=128 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 128, 2048, 2048, 1, 0, 1},
+        {"UNROLLED N=64 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 64, 2048, 2048, 1, 0, 1},
+        {"wgrad A | B SW32, 4 acc N=128", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 128, 2048, 2048, 4, 8192},
+        {"GEMM SW128, 1 acc N=256", 16, 1024, kLayoutSw128, 0, 16, 1024, kLayoutSw128, 256, 32, 32, 1, 0},
+        {"wgrad A | B SW32 N=128", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 128, 2048, 2048, 2, 8192},
+        {"wgrad A | B SW32 N=112", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 112, 2048, 2048, 1, 8192},
+        {"A Kmaj none LBO256 SBO128 (CP=16) | B SW128 N=112", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112,
+         512, 32, 1, 8192},
+    };
+    long long* cyc;
+    CK(cudaMalloc(&cyc, 148 * sizeof(long long)));
+    CK(cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024));
+    const int ksteps = 4096;
+    for (const Cfg& c : cfgs) {
+        for (int grid : {1, 148}) {
+            mma_probe<<<grid, 128, 161 * 1024>>>(c, ksteps, cyc);
+            CK(cudaDeviceSynchronize());
+            long long h[148];
+            CK(cudaMemcpy(h, cyc, grid * sizeof(long long), cudaMemcpyDeviceToHost));
+            long long mx = 0;
+            for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
+            const double per = static_cast<double>(mx) / (ksteps * c.nacc);
+            printf("%-52s grid %3d: %6.1f cyc/MMA (ideal %5.1f)\n", c.name, grid, per, 128.0 * c.n / 256.0);
+        }
+    }
+    return 0;
+}
