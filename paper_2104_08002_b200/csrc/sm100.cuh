@@ -238,6 +238,11 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst_saddr, const void*
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// Arrive on an mbarrier (counted as one of its expected arrivals) once all of this thread's
+// previously issued cp.async copies have landed.
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint32_t bar_saddr) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar_saddr) : "memory");
+}
 template <int kPending>
 __device__ __forceinline__ void cp_async_wait_group() {
     asm volatile("cp.async.wait_group %0;" ::"n"(kPending) : "memory");

@@ -35,8 +35,10 @@ using namespace sm100;
 constexpr int kThreads = 256;
 constexpr int kMaxStages = 4;
 constexpr uint32_t kTmemCols = 512;
-constexpr int kLoaderThreads = 128;
-constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage  // v3: warps 4-7 load X before running the epilogue
+constexpr int kLoaderThreads = 128;  // v3: warps 2, 3, 6, 7 stream X into the ring
+constexpr int kW2MaxStages = 6;
+constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage
+constexpr uint32_t kW2SmemBudget = 222 * 1024;  // v3 ring + stages (227 KB max per CTA, minus static + alignment)  // v3: warps 4-7 load X before running the epilogue
 
 struct WPlan {
     int cp, t, kp;
@@ -359,8 +361,8 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     int assigned = 0;
     for (int r = 0; r < p.roles; ++r) p.role_groups[r] = std::min(p.gpc, p.groups_total - p.gpc * r);
     p.role_cta_begin[0] = 0;
-    // Every role streams the same X/dY data per K-step (the data path, not the MMA count, bounds
-    // the per-step time), so the CTAs are split evenly across roles.
+    // CTAs are split evenly across roles: every role streams the same X/dY data per K-step, and a
+    // weighted split (fewer CTAs for the 1-group role) measured slower on B200.
     for (int r = 0; r < p.roles; ++r) {
         const int64_t want = static_cast<int64_t>(sms) * (r + 1) / p.roles;
         int end = static_cast<int>(std::max<int64_t>(want, assigned + 1));
@@ -378,7 +380,8 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         p.copies *= 2;
     // X lives in a ring: every stage loads only its new chunks; the window's tap span is reused.
     // Safety (a stage slot is refilled only after that slot's MMAs completed):
-    //   ring >= 2*span + (stages + 1)*kch   (incl. a full window at every item change)
+    //   ring >= 2*span + stages*kch   (the window a stage reads, the stages-1 stages the
+    //   loaders may run ahead, and one extra fresh window when an item boundary falls in there)
     // Ring positions [0, xb) are mirrored past the end, xb = the furthest chunk one stage's MMAs
     // reach beyond the stage's first chunk, so a stage never wraps.
     p.ks = kW2Ks;
@@ -392,11 +395,16 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
     p.stage_bytes = p.y_bytes;
     bool ok = false;
-    for (int st = kMaxStages; st >= 3; --st) {
+    static const int max_stages = [] {  // C1D_W2_STAGES: dev override of the stage cap
+        const char* e = getenv("C1D_W2_STAGES");
+        const int v = e ? atoi(e) : kW2MaxStages;
+        return v >= 3 && v <= kW2MaxStages ? v : kW2MaxStages;
+    }();
+    for (int st = max_stages; st >= 3; --st) {
         p.stages = st;
-        p.ring = static_cast<int>(ceil_div(2 * p.span + (st + 1) * p.kch, 4) * 4);
+        p.ring = static_cast<int>(ceil_div(2 * p.span + st * p.kch, 4) * 4);
         p.ring_bytes = ((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u;
-        if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes <= 200 * 1024) {
+        if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes <= kW2SmemBudget) {
             ok = true;
             break;
         }
@@ -417,40 +425,45 @@ struct W2Params {
     unsigned long long* prof;
 };
 
-// One full stage of MMAs, straight-line: K-step ks (copy (k0 + ks) mod R) x G tap groups.
+// One stage of MMAs: K-step ks (accumulator copy (k0 + ks) mod R) x G tap groups. Descriptors
+// advance by running adds (units of 16 B) so the per-stage prologue stays a handful of uniform
+// instructions; with G >= 2 the tensor pipe hides the per-K-step loop overhead.
+struct W2Issue {
+    uint32_t idesc, a_ks, a_g, b_k, b_box, copy_stride, cmask;
+    int per_box, n, copies;
+};
 template <int G>
-__device__ __forceinline__ void w2_issue_stage(uint32_t tmem, uint64_t a_st, uint64_t b_st, uint32_t idesc,
-                                               uint32_t a_ks, uint32_t a_g, const uint32_t (&boff)[kW2Ks],
-                                               uint32_t copy_stride, uint32_t cmask, int n, int k0) {
-#pragma unroll
-    for (int ks = 0; ks < kW2Ks; ++ks) {
-        const uint64_t b = desc_advance(b_st, boff[ks]);
-        const uint32_t d0 = tmem + (static_cast<uint32_t>(k0 + ks) & cmask) * copy_stride;
-#pragma unroll
-        for (int g = 0; g < G; ++g)
-            mma_bf16_ss(d0 + static_cast<uint32_t>(g * n), desc_advance(a_st, ks * a_ks + g * a_g), b, idesc, 1u);
-    }
-}
-// Partial / first stages and large group counts: same MMAs, runtime bounds, first-use flags.
-__device__ __forceinline__ void w2_issue_generic(uint32_t tmem, uint64_t a_st, uint64_t b_st, uint32_t idesc,
-                                                 uint32_t a_ks, uint32_t a_g, const uint32_t (&boff)[kW2Ks],
-                                                 uint32_t copy_stride, uint32_t cmask, int n, int k0, int nks,
-                                                 int g_count, int copies) {
+__device__ __forceinline__ void w2_issue_stage(const W2Issue& w, uint32_t tmem, uint64_t a, uint64_t b, int k0,
+                                               int nks, int g_count) {
+    int inbox = 0;
 #pragma unroll 1
     for (int ks = 0; ks < nks; ++ks) {
-        const uint64_t b = desc_advance(b_st, boff[ks]);
-        const uint32_t d0 = tmem + (static_cast<uint32_t>(k0 + ks) & cmask) * copy_stride;
-        const uint32_t acc = (k0 + ks) >= copies ? 1u : 0u;
+        const int kk = k0 + ks;
+        const uint32_t d0 = tmem + (static_cast<uint32_t>(kk) & w.cmask) * w.copy_stride;
+        const uint32_t acc = kk >= w.copies ? 1u : 0u;
+        if (G > 0) {
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                mma_bf16_ss(d0 + static_cast<uint32_t>(g * w.n), a + static_cast<uint64_t>(g * w.a_g), b, w.idesc, acc);
+        } else {
 #pragma unroll 1
-        for (int g = 0; g < g_count; ++g)
-            mma_bf16_ss(d0 + static_cast<uint32_t>(g * n), desc_advance(a_st, ks * a_ks + g * a_g), b, idesc, acc);
+            for (int g = 0; g < g_count; ++g)
+                mma_bf16_ss(d0 + static_cast<uint32_t>(g * w.n), a + static_cast<uint64_t>(g * w.a_g), b, w.idesc, acc);
+        }
+        a += w.a_ks;
+        if (++inbox == w.per_box) {
+            inbox = 0;
+            b += w.b_box;
+        } else {
+            b += w.b_k;
+        }
     }
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     tc_wgrad2_kernel(const __grid_constant__ CUtensorMap ymap, const W2Params p) {
     extern __shared__ uint8_t smem_raw[];
-    __shared__ uint64_t full[kMaxStages], empty[kMaxStages];
+    __shared__ uint64_t full[kW2MaxStages], empty[kW2MaxStages];
     __shared__ uint64_t acc_done;
     __shared__ uint32_t tmem_base_s;
 
@@ -526,24 +539,30 @@ __global__ void __launch_bounds__(kThreads, 1)
         const long long tb = clock64();
         int stage = 0;
         uint32_t phase = 0;
-        // per-K-step B (dY) offsets: Bq = 8 -> a K-step spans two boxes; else 16/Bq K-steps per box
-        uint32_t boff[kW2Ks];
-#pragma unroll
-        for (int ks = 0; ks < kW2Ks; ++ks) {
-            if (pl.bq == 8) {
-                boff[ks] = static_cast<uint32_t>(ks) * 2u * pl.box_bytes;
-            } else {
-                const int per_box = pl.bq / 16;
-                boff[ks] = static_cast<uint32_t>(ks / per_box) * pl.box_bytes + static_cast<uint32_t>(ks % per_box) * 32u;
-            }
+        // descriptor steps in units of 16 B. B (dY): Bq = 8 -> a K-step spans two boxes; else
+        // 16/Bq K-steps (32 B each) per box
+        W2Issue wi;
+        wi.idesc = idesc;
+        wi.a_ks = (2u * pl.chunk_bytes) >> 4;
+        wi.a_g = (static_cast<uint32_t>(pl.taps_per_group) * pl.chunk_bytes) >> 4;
+        if (pl.bq == 8) {
+            wi.per_box = 1;
+            wi.b_box = (2u * pl.box_bytes) >> 4;
+            wi.b_k = 0;
+        } else {
+            wi.per_box = pl.bq / 16;
+            wi.b_k = 32u >> 4;
+            wi.b_box = (pl.box_bytes - static_cast<uint32_t>(wi.per_box - 1) * 32u) >> 4;
         }
-        const uint32_t a_ks = 2u * pl.chunk_bytes;
-        const uint32_t a_g = static_cast<uint32_t>(pl.taps_per_group) * pl.chunk_bytes;
-        const uint32_t copy_stride = static_cast<uint32_t>(pl.gpc * pl.n);
-        const uint32_t cmask = static_cast<uint32_t>(pl.copies - 1);
+        wi.copy_stride = static_cast<uint32_t>(pl.gpc * pl.n);
+        wi.cmask = static_cast<uint32_t>(pl.copies - 1);
+        wi.n = pl.n;
+        wi.copies = pl.copies;
         int kdone = 0;  // K-steps issued so far (accumulator copy rotation)
-        int v_pos = 0, seg_pos = 0;  // ring position of the next chunk / of the segment's first chunk
-        int64_t seg_lo = 0;
+        // ring bookkeeping mirrors the loaders': a segment (item) starts a fresh window of
+        // span + kch chunks at v_pos; each later stage appends kch chunks and the window start
+        // moves by kch
+        int v_pos = 0, cur_pos = 0;
         int64_t cur = kb;
         while (cur < ke) {
             const int64_t item = cur / p.steps_per_item;
@@ -551,14 +570,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             bool seg_first = true;
             for (int64_t st = cur; st < seg_end; st += pl.ks) {
                 const int nks = static_cast<int>(imin(pl.ks, seg_end - st));
-                const int64_t q0 = (st - item * p.steps_per_item) * 16;
-                const int64_t lo = q0 / 8 + tap0;
-                if (seg_first) {  // mirror the loaders' ring bookkeeping
-                    seg_pos = v_pos;
-                    seg_lo = lo;
+                if (seg_first) {
+                    cur_pos = v_pos;
                     v_pos += pl.span + pl.kch;
                     seg_first = false;
                 } else {
+                    cur_pos += pl.kch;
+                    if (cur_pos >= pl.ring) cur_pos -= pl.ring;
                     v_pos += pl.kch;
                 }
                 if (v_pos >= pl.ring) v_pos -= pl.ring;
@@ -568,27 +586,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
                 // A (X) of K-step ks, group g starts at chunk lo + 2ks + g*tpg: ring position
-                int stage_pos = seg_pos + static_cast<int>((lo - seg_lo) % pl.ring);
-                if (stage_pos >= pl.ring) stage_pos -= pl.ring;
+                const int stage_pos = cur_pos;  // ring position of chunk `lo`
                 const uint64_t ax0 = make_smem_desc(smem_u32(smem), static_cast<uint32_t>(pl.cp * 16), 128, kLayoutNone);
                 const uint64_t by0 = make_smem_desc(smem_u32(sbase), b_lbo, b_sbo, pl.swz);
                 // One elected lane issues the whole stage. The ring mirror keeps every address of
                 // the stage wrap-free, so a full stage is a straight-line run of MMAs.
                 if (elect_one()) {
                     const uint64_t a_st = desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
-                    if (nks == kW2Ks && kdone >= pl.copies) {
-                        switch (g_count) {
-                            case 1: w2_issue_stage<1>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
-                            case 2: w2_issue_stage<2>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
-                            case 3: w2_issue_stage<3>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
-                            case 4: w2_issue_stage<4>(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone); break;
-                            default:
-                                w2_issue_generic(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone,
-                                                 kW2Ks, g_count, pl.copies);
-                        }
-                    } else {
-                        w2_issue_generic(tmem, a_st, by0, idesc, a_ks, a_g, boff, copy_stride, cmask, pl.n, kdone, nks,
-                                         g_count, pl.copies);
+                    switch (g_count) {
+                        case 1: w2_issue_stage<1>(wi, tmem, a_st, by0, kdone, nks, 1); break;
+                        case 2: w2_issue_stage<2>(wi, tmem, a_st, by0, kdone, nks, 2); break;
+                        case 3: w2_issue_stage<3>(wi, tmem, a_st, by0, kdone, nks, 3); break;
+                        case 4: w2_issue_stage<4>(wi, tmem, a_st, by0, kdone, nks, 4); break;
+                        default: w2_issue_stage<0>(wi, tmem, a_st, by0, kdone, nks, g_count);
                     }
                 }
                 kdone += nks;
@@ -608,68 +618,65 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.prof[blockIdx.x * 8 + 2] = tf_sum;
             p.prof[blockIdx.x * 8 + 4] = clock64() - tb;
         }
-    } else if (warp >= 4) {
-        // ---- X loaders (warps 4-7 until the accumulators are ready): 16-byte cp.async pieces
-        // straight from the [n][c][w] rows into the q-chunk-major ring. A warp moves 8 channels x
-        // 4 chunks: 64 contiguous bytes per channel row in global, one 128-byte smem row per chunk.
-        // (TMA moves 16-byte-wide boxes at ~16 B/clk/SM, below what the MMAs consume.)
-        {
-            const int lt = threadIdx.x - 128;
-            const int c_lo = lt & 7, j_lo = (lt >> 3) & 3;
-            const int cgroups = pl.cp / 8;
-            const uint32_t ring_s = smem_u32(smem);
-            int stage = 0, pending = -1;
-            uint32_t phase = 0;
-            int v_pos = 0;  // ring position of the next chunk loaded
-            int64_t cur = kb;
-            while (cur < ke) {
-                const int64_t item = cur / p.steps_per_item;
-                const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
-                const uint16_t* xi = p.x + item * p.c * p.w_in;
-                bool seg_first = true;
-                int64_t next_chunk = 0;
-                for (int64_t st = cur; st < seg_end; st += pl.ks) {
-                    const int64_t q0 = (st - item * p.steps_per_item) * 16;
-                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-                    const int64_t first_chunk = seg_first ? q0 / 8 + tap0 : next_chunk;
-                    const int nchunks = seg_first ? pl.span + pl.kch : pl.kch;
-                    seg_first = false;
-                    next_chunk = first_chunk + nchunks;
-                    for (int e = lt; e < nchunks * pl.cp; e += kLoaderThreads) {
-                        const int r = e >> 5;
-                        const int c = (r % cgroups) * 8 + c_lo;
-                        const int jl = (r / cgroups) * 4 + j_lo;
-                        const int64_t j = first_chunk + jl;
-                        int pos = v_pos + jl;
-                        if (pos >= pl.ring) pos -= pl.ring;
-                        const bool valid = c < p.c && j * 8 < p.w_in;
-                        const uint16_t* src = valid ? xi + static_cast<int64_t>(c) * p.w_in + j * 8 : p.x;
-                        const uint32_t dst = ring_s + static_cast<uint32_t>(pos) * pl.chunk_bytes + static_cast<uint32_t>(c) * 16u;
-                        cp_async16_zfill(dst, src, valid);
-                        if (pos < pl.xb) cp_async16_zfill(dst + static_cast<uint32_t>(pl.ring) * pl.chunk_bytes, src, valid);
-                    }
-                    cp_async_commit();
-                    v_pos += nchunks;
-                    if (v_pos >= pl.ring) v_pos -= pl.ring;
-                    if (pending >= 0) {  // the previous stage's pieces have landed: publish them
-                        cp_async_wait_group<1>();
-                        fence_async_smem();
-                        mbar_arrive(smem_u32(&full[pending]));
-                    }
-                    pending = stage;
-                    if (++stage == pl.stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
+    }
+    if (warp == 2 || warp == 3 || warp >= 6) {
+        // ---- X loaders (warps 2, 3, 6, 7: the sub-partitions of the TMA and MMA warps stay free
+        // of their issue load): 16-byte cp.async pieces straight from the [n][c][w] rows into the
+        // q-chunk-major ring. One warp instruction moves 8 channels x 4 chunks: 64 contiguous bytes
+        // per channel row in global, one 128-byte smem row per chunk. (TMA moves 16-byte-wide boxes
+        // at ~16 B/clk/SM, below what the MMAs consume.)
+        const int wl = warp < 4 ? warp - 2 : warp - 4;  // 0..3
+        const int c_lo = lane & 7, j_lo = (lane >> 3) & 3;
+        const int cshift = __ffs(pl.cp / 8) - 1;  // CP/8 channel groups (power of two)
+        const int cmask_g = pl.cp / 8 - 1;
+        const uint32_t ring_s = smem_u32(smem);
+        const uint32_t mirror_bytes = static_cast<uint32_t>(pl.ring) * pl.chunk_bytes;
+        const int64_t w_chunks = p.w_in / 8;
+        int stage = 0;
+        uint32_t phase = 0;
+        int v_pos = 0;  // ring position of the next chunk loaded
+        int64_t cur = kb;
+        while (cur < ke) {
+            const int64_t item = cur / p.steps_per_item;
+            const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
+            const uint16_t* xi = p.x + item * p.c * p.w_in;
+            bool seg_first = true;
+            int64_t next_chunk = 0;
+            for (int64_t st = cur; st < seg_end; st += pl.ks) {
+                const int64_t q0 = (st - item * p.steps_per_item) * 16;
+                mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                const int64_t first_chunk = seg_first ? q0 / 8 + tap0 : next_chunk;
+                const int nchunks = seg_first ? pl.span + pl.kch : pl.kch;
+                seg_first = false;
+                next_chunk = first_chunk + nchunks;
+                const int64_t lim = w_chunks - first_chunk;  // chunks jl < lim exist
+                const uint16_t* src0 = xi + first_chunk * 8;
+                const int rows = (nchunks * pl.cp) >> 5;
+                for (int r = wl; r < rows; r += 4) {
+                    const int c = ((r & cmask_g) << 3) + c_lo;
+                    const int jl = ((r >> cshift) << 2) + j_lo;
+                    int pos = v_pos + jl;
+                    if (pos >= pl.ring) pos -= pl.ring;
+                    const bool valid = c < p.c && jl < lim;
+                    const uint16_t* src = valid ? src0 + static_cast<int64_t>(c) * p.w_in + jl * 8 : p.x;
+                    const uint32_t dst = ring_s + static_cast<uint32_t>(pos) * pl.chunk_bytes + static_cast<uint32_t>(c) * 16u;
+                    cp_async16_zfill(dst, src, valid);
+                    if (pos < pl.xb) cp_async16_zfill(dst + mirror_bytes, src, valid);
                 }
-                cur = seg_end;
+                // the stage's full barrier counts this thread's arrival once its pieces have landed
+                cp_async_mbar_arrive_noinc(smem_u32(&full[stage]));
+                v_pos += nchunks;
+                if (v_pos >= pl.ring) v_pos -= pl.ring;
+                if (++stage == pl.stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
             }
-            if (pending >= 0) {
-                cp_async_wait_group<0>();
-                fence_async_smem();
-                mbar_arrive(smem_u32(&full[pending]));
-            }
+            cur = seg_end;
         }
+        cp_async_wait_group<0>();
+    }
+    if (warp >= 4) {
         // ---- epilogue: D rows (t, c) x columns (p', k) -> partial[cta][k][c][tap]
         const int quarter = warp - 4;
         const int row = quarter * 32 + lane;

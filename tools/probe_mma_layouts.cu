@@ -28,15 +28,26 @@ struct Cfg {
     int nacc;                 // accumulators per K-step (different A start, same B)
     uint32_t g_step;          // A start offset between accumulators
     int unroll;               // issue 8 K-steps straight-line (no address wrap)
+    int rnd;                  // random operands (else zeros)
 };
 
-__global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long* cyc) {
+__global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long* cyc, int bg, const uint4* gsrc,
+                                                    volatile int* stop) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ uint64_t bar;
     __shared__ uint32_t tmem_s;
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x)
-        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x) {
+        uint32_t h = (i * 2654435761u) ^ (blockIdx.x * 40503u);
+        uint32_t w[4];
+        for (int j = 0; j < 4; ++j) {  // random bf16 pairs in [-2, 2) when c.rnd, else zeros
+            h = h * 1664525u + 1013904223u;
+            const uint32_t lo = 0x3f80u | ((h >> 9) & 0x7fu) | ((h >> 16) & 0x8000u);
+            const uint32_t hi = 0x3f80u | ((h >> 2) & 0x7fu) | ((h << 4) & 0x8000u);
+            w[j] = c.rnd ? (lo | (hi << 16)) : 0u;
+        }
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
     if (threadIdx.x / 32 == 0) tmem_alloc<512>(&tmem_s);
     if (threadIdx.x == 0) {
         mbar_init(&bar, 1);
@@ -46,6 +57,31 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    __shared__ int done_s;
+    if (threadIdx.x == 0) done_s = 0;
+    __syncthreads();
+    if (threadIdx.x >= 32 && bg) {
+        // background smem traffic into [144 KB, 160 KB) until the MMA thread finishes
+        const uint32_t base = smem_u32(smem) + 144 * 1024;
+        const int t = threadIdx.x - 32;
+        uint32_t i = 0;
+        while (!*reinterpret_cast<volatile int*>(&done_s)) {
+            for (int r = 0; r < 16; ++r, ++i) {
+                const uint32_t off = ((i * 96 + t) & 1023) * 16;
+                if (bg == 1) {
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(base + off), "r"(i) : "memory");
+                } else {
+                    cp_async16_zfill(base + off, gsrc + ((blockIdx.x * 4096 + i * 96 + t) & ((1 << 22) - 1)), true);
+                }
+            }
+            if (bg == 2) {
+                cp_async_commit();
+                cp_async_wait_group<4>();
+            }
+            if (bg == 3) __nanosleep(200);
+        }
+        if (bg == 2) cp_async_wait_group<0>();
+    }
     if (threadIdx.x / 32 == 0 && elect_one()) {
         const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 80 * 1024);
         const uint32_t idesc = make_idesc(128, c.n, kFmtBF16, c.a_mn, 0);
@@ -76,6 +112,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
         mma_commit(smem_u32(&bar));
         mbar_wait(smem_u32(&bar), 0);
         cyc[blockIdx.x] = clock64() - t0;
+        *reinterpret_cast<volatile int*>(&done_s) = 1;
     }
     __syncwarp();
     tc_fence_before();
@@ -96,6 +133,9 @@ int main() {
         {"A SW32 | B SW32", 16, 256, kLayoutSw32, 0, 16, 256, kLayoutSw32, 256, 4096, 2048, 2, 8192},
         {"fwd row-tap A MN none LBO128 SBO16 | B Kmaj none", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512,
          8192, 1, 0},
+        {"RANDOM UNROLLED wgrad 2 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 2, 8192, 1, 1},
+        {"RANDOM GEMM SW128 2 acc", 16, 1024, kLayoutSw128, 0, 16, 1024, kLayoutSw128, 256, 32, 32, 2, 16384, 1, 1},
+        {"RANDOM fwd row-tap 1 acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512, 8192, 1, 0, 1, 1},
         {"UNROLLED same, 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 1, 0, 1},
         {"UNROLLED wgrad 2 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 2, 8192, 1},
         {"UNROLLED N=112 1 acc", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 1},
@@ -112,17 +152,23 @@ int main() {
     CK(cudaMalloc(&cyc, 148 * sizeof(long long)));
     CK(cudaFuncSetAttribute(mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 161 * 1024));
     const int ksteps = 4096;
-    for (const Cfg& c : cfgs) {
-        for (int grid : {1, 148}) {
-            mma_probe<<<grid, 128, 161 * 1024>>>(c, ksteps, cyc);
+    uint4* gsrc;
+    CK(cudaMalloc(&gsrc, (size_t(1) << 22) * 16));
+    CK(cudaMemset(gsrc, 0, (size_t(1) << 22) * 16));
+    const char* bgname[] = {"", " +st.shared bg", " +cp.async bg"};
+    for (const Cfg& c : cfgs)
+      for (int bg = 0; bg < 3; ++bg) {
+        if (bg && !c.unroll) continue;
+        for (int grid : {148}) {
+            mma_probe<<<grid, 128, 161 * 1024>>>(c, ksteps, cyc, bg, gsrc, nullptr);
             CK(cudaDeviceSynchronize());
             long long h[148];
             CK(cudaMemcpy(h, cyc, grid * sizeof(long long), cudaMemcpyDeviceToHost));
             long long mx = 0;
             for (int i = 0; i < grid; ++i) mx = h[i] > mx ? h[i] : mx;
             const double per = static_cast<double>(mx) / (ksteps * c.nacc);
-            printf("%-52s grid %3d: %6.1f cyc/MMA (ideal %5.1f)\n", c.name, grid, per, 128.0 * c.n / 256.0);
+            printf("%-40s%-16s grid %3d: %6.1f cyc/MMA (ideal %5.1f)\n", c.name, bgname[bg], grid, per, 128.0 * c.n / 256.0);
         }
-    }
+      }
     return 0;
 }
