@@ -8,7 +8,8 @@ than the 126 MB L2, so no flush is needed between steps.
   value   device-resident throughput (TFLOP/s, 3 x 2*N*K*C*S*Q per step), CUDA events, max over ranks
   e2e     the same metric through the C ABI (c1d_forward/backward_data/backward_weight, the call a
           reference host would make) with pinned HOST buffers: H2D of x and dy and D2H of y, dx
-          and dW inside every timed step
+          and dW inside every timed step, pipelined over item chunks so both PCIe directions run
+          under the passes (pipeline.HostLayerStep); the 987 MB fp32 download bounds it
   roofline  the dominant kernel's achieved TFLOP/s vs the measured B200 bf16 peak
   cpu_baseline  the unmodified reference CPU path (oracle/_ref, built from /root/reference) on a
           bounded sample of the same layer, timed on this host's cores
@@ -259,7 +260,11 @@ def main_arm(args):
     step_flops = 3 * flops_per_pass()
     value = world * step_flops / (ms_step * 1e-3) / 1e12
 
-    # ---- e2e through the C ABI with host buffers (H2D inputs, D2H outputs every step)
+    # ---- e2e through the C ABI with host buffers (H2D inputs, D2H outputs every step), the
+    # transfers pipelined against the passes over item chunks (paper_2104_08002_b200/pipeline.py)
+    from paper_2104_08002_b200.pipeline import HostLayerStep
+
+    pipe = HostLayerStep(p, n, w_in, chunks=args.e2e_chunks, device=dev, in_dtype=torch.bfloat16)
     hx = torch.empty(x.shape, dtype=torch.bfloat16, pin_memory=True)
     hdy = torch.empty(dy.shape, dtype=torch.bfloat16, pin_memory=True)
     hx.copy_(x)
@@ -267,27 +272,19 @@ def main_arm(args):
     hy = torch.empty(y.shape, dtype=torch.float32, pin_memory=True)
     hdx = torch.empty(dx.shape, dtype=torch.float32, pin_memory=True)
     hdw = torch.empty(dw.shape, dtype=torch.float32, pin_memory=True)
-    h2d = hx.numel() * 2 + hdy.numel() * 2
-    d2h = (hy.numel() + hdx.numel() + hdw.numel()) * 4
-    e2e_steps = max(1, min(args.steps, 3))
-
-    def step_e2e():
-        x.copy_(hx, non_blocking=True)
-        dy.copy_(hdy, non_blocking=True)
-        step_device()
-        hy.copy_(y, non_blocking=True)
-        hdx.copy_(dx, non_blocking=True)
-        hdw.copy_(dw, non_blocking=True)
-
-    step_e2e()
+    h2d = pipe.h2d_bytes()
+    d2h = pipe.d2h_bytes()
+    e2e_steps = max(2, min(args.steps, 5))
+    reduce_dw = (lambda t: dist.all_reduce(t)) if world > 1 else None  # the DP exchange, every step
+    pipe.run(hx, hdy, w, hy, hdx, hdw, compute=stream, reduce_dw=reduce_dw)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    f0.record(stream)
+    f0.record(pipe.s_in)
     for _ in range(e2e_steps):
-        step_e2e()
-    f1.record(stream)
+        pipe.run(hx, hdy, w, hy, hdx, hdw, compute=stream, reduce_dw=reduce_dw)
+    f1.record(pipe.s_out)
     torch.cuda.synchronize()
     te = torch.tensor([f0.elapsed_time(f1) / e2e_steps], device=dev)
     if world > 1:
@@ -340,7 +337,9 @@ def main_arm(args):
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": te.item(), "path": "c1d_* C ABI, pinned host buffers"},
+                    "ms_per_step": te.item(),
+                    "path": f"c1d_* C ABI from pinned host buffers, {args.e2e_chunks} item chunks with H2D/D2H "
+                            "overlapped with the passes (pipeline.HostLayerStep)"},
             "gpu_launches": int(launches),
             "clocks": clk,
         }
@@ -468,6 +467,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--workload", default="layer", choices=["layer", "network"])
+    ap.add_argument("--e2e-chunks", type=int, default=8, help="item chunks of the pipelined host-buffer e2e step")
     args = ap.parse_args()
     if args.impl == "reference":
         return reference_arm(args)

@@ -29,6 +29,7 @@ struct Cfg {
     uint32_t g_step;          // A start offset between accumulators
     int unroll;               // issue 8 K-steps straight-line (no address wrap)
     int rnd;                  // random operands (else zeros)
+    int d_step;               // TMEM column advance per K-step (unrolled mode), wraps at 512-N
 };
 
 __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long* cyc, int bg, const uint4* gsrc,
@@ -90,13 +91,18 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
         const long long t0 = clock64();
         uint32_t ao = 0, bo = 0;
         if (c.unroll) {
+            const uint32_t dwrap = 512 - c.n;
+            uint32_t dc = 0;
             for (int k = 0; k < ksteps; k += 8) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
+                for (int u = 0; u < 8; ++u) {
 #pragma unroll 1
                     for (int g = 0; g < c.nacc; ++g)
-                        mma_bf16_ss(tmem_s + g * c.n, desc_advance(a0, u * c.a_step + g * c.g_step),
+                        mma_bf16_ss(tmem_s + dc + g * c.n, desc_advance(a0, u * c.a_step + g * c.g_step),
                                     desc_advance(b0, u * c.b_step), idesc, 1u);
+                    dc += c.d_step;
+                    if (dc > dwrap) dc = 0;
+                }
             }
         } else
         for (int k = 0; k < ksteps; ++k) {
@@ -133,6 +139,12 @@ int main() {
         {"A SW32 | B SW32", 16, 256, kLayoutSw32, 0, 16, 256, kLayoutSw32, 256, 4096, 2048, 2, 8192},
         {"fwd row-tap A MN none LBO128 SBO16 | B Kmaj none", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512,
          8192, 1, 0},
+        {"DSTEP N=192 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 192, 512, 8192, 1, 0, 1, 1, 0},
+        {"DSTEP N=192 D+64 (overlap)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 192, 512, 8192, 1, 0, 1, 1, 64},
+        {"DSTEP N=192 D+192 (disjoint)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 192, 512, 8192, 1, 0, 1, 1, 160},
+        {"DSTEP N=256 D+64 (overlap)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512, 8192, 1, 0, 1, 1, 64},
+        {"DSTEP N=64 D+64 (disjoint)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 512, 8192, 1, 0, 1, 1, 64},
+        {"DSTEP N=128 D+128 (disjoint)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 128},
         {"RANDOM UNROLLED wgrad 2 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 256, 2048, 2048, 2, 8192, 1, 1},
         {"RANDOM GEMM SW128 2 acc", 16, 1024, kLayoutSw128, 0, 16, 1024, kLayoutSw128, 256, 32, 32, 2, 16384, 1, 1},
         {"RANDOM fwd row-tap 1 acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512, 8192, 1, 0, 1, 1},
