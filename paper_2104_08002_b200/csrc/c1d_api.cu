@@ -444,6 +444,40 @@ c1d_status c1d_round_bf16(const float* in, uint16_t* out, int64_t count, c1d_str
     return e == cudaSuccess ? C1D_OK : cuda_fail(e, "round_bf16");
 }
 
+size_t c1d_layer_backward_workspace(int64_t n, int64_t k, int64_t q) {
+    if (n <= 0 || k <= 0 || q <= 0) return 0;
+    return align_up(static_cast<size_t>(n * k * layer_bias_blocks(q)) * sizeof(float));
+}
+
+c1d_status c1d_layer_forward_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
+                                      int relu, float* act, uint16_t* act_bf16, int64_t pad, c1d_stream_t stream) {
+    t_last_error.clear();
+    if (n < 0 || k <= 0 || q < 0 || pad < 0 || !pre || n * k > 65535)
+        return fail(C1D_ERR_INVALID_ARGUMENT, "bad layer_forward_epilogue arguments");
+    if (c1d_status st = check_device(); st != C1D_OK) return st;
+    cudaError_t e = launch_layer_fwd_epilogue(pre, bias, skip, n, k, q, relu, act, act_bf16, pad,
+                                              reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_forward_epilogue");
+}
+
+c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
+                                       const float* pre, int64_t n, int64_t k, int64_t q, int relu, float* gsum,
+                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, void* workspace,
+                                       size_t workspace_bytes, c1d_stream_t stream) {
+    t_last_error.clear();
+    if (n < 0 || k <= 0 || q < 0 || !gin || gin_off < 0 || gin_w < gin_off + q || (relu && !pre) || n * k > 65535)
+        return fail(C1D_ERR_INVALID_ARGUMENT, "bad layer_backward_prologue arguments");
+    if (c1d_status st = check_device(); st != C1D_OK) return st;
+    Bump ws{};
+    const size_t need = bias_grad ? c1d_layer_backward_workspace(n, k, q) : 0;
+    if (c1d_status st = acquire_workspace(workspace, workspace_bytes, need, &ws); st != C1D_OK) return st;
+    float* part =
+        bias_grad ? ws.take<float>(static_cast<size_t>(n * k * layer_bias_blocks(q)) * sizeof(float)) : nullptr;
+    cudaError_t e = launch_layer_bwd_prologue(gin, gin_w, gin_off, gadd, pre, n, k, q, relu, gsum, grad_pre,
+                                              grad_pre_bf16, bias_grad, part, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_backward_prologue");
+}
+
 uint64_t c1d_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 }  // extern "C"

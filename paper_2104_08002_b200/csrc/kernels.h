@@ -37,6 +37,15 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
 
 cudaError_t launch_round_bf16(const float* in, uint16_t* out, int64_t count, cudaStream_t stream);
 
+// layer.cu: fused ConvLayer glue (train.cpp:173-221)
+int64_t layer_bias_blocks(int64_t q);  // bias-gradient partials per (item, channel) row
+cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
+                                      int relu, float* act, uint16_t* act_bf16, int64_t pad, cudaStream_t stream);
+cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
+                                      const float* pre, int64_t n, int64_t k, int64_t q, int relu, float* gsum,
+                                      float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
+                                      cudaStream_t stream);
+
 // ---- tcgen05 (sm_100a) kernels -----------------------------------------------------------
 // Row-tap BF16 tensor-core convolution for dilation 8 (fwd and bwd-data). Returns
 // cudaErrorNotSupported when the shape is outside its envelope.

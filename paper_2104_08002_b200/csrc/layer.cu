@@ -1,0 +1,224 @@
+// layer.cu — the per-layer glue of the reference's ConvLayer (proj/src/train.cpp:173-221), fused
+// into one memory pass each way.
+//
+// Forward (train.cpp:176-192): after the conv, pre += bias; a = ReLU(pre); a += skip. The
+// reference keeps every activation FP32 and the next BF16 layer rounds its (zero-padded) input
+// inside the conv (conv.cpp:182-183). Here one pass adds the bias in place (pre is what the
+// backward needs for the ReLU mask), applies ReLU and the skip, and writes the activation as FP32
+// (for skips / FP32 consumers) and/or straight into the next layer's zero-padded BF16 input
+// (same RNE as bf16.hpp:29-40), so no pad copy and no separate rounding pass remain.
+//
+// Backward (train.cpp:205-221): g = incoming gradient (optionally the interior of a padded
+// backward-data output, plus a skip gradient), gp = g * (pre > 0), bias grad = sum over items and
+// columns of gp, and gp feeds the next backward-weight / backward-data as FP32 or BF16. The bias
+// gradient is reduced deterministically: fixed-shape block trees, then a fixed-order sum.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace c1d {
+
+namespace {
+
+constexpr int kEltThreads = 256;
+constexpr int kEltPerThread = 4;
+constexpr int kEltPerBlock = kEltThreads * kEltPerThread;  // columns per block (one row)
+
+__device__ __forceinline__ void store_bf16x4(uint16_t* dst, const float v[4], bool vec) {
+    const uint16_t b0 = fp32_to_bf16_bits(v[0]), b1 = fp32_to_bf16_bits(v[1]);
+    const uint16_t b2 = fp32_to_bf16_bits(v[2]), b3 = fp32_to_bf16_bits(v[3]);
+    if (vec) {
+        uint2 u;
+        u.x = static_cast<uint32_t>(b0) | (static_cast<uint32_t>(b1) << 16);
+        u.y = static_cast<uint32_t>(b2) | (static_cast<uint32_t>(b3) << 16);
+        *reinterpret_cast<uint2*>(dst) = u;
+    } else {
+        dst[0] = b0;
+        dst[1] = b1;
+        dst[2] = b2;
+        dst[3] = b3;
+    }
+}
+
+// grid (ceil(q / 1024), n*k). `vec`: every row start of every operand is 16-B aligned and q % 4 == 0.
+__global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __restrict__ pre, const float* __restrict__ bias,
+                                                                  const float* __restrict__ skip, int64_t k, int64_t q,
+                                                                  int relu, float* __restrict__ act,
+                                                                  uint16_t* __restrict__ act_bf16, int64_t pad,
+                                                                  bool vec) {
+    const int64_t row = blockIdx.y;
+    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
+    if (x0 >= q) return;
+    const float b = bias ? bias[row % k] : 0.0f;
+    float* pr = pre + row * q + x0;
+    const int cnt = static_cast<int>(q - x0 < kEltPerThread ? q - x0 : kEltPerThread);
+    const bool v4 = vec && cnt == kEltPerThread;
+    float v[4], sk[4] = {0.f, 0.f, 0.f, 0.f};
+    if (v4) {
+        const float4 t = *reinterpret_cast<const float4*>(pr);
+        v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+        if (skip) {
+            const float4 s = *reinterpret_cast<const float4*>(skip + row * q + x0);
+            sk[0] = s.x, sk[1] = s.y, sk[2] = s.z, sk[3] = s.w;
+        }
+    } else {
+        for (int j = 0; j < 4; ++j) {
+            v[j] = j < cnt ? pr[j] : 0.0f;
+            if (skip && j < cnt) sk[j] = skip[row * q + x0 + j];
+        }
+    }
+    float a[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        v[j] += b;
+        a[j] = (relu && !(v[j] > 0.0f)) ? 0.0f : v[j];
+        a[j] += sk[j];
+    }
+    if (v4) {
+        if (bias) *reinterpret_cast<float4*>(pr) = make_float4(v[0], v[1], v[2], v[3]);
+        if (act) *reinterpret_cast<float4*>(act + row * q + x0) = make_float4(a[0], a[1], a[2], a[3]);
+    } else {
+        for (int j = 0; j < cnt; ++j) {
+            if (bias) pr[j] = v[j];
+            if (act) act[row * q + x0 + j] = a[j];
+        }
+    }
+    if (act_bf16) {
+        uint16_t* dst = act_bf16 + row * (q + 2 * pad) + pad + x0;
+        if (v4 && ((pad & 3) == 0)) {
+            store_bf16x4(dst, a, true);
+        } else {
+            for (int j = 0; j < cnt; ++j) dst[j] = fp32_to_bf16_bits(a[j]);
+        }
+    }
+}
+
+// grid (nbx = ceil(q / 1024), n*k). Block partial of the bias gradient -> part[row * nbx + bx].
+__global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
+    const float* __restrict__ gin, int64_t gin_w, int64_t gin_off, const float* __restrict__ gadd,
+    const float* __restrict__ pre, int64_t q, int relu, float* __restrict__ gsum, float* __restrict__ grad_pre,
+    uint16_t* __restrict__ grad_pre_bf16, float* __restrict__ part, bool vec) {
+    __shared__ float red[kEltThreads / 32];
+    const int64_t row = blockIdx.y;
+    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
+    float gp[4] = {0.f, 0.f, 0.f, 0.f};
+    if (x0 < q) {
+        const int cnt = static_cast<int>(q - x0 < kEltPerThread ? q - x0 : kEltPerThread);
+        const bool v4 = vec && cnt == kEltPerThread;
+        const float* gi = gin + row * gin_w + gin_off + x0;
+        float g[4], ad[4] = {0.f, 0.f, 0.f, 0.f}, pr[4] = {1.f, 1.f, 1.f, 1.f};
+        if (v4) {
+            const float4 t = *reinterpret_cast<const float4*>(gi);
+            g[0] = t.x, g[1] = t.y, g[2] = t.z, g[3] = t.w;
+            if (gadd) {
+                const float4 s = *reinterpret_cast<const float4*>(gadd + row * q + x0);
+                ad[0] = s.x, ad[1] = s.y, ad[2] = s.z, ad[3] = s.w;
+            }
+            if (relu) {
+                const float4 s = *reinterpret_cast<const float4*>(pre + row * q + x0);
+                pr[0] = s.x, pr[1] = s.y, pr[2] = s.z, pr[3] = s.w;
+            }
+        } else {
+            for (int j = 0; j < 4; ++j) {
+                g[j] = j < cnt ? gi[j] : 0.0f;
+                if (gadd && j < cnt) ad[j] = gadd[row * q + x0 + j];
+                if (relu && j < cnt) pr[j] = pre[row * q + x0 + j];
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            g[j] += ad[j];
+            gp[j] = (relu && !(pr[j] > 0.0f)) ? 0.0f : g[j];
+            if (j >= cnt) gp[j] = 0.0f;
+        }
+        if (v4) {
+            if (gsum) *reinterpret_cast<float4*>(gsum + row * q + x0) = make_float4(g[0], g[1], g[2], g[3]);
+            if (grad_pre) *reinterpret_cast<float4*>(grad_pre + row * q + x0) = make_float4(gp[0], gp[1], gp[2], gp[3]);
+            if (grad_pre_bf16) store_bf16x4(grad_pre_bf16 + row * q + x0, gp, true);
+        } else {
+            for (int j = 0; j < cnt; ++j) {
+                if (gsum) gsum[row * q + x0 + j] = g[j];
+                if (grad_pre) grad_pre[row * q + x0 + j] = gp[j];
+                if (grad_pre_bf16) grad_pre_bf16[row * q + x0 + j] = fp32_to_bf16_bits(gp[j]);
+            }
+        }
+    }
+    if (!part) return;
+    // fixed-shape tree: thread sum (j = 0..3), warp butterfly, then warps 0..7 in order
+    float s = ((gp[0] + gp[1]) + (gp[2] + gp[3]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.0f;
+        for (int w = 0; w < kEltThreads / 32; ++w) t += red[w];
+        part[row * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// bias_grad[c] = sum of part[(item*k + c) * nbx + bx] over items and blocks; one CTA per channel,
+// thread t sums the entries t, t+256, ... (items outer, blocks inner) in order, then a fixed tree.
+__global__ void __launch_bounds__(kEltThreads) bias_grad_reduce_kernel(const float* __restrict__ part,
+                                                                       float* __restrict__ bias_grad, int64_t n,
+                                                                       int64_t k, int64_t nbx) {
+    __shared__ float red[kEltThreads / 32];
+    const int64_t c = blockIdx.x;
+    const int64_t total = n * nbx;
+    float t = 0.0f;
+    for (int64_t e = threadIdx.x; e < total; e += kEltThreads) {
+        const int64_t i = e / nbx, b = e % nbx;
+        t += part[(i * k + c) * nbx + b];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.0f;
+        for (int w = 0; w < kEltThreads / 32; ++w) s += red[w];
+        bias_grad[c] = s;
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+int64_t layer_bias_blocks(int64_t q) { return ceil_div(q, kEltPerBlock); }
+
+cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
+                                      int relu, float* act, uint16_t* act_bf16, int64_t pad, cudaStream_t stream) {
+    if (n * k == 0 || q == 0) return cudaSuccess;
+    if (n * k > 65535) return cudaErrorInvalidValue;
+    const bool vec = (q % 4 == 0) && aligned16(pre) && (!skip || aligned16(skip)) && (!act || aligned16(act));
+    const dim3 grid(static_cast<unsigned>(ceil_div(q, kEltPerBlock)), static_cast<unsigned>(n * k));
+    fwd_epilogue_kernel<<<grid, kEltThreads, 0, stream>>>(pre, bias, skip, k, q, relu, act, act_bf16, pad,
+                                                          vec && (!act_bf16 || ((reinterpret_cast<uintptr_t>(act_bf16) & 7u) == 0 &&
+                                                                                ((q + 2 * pad) % 4) == 0)));
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
+                                      const float* pre, int64_t n, int64_t k, int64_t q, int relu, float* gsum,
+                                      float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
+                                      cudaStream_t stream) {
+    if (n * k == 0 || q == 0) return cudaSuccess;
+    if (n * k > 65535) return cudaErrorInvalidValue;
+    const bool vec = (q % 4 == 0) && (gin_w % 4 == 0) && (gin_off % 4 == 0) && aligned16(gin) &&
+                     (!gadd || aligned16(gadd)) && (!pre || aligned16(pre)) && (!gsum || aligned16(gsum)) &&
+                     (!grad_pre || aligned16(grad_pre)) &&
+                     (!grad_pre_bf16 || (reinterpret_cast<uintptr_t>(grad_pre_bf16) & 7u) == 0);
+    const int64_t nbx = layer_bias_blocks(q);
+    const dim3 grid(static_cast<unsigned>(nbx), static_cast<unsigned>(n * k));
+    bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, q, relu, gsum, grad_pre,
+                                                          grad_pre_bf16, bias_grad ? part : nullptr, vec);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || !bias_grad) return e;
+    bias_grad_reduce_kernel<<<static_cast<unsigned>(k), kEltThreads, 0, stream>>>(part, bias_grad, n, k, nbx);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace c1d

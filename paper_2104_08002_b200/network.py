@@ -1,10 +1,10 @@
-"""Config-5 residual 1D CNN training step on the B200 conv kernels (SURVEY §8(f) row 2).
+"""Config-5 residual 1D CNN training step on the B200 conv kernels (SURVEY §8(f) rows 1-2).
 
 Mirrors the reference's layer/network code (proj/src/train.cpp) on device tensors:
 
 * `ConvLayer`      ConvLayer::forward/backward (train.cpp:173-221): pad -> conv -> +bias -> ReLU
                    -> (+skip); backward: ReLU mask -> bias grad (row sums) -> backward-weight ->
-                   backward-data -> strip pad -> (+skip grad). Conv passes run through the C ABI.
+                   backward-data -> strip pad -> (+skip grad).
 * `ResidualNet`    DemoNet (train.cpp:257-305) extended to BASELINE config 5: a valid input layer
                    1 -> hidden (S=51, d=8, ReLU) consuming the 200-column pad, `blocks` residual
                    blocks of `convs_per_block` same-padded hidden -> hidden convs, and two 1-tap
@@ -19,9 +19,16 @@ Mirrors the reference's layer/network code (proj/src/train.cpp) on device tensor
                    local losses are means over local items).
 * `sgd_step`       p <- p - lr*g (train.cpp:137-141).
 
+Fused glue (csrc/layer.cu through the C ABI): every layer's forward is the
+conv plus ONE epilogue pass (bias in place, ReLU, skip, and the activation written straight into
+the next layer's zero-padded BF16 input buffer), and every backward is ONE prologue pass (the
+incoming gradient read from the interior of the padded backward-data output, plus the skip
+gradient, ReLU mask, BF16 rounding for the next passes, deterministic bias-gradient sums) plus
+the two conv passes. BF16 layers therefore never see an FP32 copy of their input: the activation
+is rounded once, exactly where the reference's conv would round it (conv.cpp:182-183).
+
 Weights are Kaiming-uniform with the reference's damping (input 1.0, body 0.3, heads 0.1;
-train.cpp:247-248, 263-268), seeded. Activations stay FP32 in HBM; BF16 layers round their
-inputs inside the conv call exactly as the reference's BF16 path does.
+train.cpp:247-248, 263-268), seeded.
 """
 from __future__ import annotations
 
@@ -30,6 +37,7 @@ import math
 import torch
 import torch.distributed as dist
 
+from . import _lib as L
 from . import conv as cv
 
 
@@ -37,8 +45,36 @@ def _uniform(shape, limit, gen, device):
     return (torch.rand(shape, generator=gen, device=device, dtype=torch.float32) * 2 - 1) * limit
 
 
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def layer_forward_epilogue(pre, bias=None, skip=None, relu=True, act=None, act_bf16=None, pad=0):
+    """C-ABI fused forward glue (c1d_layer_forward_epilogue) on pre (N, K, Q), in place."""
+    n, k, q = pre.shape
+    cv._check(L.lib().c1d_layer_forward_epilogue(pre.data_ptr(), _ptr(bias), _ptr(skip), n, k, q, int(relu),
+                                                 _ptr(act), _ptr(act_bf16), pad, _stream()))
+
+
+def layer_backward_prologue(gin, gin_off, pre, n, k, q, relu=True, gadd=None, gsum=None, grad_pre=None,
+                            grad_pre_bf16=None, bias_grad=None):
+    """C-ABI fused backward glue (c1d_layer_backward_prologue). gin is (N, K, W) with the layer's
+    gradient at columns [gin_off, gin_off + q)."""
+    cv._check(L.lib().c1d_layer_backward_prologue(gin.data_ptr(), gin.shape[-1], gin_off, _ptr(gadd), _ptr(pre), n,
+                                                  k, q, int(relu), _ptr(gsum), _ptr(grad_pre), _ptr(grad_pre_bf16),
+                                                  _ptr(bias_grad), None, 0, _stream()))
+
+
 class ConvLayer:
-    """One conv with bias, optional ReLU and optional skip input (train.hpp ConvLayer)."""
+    """One conv with bias, optional ReLU and optional skip input (train.hpp ConvLayer).
+
+    Forward reads its input from `self.x_in` (N, C, W_in) — bf16 for BF16 layers (zero-padded, as
+    written by the previous layer's epilogue), fp32 otherwise — and leaves `self.pre`
+    (N, K, Q) = conv + bias for the backward's ReLU mask."""
 
     def __init__(self, in_ch, out_ch, taps, dilation, precision, relu, same_pad, weight_scale, gen, device):
         self.p = cv.ConvParams(in_ch, out_ch, taps, dilation, precision)
@@ -49,33 +85,28 @@ class ConvLayer:
         self.b = torch.zeros(out_ch, device=device)
         self.grad_w = torch.zeros_like(self.w)
         self.grad_b = torch.zeros_like(self.b)
-        self.x_padded = None
+        self.x_in = None
         self.pre = None
 
-    def forward(self, x: torch.Tensor, skip: torch.Tensor | None = None) -> torch.Tensor:
-        xp = torch.nn.functional.pad(x, (self.pad, self.pad)) if self.pad else x
-        if self.p.precision == cv.Precision.Bf16:
-            # round once (reference RNE, bf16.hpp:29-40) and reuse it for backward-weight
-            xp = cv.round_bf16(xp)
-        self.x_padded = xp
-        pre = cv.conv1d_forward(self.x_padded, self.w, self.p)
-        pre.add_(self.b.view(1, -1, 1))
-        self.pre = pre
-        out = torch.relu(pre) if self.relu else pre.clone()
-        if skip is not None:
-            out.add_(skip)
-        return out
+    @property
+    def bf16(self) -> bool:
+        return self.p.precision == cv.Precision.Bf16
 
-    def backward(self, grad_out: torch.Tensor) -> torch.Tensor:
-        grad_pre = grad_out * (self.pre > 0) if self.relu else grad_out
-        grad_pre = grad_pre.contiguous()
-        self.grad_b.copy_(grad_pre.sum(dim=(0, 2)))
-        g = cv.round_bf16(grad_pre) if self.p.precision == cv.Precision.Bf16 else grad_pre
-        cv.conv1d_backward_weight(g, self.x_padded, self.p, out=self.grad_w)
-        grad_x = cv.conv1d_backward_data(g, cv.pack_weights_backward(self.w), self.p)
-        if self.pad:
-            grad_x = grad_x[:, :, self.pad:grad_x.shape[2] - self.pad]
-        return grad_x
+    def conv(self, x_in: torch.Tensor) -> torch.Tensor:
+        self.x_in = x_in
+        self.pre = cv.conv1d_forward(x_in, self.w, self.p, out=self.pre if self._pre_fits(x_in) else None)
+        return self.pre
+
+    def _pre_fits(self, x_in) -> bool:
+        if self.pre is None:
+            return False
+        q = x_in.shape[2] - self.p.dilation * (self.p.taps - 1)
+        return tuple(self.pre.shape) == (x_in.shape[0], self.p.filters, q)
+
+    def backward_convs(self, grad_pre: torch.Tensor, dx: torch.Tensor | None = None) -> torch.Tensor:
+        """backward-weight into grad_w and backward-data (gradient w.r.t. the padded input)."""
+        cv.conv1d_backward_weight(grad_pre, self.x_in, self.p, out=self.grad_w)
+        return cv.conv1d_backward_data(grad_pre, cv.pack_weights_backward(self.w), self.p, out=dx)
 
     def parameters(self):
         return [self.w, self.b]
@@ -90,6 +121,7 @@ class ResidualNet:
     def __init__(self, blocks=5, convs_per_block=3, hidden=15, taps=51, dilation=8,
                  precision=cv.Precision.Bf16, seed=1, device="cuda"):
         gen = torch.Generator(device=device).manual_seed(seed)
+        self.device = device
         self.input = ConvLayer(1, hidden, taps, dilation, precision, True, False, 1.0, gen, device)
         self.blocks = [[ConvLayer(hidden, hidden, taps, dilation, precision, True, True, 0.3, gen, device)
                         for _ in range(convs_per_block)] for _ in range(blocks)]
@@ -106,6 +138,7 @@ class ResidualNet:
                 views.append(self.grad_bucket[off:off + g.numel()].view_as(g))
                 off += g.numel()
             layer.grad_w, layer.grad_b = views
+        self._bufs = {}
 
     def pad(self) -> int:
         return self.input.p.dilation * (self.input.p.taps - 1) // 2
@@ -128,22 +161,99 @@ class ResidualNet:
             total += 3 * cv.conv_flops(p, batch, width)
         return total
 
+    # ---------------------------------------------------------------- activation buffers
+    def _buf(self, name, shape, dtype, zero=False):
+        """Persistent per-shape buffers (the zero borders of padded inputs are written once)."""
+        key = (name, tuple(shape), dtype)
+        t = self._bufs.get(key)
+        if t is None:
+            t = (torch.zeros if zero else torch.empty)(shape, dtype=dtype, device=self.device)
+            self._bufs[key] = t
+        return t
+
+    def _padded_input(self, name, layer: ConvLayer, n: int, width: int):
+        """Zero-bordered input buffer of a same-padded layer: bf16 for BF16 layers, fp32 otherwise."""
+        dt = torch.bfloat16 if layer.bf16 else torch.float32
+        return self._buf(name, (n, layer.p.channels, width + 2 * layer.pad), dt, zero=True)
+
+    def _epilogue_into(self, layer: ConvLayer, nxt: ConvLayer, nxt_name: str, skip=None, act=None):
+        """Fused glue after `layer`'s conv; writes the activation into `nxt`'s padded input."""
+        n, k, q = layer.pre.shape
+        nin = self._padded_input(nxt_name, nxt, n, q)
+        if nxt.bf16:
+            layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, act, nin, nxt.pad)
+            return nin
+        a = act if act is not None else self._buf(nxt_name + ".act", (n, k, q), torch.float32)
+        layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, a, None, 0)
+        nin[:, :, nxt.pad:nxt.pad + q].copy_(a)  # FP32 layers (tests / FP32 nets): plain padded copy
+        return nin
+
+    # ---------------------------------------------------------------- forward / backward
     def forward(self, x_padded: torch.Tensor):
-        h = self.input.forward(x_padded)
-        for blk in self.blocks:
+        n = x_padded.shape[0]
+        first = self.input
+        x0 = cv.round_bf16(x_padded) if first.bf16 else x_padded.float().contiguous()
+        first.conv(x0)
+        width = first.pre.shape[2]
+        h = self._buf("h.in", (n, first.p.filters, width), torch.float32)  # block input (skip source)
+        nxt = self.blocks[0][0] if self.blocks else None
+        if nxt is not None:
+            x_next = self._epilogue_into(first, nxt, "x.b0.0", act=h)
+        else:
+            layer_forward_epilogue(first.pre, first.b, None, first.relu, h)
+        for bi, blk in enumerate(self.blocks):
             skip = h
-            for i, layer in enumerate(blk):
-                h = layer.forward(h, skip if i == len(blk) - 1 else None)
-        return self.reg_head.forward(h), self.peak_head.forward(h)
+            for li, layer in enumerate(blk):
+                layer.conv(x_next)
+                last = li == len(blk) - 1
+                if not last:
+                    x_next = self._epilogue_into(layer, blk[li + 1], f"x.b{bi}.{li + 1}")
+                    continue
+                h = self._buf(f"h.b{bi}", (n, layer.p.filters, width), torch.float32)
+                if bi + 1 < len(self.blocks):
+                    x_next = self._epilogue_into(layer, self.blocks[bi + 1][0], f"x.b{bi + 1}.0", skip=skip, act=h)
+                else:
+                    layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, h)
+        self.h_last = h
+        outs = []
+        for head in (self.reg_head, self.peak_head):
+            head.conv(h)
+            layer_forward_epilogue(head.pre, head.b, None, False)
+            outs.append(head.pre)
+        return outs[0], outs[1]
 
     def backward(self, grad_pred: torch.Tensor, grad_logits: torch.Tensor) -> None:
-        grad_h = self.reg_head.backward(grad_pred) + self.peak_head.backward(grad_logits)
-        for blk in reversed(self.blocks):
-            grad_skip = grad_h
-            for layer in reversed(blk):
-                grad_h = layer.backward(grad_h)
-            grad_h = grad_h + grad_skip
-        self.input.backward(grad_h)  # gradient w.r.t. the padded input is discarded
+        h = self.h_last
+        n, hidden, width = h.shape
+        # heads: bias grads from the incoming gradients, dW, and their backward-data outputs
+        dxs = []
+        for head, g in ((self.reg_head, grad_pred), (self.peak_head, grad_logits)):
+            g = g.contiguous()
+            layer_backward_prologue(g, 0, None, n, 1, width, relu=False, bias_grad=head.grad_b)
+            dxs.append(head.backward_convs(g, self._buf(f"dx.{id(head)}", (n, hidden, width), torch.float32)))
+        gin, gin_off, gadd = dxs[0], 0, dxs[1]  # gradient w.r.t. the last block output = sum of both
+        for bi in reversed(range(len(self.blocks))):
+            blk = self.blocks[bi]
+            g_out = self._buf(f"g.b{bi}", (n, hidden, width), torch.float32)  # grad w.r.t. block output
+            for li in reversed(range(len(blk))):
+                layer = blk[li]
+                gp = self._buf(f"gp.{li}", (n, hidden, width), torch.bfloat16 if layer.bf16 else torch.float32)
+                last = li == len(blk) - 1
+                layer_backward_prologue(gin, gin_off, layer.pre, n, hidden, width, relu=layer.relu,
+                                        gadd=gadd if last else None, gsum=g_out if last else None,
+                                        grad_pre=None if layer.bf16 else gp, grad_pre_bf16=gp if layer.bf16 else None,
+                                        bias_grad=layer.grad_b)
+                dx = self._buf(f"dx.b.{li}", (n, hidden, width + 2 * layer.pad), torch.float32)
+                layer.backward_convs(gp, dx)
+                gin, gin_off, gadd = dx, layer.pad, None
+            gadd = g_out  # the skip: block input gradient = conv path + block output gradient
+        first = self.input
+        gp = self._buf("gp.in", (n, hidden, width), torch.bfloat16 if first.bf16 else torch.float32)
+        layer_backward_prologue(gin, gin_off, first.pre, n, hidden, width, relu=first.relu, gadd=gadd,
+                                grad_pre=None if first.bf16 else gp, grad_pre_bf16=gp if first.bf16 else None,
+                                bias_grad=first.grad_b)
+        # gradient w.r.t. the padded network input: computed as the reference does, then discarded
+        first.backward_convs(gp, self._buf("dx.in", (n, 1, first.x_in.shape[2]), torch.float32))
 
     def sgd_step(self, lr: float) -> None:
         if not lr > 0:

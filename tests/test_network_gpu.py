@@ -83,3 +83,42 @@ def test_grad_bucket_is_one_flat_buffer():
     # BASELINE config 5: 173,162 gradient floats in a single all-reduce bucket
     assert net.grad_bucket.numel() == net.num_parameters() == 1 * 15 * 51 + 15 + 15 * (15 * 15 * 51 + 15) + 2 * (15 + 1)
     assert net.layers()[3].grad_w.data_ptr() > net.layers()[0].grad_w.data_ptr()
+
+
+def test_fused_glue_matches_torch():
+    """c1d_layer_forward_epilogue / c1d_layer_backward_prologue vs the same glue in torch."""
+    from paper_2104_08002_b200.network import layer_backward_prologue, layer_forward_epilogue
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    n, k, q, pad = 3, 5, 1000, 12
+    pre = torch.randn((n, k, q), device="cuda", generator=g)
+    bias = torch.randn(k, device="cuda", generator=g)
+    skip = torch.randn((n, k, q), device="cuda", generator=g)
+    want_pre = pre + bias.view(1, -1, 1)
+    want_act = torch.relu(want_pre) + skip
+    act = torch.empty_like(pre)
+    act_b = torch.zeros((n, k, q + 2 * pad), dtype=torch.bfloat16, device="cuda")
+    p2 = pre.clone()
+    layer_forward_epilogue(p2, bias, skip, True, act, act_b, pad)
+    assert torch.equal(p2, want_pre)
+    assert torch.equal(act, want_act)
+    assert torch.equal(act_b[:, :, pad:pad + q], cv.round_bf16(want_act))
+    assert not act_b[:, :, :pad].any() and not act_b[:, :, pad + q:].any()
+    # backward: gradient from the interior of a padded buffer + skip gradient, ReLU mask
+    gin = torch.randn((n, k, q + 2 * pad), device="cuda", generator=g)
+    gadd = torch.randn((n, k, q), device="cuda", generator=g)
+    gsum = torch.empty_like(pre)
+    gp32 = torch.empty_like(pre)
+    gpb = torch.empty((n, k, q), dtype=torch.bfloat16, device="cuda")
+    db = torch.empty(k, device="cuda")
+    layer_backward_prologue(gin, pad, want_pre, n, k, q, relu=True, gadd=gadd, gsum=gsum, grad_pre=gp32,
+                            grad_pre_bf16=gpb, bias_grad=db)
+    want_g = gin[:, :, pad:pad + q] + gadd
+    want_gp = want_g * (want_pre > 0)
+    assert torch.equal(gsum, want_g)
+    assert torch.equal(gp32, want_gp)
+    assert torch.equal(gpb, cv.round_bf16(want_gp))
+    assert torch.allclose(db, want_gp.sum(dim=(0, 2)), rtol=1e-5, atol=1e-4)
+    db2 = torch.empty(k, device="cuda")
+    layer_backward_prologue(gin, pad, want_pre, n, k, q, relu=True, gadd=gadd, bias_grad=db2)
+    assert torch.equal(db, db2)  # deterministic

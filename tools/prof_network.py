@@ -22,4 +22,14 @@ with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) a
     train_step(net, x, t, lab)
     net.sgd_step(1e-3)
     torch.cuda.synchronize()
-print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=25))
+tot = 0.0
+rows = []
+for e in prof.key_averages():
+    t = getattr(e, "self_device_time_total", 0) or getattr(e, "self_cuda_time_total", 0)
+    if t > 0:
+        rows.append((t, e.count, e.key))
+        tot += t
+rows.sort(reverse=True)
+for t, c, k in rows[:25]:
+    print(f"{t / 1e3:8.3f} ms {t / tot * 100:5.1f}% n={c:4d}  {k[:90]}")
+print(f"total {tot / 1e3:.3f} ms")
