@@ -134,25 +134,27 @@ C1D_EXPORT c1d_status c1d_round_bf16(const float* in, uint16_t* out, int64_t cou
  * Rows are the N*K (item, channel) pairs of a (N, K, Q) activation; fp32 unless stated.
  *
  * Forward epilogue, after the conv wrote pre (N, K, Q):
- *   pre += bias[k] (in place; skipped when bias == NULL)      train.cpp:177-178
- *   a = relu ? max(pre, 0) : pre; a += skip (optional)        train.cpp:179-192
+ *   v = pre + bias[k] (bias optional); stored back into pre only if store_pre   train.cpp:177-178
+ *   a = relu ? max(v, 0) : v; a += skip (optional)                              train.cpp:179-192
  *   act      (optional, (N, K, Q))          = a
  *   act_bf16 (optional, (N, K, Q + 2*pad))  interior [pad, pad+Q) = RNE bf16(a); the 2*pad border
  *            columns are never written (keep them zero: the next layer's same padding)
  */
 C1D_EXPORT c1d_status c1d_layer_forward_epilogue(float* pre, const float* bias, const float* skip, int64_t n,
-                                                 int64_t k, int64_t q, int relu, float* act, uint16_t* act_bf16,
-                                                 int64_t pad, c1d_stream_t stream);
+                                                 int64_t k, int64_t q, int relu, int store_pre, float* act,
+                                                 uint16_t* act_bf16, int64_t pad, c1d_stream_t stream);
 /* Backward prologue:
  *   g  = gin[row * gin_w + gin_off + x] + gadd[row * Q + x] (gadd optional): the incoming gradient,
  *        e.g. the interior of a padded backward-data output plus a skip gradient
- *   gsum (optional) = g;  gp = relu ? (pre > 0 ? g : 0) : g      train.cpp:205-210
+ *   gsum (optional) = g;  gp = relu ? (pre + pre_bias[k] > 0 ? g : 0) : g  (pre_bias optional:
+ *   the bias the forward epilogue added without storing it)      train.cpp:205-210
  *   grad_pre (optional fp32) = gp;  grad_pre_bf16 (optional) = RNE bf16(gp)
  *   bias_grad (optional, K floats) = sum over items and columns of gp, fixed-order (deterministic)
  * workspace: c1d_layer_backward_workspace(n, k, q) bytes, or NULL for the internal buffer. */
 C1D_EXPORT size_t c1d_layer_backward_workspace(int64_t n, int64_t k, int64_t q);
 C1D_EXPORT c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
-                                                  const float* pre, int64_t n, int64_t k, int64_t q, int relu,
+                                                  const float* pre, const float* pre_bias, int64_t n, int64_t k,
+                                                  int64_t q, int relu,
                                                   float* gsum, float* grad_pre, uint16_t* grad_pre_bf16,
                                                   float* bias_grad, void* workspace, size_t workspace_bytes,
                                                   c1d_stream_t stream);

@@ -81,12 +81,12 @@ def lib() -> C.CDLL:
     L.c1d_round_bf16.restype = C.c_int
     L.c1d_launch_count.restype = C.c_uint64
     i64, vp = C.c_int64, C.c_void_p
-    L.c1d_layer_forward_epilogue.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, vp, vp, i64, vp]
+    L.c1d_layer_forward_epilogue.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, C.c_int, vp, vp, i64, vp]
     L.c1d_layer_forward_epilogue.restype = C.c_int
     L.c1d_layer_backward_workspace.argtypes = [i64, i64, i64]
     L.c1d_layer_backward_workspace.restype = C.c_size_t
-    L.c1d_layer_backward_prologue.argtypes = [vp, i64, i64, vp, vp, i64, i64, i64, C.c_int, vp, vp, vp, vp, vp,
-                                              C.c_size_t, vp]
+    L.c1d_layer_backward_prologue.argtypes = [vp, i64, i64, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp, vp, vp,
+                                              vp, C.c_size_t, vp]
     L.c1d_layer_backward_prologue.restype = C.c_int
     _lib = L
     return L

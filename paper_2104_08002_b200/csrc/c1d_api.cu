@@ -450,18 +450,20 @@ size_t c1d_layer_backward_workspace(int64_t n, int64_t k, int64_t q) {
 }
 
 c1d_status c1d_layer_forward_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
-                                      int relu, float* act, uint16_t* act_bf16, int64_t pad, c1d_stream_t stream) {
+                                      int relu, int store_pre, float* act, uint16_t* act_bf16, int64_t pad,
+                                      c1d_stream_t stream) {
     t_last_error.clear();
     if (n < 0 || k <= 0 || q < 0 || pad < 0 || !pre || n * k > 65535)
         return fail(C1D_ERR_INVALID_ARGUMENT, "bad layer_forward_epilogue arguments");
     if (c1d_status st = check_device(); st != C1D_OK) return st;
-    cudaError_t e = launch_layer_fwd_epilogue(pre, bias, skip, n, k, q, relu, act, act_bf16, pad,
+    cudaError_t e = launch_layer_fwd_epilogue(pre, bias, skip, n, k, q, relu, store_pre, act, act_bf16, pad,
                                               reinterpret_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_forward_epilogue");
 }
 
 c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
-                                       const float* pre, int64_t n, int64_t k, int64_t q, int relu, float* gsum,
+                                       const float* pre, const float* pre_bias, int64_t n, int64_t k, int64_t q,
+                                       int relu, float* gsum,
                                        float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, void* workspace,
                                        size_t workspace_bytes, c1d_stream_t stream) {
     t_last_error.clear();
@@ -473,7 +475,7 @@ c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_w, int64_t 
     if (c1d_status st = acquire_workspace(workspace, workspace_bytes, need, &ws); st != C1D_OK) return st;
     float* part =
         bias_grad ? ws.take<float>(static_cast<size_t>(n * k * layer_bias_blocks(q)) * sizeof(float)) : nullptr;
-    cudaError_t e = launch_layer_bwd_prologue(gin, gin_w, gin_off, gadd, pre, n, k, q, relu, gsum, grad_pre,
+    cudaError_t e = launch_layer_bwd_prologue(gin, gin_w, gin_off, gadd, pre, pre_bias, n, k, q, relu, gsum, grad_pre,
                                               grad_pre_bf16, bias_grad, part, reinterpret_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_backward_prologue");
 }

@@ -119,8 +119,74 @@ __global__ void __launch_bounds__(256) direct_conv_kernel(const TIn* __restrict_
     }
 }
 
+// ------------------------------------------------------------------------------- 1-tap (pointwise)
+// S = 1: out[n][o][x] = sum_i W[o][i] in[n][i][x + off]. Memory-bound; each thread owns 4
+// consecutive columns for all (<= OMAX) outputs, the input is read exactly once. (The config-5
+// network's two heads run as one 2-filter 1-tap conv.)
+constexpr int kPwThreads = 256;
+constexpr int kPwCols = 4 * kPwThreads;
+
+template <typename TIn, int OMAX>
+__global__ void __launch_bounds__(kPwThreads) pointwise_conv_kernel(const TIn* __restrict__ in,
+                                                                    const float* __restrict__ wg,
+                                                                    float* __restrict__ out, ConvGeom g,
+                                                                    int round_in) {
+    const int64_t n = blockIdx.y;
+    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kPwCols + threadIdx.x * 4;
+    if (x0 >= g.out_w) return;
+    const int O = static_cast<int>(g.out_ch);
+    float acc[OMAX][4];
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[o][j] = 0.0f;
+    const int cnt = static_cast<int>(g.out_w - x0 < 4 ? g.out_w - x0 : 4);
+    for (int64_t i = 0; i < g.in_ch; ++i) {
+        const int64_t base = (n * g.in_ch + i) * g.in_w + x0 + g.in_off;
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = j < cnt ? load_as_float(in, base + j, round_in != 0) : 0.0f;
+#pragma unroll
+        for (int o = 0; o < OMAX; ++o) {
+            const float w = o < O ? __ldg(wg + static_cast<int64_t>(o) * g.in_ch + i) : 0.0f;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[o][j] = fmaf(w, v[j], acc[o][j]);
+        }
+    }
+#pragma unroll
+    for (int o = 0; o < OMAX; ++o) {
+        if (o >= O) continue;
+        float* dst = out + (n * g.out_ch + o) * g.out_w + x0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (j < cnt) dst[j] = acc[o][j];
+    }
+}
+
+template <typename TIn>
+static cudaError_t launch_pointwise(const TIn* in, const float* wg, float* out, const ConvGeom& g, int round_in,
+                                    cudaStream_t stream) {
+    const dim3 grid(static_cast<unsigned>(ceil_div(g.out_w, kPwCols)), static_cast<unsigned>(g.n));
+    if (g.out_ch <= 1)
+        pointwise_conv_kernel<TIn, 1><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+    else if (g.out_ch <= 2)
+        pointwise_conv_kernel<TIn, 2><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+    else if (g.out_ch <= 4)
+        pointwise_conv_kernel<TIn, 4><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+    else if (g.out_ch <= 8)
+        pointwise_conv_kernel<TIn, 8><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+    else
+        pointwise_conv_kernel<TIn, 16><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_direct_conv(const void* in, int in_dtype, bool round_in, const float* wg, float* out,
                                const ConvGeom& g, cudaStream_t stream) {
+    if (g.taps == 1 && g.out_ch <= 16 && g.n <= 65535) {
+        if (in_dtype == 0) return launch_pointwise(static_cast<const float*>(in), wg, out, g, round_in ? 1 : 0, stream);
+        return launch_pointwise(static_cast<const uint16_t*>(in), wg, out, g, 0, stream);
+    }
     const int64_t span = kTX + (g.taps - 1) * g.dil;
     const size_t smem = sizeof(float) * static_cast<size_t>(kCC * span + kTO * kCC * g.taps);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
@@ -163,7 +229,10 @@ static int64_t wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t q) {
     return std::max<int64_t>(1, std::min<int64_t>(want, units));
 }
 
+static bool pointwise_wgrad_ok(int64_t n, int64_t c, int64_t k, int64_t s);
+
 size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t q) {
+    if (pointwise_wgrad_ok(n, c, k, s)) return sizeof(float) * static_cast<size_t>(n * ceil_div(q, 1024) * k * c);
     if (k * c * s <= 16) return sizeof(float) * static_cast<size_t>(592 * k * c * s);
     return sizeof(float) * static_cast<size_t>(wgrad_splits(n, c, k, q) * k * c * s);
 }
@@ -280,9 +349,115 @@ __global__ void __launch_bounds__(256) small_wgrad_kernel(const TIn* __restrict_
     }
 }
 
+// 1-tap gradients with few filters (K <= 4, C <= 64; e.g. the network's merged heads):
+// dw[k][c] = sum_{n,x} dy[n][k][x] x[n][c][x]. Block (bx, n) owns 1024 columns of item n; each
+// thread keeps all K*C sums for its 4 columns, then a fixed-shape tree makes one partial per block
+// and output, and a block per output sums the partials in a fixed pattern (deterministic).
+template <typename TIn, int KMAX, int CMAX>
+__global__ void __launch_bounds__(kPwThreads) pointwise_wgrad_kernel(const TIn* __restrict__ x,
+                                                                     const TIn* __restrict__ dy,
+                                                                     float* __restrict__ part, int64_t C, int64_t K,
+                                                                     int64_t Q, int round_in) {
+    __shared__ float red[kPwThreads / 32][KMAX * CMAX];
+    const int64_t n = blockIdx.y;
+    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kPwCols + threadIdx.x * 4;
+    const int cnt = static_cast<int>(x0 < Q ? (Q - x0 < 4 ? Q - x0 : 4) : 0);
+    float acc[KMAX][CMAX];
+#pragma unroll
+    for (int kk = 0; kk < KMAX; ++kk)
+#pragma unroll
+        for (int cc = 0; cc < CMAX; ++cc) acc[kk][cc] = 0.0f;
+    float gv[KMAX][4];
+#pragma unroll
+    for (int kk = 0; kk < KMAX; ++kk)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            gv[kk][j] = (kk < K && j < cnt) ? load_as_float(dy, (n * K + kk) * Q + x0 + j, round_in != 0) : 0.0f;
+#pragma unroll
+    for (int cc = 0; cc < CMAX; ++cc) {
+        if (cc >= C) break;
+        float xv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xv[j] = j < cnt ? load_as_float(x, (n * C + cc) * Q + x0 + j, round_in != 0) : 0.0f;
+#pragma unroll
+        for (int kk = 0; kk < KMAX; ++kk)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[kk][cc] = fmaf(gv[kk][j], xv[j], acc[kk][cc]);
+    }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+#pragma unroll
+    for (int kk = 0; kk < KMAX; ++kk)
+#pragma unroll
+        for (int cc = 0; cc < CMAX; ++cc) {
+            float v = acc[kk][cc];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+            if (lane == 0) red[warp][kk * CMAX + cc] = v;
+        }
+    __syncthreads();
+    const int64_t P = static_cast<int64_t>(gridDim.x) * gridDim.y;
+    const int64_t pidx = n * gridDim.x + blockIdx.x;
+    for (int o = threadIdx.x; o < KMAX * CMAX; o += kPwThreads) {
+        const int kk = o / CMAX, cc = o % CMAX;
+        if (kk >= K || cc >= C) continue;
+        float v = 0.0f;
+        for (int w = 0; w < kPwThreads / 32; ++w) v += red[w][o];
+        part[(kk * C + cc) * P + pidx] = v;  // [output][partial]
+    }
+}
+
+// out[o] = sum_p part[o * P + p], one CTA per output: thread t sums p = t, t+256, ... in order,
+// then a fixed tree.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const float* __restrict__ part,
+                                                              float* __restrict__ out, int64_t P) {
+    __shared__ float red[8];
+    const int64_t o = blockIdx.x;
+    float t = 0.0f;
+    for (int64_t p = threadIdx.x; p < P; p += 256) t += part[o * P + p];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float s = 0.0f;
+        for (int w = 0; w < 8; ++w) s += red[w];
+        out[o] = s;
+    }
+}
+
+static bool pointwise_wgrad_ok(int64_t n, int64_t c, int64_t k, int64_t s) {
+    return s == 1 && k <= 4 && c <= 64 && n <= 65535;
+}
+
+template <typename TIn>
+static cudaError_t launch_pointwise_wgrad(const TIn* x, const TIn* dy, float* dw, float* part, int64_t n, int64_t c,
+                                          int64_t k, int64_t q, int round_in, cudaStream_t stream) {
+    const dim3 grid(static_cast<unsigned>(ceil_div(q, kPwCols)), static_cast<unsigned>(n));
+    if (k <= 2 && c <= 16)
+        pointwise_wgrad_kernel<TIn, 2, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in);
+    else if (c <= 16)
+        pointwise_wgrad_kernel<TIn, 4, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in);
+    else
+        pointwise_wgrad_kernel<TIn, 4, 64><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in);
+    note_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    reduce_partials_kernel<<<static_cast<unsigned>(k * c), 256, 0, stream>>>(part, dw,
+                                                                             static_cast<int64_t>(grid.x) * grid.y);
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, bool round_in, float* dw_kcs,
                                 float* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d,
                                 int64_t q, cudaStream_t stream) {
+    if (pointwise_wgrad_ok(n, c, k, s)) {
+        if (in_dtype == 0)
+            return launch_pointwise_wgrad(static_cast<const float*>(x), static_cast<const float*>(dy), dw_kcs,
+                                          workspace, n, c, k, q, round_in ? 1 : 0, stream);
+        return launch_pointwise_wgrad(static_cast<const uint16_t*>(x), static_cast<const uint16_t*>(dy), dw_kcs,
+                                      workspace, n, c, k, q, 0, stream);
+    }
     if (k * c * s <= kSmallOut) {
         if (in_dtype == 0)
             small_wgrad_kernel<float><<<kSmallBlocks, 256, 0, stream>>>(static_cast<const float*>(x),

@@ -40,9 +40,11 @@ cudaError_t launch_round_bf16(const float* in, uint16_t* out, int64_t count, cud
 // layer.cu: fused ConvLayer glue (train.cpp:173-221)
 int64_t layer_bias_blocks(int64_t q);  // bias-gradient partials per (item, channel) row
 cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
-                                      int relu, float* act, uint16_t* act_bf16, int64_t pad, cudaStream_t stream);
+                                      int relu, int store_pre, float* act, uint16_t* act_bf16, int64_t pad,
+                                      cudaStream_t stream);
 cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
-                                      const float* pre, int64_t n, int64_t k, int64_t q, int relu, float* gsum,
+                                      const float* pre, const float* pre_bias, int64_t n, int64_t k, int64_t q,
+                                      int relu, float* gsum,
                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
                                       cudaStream_t stream);
 

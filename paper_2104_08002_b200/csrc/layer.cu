@@ -3,8 +3,9 @@
 //
 // Forward (train.cpp:176-192): after the conv, pre += bias; a = ReLU(pre); a += skip. The
 // reference keeps every activation FP32 and the next BF16 layer rounds its (zero-padded) input
-// inside the conv (conv.cpp:182-183). Here one pass adds the bias in place (pre is what the
-// backward needs for the ReLU mask), applies ReLU and the skip, and writes the activation as FP32
+// inside the conv (conv.cpp:182-183). Here one pass adds the bias (stored back only on request:
+// the backward recomputes the ReLU mask from the conv output and the bias), applies ReLU and the
+// skip, and writes the activation as FP32
 // (for skips / FP32 consumers) and/or straight into the next layer's zero-padded BF16 input
 // (same RNE as bf16.hpp:29-40), so no pad copy and no separate rounding pass remain.
 //
@@ -42,7 +43,7 @@ __device__ __forceinline__ void store_bf16x4(uint16_t* dst, const float v[4], bo
 // grid (ceil(q / 1024), n*k). `vec`: every row start of every operand is 16-B aligned and q % 4 == 0.
 __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __restrict__ pre, const float* __restrict__ bias,
                                                                   const float* __restrict__ skip, int64_t k, int64_t q,
-                                                                  int relu, float* __restrict__ act,
+                                                                  int relu, int store_pre, float* __restrict__ act,
                                                                   uint16_t* __restrict__ act_bf16, int64_t pad,
                                                                   bool vec) {
     const int64_t row = blockIdx.y;
@@ -74,11 +75,11 @@ __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __rest
         a[j] += sk[j];
     }
     if (v4) {
-        if (bias) *reinterpret_cast<float4*>(pr) = make_float4(v[0], v[1], v[2], v[3]);
+        if (bias && store_pre) *reinterpret_cast<float4*>(pr) = make_float4(v[0], v[1], v[2], v[3]);
         if (act) *reinterpret_cast<float4*>(act + row * q + x0) = make_float4(a[0], a[1], a[2], a[3]);
     } else {
         for (int j = 0; j < cnt; ++j) {
-            if (bias) pr[j] = v[j];
+            if (bias && store_pre) pr[j] = v[j];
             if (act) act[row * q + x0 + j] = a[j];
         }
     }
@@ -95,7 +96,8 @@ __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __rest
 // grid (nbx = ceil(q / 1024), n*k). Block partial of the bias gradient -> part[row * nbx + bx].
 __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
     const float* __restrict__ gin, int64_t gin_w, int64_t gin_off, const float* __restrict__ gadd,
-    const float* __restrict__ pre, int64_t q, int relu, float* __restrict__ gsum, float* __restrict__ grad_pre,
+    const float* __restrict__ pre, const float* __restrict__ pre_bias, int64_t k, int64_t q, int relu,
+    float* __restrict__ gsum, float* __restrict__ grad_pre,
     uint16_t* __restrict__ grad_pre_bf16, float* __restrict__ part, bool vec) {
     __shared__ float red[kEltThreads / 32];
     const int64_t row = blockIdx.y;
@@ -124,10 +126,11 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
                 if (relu && j < cnt) pr[j] = pre[row * q + x0 + j];
             }
         }
+        const float pb = (relu && pre_bias) ? pre_bias[row % k] : 0.0f;  // mask of pre + bias
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             g[j] += ad[j];
-            gp[j] = (relu && !(pr[j] > 0.0f)) ? 0.0f : g[j];
+            gp[j] = (relu && !(pr[j] + pb > 0.0f)) ? 0.0f : g[j];
             if (j >= cnt) gp[j] = 0.0f;
         }
         if (v4) {
@@ -187,12 +190,13 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) ==
 int64_t layer_bias_blocks(int64_t q) { return ceil_div(q, kEltPerBlock); }
 
 cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
-                                      int relu, float* act, uint16_t* act_bf16, int64_t pad, cudaStream_t stream) {
+                                      int relu, int store_pre, float* act, uint16_t* act_bf16, int64_t pad,
+                                      cudaStream_t stream) {
     if (n * k == 0 || q == 0) return cudaSuccess;
     if (n * k > 65535) return cudaErrorInvalidValue;
     const bool vec = (q % 4 == 0) && aligned16(pre) && (!skip || aligned16(skip)) && (!act || aligned16(act));
     const dim3 grid(static_cast<unsigned>(ceil_div(q, kEltPerBlock)), static_cast<unsigned>(n * k));
-    fwd_epilogue_kernel<<<grid, kEltThreads, 0, stream>>>(pre, bias, skip, k, q, relu, act, act_bf16, pad,
+    fwd_epilogue_kernel<<<grid, kEltThreads, 0, stream>>>(pre, bias, skip, k, q, relu, store_pre, act, act_bf16, pad,
                                                           vec && (!act_bf16 || ((reinterpret_cast<uintptr_t>(act_bf16) & 7u) == 0 &&
                                                                                 ((q + 2 * pad) % 4) == 0)));
     note_launch();
@@ -200,7 +204,8 @@ cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float
 }
 
 cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
-                                      const float* pre, int64_t n, int64_t k, int64_t q, int relu, float* gsum,
+                                      const float* pre, const float* pre_bias, int64_t n, int64_t k, int64_t q,
+                                      int relu, float* gsum,
                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
                                       cudaStream_t stream) {
     if (n * k == 0 || q == 0) return cudaSuccess;
@@ -211,7 +216,8 @@ cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t g
                      (!grad_pre_bf16 || (reinterpret_cast<uintptr_t>(grad_pre_bf16) & 7u) == 0);
     const int64_t nbx = layer_bias_blocks(q);
     const dim3 grid(static_cast<unsigned>(nbx), static_cast<unsigned>(n * k));
-    bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, q, relu, gsum, grad_pre,
+    bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, pre_bias, k, q, relu, gsum,
+                                                          grad_pre,
                                                           grad_pre_bf16, bias_grad ? part : nullptr, vec);
     note_launch();
     cudaError_t e = cudaGetLastError();

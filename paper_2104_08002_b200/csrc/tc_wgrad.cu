@@ -733,8 +733,18 @@ __global__ void wgrad2_reduce_kernel(const float* __restrict__ part, float* __re
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t s = e % S;
         const int role = static_cast<int>(s / (static_cast<int64_t>(pl.gpc) * pl.taps_per_group));
+        // ascending CTA order; loads batched 8 deep (the adds stay in order)
+        const int b0 = pl.role_cta_begin[role], b1 = pl.role_cta_begin[role + 1];
         float v = 0.0f;
-        for (int b = pl.role_cta_begin[role]; b < pl.role_cta_begin[role + 1]; ++b) v += part[static_cast<int64_t>(b) * count + e];
+        int b = b0;
+        for (; b + 8 <= b1; b += 8) {
+            float t[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[j] = part[static_cast<int64_t>(b + j) * count + e];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v += t[j];
+        }
+        for (; b < b1; ++b) v += part[static_cast<int64_t>(b) * count + e];
         dw[e] = v;
     }
 }

@@ -53,20 +53,21 @@ def _ptr(t):
     return None if t is None else t.data_ptr()
 
 
-def layer_forward_epilogue(pre, bias=None, skip=None, relu=True, act=None, act_bf16=None, pad=0):
-    """C-ABI fused forward glue (c1d_layer_forward_epilogue) on pre (N, K, Q), in place."""
+def layer_forward_epilogue(pre, bias=None, skip=None, relu=True, act=None, act_bf16=None, pad=0, store_pre=False):
+    """C-ABI fused forward glue (c1d_layer_forward_epilogue) on pre (N, K, Q); with store_pre the
+    biased pre-activation is written back in place."""
     n, k, q = pre.shape
     cv._check(L.lib().c1d_layer_forward_epilogue(pre.data_ptr(), _ptr(bias), _ptr(skip), n, k, q, int(relu),
-                                                 _ptr(act), _ptr(act_bf16), pad, _stream()))
+                                                 int(store_pre), _ptr(act), _ptr(act_bf16), pad, _stream()))
 
 
 def layer_backward_prologue(gin, gin_off, pre, n, k, q, relu=True, gadd=None, gsum=None, grad_pre=None,
-                            grad_pre_bf16=None, bias_grad=None):
+                            grad_pre_bf16=None, bias_grad=None, pre_bias=None):
     """C-ABI fused backward glue (c1d_layer_backward_prologue). gin is (N, K, W) with the layer's
-    gradient at columns [gin_off, gin_off + q)."""
-    cv._check(L.lib().c1d_layer_backward_prologue(gin.data_ptr(), gin.shape[-1], gin_off, _ptr(gadd), _ptr(pre), n,
-                                                  k, q, int(relu), _ptr(gsum), _ptr(grad_pre), _ptr(grad_pre_bf16),
-                                                  _ptr(bias_grad), None, 0, _stream()))
+    gradient at columns [gin_off, gin_off + q); the ReLU mask is pre + pre_bias > 0."""
+    cv._check(L.lib().c1d_layer_backward_prologue(gin.data_ptr(), gin.shape[-1], gin_off, _ptr(gadd), _ptr(pre),
+                                                  _ptr(pre_bias), n, k, q, int(relu), _ptr(gsum), _ptr(grad_pre),
+                                                  _ptr(grad_pre_bf16), _ptr(bias_grad), None, 0, _stream()))
 
 
 class ConvLayer:
@@ -127,6 +128,9 @@ class ResidualNet:
                         for _ in range(convs_per_block)] for _ in range(blocks)]
         self.reg_head = ConvLayer(hidden, 1, 1, 1, cv.Precision.Fp32, False, False, 0.1, gen, device)
         self.peak_head = ConvLayer(hidden, 1, 1, 1, cv.Precision.Fp32, False, False, 0.1, gen, device)
+        # both 1-tap heads run as ONE 2-filter FP32 conv (each output channel is accumulated on its
+        # own, so the values are the separate heads'): h is read once per pass
+        self.heads = ConvLayer(hidden, 2, 1, 1, cv.Precision.Fp32, False, False, 0.1, gen, device)
         # one flat gradient bucket (all dW and bias grads) for a single all-reduce per step
         layers = self.layers()
         n = sum(t.numel() for layer in layers for t in layer.gradients())
@@ -215,23 +219,28 @@ class ResidualNet:
                 else:
                     layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, h)
         self.h_last = h
-        outs = []
-        for head in (self.reg_head, self.peak_head):
-            head.conv(h)
-            layer_forward_epilogue(head.pre, head.b, None, False)
-            outs.append(head.pre)
-        return outs[0], outs[1]
+        heads = self.heads
+        torch.cat([self.reg_head.w, self.peak_head.w], out=heads.w)
+        torch.cat([self.reg_head.b, self.peak_head.b], out=heads.b)
+        heads.conv(h)
+        layer_forward_epilogue(heads.pre, heads.b, None, False, store_pre=True)
+        return heads.pre[:, 0:1], heads.pre[:, 1:2]
 
     def backward(self, grad_pred: torch.Tensor, grad_logits: torch.Tensor) -> None:
         h = self.h_last
         n, hidden, width = h.shape
-        # heads: bias grads from the incoming gradients, dW, and their backward-data outputs
-        dxs = []
-        for head, g in ((self.reg_head, grad_pred), (self.peak_head, grad_logits)):
-            g = g.contiguous()
-            layer_backward_prologue(g, 0, None, n, 1, width, relu=False, bias_grad=head.grad_b)
-            dxs.append(head.backward_convs(g, self._buf(f"dx.{id(head)}", (n, hidden, width), torch.float32)))
-        gin, gin_off, gadd = dxs[0], 0, dxs[1]  # gradient w.r.t. the last block output = sum of both
+        # heads (one 2-filter conv): bias grads, dW, and the gradient w.r.t. the last block output
+        # (backward-data of the 2-filter conv = the sum of both heads' backward-data)
+        heads = self.heads
+        g2 = self._buf("g.heads", (n, 2, width), torch.float32)
+        torch.cat([grad_pred, grad_logits], dim=1, out=g2)
+        layer_backward_prologue(g2, 0, None, n, 2, width, relu=False, bias_grad=heads.grad_b)
+        gin = heads.backward_convs(g2, self._buf("dx.heads", (n, hidden, width), torch.float32))
+        self.reg_head.grad_w.copy_(heads.grad_w[0:1])
+        self.peak_head.grad_w.copy_(heads.grad_w[1:2])
+        self.reg_head.grad_b.copy_(heads.grad_b[0:1])
+        self.peak_head.grad_b.copy_(heads.grad_b[1:2])
+        gin_off, gadd = 0, None
         for bi in reversed(range(len(self.blocks))):
             blk = self.blocks[bi]
             g_out = self._buf(f"g.b{bi}", (n, hidden, width), torch.float32)  # grad w.r.t. block output
@@ -242,7 +251,7 @@ class ResidualNet:
                 layer_backward_prologue(gin, gin_off, layer.pre, n, hidden, width, relu=layer.relu,
                                         gadd=gadd if last else None, gsum=g_out if last else None,
                                         grad_pre=None if layer.bf16 else gp, grad_pre_bf16=gp if layer.bf16 else None,
-                                        bias_grad=layer.grad_b)
+                                        bias_grad=layer.grad_b, pre_bias=layer.b)
                 dx = self._buf(f"dx.b.{li}", (n, hidden, width + 2 * layer.pad), torch.float32)
                 layer.backward_convs(gp, dx)
                 gin, gin_off, gadd = dx, layer.pad, None
@@ -251,7 +260,7 @@ class ResidualNet:
         gp = self._buf("gp.in", (n, hidden, width), torch.bfloat16 if first.bf16 else torch.float32)
         layer_backward_prologue(gin, gin_off, first.pre, n, hidden, width, relu=first.relu, gadd=gadd,
                                 grad_pre=None if first.bf16 else gp, grad_pre_bf16=gp if first.bf16 else None,
-                                bias_grad=first.grad_b)
+                                bias_grad=first.grad_b, pre_bias=first.b)
         # gradient w.r.t. the padded network input: computed as the reference does, then discarded
         first.backward_convs(gp, self._buf("dx.in", (n, 1, first.x_in.shape[2]), torch.float32))
 

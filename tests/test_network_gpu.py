@@ -100,6 +100,8 @@ def test_fused_glue_matches_torch():
     act_b = torch.zeros((n, k, q + 2 * pad), dtype=torch.bfloat16, device="cuda")
     p2 = pre.clone()
     layer_forward_epilogue(p2, bias, skip, True, act, act_b, pad)
+    assert torch.equal(p2, pre)  # pre untouched unless store_pre
+    layer_forward_epilogue(p2, bias, skip, True, act, act_b, pad, store_pre=True)
     assert torch.equal(p2, want_pre)
     assert torch.equal(act, want_act)
     assert torch.equal(act_b[:, :, pad:pad + q], cv.round_bf16(want_act))
@@ -122,3 +124,7 @@ def test_fused_glue_matches_torch():
     db2 = torch.empty(k, device="cuda")
     layer_backward_prologue(gin, pad, want_pre, n, k, q, relu=True, gadd=gadd, bias_grad=db2)
     assert torch.equal(db, db2)  # deterministic
+    # mask from the unbiased conv output + the bias (what the network does)
+    gpb2 = torch.empty_like(gpb)
+    layer_backward_prologue(gin, pad, pre, n, k, q, relu=True, gadd=gadd, grad_pre_bf16=gpb2, pre_bias=bias)
+    assert torch.equal(gpb2, gpb)
