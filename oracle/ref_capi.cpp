@@ -181,4 +181,14 @@ double ref_measure_kernel(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d,
     return rc == 0 ? secs : -static_cast<double>(rc);
 }
 
+// Parse a sweep CSV with the reference's own reader (bench.cpp:336-370): record count, or -1 when
+// it rejects the file. Lets tests pin paper_2104_08002_b200/sweep.py's writer to the schema.
+int64_t ref_parse_csv_count(const char* path) {
+    try {
+        return static_cast<int64_t>(parse_csv(path).size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 }  // extern "C"
