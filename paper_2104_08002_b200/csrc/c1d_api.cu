@@ -131,13 +131,111 @@ ConvGeom split_geom(const c1d_desc& d, int64_t q, c1d_pass pass) {
 }
 int64_t split_main_ch(const c1d_desc& d, c1d_pass pass) { return pass == C1D_PASS_FORWARD ? d.c : d.k; }
 
+// Dilations other than 8 on the dilation-8 tensor-core kernels (relayout.cu):
+//   phases (d < 8, 8 % d == 0): m = 8/d phase channels read with a column shift, S' = ceil(S/m)
+//   planes (d = 8m): chunk planes, N*m items of width W/m
+struct DilPlan {
+    enum Kind { kNative, kPhases, kPlanes, kNone } kind = kNone;
+    int64_t m = 1, p = 1, sp = 0;  // factor, phase count min(m, S), taps per phase (ceil(S/m))
+};
+DilPlan dil_plan(const c1d_desc& d, int64_t q) {
+    DilPlan r;
+    if (d.d == 8) {
+        r.kind = DilPlan::kNative;
+    } else if (d.d < 8 && 8 % d.d == 0) {
+        r.kind = DilPlan::kPhases;
+        r.m = 8 / d.d;
+        r.p = std::min<int64_t>(r.m, d.s);
+        r.sp = ceil_div(d.s, r.m);
+    } else if (d.d % 8 == 0 && q % d.d == 0 && d.w_in % d.d == 0) {
+        r.kind = DilPlan::kPlanes;
+        r.m = d.d / 8;
+    }
+    return r;
+}
+int64_t round8(int64_t v) { return (v + 7) / 8 * 8; }
+// Phase copies of a forward-shaped pass: out[n][b*I + i][j] = in[n][i][j + base + b*d] with
+// `base` chosen so the conv's remaining column offset is a non-negative multiple of 8 (aligned
+// TMA starts); zero columns on the left stand in for the original negative offset's zero fill.
+struct PhaseCopy {
+    int64_t base, w_out;
+};
+PhaseCopy phase_copy(const ConvGeom& g) {
+    const int64_t fb = ((g.in_off % 8) + 8) % 8;
+    const int64_t off1 = g.in_off - fb;  // multiple of 8
+    const int64_t padl = off1 < 0 ? -off1 : 0;
+    return PhaseCopy{fb - padl, round8(g.in_w + padl)};
+}
+// geometry of the dilation-8 conv over the phase copies: P*I channels, S' taps
+ConvGeom phase_geom(const ConvGeom& g, const DilPlan& dp) {
+    const PhaseCopy pc = phase_copy(g);
+    ConvGeom r = g;
+    r.in_ch = dp.p * g.in_ch;
+    r.in_w = pc.w_out;
+    r.in_off = g.in_off - pc.base;  // = original offset + left padding - fraction: >= 0, multiple of 8
+    r.taps = dp.sp;
+    r.dil = 8;
+    r.in_stride = 0;
+    return r;
+}
+// plane geometry: N*m items, widths / m, dilation 8 (in_off scales with the width)
+ConvGeom plane_geom(const ConvGeom& g, const DilPlan& dp) {
+    ConvGeom r = g;
+    r.n = g.n * dp.m;
+    r.in_w = g.in_w / dp.m;
+    r.out_w = g.out_w / dp.m;
+    r.dil = 8;
+    r.in_off = g.in_off / dp.m;
+    return r;
+}
+// Input rows whose pitch is not a multiple of 8 elements (the 16-B TMA / cp.async granule) go
+// through a zero-padded bf16 copy with pitch round8(width).
+ConvGeom pitched(ConvGeom g) {
+    if (g.in_w % 8) g.in_stride = round8(g.in_w);
+    return g;
+}
+// backward-weight: Q is padded to a multiple of 8 (zero dY columns add nothing) and x gets a
+// zero-padded pitch covering Q_pad + d(S-1) when either width is unaligned.
+struct WgradPad {
+    bool pad;
+    int64_t q_pad, x_pitch;
+};
+WgradPad wgrad_pad(const c1d_desc& d, int64_t q) {
+    WgradPad r;
+    r.pad = (d.w_in % 8) || (q % 8);
+    r.q_pad = round8(q);
+    r.x_pitch = r.pad ? round8(std::max<int64_t>(d.w_in, r.q_pad + d.d * (d.s - 1))) : d.w_in;
+    return r;
+}
+// backward-weight phases: one shifted x copy at a time, pitch covering every phase's reads
+int64_t phase_x_pitch(const c1d_desc& d, const WgradPad& wp, const DilPlan& dp) {
+    return round8(std::max<int64_t>(d.w_in, wp.q_pad + 8 * (dp.sp - 1)));
+}
+bool phase_wgrad_ok(const c1d_desc& d, int64_t q, const DilPlan& dp) {
+    const int64_t qp = wgrad_pad(d, q).q_pad;
+    for (int64_t b = 0; b < dp.p; ++b)
+        if (!tc_wgrad_v3_supported(d.n, d.c, d.k, ceil_div(d.s - b, dp.m), 8, qp)) return false;
+    return true;
+}
+
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     const bool tc_ok = [&] {
         if (!is_bf16(d)) return false;
-        if (pass == C1D_PASS_FORWARD) return tc_conv_supported(fwd_geom(d, q));
-        if (pass == C1D_PASS_BACKWARD_DATA) return tc_conv_supported(bwd_geom(d, q));
-        return tc_wgrad_supported(d.n, d.c, d.k, d.s, d.d, q);
+        const DilPlan dp = dil_plan(d, q);
+        if (dp.kind == DilPlan::kNone) return false;
+        if (pass == C1D_PASS_BACKWARD_WEIGHT) {
+            const WgradPad wp = wgrad_pad(d, q);
+            if (dp.kind == DilPlan::kNative)
+                return wp.pad ? tc_wgrad_v3_supported(d.n, d.c, d.k, d.s, 8, wp.q_pad)
+                              : tc_wgrad_supported(d.n, d.c, d.k, d.s, d.d, q);
+            if (dp.kind == DilPlan::kPhases) return phase_wgrad_ok(d, q, dp);
+            return tc_wgrad_supported(d.n * dp.m, d.c, d.k, d.s, 8, q / dp.m);
+        }
+        const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
+        if (dp.kind == DilPlan::kNative) return tc_conv_supported(g);
+        if (dp.kind == DilPlan::kPhases) return tc_conv_supported(phase_geom(g, dp));
+        return tc_conv_supported(plane_geom(g, dp));
     }();
     const bool split_ok = [&] {
         if (is_bf16(d) || d.in_dtype != C1D_DTYPE_F32) return false;
@@ -178,23 +276,48 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     }
     // tensor-core paths: BF16 copies of FP32 inputs + kernel workspace
     const bool conv_in_f32 = d.in_dtype == C1D_DTYPE_F32;
-    if (pass == C1D_PASS_FORWARD) {
-        const ConvGeom g = fwd_geom(d, q);
+    const DilPlan dp = dil_plan(d, q);
+    if (pass == C1D_PASS_BACKWARD_WEIGHT && dp.kind != DilPlan::kPlanes) {
+        const WgradPad wpd = wgrad_pad(d, q);
+        size_t b = 0;
+        if (wpd.pad)
+            b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * wpd.x_pitch)) +
+                 align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad));
+        else if (conv_in_f32)
+            b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in)) +
+                 align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        if (dp.kind == DilPlan::kPhases) {
+            size_t kws = 0;
+            for (int64_t ph = 0; ph < dp.p; ++ph)
+                kws = std::max(kws, tc_wgrad_workspace_bytes(d.n, d.c, d.k, ceil_div(d.s - ph, dp.m), 8, wpd.q_pad));
+            return b + align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * phase_x_pitch(d, wpd, dp))) +
+                   align_up(sizeof(float) * static_cast<size_t>(d.k * dp.p * d.c * dp.sp)) + align_up(kws);
+        }
+        return b + align_up(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, wpd.q_pad));
+    }
+    if (dp.kind == DilPlan::kPhases) {
+        const ConvGeom g = phase_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q), dp);
+        return wbytes + align_up(tc_conv_workspace_bytes(g)) +
+               align_up(sizeof(float) * static_cast<size_t>(g.out_ch * g.in_ch * dp.sp)) +
+               align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * g.in_w));
+    }
+    if (dp.kind == DilPlan::kNative) {
+        const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
         size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
-        if (conv_in_f32) b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
+        if (g.in_stride || conv_in_f32)
+            b += align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * (g.in_stride ? g.in_stride : g.in_w)));
         return b;
     }
-    if (pass == C1D_PASS_BACKWARD_DATA) {
-        const ConvGeom g = bwd_geom(d, q);
-        size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
-        if (conv_in_f32) b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
-        return b;
+    if (dp.kind == DilPlan::kPlanes) {
+        const size_t px = align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
+        const size_t pdy = align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        if (pass == C1D_PASS_BACKWARD_WEIGHT)
+            return px + pdy + align_up(tc_wgrad_workspace_bytes(d.n * dp.m, d.c, d.k, d.s, 8, q / dp.m));
+        const ConvGeom g = plane_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q), dp);
+        const size_t pout = align_up(sizeof(float) * static_cast<size_t>(g.n * g.out_ch * g.out_w));
+        return wbytes + (pass == C1D_PASS_FORWARD ? px : pdy) + pout + align_up(tc_conv_workspace_bytes(g));
     }
-    size_t b = align_up(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, q));
-    if (conv_in_f32)
-        b += align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in)) +
-             align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
-    return b;
+    return wbytes;  // no tensor-core plan (resolve() never selects one)
 }
 
 struct Bump {
@@ -289,16 +412,50 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         if (e != cudaSuccess) return cuda_fail(e, "direct_conv");
         return C1D_OK;
     }
+    const DilPlan dp = dil_plan(d, q);
+    if (dp.kind == DilPlan::kPlanes) {
+        // d = 8m: de-interleave the input into chunk planes, run dilation 8, re-interleave
+        const ConvGeom gp = plane_geom(g, dp);
+        uint16_t* pin = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * g.in_w));
+        float* pout = bump.take<float>(sizeof(float) * static_cast<size_t>(gp.n * gp.out_ch * gp.out_w));
+        e = launch_to_planes(in, d.in_dtype, pin, g.n, g.in_ch, g.in_w, dp.m, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "to_planes");
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gp));
+        e = launch_tc_conv(pin, wg, pout, gp, kws, stream);
+        if (e == cudaSuccess) e = launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_conv (planes)");
+        return C1D_OK;
+    }
+    if (dp.kind == DilPlan::kPhases) {
+        // d < 8: shifted phase copies (P*I channels) against phase-split weights, dilation 8
+        const ConvGeom gp = phase_geom(g, dp);
+        const PhaseCopy pc = phase_copy(g);
+        uint16_t* cp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(gp.n * gp.in_ch * gp.in_w));
+        float* wph = bump.take<float>(sizeof(float) * static_cast<size_t>(gp.out_ch * gp.in_ch * dp.sp));
+        e = launch_shift_copies(in, d.in_dtype, cp, g.n, g.in_ch, g.in_w, dp.p, pc.base, d.d, gp.in_w, stream);
+        if (e == cudaSuccess) e = launch_phase_split_weights(wg, wph, g.out_ch, g.in_ch, d.s, dp.m, dp.p, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "phase copies");
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gp));
+        e = launch_tc_conv(cp, wph, out, gp, kws, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_conv (phases)");
+        return C1D_OK;
+    }
+    const ConvGeom gq = pitched(g);
     const uint16_t* in_b = static_cast<const uint16_t*>(in);
-    if (d.in_dtype == C1D_DTYPE_F32) {
+    if (gq.in_stride) {  // unaligned row pitch: zero-padded bf16 copy (rounds FP32 storage too)
+        uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * gq.in_stride));
+        e = launch_pad_rows(in, d.in_dtype, tmp, g.n * g.in_ch, g.in_w, gq.in_stride, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
+        in_b = tmp;
+    } else if (d.in_dtype == C1D_DTYPE_F32) {
         const int64_t count = g.n * g.in_ch * g.in_w;
         uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(count));
         e = launch_round_bf16(static_cast<const float*>(in), tmp, count, stream);
         if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
         in_b = tmp;
     }
-    void* kws = bump.take<char>(tc_conv_workspace_bytes(g));
-    e = launch_tc_conv(in_b, wg, out, g, kws, stream);
+    void* kws = bump.take<char>(tc_conv_workspace_bytes(gq));
+    e = launch_tc_conv(in_b, wg, out, gq, kws, stream);
     if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
     return C1D_OK;
 }
@@ -420,9 +577,32 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         if (e != cudaSuccess) return cuda_fail(e, "direct_wgrad");
         return C1D_OK;
     }
+    const DilPlan dpl = dil_plan(d, q);
+    if (dpl.kind == DilPlan::kPlanes) {
+        // d = 8m: both operands as chunk planes; the plane items sum into the same dW
+        uint16_t* px = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
+        uint16_t* pdy = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        e = launch_to_planes(x, d.in_dtype, px, d.n, d.c, d.w_in, dpl.m, stream);
+        if (e == cudaSuccess) e = launch_to_planes(dy, d.in_dtype, pdy, d.n, d.k, q, dpl.m, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "to_planes");
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n * dpl.m, d.c, d.k, d.s, 8, q / dpl.m));
+        e = launch_tc_wgrad(px, pdy, dw_kcs, kws, d.n * dpl.m, d.c, d.k, d.s, 8, q / dpl.m, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (planes)");
+        return C1D_OK;
+    }
+    e = cudaSuccess;
+    const WgradPad wpd = wgrad_pad(d, q);
     const uint16_t* xb = static_cast<const uint16_t*>(x);
     const uint16_t* gb = static_cast<const uint16_t*>(dy);
-    if (d.in_dtype == C1D_DTYPE_F32) {
+    if (wpd.pad) {  // zero-padded bf16 copies with 8-element pitches (rounds FP32 storage too)
+        uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * wpd.x_pitch));
+        uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad));
+        e = launch_pad_rows(x, d.in_dtype, tx, d.n * d.c, d.w_in, wpd.x_pitch, stream);
+        if (e == cudaSuccess) e = launch_pad_rows(dy, d.in_dtype, tg, d.n * d.k, q, wpd.q_pad, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
+        xb = tx;
+        gb = tg;
+    } else if (d.in_dtype == C1D_DTYPE_F32) {
         uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
         uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
         e = launch_round_bf16(static_cast<const float*>(x), tx, d.n * d.c * d.w_in, stream);
@@ -431,8 +611,28 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         xb = tx;
         gb = tg;
     }
-    void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, q));
-    e = launch_tc_wgrad(xb, gb, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, q, stream);
+    const DilPlan dp = dil_plan(d, q);
+    if (dp.kind == DilPlan::kPhases) {
+        // phase b (real taps b + m*t): x shifted by b*d columns (bf16 copy), dilation-8 gradient
+        // over its taps, scattered back into dW
+        const int64_t xp = phase_x_pitch(d, wpd, dp);
+        uint16_t* xs = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * xp));
+        float* dwb = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * dp.p * d.c * dp.sp));
+        size_t kbytes = 0;
+        for (int64_t b = 0; b < dp.p; ++b)
+            kbytes = std::max(kbytes, tc_wgrad_workspace_bytes(d.n, d.c, d.k, ceil_div(d.s - b, dp.m), 8, wpd.q_pad));
+        void* kws = bump.take<char>(kbytes);
+        for (int64_t b = 0; b < dp.p && e == cudaSuccess; ++b) {
+            const int64_t sb = ceil_div(d.s - b, dp.m);
+            e = launch_shift_copies(x, d.in_dtype, xs, d.n, d.c, d.w_in, 1, b * d.d, 0, xp, stream);
+            if (e == cudaSuccess) e = launch_tc_wgrad(xs, gb, dwb, kws, d.n, d.c, d.k, sb, 8, wpd.q_pad, stream, xp);
+            if (e == cudaSuccess) e = launch_scatter_phase_wgrad(dwb, dw_kcs, d.k, d.c, d.s, dp.m, b, stream);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (phases)");
+        return C1D_OK;
+    }
+    void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, wpd.q_pad));
+    e = launch_tc_wgrad(xb, gb, dw_kcs, kws, d.n, d.c, d.k, d.s, 8, wpd.q_pad, stream, wpd.pad ? wpd.x_pitch : 0);
     if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad");
     return C1D_OK;
 }

@@ -15,8 +15,11 @@ void note_launch(int n = 1);
 // backward-data: in = dy (K ch, Q),    out = dx (C ch, W_in), wg = W' (CKS, taps reversed),
 //                in_off = -d*(S-1)  (the reference's zero_pad_width, conv.cpp:206-208, done
 //                as predicated loads instead of a padded copy)
+// in_stride: row pitch of the input in elements when it is not in_w (a zero-padded copy whose
+// pitch is a multiple of 8 elements, the TMA stride granule).
 struct ConvGeom {
     int64_t n, in_ch, in_w, out_ch, out_w, taps, dil, in_off;
+    int64_t in_stride = 0;
 };
 
 enum WeightMode { kWeightsForward = 0, kWeightsBackwardData = 1 };
@@ -61,8 +64,33 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
 
 bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+// x_w: row pitch of x (elements) if not q + d*(s-1)
 cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace,
-                            int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream);
+                            int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream,
+                            int64_t x_w = 0);
+bool tc_wgrad_v3_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+
+// relayout.cu: dilations other than 8 on the dilation-8 tensor-core kernels
+// (O, I, S) -> (O, P*I, S'), S' = ceil(S/m): out[o][b*I + i][t] = w[o][i][b + m*t] (0 past S), P = min(m, S)
+cudaError_t launch_phase_split_weights(const float* w, float* out, int64_t O, int64_t I, int64_t S, int64_t m,
+                                       int64_t P, cudaStream_t stream);
+// dW[k][c][b + m*t] = dwb[k][c][t] for t < ceil((S-b)/m)
+cudaError_t launch_scatter_phase_wgrad(const float* dwb, float* dw, int64_t K, int64_t C, int64_t S, int64_t m,
+                                       int64_t b, cudaStream_t stream);
+// planes (d = 8m): in (N, C, W) -> out (N*m, C, W/m): out[n*m + r][c][8u + e] = in[n][c][8(u*m + r) + e]
+// (bf16 out; `round` rounds FP32 input with the reference RNE); and the inverse for FP32 results.
+cudaError_t launch_to_planes(const void* in, int in_dtype, uint16_t* out, int64_t n, int64_t c, int64_t w,
+                             int64_t m, cudaStream_t stream);
+cudaError_t launch_from_planes(const float* in, float* out, int64_t n, int64_t c, int64_t w, int64_t m,
+                               cudaStream_t stream);
+// Shifted phase copies (TMA and cp.async need 16-B aligned starts, so column shifts that are not
+// multiples of 8 are materialised): out[n][b*I + i][j] = bf16(in[n][i][j + base + b*delta]) for
+// b < P, 0 where the source column is outside [0, w); out rows have pitch w_out.
+cudaError_t launch_shift_copies(const void* in, int in_dtype, uint16_t* out, int64_t n, int64_t I, int64_t w,
+                                int64_t P, int64_t base, int64_t delta, int64_t w_out, cudaStream_t stream);
+// out[r][j] = bf16(in[r][j]) for j < w, 0 for w <= j < w_pad (rows of a zero-padded bf16 copy)
+cudaError_t launch_pad_rows(const void* in, int in_dtype, uint16_t* out, int64_t rows, int64_t w, int64_t w_pad,
+                            cudaStream_t stream);
 
 // FP32-on-tensor-core operand splitting (split.cu)
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,

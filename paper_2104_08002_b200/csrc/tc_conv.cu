@@ -82,7 +82,8 @@ struct KParams {
 
 bool make_plan(const ConvGeom& g, Plan* pl, bool two_regions = false) {
     if (g.dil != 8) return false;
-    if (g.in_w % 8 != 0 || g.in_w < 8) return false;  // TMA global stride must be a multiple of 16 B
+    const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
+    if (pitch % 8 != 0 || pitch < g.in_w || g.in_w < 8) return false;  // TMA global stride: multiple of 16 B
     if (g.n * g.in_ch >= (int64_t{1} << 31) || g.in_w >= (int64_t{1} << 31)) return false;
     Plan p{};
     p.kp = g.out_ch <= 16 ? 16 : (g.out_ch <= 32 ? 32 : 64);
@@ -448,7 +449,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     }
     CUtensorMap tmap;
     const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.in_w), static_cast<cuuint64_t>(g.n * g.in_ch)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.in_w) * 2};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.in_stride ? g.in_stride : g.in_w) * 2};
     const cuuint32_t box[2] = {static_cast<cuuint32_t>(kSegQ), 1};
     const cuuint32_t estr[2] = {1, 1};
     CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(in_bf16), dims, strides,

@@ -767,10 +767,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 namespace {
 cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace, int64_t n,
-                      int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, const W2Plan& pl, cudaStream_t stream) {
+                      int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, const W2Plan& pl, cudaStream_t stream,
+                      int64_t x_w) {
     auto encode = encode_fn();
     if (!encode) return cudaErrorNotSupported;
-    const int64_t w_in = q + d * (s - 1);
+    const int64_t w_in = x_w > 0 ? x_w : q + d * (s - 1);
     CUtensorMap ymap;
     if ((reinterpret_cast<uintptr_t>(x_bf16) & 15u) || (w_in % 8)) return cudaErrorInvalidValue;
     {
@@ -855,12 +856,20 @@ size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int6
     return sizeof(float) * static_cast<size_t>(p.roles) * p.splits * static_cast<size_t>(k * c * s);
 }
 
+bool tc_wgrad_v3_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    return make_w2plan(n, c, k, s, d, q, &p2);
+}
+
 cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace,
-                            int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream) {
+                            int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream,
+                            int64_t x_w) {
     {
         W2Plan p2;
-        if (make_w2plan(n, c, k, s, d, q, &p2)) return launch_v2(x_bf16, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream);
+        if (make_w2plan(n, c, k, s, d, q, &p2))
+            return launch_v2(x_bf16, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream, x_w);
     }
+    if (x_w) return cudaErrorNotSupported;  // explicit x pitches need the v3 kernel
     WPlan pl;
     if (!make_wplan(n, c, k, s, d, q, &pl)) return cudaErrorNotSupported;
     auto encode = encode_fn();

@@ -224,3 +224,25 @@ def test_reference_acceptance_binary_on_gpu_backend():
     for crit in ("1", "3", "5", "7"):
         out = subprocess.run([exe, crit], capture_output=True, text=True, timeout=300)
         assert out.returncode == 0 and f"criterion {crit} PASS" in out.stdout, out.stdout + out.stderr
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 16, 24])
+@pytest.mark.parametrize("bf16_storage", [False, True])
+@pytest.mark.parametrize("q", [256, 253])  # 253: unaligned widths go through the padded-pitch copies
+def test_other_dilations_on_tensor_cores(d, bf16_storage, q):
+    """d != 8 through the dilation-8 tensor-core kernels (relayout.cu: phase channels for d < 8,
+    chunk planes for d = 8m) vs the oracle on BF16-rounded inputs."""
+    rng = oracle.Rng(1000 + d)
+    n, c, k, s = 2, 24, 40, 11
+    if d % 8 == 0:
+        q = 2 * d * ((q + 2 * d - 1) // (2 * d))  # planes need Q and W_in multiples of d
+    w_in = q + d * (s - 1)
+    x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
+    p = cv.ConvParams(c, k, s, d, cv.Precision.Bf16)
+    dt = 1 if bf16_storage else 0
+    for i in range(3):
+        assert cv.selected_algo(p, n, w_in, i, in_dtype=dt) == "tcgen05", (d, q, i)
+    got = run_passes(x, w, dy, d, cv.Precision.Bf16, bf16_storage=bf16_storage)
+    want = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), d)
+    for g, wv, name in zip(got, want, ("fwd", "bwd_d", "bwd_w")):
+        assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} q={q} {name}")
