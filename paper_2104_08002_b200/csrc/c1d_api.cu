@@ -214,9 +214,13 @@ int64_t phase_x_pitch(const c1d_desc& d, const WgradPad& wp, const DilPlan& dp) 
 bool phase_wgrad_ok(const c1d_desc& d, int64_t q, const DilPlan& dp) {
     const int64_t qp = wgrad_pad(d, q).q_pad;
     for (int64_t b = 0; b < dp.p; ++b)
-        if (!tc_wgrad_v3_supported(d.n, d.c, d.k, ceil_div(d.s - b, dp.m), 8, qp)) return false;
+        if (!tc_wgrad_supported(d.n, d.c, d.k, ceil_div(d.s - b, dp.m), 8, qp)) return false;
     return true;
 }
+// The row-tap kernels put 16 taps of one channel in an MMA's K; a phase carries ceil(S/m) taps, so
+// few taps x few channels leave the tensor core mostly idle and the FFMA kernels win. Measured on
+// B200 (config-4 sweep): the phase path pays off once taps-per-phase x input channels >= 96.
+bool phases_pay_off(const DilPlan& dp, int64_t in_ch) { return dp.sp * in_ch >= 96; }
 
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
@@ -226,15 +230,15 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {
             const WgradPad wp = wgrad_pad(d, q);
-            if (dp.kind == DilPlan::kNative)
-                return wp.pad ? tc_wgrad_v3_supported(d.n, d.c, d.k, d.s, 8, wp.q_pad)
-                              : tc_wgrad_supported(d.n, d.c, d.k, d.s, d.d, q);
-            if (dp.kind == DilPlan::kPhases) return phase_wgrad_ok(d, q, dp);
+            if (dp.kind == DilPlan::kNative) return tc_wgrad_supported(d.n, d.c, d.k, d.s, 8, wp.q_pad);
+            if (dp.kind == DilPlan::kPhases)
+                return (d.algo == C1D_ALGO_TCGEN05 || phases_pay_off(dp, d.c)) && phase_wgrad_ok(d, q, dp);
             return tc_wgrad_supported(d.n * dp.m, d.c, d.k, d.s, 8, q / dp.m);
         }
         const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
         if (dp.kind == DilPlan::kNative) return tc_conv_supported(g);
-        if (dp.kind == DilPlan::kPhases) return tc_conv_supported(phase_geom(g, dp));
+        if (dp.kind == DilPlan::kPhases)
+            return (d.algo == C1D_ALGO_TCGEN05 || phases_pay_off(dp, g.in_ch)) && tc_conv_supported(phase_geom(g, dp));
         return tc_conv_supported(plane_geom(g, dp));
     }();
     const bool split_ok = [&] {

@@ -869,12 +869,12 @@ cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, flo
         if (make_w2plan(n, c, k, s, d, q, &p2))
             return launch_v2(x_bf16, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream, x_w);
     }
-    if (x_w) return cudaErrorNotSupported;  // explicit x pitches need the v3 kernel
     WPlan pl;
     if (!make_wplan(n, c, k, s, d, q, &pl)) return cudaErrorNotSupported;
     auto encode = encode_fn();
     if (!encode) return cudaErrorNotSupported;
-    const int64_t w_in = q + d * (s - 1);
+    const int64_t w_in = x_w > 0 ? x_w : q + d * (s - 1);  // row pitch of x
+    if (w_in % 8) return cudaErrorInvalidValue;
     CUtensorMap xmap, ymap;
     {
         // X as (qi=8, c, q-chunk, n): element (qi, c, qc, n) at n*C*W + c*W + qc*8 + qi
