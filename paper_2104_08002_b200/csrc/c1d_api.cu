@@ -122,15 +122,6 @@ ConvGeom bwd_geom(const c1d_desc& d, int64_t q) {
     return ConvGeom{d.n, d.k, q, d.c, d.w_in, d.s, d.d, -d.d * (d.s - 1)};
 }
 
-// Geometry of the split (BF16X3) problems: fwd/bwd-d carry 4x the input channels
-// ([hi | lo | hi | lo] against weights [hi | hi | lo | lo]), bwd-w runs on 2C channels x 2K filters.
-ConvGeom split_geom(const c1d_desc& d, int64_t q, c1d_pass pass) {
-    ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
-    g.in_ch *= 4;
-    return g;
-}
-int64_t split_main_ch(const c1d_desc& d, c1d_pass pass) { return pass == C1D_PASS_FORWARD ? d.c : d.k; }
-
 // Dilations other than 8 on the dilation-8 tensor-core kernels (relayout.cu):
 //   phases (d < 8, 8 % d == 0): m = 8/d phase channels read with a column shift, S' = ceil(S/m)
 //   planes (d = 8m): chunk planes, N*m items of width W/m
@@ -222,6 +213,23 @@ bool phase_wgrad_ok(const c1d_desc& d, int64_t q, const DilPlan& dp) {
 // B200 (config-4 sweep): the phase path pays off once taps-per-phase x input channels >= 96.
 bool phases_pay_off(const DilPlan& dp, int64_t in_ch) { return dp.sp * in_ch >= 96; }
 
+// FP32 split path (split.cu) composed with the dilation plans: the split multiplies channels
+// (4x for conv-shaped passes: [hi|lo|hi|lo] inputs against [hi|hi|lo|lo] weights, main term =
+// the first block; 2C x 2K for backward-weight) and is applied after the phase copies / before the
+// plane relayout, so every rewrite feeds the same dilation-8 kernels.
+struct SplitConv {
+    ConvGeom gs;      // geometry the tensor-core kernel runs
+    int64_t main_ch;  // channels accumulating in the main TMEM region
+};
+SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const DilPlan& dp) {
+    ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
+    if (dp.kind == DilPlan::kPlanes) g = plane_geom(g, dp);
+    if (dp.kind == DilPlan::kPhases) g = phase_geom(g, dp);
+    SplitConv r{g, g.in_ch};
+    r.gs.in_ch *= 4;
+    return r;
+}
+
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     const bool tc_ok = [&] {
@@ -243,7 +251,17 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     }();
     const bool split_ok = [&] {
         if (is_bf16(d) || d.in_dtype != C1D_DTYPE_F32) return false;
-        if (pass == C1D_PASS_BACKWARD_WEIGHT) return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q);
+        const DilPlan dp = dil_plan(d, q);
+        if (dp.kind == DilPlan::kNone) return false;
+        if (pass == C1D_PASS_BACKWARD_WEIGHT) {
+            if (dp.kind == DilPlan::kPlanes) return tc_wgrad_supported(d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m);
+            if (d.w_in % 8 || q % 8) return false;
+            if (dp.kind == DilPlan::kNative) return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q);
+            if (d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, d.c)) return false;
+            for (int64_t b = 0; b < dp.p; ++b)
+                if (!tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, ceil_div(d.s - b, dp.m), 8, q)) return false;
+            return true;
+        }
         // Error model: each product carries <= 2*2^-18 relative representation error (dropped
         // residuals of the two-level split), and the tensor core's FP32 accumulation adds
         // ~1.5e-9 norm-relative per accumulated main-term product (measured); the correction
@@ -253,7 +271,9 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         constexpr int64_t kMaxSplitTerms = 3300;
         const int64_t cin = pass == C1D_PASS_FORWARD ? d.c : d.k;
         if (cin * d.s > kMaxSplitTerms) return false;
-        return tc_conv_supported(split_geom(d, q, pass), split_main_ch(d, pass));
+        if (dp.kind == DilPlan::kPhases && d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, cin)) return false;
+        const SplitConv sc = split_conv_geom(d, pass, q, dp);
+        return tc_conv_supported(sc.gs, sc.main_ch);
     }();
     if (d.algo == C1D_ALGO_AUTO) return tc_ok ? C1D_ALGO_TCGEN05 : (split_ok ? C1D_ALGO_BF16X3 : C1D_ALGO_DIRECT);
     if (d.algo == C1D_ALGO_TCGEN05 && !tc_ok) return static_cast<c1d_algo>(-1);
@@ -263,17 +283,11 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
 
 size_t align_up(size_t v) { return (v + 255) & ~size_t{255}; }
 
+size_t split_workspace(const c1d_desc& d, c1d_pass pass, int64_t q);  // dry run of the split paths
+
 size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo) {
     const size_t wbytes = align_up(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
-    if (algo == C1D_ALGO_BF16X3) {
-        if (pass == C1D_PASS_BACKWARD_WEIGHT)
-            return align_up(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * d.w_in)) +
-                   align_up(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.k * q)) + 4 * wbytes +
-                   align_up(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q));
-        const ConvGeom g = split_geom(d, q, pass);
-        return align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * g.in_w)) + 8 * wbytes +
-               align_up(tc_conv_workspace_bytes(g, split_main_ch(d, pass)));
-    }
+    if (algo == C1D_ALGO_BF16X3) return split_workspace(d, pass, q);
     if (algo == C1D_ALGO_DIRECT) {
         if (pass == C1D_PASS_BACKWARD_WEIGHT) return align_up(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
         return wbytes;
@@ -327,9 +341,13 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
 struct Bump {
     char* p;
     size_t left;
+    bool dry = false;  // sizing pass: only count (used by workspace_for for the composed paths)
+    size_t used = 0;
     template <typename T>
     T* take(size_t bytes) {
         bytes = align_up(bytes);
+        used += bytes;
+        if (dry) return reinterpret_cast<T*>(alignof(T));  // never dereferenced
         if (bytes > left) return nullptr;
         T* r = reinterpret_cast<T*>(p);
         p += bytes;
@@ -363,6 +381,126 @@ c1d_status check_device() {
     return C1D_OK;
 }
 
+// FP32 split path of a conv-shaped pass under its dilation plan (see split_conv_geom). With a dry
+// bump only the workspace is sized.
+cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const void* in, const float* w_kcs,
+                           float* out, Bump& bump, cudaStream_t stream) {
+    const DilPlan dp = dil_plan(d, q);
+    const ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
+    const SplitConv sc = split_conv_geom(d, pass, q, dp);
+    const bool run = !bump.dry;
+    const size_t kcs = static_cast<size_t>(d.k * d.c * d.s);
+    const int mode = pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData;
+    cudaError_t e = cudaSuccess;
+    auto step = [&](auto&& launch) {
+        if (run && e == cudaSuccess) e = launch();
+    };
+    if (dp.kind != DilPlan::kPhases) {
+        float* w4 = bump.take<float>(4 * sizeof(float) * kcs);
+        float* wg4 = bump.take<float>(4 * sizeof(float) * kcs);
+        if (pass == C1D_PASS_FORWARD) {  // c-blocks hi,hi,lo,lo
+            step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 1, 4, 0xCu, stream); });
+            step([&] { return launch_prep_weights(w4, wg4, d.k, 4 * d.c, d.s, kWeightsForward, false, stream); });
+        } else {  // k-blocks hi,hi,lo,lo, then the bwd-d transpose
+            step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 4, 1, 0xCu, stream); });
+            step([&] { return launch_prep_weights(w4, wg4, 4 * d.k, d.c, d.s, kWeightsBackwardData, false, stream); });
+        }
+        const size_t n4 = static_cast<size_t>(g.n * 4 * g.in_ch * g.in_w);
+        uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
+        step([&] { return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream); });
+        if (dp.kind == DilPlan::kPlanes) {
+            uint16_t* p4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
+            float* pout = bump.take<float>(sizeof(float) * static_cast<size_t>(sc.gs.n * sc.gs.out_ch * sc.gs.out_w));
+            void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
+            step([&] { return launch_to_planes(x4, C1D_DTYPE_BF16, p4, g.n, 4 * g.in_ch, g.in_w, dp.m, stream); });
+            step([&] { return launch_tc_conv(p4, wg4, pout, sc.gs, kws, stream, sc.main_ch); });
+            step([&] { return launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream); });
+            return e;
+        }
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
+        step([&] { return launch_tc_conv(x4, wg4, out, sc.gs, kws, stream, sc.main_ch); });
+        return e;
+    }
+    // phases: weights prep -> phase split -> hi/lo split; input fp32 phase copies -> hi/lo split
+    const int64_t O = g.out_ch, I = g.in_ch, PI = dp.p * g.in_ch;
+    float* wg = bump.take<float>(sizeof(float) * kcs);
+    float* wph = bump.take<float>(sizeof(float) * static_cast<size_t>(O * PI * dp.sp));
+    float* wg4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(O * PI * dp.sp));
+    step([&] { return launch_prep_weights(w_kcs, wg, d.k, d.c, d.s, mode, false, stream); });
+    step([&] { return launch_phase_split_weights(wg, wph, O, I, d.s, dp.m, dp.p, stream); });
+    step([&] { return launch_split_weights(wph, wg4, O, PI, dp.sp, 1, 4, 0xCu, stream); });
+    const PhaseCopy pc = phase_copy(g);
+    const int64_t W2 = sc.gs.in_w;
+    float* cp = bump.take<float>(sizeof(float) * static_cast<size_t>(g.n * PI * W2));
+    uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * 4 * PI * W2));
+    void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
+    step([&] {
+        return launch_shift_copies_f32(static_cast<const float*>(in), cp, g.n, I, g.in_w, dp.p, pc.base, d.d, W2, stream);
+    });
+    step([&] { return launch_split_channels(cp, x4, g.n, PI, W2, 4, 0xAu, stream); });
+    step([&] { return launch_tc_conv(x4, wg4, out, sc.gs, kws, stream, sc.main_ch); });
+    return e;
+}
+
+// FP32 split path of backward-weight: x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the four
+// (k-block, c-block) tiles of the 2K x 2C gradient are summed; under the dilation plans the split
+// operands are relaid out exactly as the BF16 ones.
+cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const void* dy, float* dw, Bump& bump,
+                            cudaStream_t stream) {
+    const DilPlan dp = dil_plan(d, q);
+    const bool run = !bump.dry;
+    cudaError_t e = cudaSuccess;
+    auto step = [&](auto&& launch) {
+        if (run && e == cudaSuccess) e = launch();
+    };
+    const size_t nx = static_cast<size_t>(2 * d.n * d.c * d.w_in), ng = static_cast<size_t>(2 * d.n * d.k * q);
+    uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * nx);
+    uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * ng);
+    step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, 0x2u, stream); });
+    step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, 0x2u, stream); });
+    if (dp.kind == DilPlan::kPhases) {
+        const int64_t pitch = round8(std::max<int64_t>(d.w_in, q + 8 * (dp.sp - 1)));
+        uint16_t* xs = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * pitch));
+        float* dw4b = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * dp.sp));
+        float* dwb = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * dp.sp));
+        size_t kb = 0;
+        for (int64_t b = 0; b < dp.p; ++b)
+            kb = std::max(kb, tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, ceil_div(d.s - b, dp.m), 8, q));
+        void* kws = bump.take<char>(kb);
+        for (int64_t b = 0; b < dp.p; ++b) {
+            const int64_t sb = ceil_div(d.s - b, dp.m);
+            step([&] { return launch_shift_copies(x2, C1D_DTYPE_BF16, xs, d.n, 2 * d.c, d.w_in, 1, b * d.d, 0, pitch, stream); });
+            step([&] { return launch_tc_wgrad(xs, g2, dw4b, kws, d.n, 2 * d.c, 2 * d.k, sb, 8, q, stream, pitch); });
+            step([&] { return launch_sum_split_blocks(dw4b, dwb, d.k, d.c, sb, stream); });
+            step([&] { return launch_scatter_phase_wgrad(dwb, dw, d.k, d.c, d.s, dp.m, b, stream); });
+        }
+        return e;
+    }
+    float* dw4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+    if (dp.kind == DilPlan::kPlanes) {
+        uint16_t* px = bump.take<uint16_t>(sizeof(uint16_t) * nx);
+        uint16_t* pg = bump.take<uint16_t>(sizeof(uint16_t) * ng);
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m));
+        step([&] { return launch_to_planes(x2, C1D_DTYPE_BF16, px, d.n, 2 * d.c, d.w_in, dp.m, stream); });
+        step([&] { return launch_to_planes(g2, C1D_DTYPE_BF16, pg, d.n, 2 * d.k, q, dp.m, stream); });
+        step([&] { return launch_tc_wgrad(px, pg, dw4, kws, d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m, stream); });
+    } else {
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, 8, q));
+        step([&] { return launch_tc_wgrad(x2, g2, dw4, kws, d.n, 2 * d.c, 2 * d.k, d.s, 8, q, stream); });
+    }
+    step([&] { return launch_sum_split_blocks(dw4, dw, d.k, d.c, d.s, stream); });
+    return e;
+}
+
+size_t split_workspace(const c1d_desc& d, c1d_pass pass, int64_t q) {
+    Bump dry{nullptr, 0, true};
+    if (pass == C1D_PASS_BACKWARD_WEIGHT)
+        split_wgrad_run(d, q, nullptr, nullptr, nullptr, dry, nullptr);
+    else
+        split_conv_run(d, pass, q, nullptr, nullptr, nullptr, dry, nullptr);
+    return dry.used;
+}
+
 // Conv-shaped pass (forward or backward-data).
 c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const float* w_kcs, float* out,
                      void* ws, size_t ws_bytes, cudaStream_t stream) {
@@ -382,26 +520,8 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     st = acquire_workspace(ws, ws_bytes, workspace_for(d, pass, q, algo), &bump);
     if (st != C1D_OK) return st;
     if (algo == C1D_ALGO_BF16X3) {
-        // FP32 via split BF16 operands (split.cu): input channel blocks [hi | lo | hi | lo] against
-        // weight blocks [hi | hi | lo | lo]; block 0 (hi*hi) accumulates in its own TMEM region.
-        const ConvGeom gs = split_geom(d, q, pass);
-        const int64_t main_ch = split_main_ch(d, pass);
-        uint16_t* in4 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(gs.n * gs.in_ch * gs.in_w));
-        float* w4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
-        float* wg4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
-        cudaError_t e = launch_split_channels(static_cast<const float*>(in), in4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "split_channels");
-        if (pass == C1D_PASS_FORWARD) {
-            e = launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 1, 4, 0xCu, stream);  // c-blocks hi,hi,lo,lo
-            if (e == cudaSuccess) e = launch_prep_weights(w4, wg4, d.k, 4 * d.c, d.s, kWeightsForward, false, stream);
-        } else {
-            e = launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 4, 1, 0xCu, stream);  // k-blocks hi,hi,lo,lo
-            if (e == cudaSuccess)
-                e = launch_prep_weights(w4, wg4, 4 * d.k, d.c, d.s, kWeightsBackwardData, false, stream);
-        }
-        if (e != cudaSuccess) return cuda_fail(e, "split_weights");
-        void* kws = bump.take<char>(tc_conv_workspace_bytes(gs, main_ch));
-        e = launch_tc_conv(in4, wg4, out, gs, kws, stream, main_ch);
+        // FP32 via split BF16 operands (split.cu), composed with the dilation plans
+        const cudaError_t e = split_conv_run(d, pass, q, in, w_kcs, out, bump, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (bf16x3)");
         return C1D_OK;
     }
@@ -560,17 +680,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     const bool bf16 = is_bf16(d);
     cudaError_t e;
     if (algo == C1D_ALGO_BF16X3) {
-        // FP32 via split BF16 operands: x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the four
-        // (k-block, c-block) tiles of the 2K x 2C gradient are summed.
-        uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * d.w_in));
-        uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.k * q));
-        float* dw4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
-        e = launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, 0x2u, stream);
-        if (e == cudaSuccess) e = launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, 0x2u, stream);
-        if (e != cudaSuccess) return cuda_fail(e, "split_channels");
-        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q));
-        e = launch_tc_wgrad(x2, g2, dw4, kws, d.n, 2 * d.c, 2 * d.k, d.s, d.d, q, stream);
-        if (e == cudaSuccess) e = launch_sum_split_blocks(dw4, dw_kcs, d.k, d.c, d.s, stream);
+        e = split_wgrad_run(d, q, x, dy, dw_kcs, bump, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (bf16x3)");
         return C1D_OK;
     }

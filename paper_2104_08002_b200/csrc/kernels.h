@@ -88,6 +88,8 @@ cudaError_t launch_from_planes(const float* in, float* out, int64_t n, int64_t c
 // b < P, 0 where the source column is outside [0, w); out rows have pitch w_out.
 cudaError_t launch_shift_copies(const void* in, int in_dtype, uint16_t* out, int64_t n, int64_t I, int64_t w,
                                 int64_t P, int64_t base, int64_t delta, int64_t w_out, cudaStream_t stream);
+cudaError_t launch_shift_copies_f32(const float* in, float* out, int64_t n, int64_t I, int64_t w, int64_t P,
+                                    int64_t base, int64_t delta, int64_t w_out, cudaStream_t stream);
 // out[r][j] = bf16(in[r][j]) for j < w, 0 for w <= j < w_pad (rows of a zero-padded bf16 copy)
 cudaError_t launch_pad_rows(const void* in, int in_dtype, uint16_t* out, int64_t rows, int64_t w, int64_t w_pad,
                             cudaStream_t stream);

@@ -98,8 +98,8 @@ __global__ void from_planes_kernel(const float* __restrict__ in, float* __restri
     }
 }
 
-template <typename TIn>
-__global__ void shift_copies_kernel(const TIn* __restrict__ in, uint16_t* __restrict__ out, int64_t n, int64_t I,
+template <typename TIn, typename TOut>
+__global__ void shift_copies_kernel(const TIn* __restrict__ in, TOut* __restrict__ out, int64_t n, int64_t I,
                                     int64_t w, int64_t P, int64_t base, int64_t delta, int64_t w_out) {
     const int64_t total = n * P * I * w_out;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -107,15 +107,19 @@ __global__ void shift_copies_kernel(const TIn* __restrict__ in, uint16_t* __rest
         const int64_t row = e / w_out;  // (n, b, i)
         const int64_t i = row % I, b = (row / I) % P, nn = row / (I * P);
         const int64_t src = j + base + b * delta;
-        uint16_t v = 0;
-        if (src >= 0 && src < w) {
-            const int64_t at = (nn * I + i) * w + src;
-            if constexpr (sizeof(TIn) == 4)
-                v = fp32_to_bf16_bits(reinterpret_cast<const float*>(in)[at]);
-            else
-                v = reinterpret_cast<const uint16_t*>(in)[at];
+        if constexpr (sizeof(TOut) == 4) {  // FP32 copy (the split-FP32 path splits afterwards)
+            out[e] = (src >= 0 && src < w) ? in[(nn * I + i) * w + src] : 0.0f;
+        } else {
+            uint16_t v = 0;
+            if (src >= 0 && src < w) {
+                const int64_t at = (nn * I + i) * w + src;
+                if constexpr (sizeof(TIn) == 4)
+                    v = fp32_to_bf16_bits(reinterpret_cast<const float*>(in)[at]);
+                else
+                    v = reinterpret_cast<const uint16_t*>(in)[at];
+            }
+            out[e] = v;
         }
-        out[e] = v;
     }
 }
 
@@ -142,11 +146,19 @@ cudaError_t launch_shift_copies(const void* in, int in_dtype, uint16_t* out, int
                                 int64_t P, int64_t base, int64_t delta, int64_t w_out, cudaStream_t stream) {
     const int64_t total = n * P * I * w_out;
     if (in_dtype == 0)
-        shift_copies_kernel<float><<<blocks_for(total), 256, 0, stream>>>(static_cast<const float*>(in), out, n, I, w,
-                                                                          P, base, delta, w_out);
+        shift_copies_kernel<float, uint16_t><<<blocks_for(total), 256, 0, stream>>>(static_cast<const float*>(in), out,
+                                                                                    n, I, w, P, base, delta, w_out);
     else
-        shift_copies_kernel<uint16_t><<<blocks_for(total), 256, 0, stream>>>(static_cast<const uint16_t*>(in), out, n,
-                                                                             I, w, P, base, delta, w_out);
+        shift_copies_kernel<uint16_t, uint16_t><<<blocks_for(total), 256, 0, stream>>>(
+            static_cast<const uint16_t*>(in), out, n, I, w, P, base, delta, w_out);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shift_copies_f32(const float* in, float* out, int64_t n, int64_t I, int64_t w, int64_t P,
+                                    int64_t base, int64_t delta, int64_t w_out, cudaStream_t stream) {
+    shift_copies_kernel<float, float><<<blocks_for(n * P * I * w_out), 256, 0, stream>>>(in, out, n, I, w, P, base,
+                                                                                         delta, w_out);
     note_launch();
     return cudaGetLastError();
 }

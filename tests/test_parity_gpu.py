@@ -246,3 +246,20 @@ def test_other_dilations_on_tensor_cores(d, bf16_storage, q):
     want = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), d)
     for g, wv, name in zip(got, want, ("fwd", "bwd_d", "bwd_w")):
         assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} q={q} {name}")
+
+
+@pytest.mark.parametrize("d", [1, 2, 4, 8, 16])
+def test_fp32_split_path_other_dilations(d):
+    """FP32 precision on the tensor cores (bf16x3 operand split) composed with the dilation
+    rewrites, vs the naive FP32 oracle at the reference's 1e-5 bound."""
+    rng = oracle.Rng(2000 + d)
+    n, c, k, s = 2, 16, 24, 9
+    q = 2 * 8 * max(d, 8) * 2
+    w_in = q + d * (s - 1)
+    x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
+    p = cv.ConvParams(c, k, s, d, cv.Precision.Fp32)
+    for i in range(3):
+        assert cv.selected_algo(p, n, w_in, i, in_dtype=0, algo="bf16x3") == "bf16x3", (d, i)
+    got = run_passes(x, w, dy, d, cv.Precision.Fp32, algo="bf16x3")
+    for g, wv, name in zip(got, oracle_passes(x, w, dy, d), ("fwd", "bwd_d", "bwd_w")):
+        assert_close(g, wv, FP32_TOL, f"d={d} {name}")
