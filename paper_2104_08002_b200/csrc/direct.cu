@@ -211,21 +211,24 @@ cudaError_t launch_direct_conv(const void* in, int in_dtype, bool round_in, cons
 }
 
 // ------------------------------------------------------------------------------- backward weight
-// Split-W partial sums: block (kb, cb, split) owns a 16x16 (filter, channel) tile and a
-// contiguous range of (item, 128-column chunk) work units; each thread owns one (k, c) pair and
-// up to 64 taps in registers. Partials land in workspace[split][k][c][s] and a second kernel
-// sums the splits in ascending order (deterministic; the reference reduces per-item partials
-// in ascending item order, conv.cpp:308-314).
+// Register-tiled FFMA gradient. Block (kt, ct, split) owns a 32-filter x 32-channel tile and a
+// contiguous range of (item, 128-column chunk) units of its split; taps are processed in groups
+// of 8 (outer loop) so every thread keeps 4 filters x 8 taps of one channel in registers. Per
+// column a thread reads 4 dY values (warp-broadcast) and 8 X values (one row per lane) from shared
+// memory for 32 FMAs. Partials land in workspace[split][k][c][s] and a second kernel sums the
+// splits in ascending order (deterministic; the reference reduces per-item partials in ascending
+// item order, conv.cpp:308-314).
 namespace {
-constexpr int kWT = 16;     // filters / channels per block tile
-constexpr int kWQ = 128;    // columns per chunk
-constexpr int kWS = 64;     // taps held in registers per pass
+constexpr int kWK = 32;     // filters per block tile
+constexpr int kWC = 32;     // channels per block tile
+constexpr int kWQ = 128;    // columns per unit
+constexpr int kWG = 8;      // taps per group
 }  // namespace
 
 static int64_t wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t q) {
-    const int64_t tiles = ceil_div(k, kWT) * ceil_div(c, kWT);
+    const int64_t tiles = ceil_div(k, kWK) * ceil_div(c, kWC);
     const int64_t units = n * ceil_div(q, kWQ);
-    const int64_t want = std::max<int64_t>(1, (2 * num_sms() + tiles - 1) / tiles);
+    const int64_t want = std::max<int64_t>(1, (4 * num_sms() + tiles - 1) / tiles);
     return std::max<int64_t>(1, std::min<int64_t>(want, units));
 }
 
@@ -241,56 +244,69 @@ template <typename TIn>
 __global__ void __launch_bounds__(256) direct_wgrad_kernel(const TIn* __restrict__ x, const TIn* __restrict__ dy,
                                                            float* __restrict__ part, int64_t N, int64_t C, int64_t K,
                                                            int64_t S, int64_t D, int64_t Q, int64_t splits,
-                                                           int round_in) {
+                                                           int tg, int xpitch, int round_in) {
     extern __shared__ float smem[];
-    const int64_t halo = (S - 1) * D;
-    const int64_t span = kWQ + halo;
-    float* xs = smem;                   // [kWT][span]
-    float* gs = smem + kWT * span;      // [kWT][kWQ]
+    float* gs = smem;                    // [kWK][kWQ]        dY chunk
+    float* xs = smem + kWK * kWQ;        // [kWC][xpitch]     X window of one tap group
     const int tid = threadIdx.x;
-    const int kl = tid / kWT, cl = tid % kWT;
-    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kWT, c0 = static_cast<int64_t>(blockIdx.y) * kWT;
+    const int cl = tid % kWC, kg = tid / kWC;  // channel lane, filter quad (0..7)
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kWK, c0 = static_cast<int64_t>(blockIdx.y) * kWC;
     const int64_t split = blockIdx.z;
     const int64_t chunks_per_item = ceil_div(Q, kWQ);
     const int64_t units = N * chunks_per_item;
     const int64_t u_begin = units * split / splits, u_end = units * (split + 1) / splits;
-    const int64_t W = Q + halo;
-
-    for (int64_t s0 = 0; s0 < S; s0 += kWS) {
-        float acc[kWS];
+    const int64_t W = Q + (S - 1) * D;
+    const int64_t span = kWQ + (tg - 1) * D;  // X columns one tap group reads per chunk
+    for (int64_t s0 = 0; s0 < S; s0 += tg) {
+        float acc[4][kWG];
 #pragma unroll
-        for (int j = 0; j < kWS; ++j) acc[j] = 0.0f;
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < kWG; ++j) acc[i][j] = 0.0f;
         for (int64_t u = u_begin; u < u_end; ++u) {
             const int64_t n = u / chunks_per_item;
             const int64_t q0 = (u % chunks_per_item) * kWQ;
             __syncthreads();
-            for (int64_t e = tid; e < kWT * span; e += blockDim.x) {
-                const int64_t cc = e / span, xx = e % span;
-                const int64_t c = c0 + cc, pos = q0 + xx;
-                xs[e] = (c < C && pos < W) ? load_as_float(x, (n * C + c) * W + pos, round_in != 0) : 0.0f;
-            }
-            for (int64_t e = tid; e < kWT * kWQ; e += blockDim.x) {
-                const int64_t kk = e / kWQ, xx = e % kWQ;
+            // dY chunk: row kk = e / kWQ (kWQ is a power of two: shifts, no 64-bit division)
+            for (int e = tid; e < kWK * kWQ; e += 256) {
+                const int kk = e / kWQ, xx = e % kWQ;
                 const int64_t k = k0 + kk, pos = q0 + xx;
                 gs[e] = (k < K && pos < Q) ? load_as_float(dy, (n * K + k) * Q + pos, round_in != 0) : 0.0f;
             }
+            const int64_t xbase = q0 + s0 * D;
+            for (int cc = tid / 32; cc < kWC; cc += 8) {  // one warp per channel row, coalesced
+                const int64_t c = c0 + cc;
+                const TIn* row = x + (n * C + c) * W;
+                for (int xx = tid % 32; xx < span; xx += 32) {
+                    const int64_t pos = xbase + xx;
+                    xs[cc * xpitch + xx] = (c < C && pos < W) ? load_as_float(row, pos, round_in != 0) : 0.0f;
+                }
+            }
             __syncthreads();
-            const float* xr = xs + cl * span + s0 * D;
-            const float* gr = gs + kl * kWQ;
+            const float* xr = xs + cl * xpitch;
+            const float* gr = gs + (kg * 4) * kWQ;
             for (int xx = 0; xx < kWQ; ++xx) {
-                const float gv = gr[xx];
+                float gv[4];
 #pragma unroll
-                for (int j = 0; j < kWS; ++j) {
-                    if (s0 + j < S) acc[j] = fmaf(xr[xx + j * D], gv, acc[j]);
+                for (int i = 0; i < 4; ++i) gv[i] = gr[i * kWQ + xx];
+#pragma unroll
+                for (int j = 0; j < kWG; ++j) {
+                    if (j >= tg) break;
+                    const float xv = xr[xx + j * D];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[i][j] = fmaf(gv[i], xv, acc[i][j]);
                 }
             }
         }
-        const int64_t k = k0 + kl, c = c0 + cl;
-        if (k < K && c < C) {
+        const int64_t c = c0 + cl;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t k = k0 + kg * 4 + i;
+            if (k >= K || c >= C) continue;
             float* dst = part + ((split * K + k) * C + c) * S;
 #pragma unroll
-            for (int j = 0; j < kWS; ++j)
-                if (s0 + j < S) dst[s0 + j] = acc[j];
+            for (int j = 0; j < kWG; ++j)
+                if (j < tg && s0 + j < S) dst[s0 + j] = acc[i][j];
         }
     }
 }
@@ -478,10 +494,17 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
         return cudaGetLastError();
     }
     const int64_t splits = wgrad_splits(n, c, k, q);
-    const int64_t span = kWQ + (s - 1) * d;
-    const size_t smem = sizeof(float) * static_cast<size_t>(kWT * span + kWT * kWQ);
+    // taps per group: 8, fewer when a huge dilation would not fit the X window in shared memory
+    int tg = static_cast<int>(std::min<int64_t>(kWG, s));
+    auto smem_for = [&](int g) {
+        const int64_t span = kWQ + (g - 1) * d;
+        return sizeof(float) * static_cast<size_t>(kWK * kWQ + kWC * (span | 1));
+    };
+    while (tg > 1 && smem_for(tg) > 200 * 1024) --tg;
+    const int xpitch = static_cast<int>((kWQ + (tg - 1) * d) | 1);  // odd: 32 channel rows, distinct banks
+    const size_t smem = smem_for(tg);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    dim3 grid(static_cast<unsigned>(ceil_div(k, kWT)), static_cast<unsigned>(ceil_div(c, kWT)),
+    dim3 grid(static_cast<unsigned>(ceil_div(k, kWK)), static_cast<unsigned>(ceil_div(c, kWC)),
               static_cast<unsigned>(splits));
     cudaError_t e;
     if (in_dtype == 0) {
@@ -490,14 +513,14 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
         if (e != cudaSuccess) return e;
         direct_wgrad_kernel<float><<<grid, 256, smem, stream>>>(static_cast<const float*>(x),
                                                                  static_cast<const float*>(dy), workspace, n, c, k, s,
-                                                                 d, q, splits, round_in ? 1 : 0);
+                                                                 d, q, splits, tg, xpitch, round_in ? 1 : 0);
     } else {
         e = cudaFuncSetAttribute(direct_wgrad_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem));
         if (e != cudaSuccess) return e;
         direct_wgrad_kernel<uint16_t><<<grid, 256, smem, stream>>>(static_cast<const uint16_t*>(x),
                                                                     static_cast<const uint16_t*>(dy), workspace, n, c,
-                                                                    k, s, d, q, splits, 0);
+                                                                    k, s, d, q, splits, tg, xpitch, 0);
     }
     note_launch();
     e = cudaGetLastError();
