@@ -67,10 +67,17 @@ struct Plan {
     size_t smem_bytes;
     int kgroups;     // filter groups of kp
     uint32_t acc2;   // TMEM column offset of the second accumulator region (0 = none)
+    // Tail taps (the last, partly filled tap block): instead of a 16-tap block per channel that
+    // is mostly zero, one MMA per (tile, stage) contracts tail x cc (tap, channel) pairs (K <= 16)
+    // from a q-chunk-major copy of the stage's channels (4-D TMA box), into the same slot.
+    int tail;              // taps in the last block (0 = off: the last block is a regular block)
+    int tail_chunks;       // q-chunks (8 columns x cc channels) of the tail box
+    uint32_t tx_stage_bytes, tw_stage_bytes;  // tail X box / tail weight image per stage
 };
 
 struct KParams {
     int64_t n_items, in_ch, in_w, out_ch, out_w, in_off;
+    const uint16_t* bimg_tail;  // this filter group's tail image: [chunk][KP rows][16] bf16
     int64_t tiles_per_item, total_tiles;
     int taps, k_begin;
     Plan pl;
@@ -80,7 +87,8 @@ struct KParams {
     unsigned long long* prof;  // optional per-CTA cycle counters (C1D_PROFILE=1), else nullptr
 };
 
-bool make_plan(const ConvGeom& g, Plan* pl, bool two_regions = false) {
+bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0) {
+    const bool two_regions = main_ch > 0;
     if (g.dil != 8) return false;
     const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
     if (pitch % 8 != 0 || pitch < g.in_w || g.in_w < 8) return false;  // TMA global stride: multiple of 16 B
@@ -109,9 +117,22 @@ bool make_plan(const ConvGeom& g, Plan* pl, bool two_regions = false) {
         const int64_t nch = ceil_div(g.in_ch, p.cc);  // balance the chunks
         p.cc = static_cast<int>(ceil_div(g.in_ch, nch));
     }
+    // tail path: wide filter blocks only (the N = (G-1)*KP main MMA stays >= 128) and the stage's
+    // (tap, channel) pairs must fit one K = 16 MMA; in split mode stages may not straddle main_ch
+    p.tail = 0;
+    {
+        const int tail = static_cast<int>(g.taps - static_cast<int64_t>(kTapsPerBlock) * (p.g - 1));
+        if (p.g >= 2 && p.kp == 64 && (p.g - 1) * p.kp >= 128 && tail * p.cc <= kTapsPerBlock &&
+            (!two_regions || main_ch % p.cc == 0) && getenv("C1D_NO_TAIL") == nullptr) {
+            p.tail = tail;
+            p.tail_chunks = 16 * p.t + static_cast<int>(ceil_div(kTapsPerBlock, p.cc));
+        }
+    }
     p.x_stage_bytes = static_cast<uint32_t>(p.cc * p.xw * 2);
     p.w_stage_bytes = static_cast<uint32_t>(p.cc) * p.b_chan_bytes;
-    const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes;
+    p.tx_stage_bytes = p.tail ? ((static_cast<uint32_t>(p.tail_chunks * p.cc * 16) + 1023) & ~1023u) : 0;
+    p.tw_stage_bytes = p.tail ? static_cast<uint32_t>(p.kp * kTapsPerBlock * 2) : 0;
+    const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.tx_stage_bytes + p.tw_stage_bytes;
     p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / stage));
     if (p.stages < 2) return false;
     p.smem_bytes = static_cast<size_t>(p.stages) * stage + 1024;
@@ -139,6 +160,27 @@ __global__ void pack_bimg_kernel(const float* __restrict__ wg, uint16_t* __restr
         if (o < out_ch && s < taps) v = wg[(o * in_ch + c) * taps + s];
         const int64_t off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
         img[(kg * in_ch + c) * per_chan + off] = fp32_to_bf16_bits(v);
+    }
+}
+
+// Tail image: img[kg][chunk h][row o][k] with k = r*cc + c (tap 16(G-1) + r of channel h*cc + c),
+// same K-major SWIZZLE_NONE core-matrix order as above; zero for k >= tail*cc or past C / K.
+__global__ void pack_tail_kernel(const float* __restrict__ wg, uint16_t* __restrict__ img, int64_t out_ch,
+                                 int64_t in_ch, int64_t taps, int kp, int g, int kgroups, int cc, int tail,
+                                 int64_t chunks) {
+    const int64_t per = static_cast<int64_t>(kp) * kTapsPerBlock;
+    const int64_t total = static_cast<int64_t>(kgroups) * chunks * per;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = e % kTapsPerBlock;
+        const int64_t row = (e / kTapsPerBlock) % kp;
+        const int64_t h = (e / per) % chunks;
+        const int64_t kg = e / (per * chunks);
+        const int64_t r = k / cc, c = h * cc + k % cc, o = kg * kp + row;
+        const int64_t s = static_cast<int64_t>(g - 1) * kTapsPerBlock + r;
+        float v = 0.0f;
+        if (r < tail && c < in_ch && o < out_ch && s < taps) v = wg[(o * in_ch + c) * taps + s];
+        const int64_t off = (row / 8) * 128 + (k / 8) * 64 + (row % 8) * 8 + (k % 8);
+        img[(kg * chunks + h) * per + off] = fp32_to_bf16_bits(v);
     }
 }
 
@@ -201,7 +243,8 @@ __device__ __forceinline__ Cursor make_cursor(const KParams& p) {
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-    tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const KParams p) {
+    tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
+                   const KParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t stage_full[kMaxStages], stage_empty[kMaxStages];
     __shared__ uint64_t tmem_full, tmem_empty;
@@ -212,6 +255,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* xs_base = smem;
     uint8_t* ws_base = smem + static_cast<size_t>(pl.stages) * pl.x_stage_bytes;
+    uint8_t* tx_base = ws_base + static_cast<size_t>(pl.stages) * pl.w_stage_bytes;
+    uint8_t* tw_base = tx_base + static_cast<size_t>(pl.stages) * pl.tx_stage_bytes;
     const int G = pl.g, T = pl.t, KP = pl.kp;
     const int64_t J = p.tiles_per_item;
     const int n_chunks = static_cast<int>(ceil_div(p.in_ch, pl.cc));
@@ -235,6 +280,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------------ TMA producer
         if (lane == 0) {
             prefetch_tmap(&tmap);
+            if (pl.tail) prefetch_tmap(&tmap_tail);
             long long t_wait = 0;
             const long long t_begin = clock64();
             Cursor cur = make_cursor(p);
@@ -251,7 +297,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(smem_u32(&stage_empty[stage]), phase ^ 1);
                     t_wait += clock64() - tw0;
                     const uint32_t full = smem_u32(&stage_full[stage]);
-                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (nseg * kSegQ * 2 + pl.b_chan_bytes);
+                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (nseg * kSegQ * 2 + pl.b_chan_bytes) +
+                                           (pl.tail ? pl.tail_chunks * pl.cc * 16u + pl.tw_stage_bytes : 0u);
                     mbar_arrive_expect_tx(full, bytes);
                     const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
                     for (int c = 0; c < ccn; ++c) {
@@ -263,6 +310,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                     bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
                              static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
+                    if (pl.tail) {
+                        // q-chunk-major box of the stage's cc channels over the same input tiles
+                        // (tap block G-1 of input tile p lands on output slot t, like block 0 of B)
+                        const uint32_t tx = smem_u32(tx_base + static_cast<size_t>(stage) * pl.tx_stage_bytes);
+                        const int32_t chunk0 = x_start / 8;  // in_off is a multiple of 8
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+                            "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(tx),
+                            "l"(&tmap_tail), "r"(0), "r"(c0), "r"(chunk0), "r"(static_cast<int32_t>(su.n)), "r"(full)
+                            : "memory");
+                        const uint32_t tw = smem_u32(tw_base + static_cast<size_t>(stage) * pl.tw_stage_bytes);
+                        bulk_g2s(tw, p.bimg_tail + static_cast<size_t>(ch) * (pl.tw_stage_bytes / 2), pl.tw_stage_bytes,
+                                 full);
+                    }
                     if (++stage == pl.stages) {
                         stage = 0;
                         phase ^= 1;
@@ -283,7 +344,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         Cursor cur = make_cursor(p);
         int stage = 0;
         uint32_t phase = 0, tphase = 0;
-        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(G * KP), kFmtBF16, 1, 0);
+        // tail mode: the main MMA covers blocks 1..G-1 (slots t+1..t+G-1), the tail MMA slot t
+        const int gm = pl.tail ? G - 1 : G;
+        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(gm * KP), kFmtBF16, 1, 0);
+        const uint32_t idesc_tail = make_idesc(128, static_cast<uint32_t>(KP), kFmtBF16, 1, 0);
+        const uint32_t main_slot = pl.tail ? static_cast<uint32_t>(KP) : 0u;       // D column offset
+        const uint32_t main_brow = pl.tail ? static_cast<uint32_t>(KP) * 32u : 0u;  // skip block 0 of B
         Super su;
         while (next_super(cur, J, G, T, &su)) {
             const long long ts0 = clock64();
@@ -301,13 +367,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
                 const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                 const uint64_t a0 = make_smem_desc(xs, 128, 16, kLayoutNone);
-                const uint64_t b0 = make_smem_desc(wsm, 128, 256, kLayoutNone);
+                const uint64_t b0 = make_smem_desc(wsm + main_brow, 128, 256, kLayoutNone);
                 if (elect_one()) {
                     uint64_t bdesc = b0;
                     uint64_t achan = a0;
                     for (int c = 0; c < ccn; ++c) {
                         uint64_t adesc = achan;
-                        uint32_t dcol = tmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u);
+                        uint32_t dcol = tmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u) + main_slot;
                         for (int t = 0; t < su.tcur; ++t) {
                             mma_bf16_ss(dcol, adesc, bdesc, idesc, 1);
                             adesc = desc_advance(adesc, static_cast<uint32_t>(kTileQ * 2));
@@ -315,6 +381,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                         bdesc = desc_advance(bdesc, pl.b_chan_bytes);
                         achan = desc_advance(achan, static_cast<uint32_t>(pl.xw * 2));
+                    }
+                    if (pl.tail) {
+                        // A[m][k = r*cc + c] = x[c][q0 + m + 8r] (tap 16(G-1) + r): MN-major, K rows
+                        // 16 B apart (contiguous), M groups of 8 columns one q-chunk (cc*16 B) apart
+                        const uint32_t tx = smem_u32(tx_base + static_cast<size_t>(stage) * pl.tx_stage_bytes);
+                        const uint32_t tw = smem_u32(tw_base + static_cast<size_t>(stage) * pl.tw_stage_bytes);
+                        uint64_t adesc = make_smem_desc(tx, 128, static_cast<uint32_t>(pl.cc * 16), kLayoutNone);
+                        const uint64_t bt = make_smem_desc(tw, 128, 256, kLayoutNone);
+                        uint32_t dcol = tmem + ((c0 >= p.main_ch) ? pl.acc2 : 0u);
+                        for (int t = 0; t < su.tcur; ++t) {
+                            mma_bf16_ss(dcol, adesc, bt, idesc_tail, 1);
+                            adesc = desc_advance(adesc, static_cast<uint32_t>(16 * pl.cc * 16));
+                            dcol += static_cast<uint32_t>(KP);
+                        }
                     }
                 }
                 __syncwarp();
@@ -423,22 +503,34 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 
 bool tc_conv_supported(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
-    return make_plan(g, &pl, main_ch > 0);
+    return make_plan(g, &pl, main_ch);
 }
 
 size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
-    if (!make_plan(g, &pl, main_ch > 0)) return 0;
-    return static_cast<size_t>(pl.kgroups) * static_cast<size_t>(g.in_ch) * pl.b_chan_bytes;
+    if (!make_plan(g, &pl, main_ch)) return 0;
+    const size_t tail = pl.tail ? static_cast<size_t>(pl.kgroups) * ceil_div(g.in_ch, pl.cc) * pl.tw_stage_bytes : 0;
+    return static_cast<size_t>(pl.kgroups) * static_cast<size_t>(g.in_ch) * pl.b_chan_bytes + ((tail + 255) & ~size_t{255});
 }
 
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g, void* workspace,
                            cudaStream_t stream, int64_t main_ch) {
     Plan pl;
-    if (!make_plan(g, &pl, main_ch > 0)) return cudaErrorNotSupported;
+    if (!make_plan(g, &pl, main_ch)) return cudaErrorNotSupported;
     auto encode = get_encode_fn();
     if (!encode) return cudaErrorNotSupported;
     uint16_t* img = static_cast<uint16_t*>(workspace);
+    const int64_t n_chunks = ceil_div(g.in_ch, pl.cc);
+    uint16_t* img_tail = img + static_cast<size_t>(pl.kgroups) * g.in_ch * (pl.b_chan_bytes / 2);
+    if (pl.tail) {
+        const int64_t total = static_cast<int64_t>(pl.kgroups) * n_chunks * pl.kp * kTapsPerBlock;
+        const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
+        pack_tail_kernel<<<blocks, 256, 0, stream>>>(wg, img_tail, g.out_ch, g.in_ch, g.taps, pl.kp, pl.g, pl.kgroups,
+                                                     pl.cc, pl.tail, n_chunks);
+        note_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
     {
         const int64_t total = static_cast<int64_t>(pl.kgroups) * g.in_ch * pl.ntot * kTapsPerBlock;
         const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
@@ -456,6 +548,20 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
                         box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    CUtensorMap tmap_tail = tmap;  // unused unless pl.tail
+    if (pl.tail) {
+        // the input as (8 columns, channel, q-chunk, item): element (e, c, u, n) at ((n*C + c)*pitch + 8u + e)
+        const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
+        const cuuint64_t d4[4] = {8, static_cast<cuuint64_t>(g.in_ch), static_cast<cuuint64_t>(pitch / 8),
+                                  static_cast<cuuint64_t>(g.n)};
+        const cuuint64_t s4[3] = {static_cast<cuuint64_t>(pitch) * 2, 16, static_cast<cuuint64_t>(g.in_ch * pitch) * 2};
+        const cuuint32_t b4[4] = {8, static_cast<cuuint32_t>(pl.cc), static_cast<cuuint32_t>(pl.tail_chunks), 1};
+        const cuuint32_t e4[4] = {1, 1, 1, 1};
+        r = encode(&tmap_tail, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(in_bf16), d4, s4, b4, e4,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
     cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
     if (e != cudaSuccess) return e;
@@ -481,7 +587,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     for (int kg = 0; kg < pl.kgroups; ++kg) {
         kp.k_begin = kg * pl.kp;
         kp.bimg = img + static_cast<size_t>(kg) * g.in_ch * (pl.b_chan_bytes / 2);
-        tc_conv_kernel<<<grid, kThreads, pl.smem_bytes, stream>>>(tmap, kp);
+        kp.bimg_tail = img_tail + static_cast<size_t>(kg) * n_chunks * (pl.tw_stage_bytes / 2);
+        tc_conv_kernel<<<grid, kThreads, pl.smem_bytes, stream>>>(tmap, tmap_tail, kp);
         note_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -263,3 +263,22 @@ def test_fp32_split_path_other_dilations(d):
     got = run_passes(x, w, dy, d, cv.Precision.Fp32, algo="bf16x3")
     for g, wv, name in zip(got, oracle_passes(x, w, dy, d), ("fwd", "bwd_d", "bwd_w")):
         assert_close(g, wv, FP32_TOL, f"d={d} {name}")
+
+
+@pytest.mark.parametrize("s", [51, 49, 36, 40, 33])
+@pytest.mark.parametrize("precision", [cv.Precision.Bf16, cv.Precision.Fp32])
+def test_tail_tap_path(s, precision):
+    """tc_conv's tail-tap MMAs (the last, partly filled tap block contracted over (tap, channel)
+    pairs from a q-chunk-major box) at KP = 64: BF16 vs the rounded oracle, FP32 (bf16x3) vs the
+    naive oracle."""
+    rng = oracle.Rng(3000 + s)
+    n, c, k, q = 2, 64, 64, 640
+    w_in = q + 8 * (s - 1)
+    x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
+    got = run_passes(x, w, dy, 8, precision)
+    if precision == cv.Precision.Bf16:
+        want, tol = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), 8), BF16_TOL_ROUNDED
+    else:
+        want, tol = oracle_passes(x, w, dy, 8), FP32_TOL
+    for g, wv, name in zip(got, want, ("fwd", "bwd_d", "bwd_w")):
+        assert_close(g, wv, tol, f"s={s} {precision.name} {name}")
