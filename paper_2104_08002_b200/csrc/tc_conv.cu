@@ -429,10 +429,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t tphase = 0;
         Super su;
         const int slots = static_cast<int>(kTmemCols) / KP;
+        long long e_store = 0, e_carry = 0, e_zero = 0;  // C1D_PROFILE counters
         while (next_super(cur, J, G, T, &su)) {
             mbar_wait_sleep(smem_u32(&tmem_full), tphase, 256);
             tphase ^= 1;
             tc_fence_after();
+            const long long e0 = clock64();
             // 1. store the completed outputs (slots 0..tcur-1)
             for (int j = 0; j < su.tcur; ++j) {
                 const int64_t o = su.i0 - (G - 1) + j;
@@ -457,6 +459,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            const long long e1 = clock64();
+            e_store += e1 - e0;
             // 2. carry the partial outputs (slots tcur..tcur+G-2) down to slots 0..G-2
             if (!su.last_in_segment) {
                 for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u)) {
@@ -470,6 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            const long long e2 = clock64();
+            e_carry += e2 - e1;
             // 3. zero the slots the next super-tile accumulates from scratch
             const uint32_t region_cols = pl.acc2 ? pl.acc2 : static_cast<uint32_t>(slots * KP);
             for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u))
@@ -478,7 +484,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
+            e_zero += clock64() - e2;
             if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+        }
+        if (p.prof && threadIdx.x == 128) {
+            p.prof[blockIdx.x * 8 + 5] = e_store;
+            p.prof[blockIdx.x * 8 + 6] = e_carry;
+            p.prof[blockIdx.x * 8 + 7] = e_zero;
         }
     }
     tc_fence_before();
@@ -599,8 +611,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         double a[8] = {0};
         for (int b = 0; b < grid; ++b)
             for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[b * 8 + i]) / grid;
-        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f (cycles, CTA avg)\n",
-                a[0], a[1], a[2], a[3], a[4]);
+        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f | epilogue store %.0f carry %.0f zero %.0f (cycles, CTA avg)\n",
+                a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
         cudaFree(kp.prof);
     }
     return cudaSuccess;
