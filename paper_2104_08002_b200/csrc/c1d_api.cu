@@ -526,17 +526,20 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         return C1D_OK;
     }
     const bool bf16 = is_bf16(d);
+    const DilPlan dp = dil_plan(d, q);
+    // (o, i, s) weights for the FFMA / relayout paths; the native tensor-core path packs straight
+    // from the caller's KCS weights (one launch fewer)
     float* wg = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
-    cudaError_t e = launch_prep_weights(w_kcs, wg, d.k, d.c, d.s,
-                                        pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData, bf16,
-                                        stream);
+    cudaError_t e = cudaSuccess;
+    if (algo == C1D_ALGO_DIRECT || dp.kind != DilPlan::kNative)
+        e = launch_prep_weights(w_kcs, wg, d.k, d.c, d.s,
+                                pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData, bf16, stream);
     if (e != cudaSuccess) return cuda_fail(e, "prep_weights");
     if (algo == C1D_ALGO_DIRECT) {
         e = launch_direct_conv(in, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, wg, out, g, stream);
         if (e != cudaSuccess) return cuda_fail(e, "direct_conv");
         return C1D_OK;
     }
-    const DilPlan dp = dil_plan(d, q);
     if (dp.kind == DilPlan::kPlanes) {
         // d = 8m: de-interleave the input into chunk planes, run dilation 8, re-interleave
         const ConvGeom gp = plane_geom(g, dp);
@@ -579,7 +582,7 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         in_b = tmp;
     }
     void* kws = bump.take<char>(tc_conv_workspace_bytes(gq));
-    e = launch_tc_conv(in_b, wg, out, gq, kws, stream);
+    e = launch_tc_conv(in_b, w_kcs, out, gq, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA);
     if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
     return C1D_OK;
 }

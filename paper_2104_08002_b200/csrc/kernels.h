@@ -59,8 +59,10 @@ struct TcConvPlan;
 // that the epilogue adds to the first, so the long accumulation chain only carries the main term.
 bool tc_conv_supported(const ConvGeom& g, int64_t main_ch = 0);
 size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch = 0);
+// wg: (o, i, s) weights of the forward-shaped problem, or with w_bwd_raw the caller's KCS weights of
+// a backward-data pass (transposed and tap-reversed while packing).
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g,
-                           void* workspace, cudaStream_t stream, int64_t main_ch = 0);
+                           void* workspace, cudaStream_t stream, int64_t main_ch = 0, bool w_bwd_raw = false);
 
 bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);

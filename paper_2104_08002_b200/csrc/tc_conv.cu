@@ -141,46 +141,52 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0) {
 }
 
 // ---------------------------------------------------------------------------- B image packing
-// img[kg][c][row][r] (row = b*KP + o, b = G-1-tap block) in the K-major SWIZZLE_NONE core-matrix order:
-//   element (row, r) at (row/8)*128 + (r/8)*64 + (row%8)*8 + (r%8)   (SBO 256 B, LBO 128 B)
-__global__ void pack_bimg_kernel(const float* __restrict__ wg, uint16_t* __restrict__ img, int64_t out_ch,
-                                 int64_t in_ch, int64_t taps, int kp, int g, int kgroups) {
-    const int64_t ntot = static_cast<int64_t>(g) * kp;
-    const int64_t per_chan = ntot * kTapsPerBlock;
-    const int64_t total = static_cast<int64_t>(kgroups) * in_ch * per_chan;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e % kTapsPerBlock;
-        const int64_t row = (e / kTapsPerBlock) % ntot;
-        const int64_t c = (e / per_chan) % in_ch;
-        const int64_t kg = e / (per_chan * in_ch);
-        // B row block b holds tap block G-1-b: input tile i0+t then writes output slot t+b, i.e.
-        // column (t+b)*KP, because tap block g of tile p lands on output tile p-g.
-        const int64_t blk = row / kp, o = kg * kp + row % kp, s = (g - 1 - blk) * kTapsPerBlock + r;
-        float v = 0.0f;
-        if (o < out_ch && s < taps) v = wg[(o * in_ch + c) * taps + s];
-        const int64_t off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
-        img[(kg * in_ch + c) * per_chan + off] = fp32_to_bf16_bits(v);
-    }
+// Weight value (o, i, s) of the forward-shaped problem: from prepped (o, i, s) weights, or straight
+// from the caller's KCS weights for backward-data (o = c, i = k, taps reversed; tensor.cpp:23-41)
+// so the separate prep launch disappears. BF16 RNE happens in the packing (bf16.hpp:29-40).
+__device__ __forceinline__ float wval(const float* __restrict__ w, int bwd_raw, int64_t O, int64_t I, int64_t S,
+                                      int64_t o, int64_t i, int64_t s) {
+    return bwd_raw ? w[(i * O + o) * S + (S - 1 - s)] : w[(o * I + i) * S + s];
 }
 
-// Tail image: img[kg][chunk h][row o][k] with k = r*cc + c (tap 16(G-1) + r of channel h*cc + c),
-// same K-major SWIZZLE_NONE core-matrix order as above; zero for k >= tail*cc or past C / K.
-__global__ void pack_tail_kernel(const float* __restrict__ wg, uint16_t* __restrict__ img, int64_t out_ch,
-                                 int64_t in_ch, int64_t taps, int kp, int g, int kgroups, int cc, int tail,
-                                 int64_t chunks) {
-    const int64_t per = static_cast<int64_t>(kp) * kTapsPerBlock;
-    const int64_t total = static_cast<int64_t>(kgroups) * chunks * per;
+// One launch packs both images, in the K-major SWIZZLE_NONE core-matrix order
+//   element (row, r) at (row/8)*128 + (r/8)*64 + (row%8)*8 + (r%8)   (SBO 256 B, LBO 128 B):
+//  main: img[kg][c][row][r], row = b*KP + o, block b holds tap block G-1-b: input tile i0+t then
+//        writes output slot t+b (column (t+b)*KP), because tap block g of tile p lands on tile p-g.
+//  tail: timg[kg][chunk h][row o][k], k = r*cc + c: tap 16(G-1) + r of channel h*cc + c, zero for
+//        k >= tail*cc or past C / K (the tail-tap MMAs, see Plan::tail).
+__global__ void pack_images_kernel(const float* __restrict__ w, int bwd_raw, uint16_t* __restrict__ img,
+                                   uint16_t* __restrict__ timg, int64_t out_ch, int64_t in_ch, int64_t taps, int kp,
+                                   int g, int kgroups, int cc, int tail, int64_t chunks) {
+    const int64_t ntot = static_cast<int64_t>(g) * kp;
+    const int64_t per_chan = ntot * kTapsPerBlock;
+    const int64_t main_total = static_cast<int64_t>(kgroups) * in_ch * per_chan;
+    const int64_t per_tail = static_cast<int64_t>(kp) * kTapsPerBlock;
+    const int64_t total = main_total + (tail ? static_cast<int64_t>(kgroups) * chunks * per_tail : 0);
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = e % kTapsPerBlock;
-        const int64_t row = (e / kTapsPerBlock) % kp;
-        const int64_t h = (e / per) % chunks;
-        const int64_t kg = e / (per * chunks);
-        const int64_t r = k / cc, c = h * cc + k % cc, o = kg * kp + row;
-        const int64_t s = static_cast<int64_t>(g - 1) * kTapsPerBlock + r;
-        float v = 0.0f;
-        if (r < tail && c < in_ch && o < out_ch && s < taps) v = wg[(o * in_ch + c) * taps + s];
-        const int64_t off = (row / 8) * 128 + (k / 8) * 64 + (row % 8) * 8 + (k % 8);
-        img[(kg * chunks + h) * per + off] = fp32_to_bf16_bits(v);
+        if (e < main_total) {
+            const int64_t r = e % kTapsPerBlock;
+            const int64_t row = (e / kTapsPerBlock) % ntot;
+            const int64_t c = (e / per_chan) % in_ch;
+            const int64_t kg = e / (per_chan * in_ch);
+            const int64_t blk = row / kp, o = kg * kp + row % kp, s = (g - 1 - blk) * kTapsPerBlock + r;
+            float v = 0.0f;
+            if (o < out_ch && s < taps) v = wval(w, bwd_raw, out_ch, in_ch, taps, o, c, s);
+            const int64_t off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
+            img[(kg * in_ch + c) * per_chan + off] = fp32_to_bf16_bits(v);
+        } else {
+            const int64_t f = e - main_total;
+            const int64_t k = f % kTapsPerBlock;
+            const int64_t row = (f / kTapsPerBlock) % kp;
+            const int64_t h = (f / per_tail) % chunks;
+            const int64_t kg = f / (per_tail * chunks);
+            const int64_t rr = k / cc, c = h * cc + k % cc, o = kg * kp + row;
+            const int64_t s = static_cast<int64_t>(g - 1) * kTapsPerBlock + rr;
+            float v = 0.0f;
+            if (rr < tail && c < in_ch && o < out_ch && s < taps) v = wval(w, bwd_raw, out_ch, in_ch, taps, o, c, s);
+            const int64_t off = (row / 8) * 128 + (k / 8) * 64 + (row % 8) * 8 + (k % 8);
+            timg[(kg * chunks + h) * per_tail + off] = fp32_to_bf16_bits(v);
+        }
     }
 }
 
@@ -526,7 +532,7 @@ size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch) {
 }
 
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g, void* workspace,
-                           cudaStream_t stream, int64_t main_ch) {
+                           cudaStream_t stream, int64_t main_ch, bool w_bwd_raw) {
     Plan pl;
     if (!make_plan(g, &pl, main_ch)) return cudaErrorNotSupported;
     auto encode = get_encode_fn();
@@ -534,19 +540,12 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     uint16_t* img = static_cast<uint16_t*>(workspace);
     const int64_t n_chunks = ceil_div(g.in_ch, pl.cc);
     uint16_t* img_tail = img + static_cast<size_t>(pl.kgroups) * g.in_ch * (pl.b_chan_bytes / 2);
-    if (pl.tail) {
-        const int64_t total = static_cast<int64_t>(pl.kgroups) * n_chunks * pl.kp * kTapsPerBlock;
-        const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
-        pack_tail_kernel<<<blocks, 256, 0, stream>>>(wg, img_tail, g.out_ch, g.in_ch, g.taps, pl.kp, pl.g, pl.kgroups,
-                                                     pl.cc, pl.tail, n_chunks);
-        note_launch();
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return e;
-    }
     {
-        const int64_t total = static_cast<int64_t>(pl.kgroups) * g.in_ch * pl.ntot * kTapsPerBlock;
+        const int64_t total = static_cast<int64_t>(pl.kgroups) *
+                              (g.in_ch * pl.ntot + (pl.tail ? n_chunks * pl.kp : 0)) * kTapsPerBlock;
         const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
-        pack_bimg_kernel<<<blocks, 256, 0, stream>>>(wg, img, g.out_ch, g.in_ch, g.taps, pl.kp, pl.g, pl.kgroups);
+        pack_images_kernel<<<blocks, 256, 0, stream>>>(wg, w_bwd_raw ? 1 : 0, img, img_tail, g.out_ch, g.in_ch, g.taps,
+                                                       pl.kp, pl.g, pl.kgroups, pl.cc, pl.tail, n_chunks);
         note_launch();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -727,26 +727,32 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
 }
 
-__global__ void wgrad2_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw, int64_t K, int64_t C,
-                                     int64_t S, const W2Plan pl) {
+// dw[e] = sum over the role's CTAs (ascending) of part[cta][e]. A block covers 64 outputs x 4
+// CTA quarters: each thread sums its quarter of the CTAs in order (all loads in flight), then the
+// four quarter sums are added in order (fixed shape, deterministic).
+__global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
+                                                            int64_t K, int64_t C, int64_t S, const W2Plan pl) {
+    __shared__ float red[4][64];
     const int64_t count = K * C * S;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = static_cast<int64_t>(blockIdx.x) * 64 + (threadIdx.x % 64);
+    const int quarter = threadIdx.x / 64;
+    float v = 0.0f;
+    if (e < count) {
         const int64_t s = e % S;
         const int role = static_cast<int>(s / (static_cast<int64_t>(pl.gpc) * pl.taps_per_group));
-        // ascending CTA order; loads batched 8 deep (the adds stay in order)
         const int b0 = pl.role_cta_begin[role], b1 = pl.role_cta_begin[role + 1];
-        float v = 0.0f;
-        int b = b0;
-        for (; b + 8 <= b1; b += 8) {
-            float t[8];
+        const int n = b1 - b0;
+        const int lo = b0 + n * quarter / 4, hi = b0 + n * (quarter + 1) / 4;
+        float t[16];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) t[j] = part[static_cast<int64_t>(b + j) * count + e];
+        for (int j = 0; j < 16; ++j) t[j] = (lo + j < hi) ? part[static_cast<int64_t>(lo + j) * count + e] : 0.0f;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) v += t[j];
-        }
-        for (; b < b1; ++b) v += part[static_cast<int64_t>(b) * count + e];
-        dw[e] = v;
+        for (int j = 0; j < 16; ++j) v += t[j];
+        for (int b = lo + 16; b < hi; ++b) v += part[static_cast<int64_t>(b) * count + e];
     }
+    red[quarter][threadIdx.x % 64] = v;
+    __syncthreads();
+    if (threadIdx.x < 64 && e < count) dw[e] = ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
 }
 
 }  // namespace
@@ -834,8 +840,7 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         cudaFree(wp.prof);
     }
     const int64_t count = k * c * s;
-    wgrad2_reduce_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 4096)), 256, 0, stream>>>(
-        wp.part, dw_kcs, k, c, s, pl);
+    wgrad2_reduce_kernel<<<static_cast<unsigned>(ceil_div(count, 64)), 256, 0, stream>>>(wp.part, dw_kcs, k, c, s, pl);
     note_launch();
     return cudaGetLastError();
 }
