@@ -73,6 +73,10 @@ struct Plan {
     int tail;              // taps in the last block (0 = off: the last block is a regular block)
     int tail_chunks;       // q-chunks (8 columns x cc channels) of the tail box
     uint32_t tx_stage_bytes, tw_stage_bytes;  // tail X box / tail weight image per stage
+    // Double-buffered TMEM (narrow filter blocks): super-tiles alternate between two 256-column
+    // regions, so the epilogue's output stores overlap the next super-tile's MMAs; the MMA only
+    // waits for the carry of the G-1 partial slots into the other region.
+    int dbuf;
 };
 
 struct KParams {
@@ -102,9 +106,13 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0) {
     if (p.ntot > 256) return false;  // one MMA covers all tap blocks of a tile
     p.t = std::min(8, p.r - (p.g - 1));  // linear TMEM: T + G - 1 slots
     p.acc2 = 0;
+    p.dbuf = 0;
     if (two_regions) {  // two accumulator regions of 256 columns each
         p.t = std::min(p.t, 256 / p.kp - (p.g - 1));
         p.acc2 = 256;
+    } else if (std::min(8, 256 / p.kp - (p.g - 1)) >= 4 && getenv("C1D_NO_DBUF") == nullptr) {
+        p.t = std::min(8, 256 / p.kp - (p.g - 1));
+        p.dbuf = 1;
     }
     if (p.t < 1) return false;
     p.n_seg = static_cast<int>(ceil_div(p.t * kTileQ + 8 * (kTapsPerBlock - 1), kSegQ));
@@ -356,6 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t idesc_tail = make_idesc(128, static_cast<uint32_t>(KP), kFmtBF16, 1, 0);
         const uint32_t main_slot = pl.tail ? static_cast<uint32_t>(KP) : 0u;       // D column offset
         const uint32_t main_brow = pl.tail ? static_cast<uint32_t>(KP) * 32u : 0u;  // skip block 0 of B
+        uint32_t region = 0;  // TMEM region of the current super-tile (double buffering)
         Super su;
         while (next_super(cur, J, G, T, &su)) {
             const long long ts0 = clock64();
@@ -363,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tphase ^= 1;
             t_tmem += clock64() - ts0;
             tc_fence_after();
+            const uint32_t rtmem = tmem + region;
             for (int ch = 0; ch < n_chunks; ++ch) {
                 const int c0 = ch * pl.cc;
                 const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - c0));
@@ -379,7 +389,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint64_t achan = a0;
                     for (int c = 0; c < ccn; ++c) {
                         uint64_t adesc = achan;
-                        uint32_t dcol = tmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u) + main_slot;
+                        uint32_t dcol = rtmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u) + main_slot;
                         for (int t = 0; t < su.tcur; ++t) {
                             mma_bf16_ss(dcol, adesc, bdesc, idesc, 1);
                             adesc = desc_advance(adesc, static_cast<uint32_t>(kTileQ * 2));
@@ -395,7 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t tw = smem_u32(tw_base + static_cast<size_t>(stage) * pl.tw_stage_bytes);
                         uint64_t adesc = make_smem_desc(tx, 128, static_cast<uint32_t>(pl.cc * 16), kLayoutNone);
                         const uint64_t bt = make_smem_desc(tw, 128, 256, kLayoutNone);
-                        uint32_t dcol = tmem + ((c0 >= p.main_ch) ? pl.acc2 : 0u);
+                        uint32_t dcol = rtmem + ((c0 >= p.main_ch) ? pl.acc2 : 0u);
                         for (int t = 0; t < su.tcur; ++t) {
                             mma_bf16_ss(dcol, adesc, bt, idesc_tail, 1);
                             adesc = desc_advance(adesc, static_cast<uint32_t>(16 * pl.cc * 16));
@@ -413,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (elect_one()) mma_commit(smem_u32(&tmem_full));
             __syncwarp();
+            if (pl.dbuf) region ^= 256u;
         }
         if (p.prof && lane == 0) {
             p.prof[blockIdx.x * 8 + 2] = t_full;
@@ -434,21 +445,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         Cursor cur = make_cursor(p);
         uint32_t tphase = 0;
         Super su;
-        const int slots = static_cast<int>(kTmemCols) / KP;
         long long e_store = 0, e_carry = 0, e_zero = 0;  // C1D_PROFILE counters
+        uint32_t region = 0;  // mirrors the MMA warp's double-buffer region
+        const uint32_t used_cols = static_cast<uint32_t>((T + G - 1) * KP);
+        // carry the G-1 partial slots (tcur..tcur+G-2) of `src` into slots 0..G-2 of `dst` (or zero
+        // them at a segment end) and zero dst's remaining used slots: dst is then ready
+        auto prepare = [&](uint32_t src, uint32_t dst, const Super& s2) {
+            for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u)) {
+                for (int j = 0; j < G - 1; ++j) {
+                    for (int kb = 0; kb < KP; kb += 16) {
+                        uint32_t v[16];
+                        if (!s2.last_in_segment) {
+                            tmem_ld16(lane_base + src + reg + static_cast<uint32_t>((s2.tcur + j) * KP + kb), v);
+                            tmem_ld_wait();
+                            tmem_st16(lane_base + dst + reg + static_cast<uint32_t>(j * KP + kb), v);
+                        } else if (dst != src) {
+                            tmem_st16(lane_base + dst + reg + static_cast<uint32_t>(j * KP + kb), z);
+                        }
+                    }
+                }
+                for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < used_cols; col += 16)
+                    tmem_st16(lane_base + dst + reg + col, z);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+        };
         while (next_super(cur, J, G, T, &su)) {
             mbar_wait_sleep(smem_u32(&tmem_full), tphase, 256);
             tphase ^= 1;
             tc_fence_after();
             const long long e0 = clock64();
-            // 1. store the completed outputs (slots 0..tcur-1)
+            if (pl.dbuf) prepare(region, region ^ 256u, su);  // next super-tile may start now
+            const long long e1 = clock64();
+            // store the completed outputs (slots 0..tcur-1)
+            const int64_t out_w = p.out_w;
+            float* const out_item = p.out + su.n * p.out_ch * out_w;
             for (int j = 0; j < su.tcur; ++j) {
                 const int64_t o = su.i0 - (G - 1) + j;
                 if (o < su.j0 || o > su.j1) continue;  // phantom (warm-up / beyond the segment)
                 const int64_t q = o * kTileQ + quarter * 32 + lane;
                 for (int kb = 0; kb < KP; kb += 16) {
                     uint32_t v[16];
-                    tmem_ld16(lane_base + static_cast<uint32_t>(j * KP + kb), v);
+                    tmem_ld16(lane_base + region + static_cast<uint32_t>(j * KP + kb), v);
                     tmem_ld_wait();
                     if (pl.acc2) {  // main term + the correction terms' separate accumulator
                         uint32_t v2[16];
@@ -458,40 +498,28 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(v2[jj]));
                     }
                     if (q < p.out_w) {
-                        float* dst = p.out + (su.n * p.out_ch + p.k_begin + kb) * p.out_w + q;
+                        // running pointer: one add + one store per channel row (the stores, not the
+                        // address math, should limit this loop: it shares sub-partitions with the
+                        // TMA and MMA warps)
+                        float* dst = out_item + (p.k_begin + kb) * out_w + q;
+                        const int kvalid = static_cast<int>(imin64(16, p.out_ch - p.k_begin - kb));
 #pragma unroll
-                        for (int jj = 0; jj < 16; ++jj)
-                            if (p.k_begin + kb + jj < p.out_ch) dst[static_cast<int64_t>(jj) * p.out_w] = __uint_as_float(v[jj]);
-                    }
-                }
-            }
-            const long long e1 = clock64();
-            e_store += e1 - e0;
-            // 2. carry the partial outputs (slots tcur..tcur+G-2) down to slots 0..G-2
-            if (!su.last_in_segment) {
-                for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u)) {
-                    for (int j = 0; j < G - 1; ++j) {
-                        for (int kb = 0; kb < KP; kb += 16) {
-                            uint32_t v[16];
-                            tmem_ld16(lane_base + reg + static_cast<uint32_t>((su.tcur + j) * KP + kb), v);
-                            tmem_ld_wait();
-                            tmem_st16(lane_base + reg + static_cast<uint32_t>(j * KP + kb), v);
+                        for (int jj = 0; jj < 16; ++jj) {
+                            if (jj < kvalid) *dst = __uint_as_float(v[jj]);
+                            dst += out_w;
                         }
                     }
                 }
             }
             const long long e2 = clock64();
-            e_carry += e2 - e1;
-            // 3. zero the slots the next super-tile accumulates from scratch
-            const uint32_t region_cols = pl.acc2 ? pl.acc2 : static_cast<uint32_t>(slots * KP);
-            for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u))
-                for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < region_cols; col += 16)
-                    tmem_st16(lane_base + reg + col, z);
-            tmem_st_wait();
-            tc_fence_before();
-            __syncwarp();
-            e_zero += clock64() - e2;
-            if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+            e_store += e2 - e1;
+            if (!pl.dbuf) {
+                prepare(0, 0, su);  // in place: carry down, zero the rest, release
+                e_carry += clock64() - e2;
+            } else {
+                e_carry += e1 - e0;
+                region ^= 256u;
+            }
         }
         if (p.prof && threadIdx.x == 128) {
             p.prof[blockIdx.x * 8 + 5] = e_store;
