@@ -159,6 +159,55 @@ C1D_EXPORT c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_
                                                   float* bias_grad, void* workspace, size_t workspace_bytes,
                                                   c1d_stream_t stream);
 
+/* ---- Layer-glued conv passes: the conv and the ConvLayer glue in one call ----
+ * On the tcgen05 path (dilation 8 and the d < 8 phase rewrite) the glue runs inside the conv's
+ * TMEM -> global epilogue, so the FP32 conv output never reaches HBM; elsewhere the call runs the
+ * conv into workspace scratch followed by one glue pass (same results up to the bias-gradient
+ * summation order; both orders are fixed, so every call is deterministic). ReLU masks are
+ * channel-block words: an (N, ceil(K/16), width) uint32 tensor whose word (n, b, x) holds the bits of
+ * channels 16b .. 16b+15 at column x (bit j = channel 16b + j; bits 16-31 zero). BF16 outputs use
+ * the reference's round-to-nearest-even for every non-NaN value; a NaN becomes the canonical bf16
+ * NaN (its payload is not kept).
+ *
+ * Forward (train.cpp:176-192) on y = conv(x, w):
+ *   v = y + bias[k];  mask bit = (v > 0);  a = relu ? (v > 0 ? v : 0) : v;  a += skip
+ *   pre = v, act = a, act_bf16[(n*K + k)*(Q + 2*act_pad) + act_pad + q] = RNE bf16(a)
+ *   (every output optional; the 2*act_pad border columns of act_bf16 are never written)   */
+typedef struct c1d_fwd_glue {
+    const float* bias;  /* (K) or NULL */
+    const float* skip;  /* (N, K, Q) added after the ReLU, or NULL */
+    float* pre;         /* (N, K, Q) conv + bias, or NULL */
+    float* act;         /* (N, K, Q) activation, or NULL */
+    uint16_t* act_bf16; /* (N, K, Q + 2*act_pad) zero-bordered bf16 activation, or NULL */
+    uint32_t* mask;     /* (N, ceil(K/16), Q) ReLU mask words, or NULL */
+    int64_t act_pad;
+    int32_t relu;
+    int32_t reserved; /* 0 */
+} c1d_fwd_glue;
+/* Backward (train.cpp:205-221) on dx = backward_data(dy, w), (N, C, W_in): the glued layer (the one
+ * whose activation fed this conv) owns columns [off, off + q) of dx:
+ *   g = dx[:, :, off + x] + gadd;  gp = mask ? (bit x ? g : 0) : g   (mask NULL = no ReLU)
+ *   gsum = g, grad_pre = gp, grad_pre_bf16 = RNE bf16(gp)  ((N, C, q) each, optional)
+ *   bias_grad (C floats, optional) = sum of gp over items and columns, fixed order   */
+typedef struct c1d_bwd_glue {
+    int64_t off, q;
+    const float* gadd;     /* (N, C, q) or NULL */
+    const uint32_t* mask;  /* (N, ceil(C/16), q) words from the glued layer's forward, or NULL */
+    float* gsum;
+    float* grad_pre;
+    uint16_t* grad_pre_bf16;
+    float* bias_grad;
+} c1d_bwd_glue;
+/* Workspace for a glued pass (glue_q = the backward window q; ignored for the forward) and whether
+ * the glue runs fused in the conv epilogue (*fused = 1) or as a separate pass (0). */
+C1D_EXPORT c1d_status c1d_glued_workspace_size(const c1d_desc* desc, c1d_pass pass, int64_t glue_q, size_t* bytes,
+                                               int* fused);
+C1D_EXPORT c1d_status c1d_forward_glued(const c1d_desc* desc, const void* x, const float* w_kcs,
+                                        const c1d_fwd_glue* glue, void* workspace, size_t workspace_bytes,
+                                        c1d_stream_t stream);
+C1D_EXPORT c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const float* w_kcs,
+                                              const c1d_bwd_glue* glue, void* workspace, size_t workspace_bytes,
+                                              c1d_stream_t stream);
 /* Number of kernels this library has launched since load (instrumentation for benchmarks). */
 C1D_EXPORT uint64_t c1d_launch_count(void);
 

@@ -38,6 +38,37 @@ class Desc(C.Structure):
     ]
 
 
+class FwdGlue(C.Structure):
+    """Mirror of c1d_fwd_glue."""
+
+    _fields_ = [
+        ("bias", C.c_void_p),
+        ("skip", C.c_void_p),
+        ("pre", C.c_void_p),
+        ("act", C.c_void_p),
+        ("act_bf16", C.c_void_p),
+        ("mask", C.c_void_p),
+        ("act_pad", C.c_int64),
+        ("relu", C.c_int32),
+        ("reserved", C.c_int32),
+    ]
+
+
+class BwdGlue(C.Structure):
+    """Mirror of c1d_bwd_glue."""
+
+    _fields_ = [
+        ("off", C.c_int64),
+        ("q", C.c_int64),
+        ("gadd", C.c_void_p),
+        ("mask", C.c_void_p),
+        ("gsum", C.c_void_p),
+        ("grad_pre", C.c_void_p),
+        ("grad_pre_bf16", C.c_void_p),
+        ("bias_grad", C.c_void_p),
+    ]
+
+
 def exported_symbols() -> list[str]:
     """Function names declared C1D_EXPORT in include/c1d.h."""
     with open(HEADER_PATH) as f:
@@ -88,5 +119,11 @@ def lib() -> C.CDLL:
     L.c1d_layer_backward_prologue.argtypes = [vp, i64, i64, vp, vp, vp, i64, i64, i64, C.c_int, vp, vp, vp, vp,
                                               vp, C.c_size_t, vp]
     L.c1d_layer_backward_prologue.restype = C.c_int
+    L.c1d_glued_workspace_size.argtypes = [P(Desc), C.c_int, i64, P(C.c_size_t), P(C.c_int)]
+    L.c1d_glued_workspace_size.restype = C.c_int
+    L.c1d_forward_glued.argtypes = [P(Desc), vp, vp, P(FwdGlue), vp, C.c_size_t, vp]
+    L.c1d_forward_glued.restype = C.c_int
+    L.c1d_backward_data_glued.argtypes = [P(Desc), vp, vp, P(BwdGlue), vp, C.c_size_t, vp]
+    L.c1d_backward_data_glued.restype = C.c_int
     _lib = L
     return L

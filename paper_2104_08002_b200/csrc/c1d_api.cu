@@ -502,15 +502,17 @@ size_t split_workspace(const c1d_desc& d, c1d_pass pass, int64_t q) {
 }
 
 // Conv-shaped pass (forward or backward-data).
+// glue (optional): layer glue fused into the tensor-core epilogue; only for glue_fusable() passes,
+// and `out` may then be NULL.
 c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const float* w_kcs, float* out,
-                     void* ws, size_t ws_bytes, cudaStream_t stream) {
+                     void* ws, size_t ws_bytes, cudaStream_t stream, const LayerGlue* glue = nullptr) {
     t_last_error.clear();
     int64_t q = 0;
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
     const c1d_desc& d = *desc;
     if (d.n == 0) return C1D_OK;
-    if (!in || !w_kcs || !out) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
+    if (!in || !w_kcs || (!out && !glue)) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
     st = check_device();
     if (st != C1D_OK) return st;
     const c1d_algo algo = resolve(d, pass, q);
@@ -563,7 +565,7 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         if (e == cudaSuccess) e = launch_phase_split_weights(wg, wph, g.out_ch, g.in_ch, d.s, dp.m, dp.p, stream);
         if (e != cudaSuccess) return cuda_fail(e, "phase copies");
         void* kws = bump.take<char>(tc_conv_workspace_bytes(gp));
-        e = launch_tc_conv(cp, wph, out, gp, kws, stream);
+        e = launch_tc_conv(cp, wph, out, gp, kws, stream, 0, false, glue);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (phases)");
         return C1D_OK;
     }
@@ -582,9 +584,38 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         in_b = tmp;
     }
     void* kws = bump.take<char>(tc_conv_workspace_bytes(gq));
-    e = launch_tc_conv(in_b, w_kcs, out, gq, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA);
+    e = launch_tc_conv(in_b, w_kcs, out, gq, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
     if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
     return C1D_OK;
+}
+
+
+// ---- layer-glued conv passes (c1d_forward_glued / c1d_backward_data_glued) ----
+// Fused: the glue runs in the tcgen05 conv epilogue (native dilation 8 and the phase rewrite, whose
+// output layout is the caller's). Otherwise the conv writes an FP32 scratch tensor and one
+// layer.cu glue pass follows.
+bool glue_fusable(const c1d_desc& d, int64_t q, c1d_algo algo) {
+    if (algo != C1D_ALGO_TCGEN05) return false;
+    const DilPlan dp = dil_plan(d, q);
+    return dp.kind == DilPlan::kNative || dp.kind == DilPlan::kPhases;
+}
+struct GlueSizes {
+    bool fused;
+    size_t conv, scratch, part;
+    size_t total() const { return conv + scratch + part; }
+};
+GlueSizes glue_sizes(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo, int64_t glue_q) {
+    GlueSizes r{};
+    r.fused = glue_fusable(d, q, algo);
+    r.conv = align_up(workspace_for(d, pass, q, algo));
+    const bool fwd = pass == C1D_PASS_FORWARD;
+    const int64_t out_elems = fwd ? d.n * d.k * q : d.n * d.c * d.w_in;
+    r.scratch = r.fused ? 0 : align_up(sizeof(float) * static_cast<size_t>(out_elems));
+    if (!fwd) {
+        const int64_t parts = r.fused ? d.c * num_sms() : d.n * d.c * layer_bias_blocks(glue_q);
+        r.part = align_up(sizeof(float) * static_cast<size_t>(parts));
+    }
+    return r;
 }
 
 }  // namespace
@@ -773,7 +804,7 @@ c1d_status c1d_layer_forward_epilogue(float* pre, const float* bias, const float
     if (n < 0 || k <= 0 || q < 0 || pad < 0 || !pre || n * k > 65535)
         return fail(C1D_ERR_INVALID_ARGUMENT, "bad layer_forward_epilogue arguments");
     if (c1d_status st = check_device(); st != C1D_OK) return st;
-    cudaError_t e = launch_layer_fwd_epilogue(pre, bias, skip, n, k, q, relu, store_pre, act, act_bf16, pad,
+    cudaError_t e = launch_layer_fwd_epilogue(pre, bias, skip, n, k, q, relu, store_pre, act, act_bf16, pad, nullptr,
                                               reinterpret_cast<cudaStream_t>(stream));
     return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_forward_epilogue");
 }
@@ -792,8 +823,114 @@ c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_w, int64_t 
     if (c1d_status st = acquire_workspace(workspace, workspace_bytes, need, &ws); st != C1D_OK) return st;
     float* part =
         bias_grad ? ws.take<float>(static_cast<size_t>(n * k * layer_bias_blocks(q)) * sizeof(float)) : nullptr;
-    cudaError_t e = launch_layer_bwd_prologue(gin, gin_w, gin_off, gadd, pre, pre_bias, n, k, q, relu, gsum, grad_pre,
+    cudaError_t e = launch_layer_bwd_prologue(gin, gin_w, gin_off, gadd, pre, pre_bias, nullptr, n, k, q, relu, gsum, grad_pre,
                                               grad_pre_bf16, bias_grad, part, reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_backward_prologue");
+}
+
+c1d_status c1d_glued_workspace_size(const c1d_desc* desc, c1d_pass pass, int64_t glue_q, size_t* bytes, int* fused) {
+    t_last_error.clear();
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    if (pass == C1D_PASS_BACKWARD_WEIGHT) return fail(C1D_ERR_INVALID_ARGUMENT, "glue applies to conv-shaped passes");
+    const c1d_algo a = resolve(*desc, pass, q);
+    if (static_cast<int>(a) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    const GlueSizes gs = glue_sizes(*desc, pass, q, a, glue_q > 0 ? glue_q : 1);
+    if (bytes) *bytes = gs.total();
+    if (fused) *fused = gs.fused ? 1 : 0;
+    return C1D_OK;
+}
+
+c1d_status c1d_forward_glued(const c1d_desc* desc, const void* x, const float* w_kcs, const c1d_fwd_glue* glue,
+                             void* workspace, size_t workspace_bytes, c1d_stream_t stream_) {
+    t_last_error.clear();
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const c1d_desc& d = *desc;
+    if (!glue || glue->act_pad < 0) return fail(C1D_ERR_INVALID_ARGUMENT, "bad forward glue");
+    if (d.n == 0) return C1D_OK;
+    if (d.n * d.k > 65535) return fail(C1D_ERR_UNSUPPORTED, "glue supports N*K <= 65535 rows");
+    if (c1d_status s2 = check_device(); s2 != C1D_OK) return s2;
+    const c1d_algo algo = resolve(d, C1D_PASS_FORWARD, q);
+    if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    const GlueSizes gs = glue_sizes(d, C1D_PASS_FORWARD, q, algo, q);
+    Bump bump{};
+    st = acquire_workspace(workspace, workspace_bytes, gs.total(), &bump);
+    if (st != C1D_OK) return st;
+    char* conv_ws = bump.take<char>(gs.conv);
+    if (gs.fused) {
+        LayerGlue lg;
+        lg.mode = 1;
+        lg.relu = glue->relu;
+        lg.bias = glue->bias;
+        lg.skip = glue->skip;
+        lg.pre = glue->pre;
+        lg.act = glue->act;
+        lg.act_bf16 = glue->act_bf16;
+        lg.act_pitch = q + 2 * glue->act_pad;
+        lg.act_off = glue->act_pad;
+        lg.mask_out = glue->mask;
+        return conv_pass(desc, C1D_PASS_FORWARD, x, w_kcs, nullptr, conv_ws, gs.conv, stream, &lg);
+    }
+    float* pre = glue->pre ? glue->pre : bump.take<float>(gs.scratch);
+    st = conv_pass(desc, C1D_PASS_FORWARD, x, w_kcs, pre, conv_ws, gs.conv, stream);
+    if (st != C1D_OK) return st;
+    const cudaError_t e = launch_layer_fwd_epilogue(pre, glue->bias, glue->skip, d.n, d.k, q, glue->relu,
+                                                    glue->pre != nullptr, glue->act, glue->act_bf16, glue->act_pad,
+                                                    glue->mask, stream);
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_forward_epilogue");
+}
+
+c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const float* w_kcs, const c1d_bwd_glue* glue,
+                                   void* workspace, size_t workspace_bytes, c1d_stream_t stream_) {
+    t_last_error.clear();
+    cudaStream_t stream = reinterpret_cast<cudaStream_t>(stream_);
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const c1d_desc& d = *desc;
+    if (!glue || glue->off < 0 || glue->q <= 0 || glue->off + glue->q > d.w_in)
+        return fail(C1D_ERR_INVALID_ARGUMENT, "bad backward glue window");
+    if (d.n == 0) {
+        if (glue->bias_grad) {
+            const cudaError_t e = cudaMemsetAsync(glue->bias_grad, 0, sizeof(float) * static_cast<size_t>(d.c), stream);
+            if (e != cudaSuccess) return cuda_fail(e, "memset");
+        }
+        return C1D_OK;
+    }
+    if (d.n * d.c > 65535) return fail(C1D_ERR_UNSUPPORTED, "glue supports N*C <= 65535 rows");
+    if (c1d_status s2 = check_device(); s2 != C1D_OK) return s2;
+    const c1d_algo algo = resolve(d, C1D_PASS_BACKWARD_DATA, q);
+    if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
+    const GlueSizes gs = glue_sizes(d, C1D_PASS_BACKWARD_DATA, q, algo, glue->q);
+    Bump bump{};
+    st = acquire_workspace(workspace, workspace_bytes, gs.total(), &bump);
+    if (st != C1D_OK) return st;
+    char* conv_ws = bump.take<char>(gs.conv);
+    float* part = bump.take<float>(gs.part);
+    if (gs.fused) {
+        LayerGlue lg;
+        lg.mode = 2;
+        lg.g_off = glue->off;
+        lg.g_q = glue->q;
+        lg.gadd = glue->gadd;
+        lg.mask_in = glue->mask;
+        lg.gsum = glue->gsum;
+        lg.gp = glue->grad_pre;
+        lg.gp_bf16 = glue->grad_pre_bf16;
+        lg.part = glue->bias_grad ? part : nullptr;
+        lg.bias_grad = glue->bias_grad;
+        return conv_pass(desc, C1D_PASS_BACKWARD_DATA, dy, w_kcs, nullptr, conv_ws, gs.conv, stream, &lg);
+    }
+    float* dx = bump.take<float>(gs.scratch);
+    st = conv_pass(desc, C1D_PASS_BACKWARD_DATA, dy, w_kcs, dx, conv_ws, gs.conv, stream);
+    if (st != C1D_OK) return st;
+    const cudaError_t e = launch_layer_bwd_prologue(dx, d.w_in, glue->off, glue->gadd, nullptr, nullptr, glue->mask, d.n,
+                                                    d.c, glue->q, glue->mask != nullptr, glue->gsum, glue->grad_pre,
+                                                    glue->grad_pre_bf16, glue->bias_grad, part, stream);
     return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_backward_prologue");
 }
 

@@ -42,14 +42,52 @@ cudaError_t launch_round_bf16(const float* in, uint16_t* out, int64_t count, cud
 
 // layer.cu: fused ConvLayer glue (train.cpp:173-221)
 int64_t layer_bias_blocks(int64_t q);  // bias-gradient partials per (item, channel) row
+// mask: optional ReLU mask (pre + bias > 0) in the LayerGlue channel-block layout (written by the
+// forward epilogue; read by the backward prologue instead of pre + pre_bias).
 cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
                                       int relu, int store_pre, float* act, uint16_t* act_bf16, int64_t pad,
-                                      cudaStream_t stream);
+                                      uint32_t* mask, cudaStream_t stream);
 cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
-                                      const float* pre, const float* pre_bias, int64_t n, int64_t k, int64_t q,
-                                      int relu, float* gsum,
+                                      const float* pre, const float* pre_bias, const uint32_t* mask, int64_t n,
+                                      int64_t k, int64_t q, int relu, float* gsum,
                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
                                       cudaStream_t stream);
+// bias_grad[c] = fixed-order sum of part[(i*k + c)*nbx + b] over items i < n and blocks b < nbx
+cudaError_t launch_bias_grad_reduce(const float* part, float* bias_grad, int64_t n, int64_t k, int64_t nbx,
+                                    cudaStream_t stream);
+
+// Layer glue applied inside a conv's output stage (tc_conv epilogue). With
+// v0 the conv output at (item n, channel k, column x):
+//  mode 1 (forward, train.cpp:176-192): v = v0 + bias[k]; mask bit of (n, k, x) = v > 0;
+//         r = relu ? (v > 0 ? v : 0) : v; a = r + skip; pre = v, act = a,
+//         act_bf16[row * act_pitch + act_off + x] = RNE bf16(a)   (each output optional)
+//  mode 2 (backward, train.cpp:205-221), xi = x - g_off in [0, g_q) (other columns dropped):
+//         g = v0 + gadd; gp = (mask_in ? bit xi : 1) ? g : 0; gsum = g, gp32 = gp, gp_bf16 = bf16(gp);
+//         bias_grad[k] = sum of gp over items and columns (fixed-order: per-CTA partials in
+//         part[k * num_sms() + cta], then one reduce launch)
+// ReLU masks are channel-block words: word (n, b, x) of an (N, ceil(K/16), width) uint32 tensor holds
+// channels 16b .. 16b+15 of column x in bits 0..15 (width = the conv output width in mode 1, g_q in
+// mode 2), so a backward epilogue lane reads one word per 16-row block of its own column.
+struct LayerGlue {
+    int mode = 0;
+    int relu = 0;
+    const float* bias = nullptr;
+    const float* skip = nullptr;
+    float* pre = nullptr;
+    float* act = nullptr;
+    uint16_t* act_bf16 = nullptr;
+    int64_t act_pitch = 0, act_off = 0;
+    uint32_t* mask_out = nullptr;
+    int64_t g_off = 0, g_q = 0;
+    const float* gadd = nullptr;
+    const uint32_t* mask_in = nullptr;
+    float* gsum = nullptr;
+    float* gp = nullptr;
+    uint16_t* gp_bf16 = nullptr;
+    float* part = nullptr;
+    float* bias_grad = nullptr;
+    int64_t part_stride = 0;  // set by the launcher
+};
 
 // ---- tcgen05 (sm_100a) kernels -----------------------------------------------------------
 // Row-tap BF16 tensor-core convolution for dilation 8 (fwd and bwd-data). Returns
@@ -61,8 +99,11 @@ bool tc_conv_supported(const ConvGeom& g, int64_t main_ch = 0);
 size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch = 0);
 // wg: (o, i, s) weights of the forward-shaped problem, or with w_bwd_raw the caller's KCS weights of
 // a backward-data pass (transposed and tap-reversed while packing).
+// glue (optional, mode 1/2): the layer glue replaces the plain FP32 store of `out` (which may then be
+// NULL); its bias-gradient partials need out_ch * num_sms() floats at glue->part.
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g,
-                           void* workspace, cudaStream_t stream, int64_t main_ch = 0, bool w_bwd_raw = false);
+                           void* workspace, cudaStream_t stream, int64_t main_ch = 0, bool w_bwd_raw = false,
+                           const LayerGlue* glue = nullptr);
 
 bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);

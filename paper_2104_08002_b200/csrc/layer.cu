@@ -41,19 +41,20 @@ __device__ __forceinline__ void store_bf16x4(uint16_t* dst, const float v[4], bo
 }
 
 // grid (ceil(q / 1024), n*k). `vec`: every row start of every operand is 16-B aligned and q % 4 == 0.
+// mask: (pre + bias > 0) as channel-block words (kernels.h LayerGlue), zeroed by the launcher.
 __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __restrict__ pre, const float* __restrict__ bias,
                                                                   const float* __restrict__ skip, int64_t k, int64_t q,
                                                                   int relu, int store_pre, float* __restrict__ act,
                                                                   uint16_t* __restrict__ act_bf16, int64_t pad,
-                                                                  bool vec) {
+                                                                  uint32_t* __restrict__ mask, bool vec) {
     const int64_t row = blockIdx.y;
     const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
-    if (x0 >= q) return;
+    const bool live = x0 < q;
     const float b = bias ? bias[row % k] : 0.0f;
     float* pr = pre + row * q + x0;
-    const int cnt = static_cast<int>(q - x0 < kEltPerThread ? q - x0 : kEltPerThread);
+    const int cnt = live ? static_cast<int>(q - x0 < kEltPerThread ? q - x0 : kEltPerThread) : 0;
     const bool v4 = vec && cnt == kEltPerThread;
-    float v[4], sk[4] = {0.f, 0.f, 0.f, 0.f};
+    float v[4] = {0.f, 0.f, 0.f, 0.f}, sk[4] = {0.f, 0.f, 0.f, 0.f};
     if (v4) {
         const float4 t = *reinterpret_cast<const float4*>(pr);
         v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
@@ -73,6 +74,14 @@ __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __rest
         v[j] += b;
         a[j] = (relu && !(v[j] > 0.0f)) ? 0.0f : v[j];
         a[j] += sk[j];
+    }
+    if (!live) return;
+    if (mask) {  // channel-block words (kernels.h): OR this row's bit into the 4 columns' words
+        const int64_t n = row / k, c = row % k;
+        uint32_t* wd = mask + (n * ((k + 15) / 16) + c / 16) * q + x0;
+        const uint32_t bit = 1u << (c % 16);
+        for (int j = 0; j < cnt; ++j)
+            if (v[j] > 0.0f) atomicOr(wd + j, bit);
     }
     if (v4) {
         if (bias && store_pre) *reinterpret_cast<float4*>(pr) = make_float4(v[0], v[1], v[2], v[3]);
@@ -96,8 +105,8 @@ __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __rest
 // grid (nbx = ceil(q / 1024), n*k). Block partial of the bias gradient -> part[row * nbx + bx].
 __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
     const float* __restrict__ gin, int64_t gin_w, int64_t gin_off, const float* __restrict__ gadd,
-    const float* __restrict__ pre, const float* __restrict__ pre_bias, int64_t k, int64_t q, int relu,
-    float* __restrict__ gsum, float* __restrict__ grad_pre,
+    const float* __restrict__ pre, const float* __restrict__ pre_bias, const uint32_t* __restrict__ mask, int64_t k,
+    int64_t q, int relu, float* __restrict__ gsum, float* __restrict__ grad_pre,
     uint16_t* __restrict__ grad_pre_bf16, float* __restrict__ part, bool vec) {
     __shared__ float red[kEltThreads / 32];
     const int64_t row = blockIdx.y;
@@ -115,7 +124,7 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
                 const float4 s = *reinterpret_cast<const float4*>(gadd + row * q + x0);
                 ad[0] = s.x, ad[1] = s.y, ad[2] = s.z, ad[3] = s.w;
             }
-            if (relu) {
+            if (relu && !mask) {
                 const float4 s = *reinterpret_cast<const float4*>(pre + row * q + x0);
                 pr[0] = s.x, pr[1] = s.y, pr[2] = s.z, pr[3] = s.w;
             }
@@ -123,14 +132,18 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
             for (int j = 0; j < 4; ++j) {
                 g[j] = j < cnt ? gi[j] : 0.0f;
                 if (gadd && j < cnt) ad[j] = gadd[row * q + x0 + j];
-                if (relu && j < cnt) pr[j] = pre[row * q + x0 + j];
+                if (relu && !mask && j < cnt) pr[j] = pre[row * q + x0 + j];
             }
         }
         const float pb = (relu && pre_bias) ? pre_bias[row % k] : 0.0f;  // mask of pre + bias
+        // or the forward's mask words: bit c % 16 of word (n, c / 16, x)
+        const uint32_t* mwd = mask ? mask + ((row / k) * ((k + 15) / 16) + (row % k) / 16) * q + x0 : nullptr;
+        const uint32_t mbit = 1u << ((row % k) % 16);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             g[j] += ad[j];
-            gp[j] = (relu && !(pr[j] + pb > 0.0f)) ? 0.0f : g[j];
+            const bool keep = mask ? (j < cnt && (mwd[j] & mbit) != 0) : (pr[j] + pb > 0.0f);
+            gp[j] = (relu && !keep) ? 0.0f : g[j];
             if (j >= cnt) gp[j] = 0.0f;
         }
         if (v4) {
@@ -191,12 +204,16 @@ int64_t layer_bias_blocks(int64_t q) { return ceil_div(q, kEltPerBlock); }
 
 cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float* skip, int64_t n, int64_t k, int64_t q,
                                       int relu, int store_pre, float* act, uint16_t* act_bf16, int64_t pad,
-                                      cudaStream_t stream) {
+                                      uint32_t* mask, cudaStream_t stream) {
     if (n * k == 0 || q == 0) return cudaSuccess;
     if (n * k > 65535) return cudaErrorInvalidValue;
     const bool vec = (q % 4 == 0) && aligned16(pre) && (!skip || aligned16(skip)) && (!act || aligned16(act));
+    if (mask) {
+        const cudaError_t e = cudaMemsetAsync(mask, 0, sizeof(uint32_t) * static_cast<size_t>(n * ceil_div(k, 16) * q), stream);
+        if (e != cudaSuccess) return e;
+    }
     const dim3 grid(static_cast<unsigned>(ceil_div(q, kEltPerBlock)), static_cast<unsigned>(n * k));
-    fwd_epilogue_kernel<<<grid, kEltThreads, 0, stream>>>(pre, bias, skip, k, q, relu, store_pre, act, act_bf16, pad,
+    fwd_epilogue_kernel<<<grid, kEltThreads, 0, stream>>>(pre, bias, skip, k, q, relu, store_pre, act, act_bf16, pad, mask,
                                                           vec && (!act_bf16 || ((reinterpret_cast<uintptr_t>(act_bf16) & 7u) == 0 &&
                                                                                 ((q + 2 * pad) % 4) == 0)));
     note_launch();
@@ -204,8 +221,8 @@ cudaError_t launch_layer_fwd_epilogue(float* pre, const float* bias, const float
 }
 
 cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t gin_off, const float* gadd,
-                                      const float* pre, const float* pre_bias, int64_t n, int64_t k, int64_t q,
-                                      int relu, float* gsum,
+                                      const float* pre, const float* pre_bias, const uint32_t* mask, int64_t n,
+                                      int64_t k, int64_t q, int relu, float* gsum,
                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
                                       cudaStream_t stream) {
     if (n * k == 0 || q == 0) return cudaSuccess;
@@ -216,12 +233,17 @@ cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t g
                      (!grad_pre_bf16 || (reinterpret_cast<uintptr_t>(grad_pre_bf16) & 7u) == 0);
     const int64_t nbx = layer_bias_blocks(q);
     const dim3 grid(static_cast<unsigned>(nbx), static_cast<unsigned>(n * k));
-    bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, pre_bias, k, q, relu, gsum,
+    bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, pre_bias, mask, k, q, relu, gsum,
                                                           grad_pre,
                                                           grad_pre_bf16, bias_grad ? part : nullptr, vec);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !bias_grad) return e;
+    return launch_bias_grad_reduce(part, bias_grad, n, k, nbx, stream);
+}
+
+cudaError_t launch_bias_grad_reduce(const float* part, float* bias_grad, int64_t n, int64_t k, int64_t nbx,
+                                    cudaStream_t stream) {
     bias_grad_reduce_kernel<<<static_cast<unsigned>(k), kEltThreads, 0, stream>>>(part, bias_grad, n, k, nbx);
     note_launch();
     return cudaGetLastError();

@@ -237,6 +237,11 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst_saddr, const void*
                  "r"(valid ? 16 : 0)
                  : "memory");
 }
+// 4-byte variant (L1-allocating .ca, the only mode for sizes below 16)
+__device__ __forceinline__ void cp_async4_zfill(uint32_t dst_saddr, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst_saddr), "l"(src), "r"(valid ? 4 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 // Arrive on an mbarrier (counted as one of its expected arrivals) once all of this thread's
 // previously issued cp.async copies have landed.
@@ -274,6 +279,23 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst_saddr, const void* tmap
         "[%1, {%2, %3, %4}], [%5];" ::"r"(dst_saddr),
         "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar_saddr)
         : "memory");
+}
+// 3-D tiled TMA store shared -> global (bulk-group completion; out-of-bounds elements are dropped).
+__device__ __forceinline__ void tma_store_3d(const void* tmap, uint32_t src_saddr, int32_t c0, int32_t c1,
+                                             int32_t c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(tmap),
+                 "r"(src_saddr), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// wait until at most N bulk groups of this thread still READ their shared-memory source
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait() {
+    asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory");
 }
 __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");

@@ -49,6 +49,7 @@ constexpr int kSegQ = 256;       // TMA box width in elements
 constexpr int kTapsPerBlock = 16;
 constexpr int kMaxStages = 6;
 constexpr int kThreads = 256;
+constexpr int kPfRing = 4;  // layer glue: input blocks in flight per epilogue warp
 constexpr uint32_t kTmemCols = 512;
 
 struct Plan {
@@ -89,9 +90,19 @@ struct KParams {
     int64_t main_ch;       // channels < main_ch -> region 0, others -> region acc2 (split FP32)
     float* out;
     unsigned long long* prof;  // optional per-CTA cycle counters (C1D_PROFILE=1), else nullptr
+    LayerGlue glue;            // mode 0: plain FP32 store of `out`
+    // glue outputs through shared-memory staging + TMA stores: slot bits 1 = fp32 A (pre / gsum),
+    // 2 = fp32 B (act / gp), 4 = bf16 C (act_bf16 / gp_bf16); 0 = per-lane global stores
+    uint32_t tma_slots;
+    uint32_t stg_off;    // staging area offset in the aligned dynamic shared memory
+    uint32_t stg_bytes;  // one staging buffer (each epilogue warp owns two)
+    uint32_t stg_a, stg_b, stg_c;  // slot offsets inside a buffer
+    // glue inputs (skip / gadd rows, mask words) prefetched kPfRing blocks ahead with cp.async into
+    // per-warp rings: pf_rows / pf_mask = slot has 16 x 32 fp32 rows / 32 mask words
+    uint32_t pf_off, pf_slot_bytes, pf_rows, pf_mask;
 };
 
-bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0) {
+bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserve = 0) {
     const bool two_regions = main_ch > 0;
     if (g.dil != 8) return false;
     const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
@@ -141,7 +152,7 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0) {
     p.tx_stage_bytes = p.tail ? ((static_cast<uint32_t>(p.tail_chunks * p.cc * 16) + 1023) & ~1023u) : 0;
     p.tw_stage_bytes = p.tail ? static_cast<uint32_t>(p.kp * kTapsPerBlock * 2) : 0;
     const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.tx_stage_bytes + p.tw_stage_bytes;
-    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024) / stage));
+    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve) / stage));
     if (p.stages < 2) return false;
     p.smem_bytes = static_cast<size_t>(p.stages) * stage + 1024;
     *pl = p;
@@ -256,13 +267,269 @@ __device__ __forceinline__ Cursor make_cursor(const KParams& p) {
     return c;
 }
 
+// ---------------------------------------------------------------------------- layer glue
+// The glue runs on the four epilogue warps, one output column per lane and 16 channel rows per
+// TMEM load. It is written for instruction count (the plain store loop is ~50 instructions per 16
+// rows; a straightforward glue with per-element optional outputs was ~800 and ran 6x slower):
+// every optional output is one guarded loop with a running pointer, the bias comes from shared
+// memory, mask words move one per lane (a ballot per row, one store / load per warp), and all
+// loads of a block are issued before its stores.
+
+// branch-free fp32_to_bf16_bits (RNE, NaN -> quiet NaN; inf falls out of the RNE formula)
+__device__ __forceinline__ uint16_t bf16_rne_bits(float f) {
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t r = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    return static_cast<uint16_t>(((u & 0x7fffffffu) > 0x7f800000u) ? ((u >> 16) | 0x40u) : r);
+}
+
+// 16 values -> 8 words of bf16 pairs (rows 2i | 2i+1 << 16), hardware round-to-nearest-even:
+// identical to the reference's fp32_to_bf16 (bf16.hpp:29-40) for every non-NaN value, denormals and
+// overflow included; NaN becomes the canonical bf16 NaN instead of keeping its payload (a NaN
+// activation or gradient stays NaN, and the tensor core canonicalises NaN operands anyway).
+__device__ __forceinline__ void pack_bf16_rows(const float (&v)[16], uint32_t (&pk)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(pk[i]) : "f"(v[2 * i + 1]), "f"(v[2 * i]));
+}
+
+// Stage 16 rows x 32 columns of up to three outputs in this warp's shared-memory buffer and write
+// them with one TMA store each (rows past the channel count and columns past the width fall
+// outside the tensor maps and are dropped, so no per-element predicates). Two buffers per warp:
+// lane 0 waits until the older store has read its buffer before the warp refills it.
+__device__ __forceinline__ void st_shared_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+// rows 2i and 2i+1 of a bf16 staging tile (64-B rows)
+__device__ __forceinline__ void st_shared_bf16_pair(uint32_t a, uint32_t pk) {
+    asm volatile("{.reg .b16 l, h; mov.b32 {l, h}, %1; st.shared.b16 [%0], l; st.shared.b16 [%0+64], h;}" ::"r"(a),
+                 "r"(pk)
+                 : "memory");
+}
+__device__ __forceinline__ void glue_tma_store(const KParams& p, uint32_t& sbuf, uint32_t wbase, int lane,
+                                               const float (&va)[16], const float (&vb)[16],
+                                               const uint32_t (&pc)[8], const CUtensorMap* m0,
+                                               const CUtensorMap* m1, const CUtensorMap* m2, int32_t col,
+                                               int32_t col_c, int32_t row, int32_t item) {
+    const uint32_t slots = p.tma_slots;
+    const uint32_t b = wbase + sbuf * p.stg_bytes;
+    if (lane == 0) bulk_wait_read<1>();
+    __syncwarp();
+    if (slots & 1u) {
+        const uint32_t a = b + p.stg_a + static_cast<uint32_t>(lane) * 4u;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) st_shared_f32(a + jj * 128, va[jj]);
+    }
+    if (slots & 2u) {
+        const uint32_t a = b + p.stg_b + static_cast<uint32_t>(lane) * 4u;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) st_shared_f32(a + jj * 128, vb[jj]);
+    }
+    if (slots & 4u) {
+        const uint32_t a = b + p.stg_c + static_cast<uint32_t>(lane) * 2u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) st_shared_bf16_pair(a + i * 128, pc[i]);
+    }
+    fence_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        if (slots & 1u) tma_store_3d(m0, b + p.stg_a, col, row, item);
+        if (slots & 2u) tma_store_3d(m1, b + p.stg_b, col, row, item);
+        if (slots & 4u) tma_store_3d(m2, b + p.stg_c, col_c, row, item);
+        bulk_commit();
+    }
+    sbuf ^= 1u;
+}
+
+// Prefetch the glue inputs of one (tile, 16-row block) into a ring slot: each lane copies its own
+// column of the 16 rows (zero-filled outside the tensor) and, for the backward, one mask word
+// (lanes 0-15: word w0 of rows 0-15, lanes 16-31: w0 + 1; see glue_backward16).
+__device__ __forceinline__ void glue_prefetch(const KParams& p, int64_t n, int64_t o, int kbi, uint32_t slot,
+                                              int quarter, int lane) {
+    const LayerGlue& gl = p.glue;
+    const int64_t x = o * kTileQ + quarter * 32 + lane;
+    const int64_t k0 = p.k_begin + kbi * 16;
+    const int kvalid = static_cast<int>(imin64(16, p.out_ch - k0));
+    const int64_t row0 = n * p.out_ch + k0;
+    if (p.pf_rows) {
+        const float* base = gl.mode == 1 ? gl.skip : gl.gadd;
+        const int64_t w = gl.mode == 1 ? p.out_w : gl.g_q;
+        const int64_t c = gl.mode == 1 ? x : x - gl.g_off;
+        const bool cv = c >= 0 && c < w;
+        const float* src = base + row0 * w + c;
+        const uint32_t dst = slot + static_cast<uint32_t>(lane) * 4u;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            const bool v = cv && jj < kvalid;
+            cp_async4_zfill(dst + jj * 128, v ? src : base, v);
+            src += w;
+        }
+    }
+    if (p.pf_mask) {
+        const int64_t gq = gl.g_q;
+        const int64_t xi = x - gl.g_off;
+        const bool v = xi >= 0 && xi < gq && kvalid > 0;
+        const int64_t kblocks = (p.out_ch + 15) >> 4;
+        cp_async4_zfill(slot + (p.pf_rows ? 2048u : 0u) + static_cast<uint32_t>(lane) * 4u,
+                        v ? gl.mask_in + (n * kblocks + (k0 >> 4)) * gq + xi : gl.mask_in, v);
+    }
+}
+
+__device__ __forceinline__ float ld_shared_f32(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
+// forward glue for rows k0 .. k0+15 of column q; bias16 = those rows' bias (0 past the channel count)
+__device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t (&v)[16], int64_t n, int64_t q,
+                                               int64_t k0, int lane, const float (&bias16)[16], uint32_t& sbuf,
+                                               uint32_t wbase, const CUtensorMap* m0, const CUtensorMap* m1,
+                                               const CUtensorMap* m2, uint32_t pf_slot) {
+    const LayerGlue& gl = p.glue;
+    const int64_t out_w = p.out_w;
+    const bool qv = q < out_w;
+    const int kvalid = static_cast<int>(imin64(16, p.out_ch - k0));
+    const int64_t row0 = n * p.out_ch + k0;
+    float x[16], a[16];
+    const bool relu = gl.relu != 0;
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) {
+        x[jj] = __uint_as_float(v[jj]) + bias16[jj];
+        a[jj] = (relu && !(x[jj] > 0.0f)) ? 0.0f : x[jj];
+    }
+    if (gl.skip) {  // prefetched rows (zero outside the tensor)
+        const uint32_t src = pf_slot + static_cast<uint32_t>(lane) * 4u;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) a[jj] += ld_shared_f32(src + jj * 128);
+    }
+    if (gl.mask_out) {  // one word per column and 16-channel block: bit jj = row k0 + jj
+        uint32_t m = 0;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) m |= (x[jj] > 0.0f ? 1u : 0u) << jj;
+        const int64_t kblocks = (p.out_ch + 15) >> 4;
+        if (qv && kvalid > 0) gl.mask_out[(n * kblocks + (k0 >> 4)) * out_w + q] = m;
+    }
+    uint32_t pc[8];
+    if (gl.act_bf16) pack_bf16_rows(a, pc);
+    if (p.tma_slots) {
+        glue_tma_store(p, sbuf, wbase, lane, x, a, pc, m0, m1, m2, static_cast<int32_t>(q - lane),
+                       static_cast<int32_t>(gl.act_off + q - lane), static_cast<int32_t>(k0), static_cast<int32_t>(n));
+        return;
+    }
+    if (!qv) return;
+    if (gl.pre) {
+        float* d = gl.pre + row0 * out_w + q;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            if (jj < kvalid) *d = x[jj];
+            d += out_w;
+        }
+    }
+    if (gl.act) {
+        float* d = gl.act + row0 * out_w + q;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            if (jj < kvalid) *d = a[jj];
+            d += out_w;
+        }
+    }
+    if (gl.act_bf16) {
+        const int64_t pitch = gl.act_pitch;
+        uint16_t* d = gl.act_bf16 + row0 * pitch + gl.act_off + q;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            if (jj < kvalid) *d = static_cast<uint16_t>(pc[jj / 2] >> (16 * (jj & 1)));
+            d += pitch;
+        }
+    }
+}
+
+// backward glue for rows k0 .. k0+15 of padded column x (the glued layer's column xi = x - g_off)
+__device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t (&v)[16], int64_t n, int64_t x,
+                                                int64_t k0, int lane, float (&bs)[16], uint32_t& sbuf,
+                                                uint32_t wbase, const CUtensorMap* m0, const CUtensorMap* m1,
+                                                const CUtensorMap* m2, uint32_t pf_slot) {
+    const LayerGlue& gl = p.glue;
+    const int64_t gq = gl.g_q;
+    const int64_t xi = x - gl.g_off;
+    const bool xv = xi >= 0 && xi < gq;
+    const int kvalid = static_cast<int>(imin64(16, p.out_ch - k0));
+    const int64_t row0 = n * p.out_ch + k0;
+    // ReLU mask: this column's word for the 16-row block (prefetched; bit jj = row k0 + jj)
+    const uint32_t mword = gl.mask_in ? ld_shared_u32(pf_slot + (p.pf_rows ? 2048u : 0u) + static_cast<uint32_t>(lane) * 4u)
+                                      : 0xffffu;
+    float g[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) g[jj] = __uint_as_float(v[jj]);
+    if (gl.gadd) {  // prefetched rows (zero outside the window)
+        const uint32_t src = pf_slot + static_cast<uint32_t>(lane) * 4u;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) g[jj] += ld_shared_f32(src + jj * 128);
+    }
+    float gp[16];
+#pragma unroll
+    for (int jj = 0; jj < 16; ++jj) gp[jj] = (mword & (1u << jj)) ? g[jj] : 0.0f;
+    if (xv) {
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj)
+            if (jj < kvalid) bs[jj] += gp[jj];
+    }
+    uint32_t pc[8];
+    if (gl.gp_bf16) pack_bf16_rows(gp, pc);
+    // TMA stores need a non-negative start column: the warp straddling the glued window's left
+    // edge (once per item) takes the per-lane path
+    const int64_t col = xi - lane;
+    if (p.tma_slots && col >= 0) {
+        glue_tma_store(p, sbuf, wbase, lane, g, gp, pc, m0, m1, m2, static_cast<int32_t>(col),
+                       static_cast<int32_t>(col), static_cast<int32_t>(k0), static_cast<int32_t>(n));
+        return;
+    }
+    if (!xv) return;
+    const int64_t e = row0 * gq + xi;
+    if (gl.gsum) {
+        float* d = gl.gsum + e;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            if (jj < kvalid) *d = g[jj];
+            d += gq;
+        }
+    }
+    if (gl.gp) {
+        float* d = gl.gp + e;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            if (jj < kvalid) *d = gp[jj];
+            d += gq;
+        }
+    }
+    if (gl.gp_bf16) {
+        uint16_t* d = gl.gp_bf16 + e;
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+            if (jj < kvalid) *d = static_cast<uint16_t>(pc[jj / 2] >> (16 * (jj & 1)));
+            d += gq;
+        }
+    }
+}
+
+// kMode: 0 plain FP32 store, 1 forward glue, 2 backward glue (p.glue.mode); kKPB (modes 1-2): 16-channel
+// blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
+// mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
+// and TMA warps, and an all-modes kernel (~30k instructions) ran the epilogue 6x slower.
+template <int kMode, int kKPB>
 __global__ void __launch_bounds__(kThreads, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
-                   const KParams p) {
+                   const __grid_constant__ CUtensorMap om0, const __grid_constant__ CUtensorMap om1,
+                   const __grid_constant__ CUtensorMap om2, const KParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t stage_full[kMaxStages], stage_empty[kMaxStages];
     __shared__ uint64_t tmem_full, tmem_empty;
     __shared__ uint32_t tmem_base_s;
+    __shared__ float bias_red[4 * 64];  // layer glue: per-quarter bias-gradient sums
 
     const Plan& pl = p.pl;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -446,6 +713,61 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t tphase = 0;
         Super su;
         long long e_store = 0, e_carry = 0, e_zero = 0;  // C1D_PROFILE counters
+        constexpr int kBR = kMode == 1 ? kKPB : 1;
+        float bias_r[kBR][16];  // layer glue (mode 1): this filter group's bias, 0 past the channels
+#pragma unroll
+        for (int a = 0; a < kBR; ++a)
+#pragma unroll
+            for (int b = 0; b < 16; ++b) {
+                const int64_t k = p.k_begin + a * 16 + b;
+                bias_r[a][b] = (kMode == 1 && p.glue.bias && k < p.out_ch) ? __ldg(p.glue.bias + k) : 0.0f;
+            }
+        // layer glue input prefetch: this warp's blocks are (tile, kbi) for the CTA's tiles [cta_b, cta_e)
+        // in order (the super-tile walk emits every output tile once, in increasing order)
+        constexpr int kB = kKPB > 0 ? kKPB : 1;
+        const int64_t cta_b = p.total_tiles * blockIdx.x / gridDim.x;
+        const int64_t nblk = (p.total_tiles * (blockIdx.x + 1) / gridDim.x - cta_b) * kB;
+        const bool pf_on = kMode != 0 && (p.pf_rows | p.pf_mask) != 0;
+        const uint32_t pf_base = smem_u32(smem) + p.pf_off + static_cast<uint32_t>(quarter * kPfRing) * p.pf_slot_bytes;
+        int64_t blk = 0, pf_next = 0;
+        int64_t pf_n = cta_b / p.tiles_per_item, pf_o = cta_b % p.tiles_per_item;  // tile of block pf_next
+        int pf_kbi = 0;
+        auto pf_issue = [&]() {
+            if (pf_next < nblk) {
+                glue_prefetch(p, pf_n, pf_o, pf_kbi, pf_base + static_cast<uint32_t>(pf_next & (kPfRing - 1)) * p.pf_slot_bytes,
+                              quarter, lane);
+                if (++pf_kbi == kB) {
+                    pf_kbi = 0;
+                    if (++pf_o == p.tiles_per_item) {
+                        pf_o = 0;
+                        ++pf_n;
+                    }
+                }
+            }
+            cp_async_commit();
+            ++pf_next;
+        };
+        if (pf_on)
+            for (int i = 0; i < kPfRing - 1; ++i) pf_issue();
+        // the slot of the next block, once its copies have landed
+        auto pf_take = [&]() -> uint32_t {
+            uint32_t slot = 0;
+            if (pf_on) {
+                pf_issue();
+                cp_async_wait_group<kPfRing - 1>();
+                slot = pf_base + static_cast<uint32_t>(blk & (kPfRing - 1)) * p.pf_slot_bytes;
+            }
+            ++blk;
+            return slot;
+        };
+        uint32_t sbuf = 0;  // layer glue: this warp's staging buffer (0/1) and its shared-memory base
+        const uint32_t wbase = smem_u32(smem) + p.stg_off + static_cast<uint32_t>(quarter) * 2u * p.stg_bytes;
+        constexpr int kBS = kMode == 2 ? kKPB : 1;
+        float bsum[kBS][16];  // layer glue (mode 2): this lane's bias-gradient sums per channel
+#pragma unroll
+        for (int a = 0; a < kBS; ++a)
+#pragma unroll
+            for (int b = 0; b < 16; ++b) bsum[a][b] = 0.0f;
         uint32_t region = 0;  // mirrors the MMA warp's double-buffer region
         const uint32_t used_cols = static_cast<uint32_t>((T + G - 1) * KP);
         // carry the G-1 partial slots (tcur..tcur+G-2) of `src` into slots 0..G-2 of `dst` (or zero
@@ -482,6 +804,51 @@ __global__ void __launch_bounds__(kThreads, 1)
             // store the completed outputs (slots 0..tcur-1)
             const int64_t out_w = p.out_w;
             float* const out_item = p.out + su.n * p.out_ch * out_w;
+            if constexpr (kMode == 1) {  // fused forward glue instead of the plain store
+                for (int j = 0; j < su.tcur; ++j) {
+                    const int64_t o = su.i0 - (G - 1) + j;
+                    if (o < su.j0 || o > su.j1) continue;
+                    const int64_t q = o * kTileQ + quarter * 32 + lane;
+#pragma unroll
+                    for (int kbi = 0; kbi < kKPB; ++kbi) {
+                        uint32_t v[16];
+                        tmem_ld16(lane_base + region + static_cast<uint32_t>(j * KP + kbi * 16), v);
+                        tmem_ld_wait();
+                        if (pl.acc2) {
+                            uint32_t v2[16];
+                            tmem_ld16(lane_base + pl.acc2 + static_cast<uint32_t>(j * KP + kbi * 16), v2);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(v2[jj]));
+                        }
+                        const uint32_t slot = pf_take();
+                        glue_forward16(p, v, su.n, q, p.k_begin + kbi * 16, lane, bias_r[kbi], sbuf, wbase, &om0,
+                                       &om1, &om2, slot);
+                    }
+                }
+            } else if constexpr (kMode == 2) {  // fused backward glue
+                for (int j = 0; j < su.tcur; ++j) {
+                    const int64_t o = su.i0 - (G - 1) + j;
+                    if (o < su.j0 || o > su.j1) continue;
+                    const int64_t q = o * kTileQ + quarter * 32 + lane;
+#pragma unroll
+                    for (int kbi = 0; kbi < kKPB; ++kbi) {
+                        uint32_t v[16];
+                        tmem_ld16(lane_base + region + static_cast<uint32_t>(j * KP + kbi * 16), v);
+                        tmem_ld_wait();
+                        if (pl.acc2) {
+                            uint32_t v2[16];
+                            tmem_ld16(lane_base + pl.acc2 + static_cast<uint32_t>(j * KP + kbi * 16), v2);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(v2[jj]));
+                        }
+                        const uint32_t slot = pf_take();
+                        glue_backward16(p, v, su.n, q, p.k_begin + kbi * 16, lane, bsum[kbi], sbuf, wbase, &om0,
+                                        &om1, &om2, slot);
+                    }
+                }
+            } else
             for (int j = 0; j < su.tcur; ++j) {
                 const int64_t o = su.i0 - (G - 1) + j;
                 if (o < su.j0 || o > su.j1) continue;  // phantom (warm-up / beyond the segment)
@@ -521,6 +888,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                 region ^= 256u;
             }
         }
+        if (kMode != 0 && p.tma_slots && lane == 0) bulk_wait<0>();
+        if (kMode == 2 && p.glue.part) {
+            // fixed-order CTA partial per channel: warp butterfly, then quarters 0..3 in order
+#pragma unroll
+            for (int kbi = 0; kbi < kBS; ++kbi) {
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj) {
+                    float t = bsum[kbi][jj];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+                    if (lane == 0) bias_red[quarter * 64 + kbi * 16 + jj] = t;
+                }
+            }
+            asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
+            const int c = threadIdx.x - 128;
+            if (c < KP && p.k_begin + c < p.out_ch) {
+                const float t = ((bias_red[c] + bias_red[64 + c]) + bias_red[128 + c]) + bias_red[192 + c];
+                p.glue.part[(p.k_begin + c) * p.glue.part_stride + blockIdx.x] = t;
+            }
+        }
         if (p.prof && threadIdx.x == 128) {
             p.prof[blockIdx.x * 8 + 5] = e_store;
             p.prof[blockIdx.x * 8 + 6] = e_carry;
@@ -545,6 +932,50 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
+
+// Tensor maps of the glue outputs for the TMA-store epilogue: (width, channel rows, items) with a
+// 32 x 16 x 1 box. Every requested output must be 16-B aligned with 16-B row pitches and start at
+// a column that is a multiple of 8 (the tiles start at multiples of 32); otherwise the epilogue
+// uses per-lane global stores for the whole launch.
+struct GlueMaps {
+    CUtensorMap m[3];
+    uint32_t slots = 0, stg_bytes = 0, a = 0, b = 0, c = 0;
+};
+bool glue_maps(const ConvGeom& g, const LayerGlue& gl, PFN_cuTensorMapEncodeTiled_v12000 encode, GlueMaps* out) {
+    const bool fwd = gl.mode == 1;
+    const int64_t width = fwd ? g.out_w : gl.g_q;
+    void* ptr[3] = {fwd ? static_cast<void*>(gl.pre) : static_cast<void*>(gl.gsum),
+                    fwd ? static_cast<void*>(gl.act) : static_cast<void*>(gl.gp),
+                    fwd ? static_cast<void*>(gl.act_bf16) : static_cast<void*>(gl.gp_bf16)};
+    const int64_t pitch[3] = {width, width, fwd ? gl.act_pitch : width};
+    const int64_t dim0[3] = {width, width, fwd ? gl.act_off + width : width};
+    const int64_t col_off = fwd ? gl.act_off : gl.g_off;
+    if (col_off % 8) return false;
+    GlueMaps r;
+    uint32_t off = 0;
+    for (int i = 0; i < 3; ++i) {
+        if (!ptr[i]) continue;
+        const int64_t esz = i == 2 ? 2 : 4;
+        if ((reinterpret_cast<uintptr_t>(ptr[i]) & 15u) || (pitch[i] * esz) % 16) return false;
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(dim0[i]), static_cast<cuuint64_t>(g.out_ch),
+                                    static_cast<cuuint64_t>(g.n)};
+        const cuuint64_t strides[2] = {static_cast<cuuint64_t>(pitch[i] * esz),
+                                       static_cast<cuuint64_t>(pitch[i] * esz * g.out_ch)};
+        const cuuint32_t box[3] = {32, 16, 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (encode(&r.m[i], i == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, ptr[i], dims,
+                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return false;
+        r.slots |= 1u << i;
+        (i == 0 ? r.a : i == 1 ? r.b : r.c) = off;
+        off += static_cast<uint32_t>(32 * 16 * esz);
+    }
+    r.stg_bytes = off;
+    *out = r;
+    return true;
+}
+
 }  // namespace
 
 bool tc_conv_supported(const ConvGeom& g, int64_t main_ch) {
@@ -560,11 +991,28 @@ size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch) {
 }
 
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g, void* workspace,
-                           cudaStream_t stream, int64_t main_ch, bool w_bwd_raw) {
-    Plan pl;
-    if (!make_plan(g, &pl, main_ch)) return cudaErrorNotSupported;
+                           cudaStream_t stream, int64_t main_ch, bool w_bwd_raw, const LayerGlue* glue) {
     auto encode = get_encode_fn();
     if (!encode) return cudaErrorNotSupported;
+    GlueMaps gm;
+    static const bool no_glue_tma = getenv("C1D_NO_GLUE_TMA") != nullptr;  // dev A/B switch
+    if (glue && glue->mode != 0 && !no_glue_tma && !glue_maps(g, *glue, encode, &gm)) gm = GlueMaps{};
+    const uint32_t stg_total = 8u * gm.stg_bytes;  // 4 epilogue warps x 2 buffers
+    const int mode = glue ? glue->mode : 0;
+    const uint32_t pf_rows = (mode == 1 && glue->skip) || (mode == 2 && glue->gadd);
+    const uint32_t pf_mask = mode == 2 && glue->mask_in;
+    const uint32_t pf_slot = pf_rows * 2048u + pf_mask * 128u;  // rows: 16 x 32 fp32, mask: 32 words
+    const uint32_t pf_total = 4u * kPfRing * pf_slot;
+    const uint32_t extra = stg_total + pf_total;
+    Plan pl;
+    if (!make_plan(g, &pl, main_ch, extra ? extra + 1024 : 0)) return cudaErrorNotSupported;
+    uint32_t stg_off = 0, pf_off = 0;
+    if (extra) {
+        const uint32_t stage = pl.x_stage_bytes + pl.w_stage_bytes + pl.tx_stage_bytes + pl.tw_stage_bytes;
+        stg_off = (static_cast<uint32_t>(pl.stages) * stage + 127u) & ~127u;
+        pf_off = stg_off + stg_total;
+        pl.smem_bytes = pf_off + pf_total + 1024;
+    }
     uint16_t* img = static_cast<uint16_t*>(workspace);
     const int64_t n_chunks = ceil_div(g.in_ch, pl.cc);
     uint16_t* img_tail = img + static_cast<size_t>(pl.kgroups) * g.in_ch * (pl.b_chan_bytes / 2);
@@ -601,7 +1049,10 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-    cudaError_t e = cudaFuncSetAttribute(tc_conv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    auto kernel = tc_conv_kernel<0, 0>;
+    if (mode == 1) kernel = pl.kp == 16 ? tc_conv_kernel<1, 1> : (pl.kp == 32 ? tc_conv_kernel<1, 2> : tc_conv_kernel<1, 4>);
+    if (mode == 2) kernel = pl.kp == 16 ? tc_conv_kernel<2, 1> : (pl.kp == 32 ? tc_conv_kernel<2, 2> : tc_conv_kernel<2, 4>);
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
     if (e != cudaSuccess) return e;
     KParams kp{};
@@ -617,7 +1068,22 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     kp.main_ch = main_ch > 0 ? main_ch : g.in_ch;
     kp.pl = pl;
     kp.out = out;
+    kp.tma_slots = gm.slots;
+    kp.stg_off = stg_off;
+    kp.stg_bytes = gm.stg_bytes;
+    kp.stg_a = gm.a;
+    kp.stg_b = gm.b;
+    kp.stg_c = gm.c;
+    kp.pf_off = pf_off;
+    kp.pf_slot_bytes = pf_slot;
+    kp.pf_rows = pf_rows;
+    kp.pf_mask = pf_mask;
     const int grid = static_cast<int>(std::min<int64_t>(num_sms(), kp.total_tiles));
+    if (glue && glue->mode != 0) {
+        kp.glue = *glue;
+        kp.glue.part_stride = grid;
+        if (glue->mode == 2 && glue->bias_grad && !glue->part) return cudaErrorInvalidValue;
+    }
     static const bool profile = getenv("C1D_PROFILE") != nullptr;
     if (profile) {
         cudaMalloc(&kp.prof, sizeof(unsigned long long) * 8 * grid);
@@ -627,9 +1093,15 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         kp.k_begin = kg * pl.kp;
         kp.bimg = img + static_cast<size_t>(kg) * g.in_ch * (pl.b_chan_bytes / 2);
         kp.bimg_tail = img_tail + static_cast<size_t>(kg) * n_chunks * (pl.tw_stage_bytes / 2);
-        tc_conv_kernel<<<grid, kThreads, pl.smem_bytes, stream>>>(tmap, tmap_tail, kp);
+        kernel<<<grid, kThreads, pl.smem_bytes, stream>>>(tmap, tmap_tail, gm.slots & 1u ? gm.m[0] : tmap,
+                                                          gm.slots & 2u ? gm.m[1] : tmap,
+                                                          gm.slots & 4u ? gm.m[2] : tmap, kp);
         note_launch();
         e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    if (kp.glue.mode == 2 && kp.glue.bias_grad) {
+        e = launch_bias_grad_reduce(kp.glue.part, kp.glue.bias_grad, 1, g.out_ch, grid, stream);
         if (e != cudaSuccess) return e;
     }
     if (profile) {

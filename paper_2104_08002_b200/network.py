@@ -19,19 +19,22 @@ Mirrors the reference's layer/network code (proj/src/train.cpp) on device tensor
                    local losses are means over local items).
 * `sgd_step`       p <- p - lr*g (train.cpp:137-141).
 
-Fused glue (csrc/layer.cu through the C ABI): every layer's forward is the
-conv plus ONE epilogue pass (bias in place, ReLU, skip, and the activation written straight into
-the next layer's zero-padded BF16 input buffer), and every backward is ONE prologue pass (the
-incoming gradient read from the interior of the padded backward-data output, plus the skip
-gradient, ReLU mask, BF16 rounding for the next passes, deterministic bias-gradient sums) plus
-the two conv passes. BF16 layers therefore never see an FP32 copy of their input: the activation
-is rounded once, exactly where the reference's conv would round it (conv.cpp:182-183).
+Fused glue (through the C ABI's glued passes): every layer's forward is ONE
+call, c1d_forward_glued, whose tcgen05 epilogue adds the bias, applies ReLU and the skip, writes
+the ReLU-mask bits and the activation straight into the next layer's zero-padded BF16 input
+buffer (the FP32 conv output never reaches HBM). Every backward-data pass is ONE call,
+c1d_backward_data_glued, whose epilogue applies the glue of the layer below: the interior of the
+input gradient plus the skip gradient, the ReLU mask, BF16 rounding for that layer's own backward
+passes and deterministic bias-gradient partial sums. BF16 layers never see an FP32 copy of their
+input: the activation is rounded once, where the reference's conv would round it
+(conv.cpp:182-183). Shapes off the tensor-core path run the same calls as conv + one glue pass.
 
 Weights are Kaiming-uniform with the reference's damping (input 1.0, body 0.3, heads 0.1;
 train.cpp:247-248, 263-268), seeded.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 
 import torch
@@ -70,12 +73,52 @@ def layer_backward_prologue(gin, gin_off, pre, n, k, q, relu=True, gadd=None, gs
                                                   _ptr(grad_pre_bf16), _ptr(bias_grad), None, 0, _stream()))
 
 
+def mask_shape(n: int, channels: int, q: int) -> tuple:
+    """ReLU-mask tensor (int32): word (n, b, x) holds channels 16b..16b+15 of column x (c1d.h)."""
+    return (n, (channels + 15) // 16, q)
+
+
+def _desc_for(x: torch.Tensor, p: cv.ConvParams, w_in: int):
+    dt = L.DTYPE_BF16 if x.dtype == torch.bfloat16 else L.DTYPE_F32
+    return cv.make_desc(p, x.shape[0], w_in, dt)
+
+
+def conv_forward_glued(x, w_kcs, p: cv.ConvParams, *, bias=None, skip=None, relu=True, pre=None, act=None,
+                       act_bf16=None, act_pad=0, mask=None):
+    """c1d_forward_glued: conv + bias + ReLU (+ skip) in one call; the glue runs in the tcgen05 conv
+    epilogue where the shape allows it. mask: int32 mask_shape(N, K, Q) ReLU-mask words."""
+    desc = _desc_for(x, p, x.shape[2])
+    glue = L.FwdGlue(_ptr(bias), _ptr(skip), _ptr(pre), _ptr(act), _ptr(act_bf16), _ptr(mask), act_pad, int(relu), 0)
+    cv._check(L.lib().c1d_forward_glued(C.byref(desc), x.data_ptr(), w_kcs.data_ptr(), C.byref(glue), None, 0,
+                                        _stream()))
+
+
+def conv_backward_data_glued(dy, w_kcs, p: cv.ConvParams, off: int, q: int, *, gadd=None, mask=None, gsum=None,
+                             grad_pre=None, grad_pre_bf16=None, bias_grad=None):
+    """c1d_backward_data_glued: backward-data, then the glue of the layer that owns columns
+    [off, off + q) of the input gradient (skip gradient, ReLU mask bits, BF16 rounding, bias grad)."""
+    w_in = dy.shape[2] + p.dilation * (p.taps - 1)
+    desc = _desc_for(dy, p, w_in)
+    glue = L.BwdGlue(off, q, _ptr(gadd), _ptr(mask), _ptr(gsum), _ptr(grad_pre), _ptr(grad_pre_bf16),
+                     _ptr(bias_grad))
+    cv._check(L.lib().c1d_backward_data_glued(C.byref(desc), dy.data_ptr(), w_kcs.data_ptr(), C.byref(glue), None,
+                                              0, _stream()))
+
+
+def glue_is_fused(p: cv.ConvParams, n: int, w_in: int, pass_: int, in_dtype: int = L.DTYPE_BF16) -> bool:
+    """Whether the glued pass runs its glue inside the tcgen05 conv epilogue."""
+    b, f = C.c_size_t(0), C.c_int(0)
+    cv._check(L.lib().c1d_glued_workspace_size(C.byref(cv.make_desc(p, n, w_in, in_dtype)), pass_, 1, C.byref(b),
+                                               C.byref(f)))
+    return bool(f.value)
+
+
 class ConvLayer:
     """One conv with bias, optional ReLU and optional skip input (train.hpp ConvLayer).
 
-    Forward reads its input from `self.x_in` (N, C, W_in) — bf16 for BF16 layers (zero-padded, as
-    written by the previous layer's epilogue), fp32 otherwise — and leaves `self.pre`
-    (N, K, Q) = conv + bias for the backward's ReLU mask."""
+    The forward reads `self.x_in` (N, C, W_in) — bf16 for BF16 layers (zero-padded, as written by
+    the previous layer's glued epilogue), fp32 otherwise — and leaves `self.mask`, the ReLU-mask
+    bits of conv + bias > 0 that the backward glue reads (no FP32 pre-activation is kept)."""
 
     def __init__(self, in_ch, out_ch, taps, dilation, precision, relu, same_pad, weight_scale, gen, device):
         self.p = cv.ConvParams(in_ch, out_ch, taps, dilation, precision)
@@ -87,27 +130,38 @@ class ConvLayer:
         self.grad_w = torch.zeros_like(self.w)
         self.grad_b = torch.zeros_like(self.b)
         self.x_in = None
-        self.pre = None
+        self.mask = None
 
     @property
     def bf16(self) -> bool:
         return self.p.precision == cv.Precision.Bf16
 
-    def conv(self, x_in: torch.Tensor) -> torch.Tensor:
+    def out_width(self, x_in: torch.Tensor) -> int:
+        return x_in.shape[2] - self.p.dilation * (self.p.taps - 1)
+
+    def forward(self, x_in: torch.Tensor, *, skip=None, act=None, act_bf16=None, act_pad=0, pre=None):
+        """Glued forward (c1d_forward_glued): conv, bias, ReLU, skip, activation outputs."""
         self.x_in = x_in
-        self.pre = cv.conv1d_forward(x_in, self.w, self.p, out=self.pre if self._pre_fits(x_in) else None)
-        return self.pre
+        n, q = x_in.shape[0], self.out_width(x_in)
+        mask = None
+        if self.relu:
+            shape = mask_shape(n, self.p.filters, q)
+            if self.mask is None or tuple(self.mask.shape) != shape:
+                self.mask = torch.empty(shape, dtype=torch.int32, device=x_in.device)
+            mask = self.mask
+        conv_forward_glued(x_in, self.w, self.p, bias=self.b, skip=skip, relu=self.relu, pre=pre, act=act,
+                           act_bf16=act_bf16, act_pad=act_pad, mask=mask)
 
-    def _pre_fits(self, x_in) -> bool:
-        if self.pre is None:
-            return False
-        q = x_in.shape[2] - self.p.dilation * (self.p.taps - 1)
-        return tuple(self.pre.shape) == (x_in.shape[0], self.p.filters, q)
-
-    def backward_convs(self, grad_pre: torch.Tensor, dx: torch.Tensor | None = None) -> torch.Tensor:
-        """backward-weight into grad_w and backward-data (gradient w.r.t. the padded input)."""
+    def backward_weight(self, grad_pre: torch.Tensor) -> None:
         cv.conv1d_backward_weight(grad_pre, self.x_in, self.p, out=self.grad_w)
-        return cv.conv1d_backward_data(grad_pre, cv.pack_weights_backward(self.w), self.p, out=dx)
+
+    def backward_data_into(self, dy: torch.Tensor, target: "ConvLayer | None", q: int, **glue) -> None:
+        """backward-data of this layer (dy = its pre-activation gradient) glued to `target`'s
+        backward (the layer whose activation is this layer's input, at columns [pad, pad + q) of
+        the padded input gradient)."""
+        conv_backward_data_glued(dy, self.w, self.p, self.pad, q,
+                                 mask=target.mask if target is not None and target.relu else None,
+                                 bias_grad=target.grad_b if target is not None else None, **glue)
 
     def parameters(self):
         return [self.w, self.b]
@@ -180,15 +234,19 @@ class ResidualNet:
         dt = torch.bfloat16 if layer.bf16 else torch.float32
         return self._buf(name, (n, layer.p.channels, width + 2 * layer.pad), dt, zero=True)
 
-    def _epilogue_into(self, layer: ConvLayer, nxt: ConvLayer, nxt_name: str, skip=None, act=None):
-        """Fused glue after `layer`'s conv; writes the activation into `nxt`'s padded input."""
-        n, k, q = layer.pre.shape
+    def _run_into(self, layer: ConvLayer, x_in, nxt: ConvLayer | None, nxt_name: str, skip=None, act=None):
+        """Glued forward of `layer`; its activation goes straight into `nxt`'s padded input (BF16) or
+        through `act` (FP32 consumers). Returns nxt's input (or None)."""
+        n, q = x_in.shape[0], layer.out_width(x_in)
+        if nxt is None:
+            layer.forward(x_in, skip=skip, act=act)
+            return None
         nin = self._padded_input(nxt_name, nxt, n, q)
         if nxt.bf16:
-            layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, act, nin, nxt.pad)
+            layer.forward(x_in, skip=skip, act=act, act_bf16=nin, act_pad=nxt.pad)
             return nin
-        a = act if act is not None else self._buf(nxt_name + ".act", (n, k, q), torch.float32)
-        layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, a, None, 0)
+        a = act if act is not None else self._buf(nxt_name + ".act", (n, layer.p.filters, q), torch.float32)
+        layer.forward(x_in, skip=skip, act=a)
         nin[:, :, nxt.pad:nxt.pad + q].copy_(a)  # FP32 layers (tests / FP32 nets): plain padded copy
         return nin
 
@@ -197,72 +255,86 @@ class ResidualNet:
         n = x_padded.shape[0]
         first = self.input
         x0 = cv.round_bf16(x_padded) if first.bf16 else x_padded.float().contiguous()
-        first.conv(x0)
-        width = first.pre.shape[2]
+        width = first.out_width(x0)
         h = self._buf("h.in", (n, first.p.filters, width), torch.float32)  # block input (skip source)
-        nxt = self.blocks[0][0] if self.blocks else None
-        if nxt is not None:
-            x_next = self._epilogue_into(first, nxt, "x.b0.0", act=h)
-        else:
-            layer_forward_epilogue(first.pre, first.b, None, first.relu, h)
+        x_next = self._run_into(first, x0, self.blocks[0][0] if self.blocks else None, "x.b0.0", act=h)
         for bi, blk in enumerate(self.blocks):
             skip = h
             for li, layer in enumerate(blk):
-                layer.conv(x_next)
-                last = li == len(blk) - 1
-                if not last:
-                    x_next = self._epilogue_into(layer, blk[li + 1], f"x.b{bi}.{li + 1}")
+                if li < len(blk) - 1:
+                    x_next = self._run_into(layer, x_next, blk[li + 1], f"x.b{bi}.{li + 1}")
                     continue
                 h = self._buf(f"h.b{bi}", (n, layer.p.filters, width), torch.float32)
-                if bi + 1 < len(self.blocks):
-                    x_next = self._epilogue_into(layer, self.blocks[bi + 1][0], f"x.b{bi + 1}.0", skip=skip, act=h)
-                else:
-                    layer_forward_epilogue(layer.pre, layer.b, skip, layer.relu, h)
+                nxt = self.blocks[bi + 1][0] if bi + 1 < len(self.blocks) else None
+                x_next = self._run_into(layer, x_next, nxt, f"x.b{bi + 1}.0", skip=skip, act=h)
         self.h_last = h
         heads = self.heads
         torch.cat([self.reg_head.w, self.peak_head.w], out=heads.w)
         torch.cat([self.reg_head.b, self.peak_head.b], out=heads.b)
-        heads.conv(h)
-        layer_forward_epilogue(heads.pre, heads.b, None, False, store_pre=True)
-        return heads.pre[:, 0:1], heads.pre[:, 1:2]
+        pre = self._buf("heads.pre", (n, 2, width), torch.float32)
+        heads.forward(h, pre=pre)
+        return pre[:, 0:1], pre[:, 1:2]
 
     def backward(self, grad_pred: torch.Tensor, grad_logits: torch.Tensor) -> None:
+        """Each backward-data pass carries the glue of the layer below it (c1d_backward_data_glued):
+        skip gradient, ReLU mask, BF16 rounding and bias gradient happen in the conv epilogue."""
         h = self.h_last
         n, hidden, width = h.shape
-        # heads (one 2-filter conv): bias grads, dW, and the gradient w.r.t. the last block output
-        # (backward-data of the 2-filter conv = the sum of both heads' backward-data)
         heads = self.heads
         g2 = self._buf("g.heads", (n, 2, width), torch.float32)
         torch.cat([grad_pred, grad_logits], dim=1, out=g2)
         layer_backward_prologue(g2, 0, None, n, 2, width, relu=False, bias_grad=heads.grad_b)
-        gin = heads.backward_convs(g2, self._buf("dx.heads", (n, hidden, width), torch.float32))
+        heads.backward_weight(g2)
+        chain = [self.input] + [layer for blk in self.blocks for layer in blk]  # forward order
+
+        def gp_buf(layer, slot):
+            return self._buf(f"gp.{slot}", (n, hidden, width), torch.bfloat16 if layer.bf16 else torch.float32)
+
+        def glue_out(layer, slot):
+            gp = gp_buf(layer, slot)
+            return gp, ({"grad_pre_bf16": gp} if layer.bf16 else {"grad_pre": gp})
+
+        # chain index of each block's first conv: its backward-data feeds the block input, which
+        # also receives the block output's gradient through the skip
+        first_of_block = {}
+        idx = 1
+        for bi, blk in enumerate(self.blocks):
+            first_of_block[idx] = bi
+            idx += len(blk)
+
+        # heads' backward-data -> glue of the last chain layer (the last block's output layer)
+        top = chain[-1]
+        slot = 0
+        gp, kw = glue_out(top, slot)
+        g_out = None
+        if self.blocks:
+            g_out = self._buf(f"g.b{len(self.blocks) - 1}", (n, hidden, width), torch.float32)
+            kw["gsum"] = g_out
+        heads.backward_data_into(g2, top, width, **kw)
         self.reg_head.grad_w.copy_(heads.grad_w[0:1])
         self.peak_head.grad_w.copy_(heads.grad_w[1:2])
         self.reg_head.grad_b.copy_(heads.grad_b[0:1])
         self.peak_head.grad_b.copy_(heads.grad_b[1:2])
-        gin_off, gadd = 0, None
-        for bi in reversed(range(len(self.blocks))):
-            blk = self.blocks[bi]
-            g_out = self._buf(f"g.b{bi}", (n, hidden, width), torch.float32)  # grad w.r.t. block output
-            for li in reversed(range(len(blk))):
-                layer = blk[li]
-                gp = self._buf(f"gp.{li}", (n, hidden, width), torch.bfloat16 if layer.bf16 else torch.float32)
-                last = li == len(blk) - 1
-                layer_backward_prologue(gin, gin_off, layer.pre, n, hidden, width, relu=layer.relu,
-                                        gadd=gadd if last else None, gsum=g_out if last else None,
-                                        grad_pre=None if layer.bf16 else gp, grad_pre_bf16=gp if layer.bf16 else None,
-                                        bias_grad=layer.grad_b, pre_bias=layer.b)
-                dx = self._buf(f"dx.b.{li}", (n, hidden, width + 2 * layer.pad), torch.float32)
-                layer.backward_convs(gp, dx)
-                gin, gin_off, gadd = dx, layer.pad, None
-            gadd = g_out  # the skip: block input gradient = conv path + block output gradient
+        g_outs = {len(self.blocks) - 1: g_out} if self.blocks else {}
+        for li in range(len(chain) - 1, 0, -1):
+            layer, below = chain[li], chain[li - 1]
+            layer.backward_weight(gp)
+            slot ^= 1
+            gp_next, kw = glue_out(below, slot)
+            if li in first_of_block:
+                # below = the previous block's output (or the input layer): + the skip gradient
+                bi = first_of_block[li]
+                kw["gadd"] = g_outs[bi]
+                if bi > 0:
+                    g_outs[bi - 1] = self._buf(f"g.b{bi - 1}", (n, hidden, width), torch.float32)
+                    kw["gsum"] = g_outs[bi - 1]
+            layer.backward_data_into(gp, below, width, **kw)
+            gp = gp_next
         first = self.input
-        gp = self._buf("gp.in", (n, hidden, width), torch.bfloat16 if first.bf16 else torch.float32)
-        layer_backward_prologue(gin, gin_off, first.pre, n, hidden, width, relu=first.relu, gadd=gadd,
-                                grad_pre=None if first.bf16 else gp, grad_pre_bf16=gp if first.bf16 else None,
-                                bias_grad=first.grad_b, pre_bias=first.b)
+        first.backward_weight(gp)
         # gradient w.r.t. the padded network input: computed as the reference does, then discarded
-        first.backward_convs(gp, self._buf("dx.in", (n, 1, first.x_in.shape[2]), torch.float32))
+        cv.conv1d_backward_data(gp, first.w, first.p, out=self._buf("dx.in", (n, 1, first.x_in.shape[2]),
+                                                                     torch.float32))
 
     def sgd_step(self, lr: float) -> None:
         if not lr > 0:
