@@ -185,6 +185,13 @@ ConvGeom pitched(ConvGeom g) {
     if (g.in_w % 8) g.in_stride = round8(g.in_w);
     return g;
 }
+// Expanded-row geometry (d = 1, 2, 4): the conv runs on the row tensor E (launch_expand_rows),
+// which absorbs the column offset, so in_off becomes 0.
+ConvGeom xr_geom(ConvGeom g) {
+    g.xr_rows = tc_conv_xr_rows(g);
+    return g;
+}
+bool xr_ok(const ConvGeom& g) { return (g.dil == 1 || g.dil == 2 || g.dil == 4) && tc_conv_supported(xr_geom(g)); }
 // backward-weight: Q is padded to a multiple of 8 (zero dY columns add nothing) and x gets a
 // zero-padded pitch covering Q_pad + d(S-1) when either width is unaligned.
 struct WgradPad {
@@ -245,8 +252,10 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         }
         const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
         if (dp.kind == DilPlan::kNative) return tc_conv_supported(g);
-        if (dp.kind == DilPlan::kPhases)
+        if (dp.kind == DilPlan::kPhases) {
+            if (xr_ok(g)) return true;
             return (d.algo == C1D_ALGO_TCGEN05 || phases_pay_off(dp, g.in_ch)) && tc_conv_supported(phase_geom(g, dp));
+        }
         return tc_conv_supported(plane_geom(g, dp));
     }();
     const bool split_ok = [&] {
@@ -312,6 +321,11 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
                    align_up(sizeof(float) * static_cast<size_t>(d.k * dp.p * d.c * dp.sp)) + align_up(kws);
         }
         return b + align_up(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, wpd.q_pad));
+    }
+    if (dp.kind == DilPlan::kPhases && xr_ok(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q))) {
+        const ConvGeom g = xr_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
+        return wbytes + align_up(tc_conv_workspace_bytes(g)) +
+               align_up(sizeof(uint16_t) * 8 * static_cast<size_t>(g.n * g.in_ch * g.xr_rows));
     }
     if (dp.kind == DilPlan::kPhases) {
         const ConvGeom g = phase_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q), dp);
@@ -533,7 +547,8 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     // from the caller's KCS weights (one launch fewer)
     float* wg = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
     cudaError_t e = cudaSuccess;
-    if (algo == C1D_ALGO_DIRECT || dp.kind != DilPlan::kNative)
+    const bool use_xr = algo == C1D_ALGO_TCGEN05 && dp.kind == DilPlan::kPhases && xr_ok(g);
+    if (algo == C1D_ALGO_DIRECT || (dp.kind != DilPlan::kNative && !use_xr))
         e = launch_prep_weights(w_kcs, wg, d.k, d.c, d.s,
                                 pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData, bf16, stream);
     if (e != cudaSuccess) return cuda_fail(e, "prep_weights");
@@ -553,6 +568,17 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         e = launch_tc_conv(pin, wg, pout, gp, kws, stream);
         if (e == cudaSuccess) e = launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (planes)");
+        return C1D_OK;
+    }
+    if (use_xr) {
+        // d < 8: expanded rows (E = 8-element rows at every d-column start), 16 taps per MMA
+        const ConvGeom gx = xr_geom(g);
+        uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(gx.n * gx.in_ch * gx.xr_rows));
+        e = launch_expand_rows(in, d.in_dtype, ex, g.n * g.in_ch, g.in_w, g.dil, g.in_off, gx.xr_rows, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "expand_rows");
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gx));
+        e = launch_tc_conv(ex, w_kcs, out, gx, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_conv (expanded rows)");
         return C1D_OK;
     }
     if (dp.kind == DilPlan::kPhases) {

@@ -20,6 +20,9 @@ void note_launch(int n = 1);
 struct ConvGeom {
     int64_t n, in_ch, in_w, out_ch, out_w, taps, dil, in_off;
     int64_t in_stride = 0;
+    // expanded rows (d = 1, 2, 4): the input is the row tensor E of launch_expand_rows, rows of 8
+    // bf16 elements E[n*C + c][r][e] = x[n][c][d*r + e + in_off]; out[q] uses rows q/d + s.
+    int64_t xr_rows = 0;  // rows per (item, channel) of E; 0 = natural rows
 };
 
 enum WeightMode { kWeightsForward = 0, kWeightsBackwardData = 1 };
@@ -136,6 +139,13 @@ cudaError_t launch_shift_copies_f32(const float* in, float* out, int64_t n, int6
 // out[r][j] = bf16(in[r][j]) for j < w, 0 for w <= j < w_pad (rows of a zero-padded bf16 copy)
 cudaError_t launch_pad_rows(const void* in, int in_dtype, uint16_t* out, int64_t rows, int64_t w, int64_t w_pad,
                             cudaStream_t stream);
+
+// Row tensor for the expanded-row tensor-core mode (dilations 1, 2, 4): out[nc][r][e] =
+// bf16(in[nc][d*r + e + off]) (0 outside [0, w)), r < rows; 16-B rows.
+cudaError_t launch_expand_rows(const void* in, int in_dtype, uint16_t* out, int64_t nc, int64_t w, int64_t d,
+                               int64_t off, int64_t rows, cudaStream_t stream);
+// rows of E a tc_conv launch over geometry g (dil 1, 2, 4) reads per (item, channel)
+int64_t tc_conv_xr_rows(const ConvGeom& g);
 
 // FP32-on-tensor-core operand splitting (split.cu)
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,

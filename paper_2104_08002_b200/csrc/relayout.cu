@@ -9,6 +9,10 @@
 //     cp.async need 16-B aligned starts, so the shifted channels are materialised as bf16 copies
 //     (shift_copies). Backward-weight runs one launch per phase on that phase's shifted x copy and
 //     scatters tap t of phase b back to tap b + m*t.
+//  d < 8 (the default since round 1's expanded-row mode; phases remain the fallback): expanded
+//     rows. E[nc][r] = the 8 elements x[d*r .. d*r+7] (a (8/d)x larger bf16 tensor). In E a tap is
+//     one 16-B row and 8 output columns are 8/d rows, so tc_conv reads the MMA's A operand straight
+//     from E with an M-group stride of 128/d bytes: 16 consecutive taps per MMA at any d | 8.
 //  d = 8m (m >= 2): chunk planes. Column 8u+e lives in plane u mod m; a dilation-8m tap step is one
 //     chunk inside a plane, so the conv is a dilation-8 conv on N*m planes of width W/m (inputs
 //     de-interleaved here, outputs re-interleaved).
@@ -140,7 +144,51 @@ __global__ void pad_rows_kernel(const TIn* __restrict__ in, uint16_t* __restrict
     }
 }
 
+// one 16-B row per thread: out[nc][r][0..7] = in[nc][d*r + off + 0..7]
+template <typename TIn>
+__global__ void expand_rows_kernel(const TIn* __restrict__ in, uint4* __restrict__ out, int64_t nc, int64_t w,
+                                   int64_t d, int64_t off, int64_t rows) {
+    const int64_t total = nc * rows;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = e % rows, row = e / rows;
+        const int64_t c0 = d * r + off;
+        const TIn* src = in + row * w;
+        uint16_t v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int64_t col = c0 + j;
+            uint16_t b = 0;
+            if (col >= 0 && col < w) {
+                if constexpr (sizeof(TIn) == 4)
+                    b = fp32_to_bf16_bits(reinterpret_cast<const float*>(src)[col]);
+                else
+                    b = reinterpret_cast<const uint16_t*>(src)[col];
+            }
+            v[j] = b;
+        }
+        uint4 pk;
+        pk.x = v[0] | (static_cast<uint32_t>(v[1]) << 16);
+        pk.y = v[2] | (static_cast<uint32_t>(v[3]) << 16);
+        pk.z = v[4] | (static_cast<uint32_t>(v[5]) << 16);
+        pk.w = v[6] | (static_cast<uint32_t>(v[7]) << 16);
+        out[e] = pk;
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_expand_rows(const void* in, int in_dtype, uint16_t* out, int64_t nc, int64_t w, int64_t d,
+                               int64_t off, int64_t rows, cudaStream_t stream) {
+    const unsigned blocks = blocks_for(nc * rows);
+    if (in_dtype == 0)
+        expand_rows_kernel<float><<<blocks, 256, 0, stream>>>(static_cast<const float*>(in), reinterpret_cast<uint4*>(out),
+                                                              nc, w, d, off, rows);
+    else
+        expand_rows_kernel<uint16_t><<<blocks, 256, 0, stream>>>(static_cast<const uint16_t*>(in),
+                                                                 reinterpret_cast<uint4*>(out), nc, w, d, off, rows);
+    note_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_shift_copies(const void* in, int in_dtype, uint16_t* out, int64_t n, int64_t I, int64_t w,
                                 int64_t P, int64_t base, int64_t delta, int64_t w_out, cudaStream_t stream) {

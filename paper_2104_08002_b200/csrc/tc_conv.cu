@@ -78,6 +78,14 @@ struct Plan {
     // regions, so the epilogue's output stores overlap the next super-tile's MMAs; the MMA only
     // waits for the carry of the G-1 partial slots into the other region.
     int dbuf;
+    // Expanded-row mode (dilation 1, 2, 4; ConvGeom.xr_rows): the input is the row tensor E (one
+    // tap = one 16-B row, 8 output columns = 8/d rows). Each output tile accumulates its G tap
+    // blocks directly (one N = KP MMA per (channel, block, tile) at row offset 128t/d + 16g), so
+    // there is no carry: the schedule runs with one "block" and T slots per super-tile.
+    int xr;          // dilation of the expanded rows (0 = natural rows, d = 8)
+    int rows_alloc;  // E rows per channel in a stage (n_box * box_rows)
+    int box_rows;    // rows per TMA box
+    int n_box;       // boxes per channel
 };
 
 struct KParams {
@@ -102,7 +110,53 @@ struct KParams {
     uint32_t pf_off, pf_slot_bytes, pf_rows, pf_mask;
 };
 
+bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve) {
+    if (main_ch > 0) return false;
+    if (g.dil != 1 && g.dil != 2 && g.dil != 4) return false;
+    if (g.n * g.in_ch >= (int64_t{1} << 31) || g.xr_rows >= (int64_t{1} << 31)) return false;
+    Plan p{};
+    p.xr = static_cast<int>(g.dil);
+    p.kp = g.out_ch <= 16 ? 16 : (g.out_ch <= 32 ? 32 : 64);
+    p.kgroups = static_cast<int>(ceil_div(g.out_ch, p.kp));
+    p.g = static_cast<int>(ceil_div(g.taps, kTapsPerBlock));
+    p.r = static_cast<int>(kTmemCols) / p.kp;
+    p.ntot = p.g * p.kp;
+    if (p.ntot > 256) return false;
+    p.t = std::min(8, 256 / p.kp);  // no carry: T slots per 256-column region, double-buffered
+    p.dbuf = getenv("C1D_NO_DBUF") == nullptr ? 1 : 0;
+    if (!p.dbuf) p.t = std::min(8, p.r);
+    p.acc2 = 0;
+    p.tail = 0;
+    // E is read as (64 elements = 8 rows, row octets, item x channel) boxes: 128-B inner box rows
+    // keep TMA on its fast path (16-B inner rows run at a third of the rate)
+    if (g.xr_rows % 8) return false;
+    const int rows_stage = static_cast<int>(ceil_div(p.t * (kTileQ / p.xr) + kTapsPerBlock * p.g, 8) * 8);
+    p.box_rows = std::min(256 * 8, rows_stage);
+    p.n_box = static_cast<int>(ceil_div(rows_stage, p.box_rows));
+    p.rows_alloc = p.n_box * p.box_rows;
+    p.n_seg = 0;
+    p.xw = 0;
+    p.b_chan_bytes = static_cast<uint32_t>(p.ntot * kTapsPerBlock * 2);
+    const uint32_t per_chan = static_cast<uint32_t>(p.rows_alloc * 16) + p.b_chan_bytes;
+    p.cc = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(48 * 1024 / per_chan, 16)));
+    p.cc = static_cast<int>(std::min<int64_t>(p.cc, g.in_ch));
+    {
+        const int64_t nch = ceil_div(g.in_ch, p.cc);
+        p.cc = static_cast<int>(ceil_div(g.in_ch, nch));
+    }
+    p.x_stage_bytes = static_cast<uint32_t>(p.cc * p.rows_alloc * 16);
+    p.w_stage_bytes = static_cast<uint32_t>(p.cc) * p.b_chan_bytes;
+    p.tx_stage_bytes = p.tw_stage_bytes = 0;
+    const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes;
+    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve) / stage));
+    if (p.stages < 2) return false;
+    p.smem_bytes = static_cast<size_t>(p.stages) * stage + 1024;
+    *pl = p;
+    return true;
+}
+
 bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserve = 0) {
+    if (g.xr_rows > 0) return make_plan_xr(g, pl, main_ch, reserve);
     const bool two_regions = main_ch > 0;
     if (g.dil != 8) return false;
     const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
@@ -274,13 +328,6 @@ __device__ __forceinline__ Cursor make_cursor(const KParams& p) {
 // every optional output is one guarded loop with a running pointer, the bias comes from shared
 // memory, mask words move one per lane (a ballot per row, one store / load per warp), and all
 // loads of a block are issued before its stores.
-
-// branch-free fp32_to_bf16_bits (RNE, NaN -> quiet NaN; inf falls out of the RNE formula)
-__device__ __forceinline__ uint16_t bf16_rne_bits(float f) {
-    const uint32_t u = __float_as_uint(f);
-    const uint32_t r = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
-    return static_cast<uint16_t>(((u & 0x7fffffffu) > 0x7f800000u) ? ((u >> 16) | 0x40u) : r);
-}
 
 // 16 values -> 8 words of bf16 pairs (rows 2i | 2i+1 << 16), hardware round-to-nearest-even:
 // identical to the reference's fp32_to_bf16 (bf16.hpp:29-40) for every non-NaN value, denormals and
@@ -538,7 +585,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* ws_base = smem + static_cast<size_t>(pl.stages) * pl.x_stage_bytes;
     uint8_t* tx_base = ws_base + static_cast<size_t>(pl.stages) * pl.w_stage_bytes;
     uint8_t* tw_base = tx_base + static_cast<size_t>(pl.stages) * pl.tx_stage_bytes;
-    const int G = pl.g, T = pl.t, KP = pl.kp;
+    // G: tap blocks the schedule carries between tiles (1 in expanded-row mode: no carry)
+    const int G = pl.xr ? 1 : pl.g, T = pl.t, KP = pl.kp;
     const int64_t J = p.tiles_per_item;
     const int n_chunks = static_cast<int>(ceil_div(p.in_ch, pl.cc));
 
@@ -578,15 +626,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(smem_u32(&stage_empty[stage]), phase ^ 1);
                     t_wait += clock64() - tw0;
                     const uint32_t full = smem_u32(&stage_full[stage]);
-                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (nseg * kSegQ * 2 + pl.b_chan_bytes) +
+                    const uint32_t xbytes = pl.xr ? static_cast<uint32_t>(pl.rows_alloc * 16) : static_cast<uint32_t>(nseg * kSegQ * 2);
+                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (xbytes + pl.b_chan_bytes) +
                                            (pl.tail ? pl.tail_chunks * pl.cc * 16u + pl.tw_stage_bytes : 0u);
                     mbar_arrive_expect_tx(full, bytes);
                     const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
-                    for (int c = 0; c < ccn; ++c) {
-                        const int32_t row = static_cast<int32_t>(su.n * p.in_ch + c0 + c);
-                        for (int sg = 0; sg < nseg; ++sg)
-                            tma_load_2d(xs + static_cast<uint32_t>((c * pl.xw + sg * kSegQ) * 2), &tmap,
-                                        x_start + sg * kSegQ, row, full);
+                    if (pl.xr) {  // E rows [128 i0 / d, ...) of each channel, n_box boxes
+                        const int32_t r0 = static_cast<int32_t>(su.i0 * (kTileQ / pl.xr));
+                        for (int c = 0; c < ccn; ++c) {
+                            const int32_t row = static_cast<int32_t>(su.n * p.in_ch + c0 + c);
+                            for (int b = 0; b < pl.n_box; ++b)
+                                tma_load_3d(xs + static_cast<uint32_t>((c * pl.rows_alloc + b * pl.box_rows) * 16), &tmap,
+                                            0, (r0 + b * pl.box_rows) / 8, row, full);
+                        }
+                    } else {
+                        for (int c = 0; c < ccn; ++c) {
+                            const int32_t row = static_cast<int32_t>(su.n * p.in_ch + c0 + c);
+                            for (int sg = 0; sg < nseg; ++sg)
+                                tma_load_2d(xs + static_cast<uint32_t>((c * pl.xw + sg * kSegQ) * 2), &tmap,
+                                            x_start + sg * kSegQ, row, full);
+                        }
                     }
                     const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                     bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
@@ -651,7 +710,34 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                 const uint64_t a0 = make_smem_desc(xs, 128, 16, kLayoutNone);
                 const uint64_t b0 = make_smem_desc(wsm + main_brow, 128, 256, kLayoutNone);
-                if (elect_one()) {
+                if (pl.xr) {
+                    // expanded rows: A = E rows (16 B, one tap each), M groups 128/d B apart;
+                    // tile t, block g at row 128t/d + 16g; B block g = image block G-1-g
+                    if (elect_one()) {
+                        const uint32_t tile_bytes = static_cast<uint32_t>((kTileQ / pl.xr) * 16);
+                        const uint32_t idesc_x = make_idesc(128, static_cast<uint32_t>(KP), kFmtBF16, 1, 0);
+                        uint64_t achan = make_smem_desc(xs, 128, static_cast<uint32_t>(128 / pl.xr), kLayoutNone);
+                        uint64_t bchan = make_smem_desc(wsm, 128, 256, kLayoutNone);
+                        for (int c = 0; c < ccn; ++c) {
+                            // image block b (ascending) holds tap block gb = G-1-b (A rows 16 gb)
+                            uint64_t ablk = desc_advance(achan, static_cast<uint32_t>((pl.g - 1) * kTapsPerBlock * 16));
+                            uint64_t bblk = bchan;
+                            for (int b = 0; b < pl.g; ++b) {
+                                uint64_t adesc = ablk;
+                                uint32_t dcol = rtmem;
+                                for (int t = 0; t < su.tcur; ++t) {
+                                    mma_bf16_ss(dcol, adesc, bblk, idesc_x, 1);
+                                    adesc = desc_advance(adesc, tile_bytes);
+                                    dcol += static_cast<uint32_t>(KP);
+                                }
+                                ablk -= static_cast<uint64_t>(kTapsPerBlock);  // 16 rows x 16 B, in 16-B units
+                                bblk = desc_advance(bblk, static_cast<uint32_t>(KP * 32));
+                            }
+                            achan = desc_advance(achan, static_cast<uint32_t>(pl.rows_alloc * 16));
+                            bchan = desc_advance(bchan, pl.b_chan_bytes);
+                        }
+                    }
+                } else if (elect_one()) {
                     uint64_t bdesc = b0;
                     uint64_t achan = a0;
                     for (int c = 0; c < ccn; ++c) {
@@ -978,6 +1064,11 @@ bool glue_maps(const ConvGeom& g, const LayerGlue& gl, PFN_cuTensorMapEncodeTile
 
 }  // namespace
 
+int64_t tc_conv_xr_rows(const ConvGeom& g) {
+    if (g.dil != 1 && g.dil != 2 && g.dil != 4) return 0;
+    return ceil_div(g.out_w, kTileQ) * (kTileQ / g.dil) + kTapsPerBlock * ceil_div(g.taps, kTapsPerBlock) + 8;
+}
+
 bool tc_conv_supported(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
     return make_plan(g, &pl, main_ch);
@@ -1027,13 +1118,24 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         if (e != cudaSuccess) return e;
     }
     CUtensorMap tmap;
-    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.in_w), static_cast<cuuint64_t>(g.n * g.in_ch)};
-    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.in_stride ? g.in_stride : g.in_w) * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(kSegQ), 1};
-    const cuuint32_t estr[2] = {1, 1};
-    CUresult r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(in_bf16), dims, strides,
-                        box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    CUresult r;
+    if (pl.xr) {  // the row tensor E: (8 elements, rows, item x channel)
+        const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(g.xr_rows / 8), static_cast<cuuint64_t>(g.n * g.in_ch)};
+        const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(g.xr_rows) * 16};
+        const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(pl.box_rows / 8), 1};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(in_bf16), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.in_w), static_cast<cuuint64_t>(g.n * g.in_ch)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.in_stride ? g.in_stride : g.in_w) * 2};
+        const cuuint32_t box[2] = {static_cast<cuuint32_t>(kSegQ), 1};
+        const cuuint32_t estr[2] = {1, 1};
+        r = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(in_bf16), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     CUtensorMap tmap_tail = tmap;  // unused unless pl.tail
     if (pl.tail) {

@@ -248,6 +248,24 @@ def test_other_dilations_on_tensor_cores(d, bf16_storage, q):
         assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} q={q} {name}")
 
 
+@pytest.mark.parametrize("d", [1, 2, 4])
+@pytest.mark.parametrize("c,k", [(15, 15), (64, 64)])
+def test_expanded_rows_long_filters(d, c, k):
+    """d < 8 on the expanded-row tensor-core mode with 4 tap blocks (S = 51), several super-tiles
+    per item and a ragged last tile, vs the oracle on BF16-rounded inputs (AUTO selection)."""
+    rng = oracle.Rng(3000 + 10 * d + c)
+    n, s, q = 2, 51, 1500
+    w_in = q + d * (s - 1)
+    x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
+    p = cv.ConvParams(c, k, s, d, cv.Precision.Bf16)
+    for i in range(2):
+        assert cv.selected_algo(p, n, w_in, i, in_dtype=1) == "tcgen05", (d, i)
+    got = run_passes(x, w, dy, d, cv.Precision.Bf16, bf16_storage=True)
+    want = oracle_passes(oracle.round_bf16(x), oracle.round_bf16(w), oracle.round_bf16(dy), d)
+    for g, wv, name in zip(got, want, ("fwd", "bwd_d", "bwd_w")):
+        assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} c={c} {name}")
+
+
 @pytest.mark.parametrize("d", [1, 2, 4, 8, 16])
 def test_fp32_split_path_other_dilations(d):
     """FP32 precision on the tensor cores (bf16x3 operand split) composed with the dilation

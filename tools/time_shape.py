@@ -1,6 +1,7 @@
 """Time one pass on an ad-hoc d=8 BF16 shape (dev tool).
 
 usage: python tools/time_shape.py N C K S Q [pass ...]     pass in {fwd,bwd_d,bwd_w}
+(env D = dilation, default 8)
 """
 import os
 import sys
@@ -12,8 +13,9 @@ from paper_2104_08002_b200 import conv as cv  # noqa: E402
 
 n, c, k, s, q = (int(a) for a in sys.argv[1:6])
 passes = sys.argv[6:] or ["fwd", "bwd_d", "bwd_w"]
-w_in = q + 8 * (s - 1)
-p = cv.ConvParams(c, k, s, 8, cv.Precision.Bf16)
+dil = int(os.environ.get("D", "8"))
+w_in = q + dil * (s - 1)
+p = cv.ConvParams(c, k, s, dil, cv.Precision.Bf16)
 x = torch.randn((n, c, w_in), device="cuda").bfloat16()
 dy = torch.randn((n, k, q), device="cuda").bfloat16()
 w = torch.randn((k, c, s), device="cuda") * 0.05
@@ -39,4 +41,4 @@ for name in passes:
         torch.cuda.synchronize()
         ts.append(a.elapsed_time(b) * 1e3)
     ts.sort()
-    print(f"N={n} C={c} K={k} S={s} Q={q} {name:6s} median {ts[5]:8.1f} us  {flops / ts[5] / 1e6:7.1f} TFLOP/s")
+    print(f"N={n} C={c} K={k} S={s} d={dil} Q={q} {name:6s} median {ts[5]:8.1f} us  {flops / ts[5] / 1e6:7.1f} TFLOP/s")
