@@ -192,6 +192,12 @@ ConvGeom xr_geom(ConvGeom g) {
     return g;
 }
 bool xr_ok(const ConvGeom& g) { return (g.dil == 1 || g.dil == 2 || g.dil == 4) && tc_conv_supported(xr_geom(g)); }
+// backward-weight on expanded rows (d = 1, 2, 4): one tc_wgrad launch over E (rows of x at every
+// d-column start) instead of one launch per phase
+int64_t xr_wgrad_rows(const c1d_desc& d, int64_t q_pad) { return ceil_div(q_pad + d.d * (d.s - 1), d.d) + 16; }
+bool xr_wgrad_ok(const c1d_desc& d, int64_t q_pad) {
+    return (d.d == 1 || d.d == 2 || d.d == 4) && tc_wgrad_v3_supported(d.n, d.c, d.k, d.s, d.d, q_pad);
+}
 // backward-weight: Q is padded to a multiple of 8 (zero dY columns add nothing) and x gets a
 // zero-padded pitch covering Q_pad + d(S-1) when either width is unaligned.
 struct WgradPad {
@@ -247,7 +253,8 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
             const WgradPad wp = wgrad_pad(d, q);
             if (dp.kind == DilPlan::kNative) return tc_wgrad_supported(d.n, d.c, d.k, d.s, 8, wp.q_pad);
             if (dp.kind == DilPlan::kPhases)
-                return (d.algo == C1D_ALGO_TCGEN05 || phases_pay_off(dp, d.c)) && phase_wgrad_ok(d, q, dp);
+                return xr_wgrad_ok(d, wp.q_pad) ||
+                       ((d.algo == C1D_ALGO_TCGEN05 || phases_pay_off(dp, d.c)) && phase_wgrad_ok(d, q, dp));
             return tc_wgrad_supported(d.n * dp.m, d.c, d.k, d.s, 8, q / dp.m);
         }
         const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
@@ -304,6 +311,12 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     // tensor-core paths: BF16 copies of FP32 inputs + kernel workspace
     const bool conv_in_f32 = d.in_dtype == C1D_DTYPE_F32;
     const DilPlan dp = dil_plan(d, q);
+    if (pass == C1D_PASS_BACKWARD_WEIGHT && dp.kind == DilPlan::kPhases && xr_wgrad_ok(d, wgrad_pad(d, q).q_pad)) {
+        const WgradPad wpd = wgrad_pad(d, q);
+        return align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad)) +
+               align_up(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * d.c * xr_wgrad_rows(d, wpd.q_pad))) +
+               align_up(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+    }
     if (pass == C1D_PASS_BACKWARD_WEIGHT && dp.kind != DilPlan::kPlanes) {
         const WgradPad wpd = wgrad_pad(d, q);
         size_t b = 0;
@@ -766,6 +779,25 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     }
     e = cudaSuccess;
     const WgradPad wpd = wgrad_pad(d, q);
+    if (dpl.kind == DilPlan::kPhases && xr_wgrad_ok(d, wpd.q_pad)) {
+        // d < 8: x as expanded rows (rounded to BF16 on the way), dY padded / rounded if needed
+        const uint16_t* g16 = static_cast<const uint16_t*>(dy);
+        if (wpd.pad || d.in_dtype == C1D_DTYPE_F32) {
+            uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad));
+            e = wpd.pad ? launch_pad_rows(dy, d.in_dtype, tg, d.n * d.k, q, wpd.q_pad, stream)
+                        : launch_round_bf16(static_cast<const float*>(dy), tg, d.n * d.k * q, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "dy copy");
+            g16 = tg;
+        }
+        const int64_t rows = xr_wgrad_rows(d, wpd.q_pad);
+        uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * d.c * rows));
+        e = launch_expand_rows(x, d.in_dtype, ex, d.n * d.c, d.w_in, d.d, 0, rows, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "expand_rows");
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+        e = launch_tc_wgrad(ex, g16, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, wpd.q_pad, stream, rows * 8);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (expanded rows)");
+        return C1D_OK;
+    }
     const uint16_t* xb = static_cast<const uint16_t*>(x);
     const uint16_t* gb = static_cast<const uint16_t*>(dy);
     if (wpd.pad) {  // zero-padded bf16 copies with 8-element pitches (rounds FP32 storage too)

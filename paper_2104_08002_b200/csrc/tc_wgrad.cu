@@ -331,19 +331,26 @@ struct W2Plan {
     int xb, span, kch, ring;
     uint32_t chunk_bytes, ring_bytes;
     int copies;  // accumulator copies per group (power of two)
+    // Expanded rows (d = 1, 2, 4): X arrives as the row tensor E (rows of 8 elements at every
+    // d-column start, launch_expand_rows). A ring "chunk" is then one E row per channel, i.e. a
+    // column step of d: a tap is one chunk for every d, and 8 columns are ph = 8/d chunks (the
+    // K-group stride). dY copies are off (P = 1): their Bq-column shift would need sub-16-B boxes.
+    int ph;
 };
 
 bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out) {
-    if (d != 8 || q % 8 != 0 || q < 16) return false;
+    if (q % 8 != 0 || q < 16) return false;
+    if (d != 8 && d != 1 && d != 2 && d != 4) return false;
     if (c > 128 || k > 128) return false;
     if (n * c >= (int64_t{1} << 31) || n * k >= (int64_t{1} << 31)) return false;
     W2Plan p{};
+    p.ph = static_cast<int>(8 / d);
     p.cp = 16;
     while (p.cp < c) p.cp *= 2;
     p.t = 128 / p.cp;
     p.kpw = 16;
     while (p.kpw < k) p.kpw *= 2;
-    p.p = std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t)));
+    p.p = d == 8 ? std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t))) : 1;
     p.n = p.p * p.kpw;
     p.bq = 8 * p.t;
     if (p.bq > 64) return false;
@@ -383,30 +390,35 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     //   ring >= 2*span + stages*kch   (the window a stage reads, the stages-1 stages the
     //   loaders may run ahead, and one extra fresh window when an item boundary falls in there)
     // Ring positions [0, xb) are mirrored past the end, xb = the furthest chunk one stage's MMAs
-    // reach beyond the stage's first chunk, so a stage never wraps.
-    p.ks = kW2Ks;
-    p.stage_q = 16 * p.ks;
-    p.kch = 2 * p.ks;
-    p.xb = 2 * (p.ks - 1) + (p.gpc - 1) * p.taps_per_group + p.t + 1;
+    // reach beyond the stage's first chunk, so a stage never wraps. Expanded rows take ph chunks
+    // per 8 columns, so their stages shrink (fewer K-steps) until the ring fits.
     p.chunk_bytes = static_cast<uint32_t>(p.cp * 16);
-    p.span = static_cast<int>(ceil_div(p.gpc * p.taps_per_group + p.t + 1, 4) * 4);
-    p.x_chunks = p.kch + p.span;
-    p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
-    p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
-    p.stage_bytes = p.y_bytes;
-    bool ok = false;
+    p.span = static_cast<int>(ceil_div(p.gpc * p.taps_per_group + p.t + p.ph, 4) * 4);
     static const int max_stages = [] {  // C1D_W2_STAGES: dev override of the stage cap
         const char* e = getenv("C1D_W2_STAGES");
         const int v = e ? atoi(e) : kW2MaxStages;
         return v >= 3 && v <= kW2MaxStages ? v : kW2MaxStages;
     }();
-    for (int st = max_stages; st >= 3; --st) {
-        p.stages = st;
-        p.ring = static_cast<int>(ceil_div(2 * p.span + st * p.kch, 4) * 4);
-        p.ring_bytes = ((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u;
-        if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes <= kW2SmemBudget) {
-            ok = true;
-            break;
+    const int ks_unit = std::max(1, p.bq / 16);  // K-steps per dY box
+    bool ok = false;
+    for (int ks = kW2Ks; ks >= 1 && !ok; --ks) {
+        if (ks % ks_unit || (2 * ks * p.ph) % 4) continue;
+        p.ks = ks;
+        p.stage_q = 16 * p.ks;
+        p.kch = 2 * p.ks * p.ph;
+        p.xb = 2 * p.ph * (p.ks - 1) + (p.gpc - 1) * p.taps_per_group + p.t + p.ph;
+        p.x_chunks = p.kch + p.span;
+        p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
+        p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
+        p.stage_bytes = p.y_bytes;
+        for (int st = max_stages; st >= 3; --st) {
+            p.stages = st;
+            p.ring = static_cast<int>(ceil_div(2 * p.span + st * p.kch, 4) * 4);
+            p.ring_bytes = ((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u;
+            if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes <= kW2SmemBudget) {
+                ok = true;
+                break;
+            }
         }
     }
     if (!ok) return false;
@@ -543,7 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // 16/Bq K-steps (32 B each) per box
         W2Issue wi;
         wi.idesc = idesc;
-        wi.a_ks = (2u * pl.chunk_bytes) >> 4;
+        wi.a_ks = (2u * static_cast<uint32_t>(pl.ph) * pl.chunk_bytes) >> 4;
         wi.a_g = (static_cast<uint32_t>(pl.taps_per_group) * pl.chunk_bytes) >> 4;
         if (pl.bq == 8) {
             wi.per_box = 1;
@@ -587,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
                 // A (X) of K-step ks, group g starts at chunk lo + 2ks + g*tpg: ring position
                 const int stage_pos = cur_pos;  // ring position of chunk `lo`
-                const uint64_t ax0 = make_smem_desc(smem_u32(smem), static_cast<uint32_t>(pl.cp * 16), 128, kLayoutNone);
+                const uint64_t ax0 = make_smem_desc(smem_u32(smem), static_cast<uint32_t>(pl.ph * pl.cp * 16), 128, kLayoutNone);
                 const uint64_t by0 = make_smem_desc(smem_u32(sbase), b_lbo, b_sbo, pl.swz);
                 // One elected lane issues the whole stage. The ring mirror keeps every address of
                 // the stage wrap-free, so a full stage is a straight-line run of MMAs.
@@ -645,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int64_t st = cur; st < seg_end; st += pl.ks) {
                 const int64_t q0 = (st - item * p.steps_per_item) * 16;
                 mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-                const int64_t first_chunk = seg_first ? q0 / 8 + tap0 : next_chunk;
+                const int64_t first_chunk = seg_first ? q0 * pl.ph / 8 + tap0 : next_chunk;
                 const int nchunks = seg_first ? pl.span + pl.kch : pl.kch;
                 seg_first = false;
                 next_chunk = first_chunk + nchunks;
