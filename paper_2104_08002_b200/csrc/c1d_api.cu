@@ -236,6 +236,12 @@ struct SplitConv {
 };
 SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const DilPlan& dp) {
     ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
+    if (dp.kind == DilPlan::kPhases) {  // expanded rows of the split channels when the kernel fits
+        ConvGeom g4 = g;
+        g4.in_ch *= 4;
+        g4 = xr_geom(g4);
+        if ((g.dil == 1 || g.dil == 2 || g.dil == 4) && tc_conv_supported(g4, g.in_ch)) return SplitConv{g4, g.in_ch};
+    }
     if (dp.kind == DilPlan::kPlanes) g = plane_geom(g, dp);
     if (dp.kind == DilPlan::kPhases) g = phase_geom(g, dp);
     SplitConv r{g, g.in_ch};
@@ -271,6 +277,10 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {
             if (dp.kind == DilPlan::kPlanes) return tc_wgrad_supported(d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m);
+            if (dp.kind == DilPlan::kPhases && d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, d.c)) return false;
+            if (dp.kind == DilPlan::kPhases && q % 8 == 0 && (d.d == 1 || d.d == 2 || d.d == 4) &&
+                tc_wgrad_v3_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q))
+                return true;  // expanded rows
             if (d.w_in % 8 || q % 8) return false;
             if (dp.kind == DilPlan::kNative) return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q);
             if (d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, d.c)) return false;
@@ -287,6 +297,8 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         constexpr int64_t kMaxSplitTerms = 3300;
         const int64_t cin = pass == C1D_PASS_FORWARD ? d.c : d.k;
         if (cin * d.s > kMaxSplitTerms) return false;
+        // Small FP32 problems stay on FFMA (exact FP32 products, smooth in the inputs: the reference's
+        // finite-difference acceptance checks at eps 1e-3 resolve the split's 1e-6-level error).
         if (dp.kind == DilPlan::kPhases && d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, cin)) return false;
         const SplitConv sc = split_conv_geom(d, pass, q, dp);
         return tc_conv_supported(sc.gs, sc.main_ch);
@@ -422,7 +434,7 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
     auto step = [&](auto&& launch) {
         if (run && e == cudaSuccess) e = launch();
     };
-    if (dp.kind != DilPlan::kPhases) {
+    if (dp.kind != DilPlan::kPhases || sc.gs.xr_rows > 0) {
         float* w4 = bump.take<float>(4 * sizeof(float) * kcs);
         float* wg4 = bump.take<float>(4 * sizeof(float) * kcs);
         if (pass == C1D_PASS_FORWARD) {  // c-blocks hi,hi,lo,lo
@@ -442,6 +454,16 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
             step([&] { return launch_to_planes(x4, C1D_DTYPE_BF16, p4, g.n, 4 * g.in_ch, g.in_w, dp.m, stream); });
             step([&] { return launch_tc_conv(p4, wg4, pout, sc.gs, kws, stream, sc.main_ch); });
             step([&] { return launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream); });
+            return e;
+        }
+        if (sc.gs.xr_rows > 0) {  // d < 8: expanded rows of the split channels
+            uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(g.n * 4 * g.in_ch * sc.gs.xr_rows));
+            void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
+            step([&] {
+                return launch_expand_rows(x4, C1D_DTYPE_BF16, ex, g.n * 4 * g.in_ch, g.in_w, g.dil, g.in_off, sc.gs.xr_rows,
+                                          stream);
+            });
+            step([&] { return launch_tc_conv(ex, wg4, out, sc.gs, kws, stream, sc.main_ch); });
             return e;
         }
         void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
@@ -485,6 +507,18 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
     uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * ng);
     step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, 0x2u, stream); });
     step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, 0x2u, stream); });
+    if (dp.kind == DilPlan::kPhases && (d.d == 1 || d.d == 2 || d.d == 4) &&
+        tc_wgrad_v3_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q)) {
+        // expanded rows of the split x, one launch
+        const int64_t rows = xr_wgrad_rows(d, q);
+        uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(2 * d.n * d.c * rows));
+        float* dw4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q));
+        step([&] { return launch_expand_rows(x2, C1D_DTYPE_BF16, ex, 2 * d.n * d.c, d.w_in, d.d, 0, rows, stream); });
+        step([&] { return launch_tc_wgrad(ex, g2, dw4, kws, d.n, 2 * d.c, 2 * d.k, d.s, d.d, q, stream, rows * 8); });
+        step([&] { return launch_sum_split_blocks(dw4, dw, d.k, d.c, d.s, stream); });
+        return e;
+    }
     if (dp.kind == DilPlan::kPhases) {
         const int64_t pitch = round8(std::max<int64_t>(d.w_in, q + 8 * (dp.sp - 1)));
         uint16_t* xs = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * pitch));

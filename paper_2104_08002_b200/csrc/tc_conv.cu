@@ -111,7 +111,6 @@ struct KParams {
 };
 
 bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve) {
-    if (main_ch > 0) return false;
     if (g.dil != 1 && g.dil != 2 && g.dil != 4) return false;
     if (g.n * g.in_ch >= (int64_t{1} << 31) || g.xr_rows >= (int64_t{1} << 31)) return false;
     Plan p{};
@@ -126,6 +125,11 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.dbuf = getenv("C1D_NO_DBUF") == nullptr ? 1 : 0;
     if (!p.dbuf) p.t = std::min(8, p.r);
     p.acc2 = 0;
+    if (main_ch > 0) {  // split FP32: the second 256-column region holds the correction terms
+        p.dbuf = 0;
+        p.t = std::min(8, 256 / p.kp);
+        p.acc2 = 256;
+    }
     p.tail = 0;
     // E is read as (64 elements = 8 rows, row octets, item x channel) boxes: 128-B inner box rows
     // keep TMA on its fast path (16-B inner rows run at a third of the rate)
@@ -722,9 +726,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // image block b (ascending) holds tap block gb = G-1-b (A rows 16 gb)
                             uint64_t ablk = desc_advance(achan, static_cast<uint32_t>((pl.g - 1) * kTapsPerBlock * 16));
                             uint64_t bblk = bchan;
+                            const uint32_t dbase = rtmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u);
                             for (int b = 0; b < pl.g; ++b) {
                                 uint64_t adesc = ablk;
-                                uint32_t dcol = rtmem;
+                                uint32_t dcol = dbase;
                                 for (int t = 0; t < su.tcur; ++t) {
                                     mma_bf16_ss(dcol, adesc, bblk, idesc_x, 1);
                                     adesc = desc_advance(adesc, tile_bytes);
