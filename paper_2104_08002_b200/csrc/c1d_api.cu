@@ -667,10 +667,11 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
 // Fused: the glue runs in the tcgen05 conv epilogue (native dilation 8 and the phase rewrite, whose
 // output layout is the caller's). Otherwise the conv writes an FP32 scratch tensor and one
 // layer.cu glue pass follows.
-bool glue_fusable(const c1d_desc& d, int64_t q, c1d_algo algo) {
+bool glue_fusable(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo) {
     if (algo != C1D_ALGO_TCGEN05) return false;
     const DilPlan dp = dil_plan(d, q);
-    return dp.kind == DilPlan::kNative || dp.kind == DilPlan::kPhases;
+    // the glue epilogue handles filter blocks of up to 64 (the expanded-row mode takes KP = 128 above)
+    return dp.kind == DilPlan::kNative || (dp.kind == DilPlan::kPhases && (pass == C1D_PASS_FORWARD ? d.k : d.c) <= 64);
 }
 struct GlueSizes {
     bool fused;
@@ -679,7 +680,7 @@ struct GlueSizes {
 };
 GlueSizes glue_sizes(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo, int64_t glue_q) {
     GlueSizes r{};
-    r.fused = glue_fusable(d, q, algo);
+    r.fused = glue_fusable(d, pass, q, algo);
     r.conv = align_up(workspace_for(d, pass, q, algo));
     const bool fwd = pass == C1D_PASS_FORWARD;
     const int64_t out_elems = fwd ? d.n * d.k * q : d.n * d.c * d.w_in;

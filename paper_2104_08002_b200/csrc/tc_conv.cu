@@ -115,14 +115,16 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     if (g.n * g.in_ch >= (int64_t{1} << 31) || g.xr_rows >= (int64_t{1} << 31)) return false;
     Plan p{};
     p.xr = static_cast<int>(g.dil);
-    p.kp = g.out_ch <= 16 ? 16 : (g.out_ch <= 32 ? 32 : 64);
+    // N = KP per MMA here, so wide filter blocks pay: KP = 128 halves the A-tile re-reads per filter
+    // and reads E once (one filter group) — single-buffered, 4 tiles per super-tile
+    p.kp = g.out_ch <= 16 ? 16 : (g.out_ch <= 32 ? 32 : (g.out_ch <= 64 || main_ch > 0 ? 64 : 128));
     p.kgroups = static_cast<int>(ceil_div(g.out_ch, p.kp));
     p.g = static_cast<int>(ceil_div(g.taps, kTapsPerBlock));
     p.r = static_cast<int>(kTmemCols) / p.kp;
     p.ntot = p.g * p.kp;
-    if (p.ntot > 256) return false;
+    if (p.ntot > 1024) return false;
     p.t = std::min(8, 256 / p.kp);  // no carry: T slots per 256-column region, double-buffered
-    p.dbuf = getenv("C1D_NO_DBUF") == nullptr ? 1 : 0;
+    p.dbuf = getenv("C1D_NO_DBUF") == nullptr && p.kp <= 64 ? 1 : 0;
     if (!p.dbuf) p.t = std::min(8, p.r);
     p.acc2 = 0;
     if (main_ch > 0) {  // split FP32: the second 256-column region holds the correction terms
@@ -1074,6 +1076,11 @@ int64_t tc_conv_xr_rows(const ConvGeom& g) {
     return ceil_div(g.out_w, kTileQ) * (kTileQ / g.dil) + kTapsPerBlock * ceil_div(g.taps, kTapsPerBlock) + 8;
 }
 
+int pl_probe_kp(const ConvGeom& g, int64_t main_ch) {
+    Plan pl;
+    return make_plan(g, &pl, main_ch) ? pl.kp : 0;
+}
+
 bool tc_conv_supported(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
     return make_plan(g, &pl, main_ch);
@@ -1095,6 +1102,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     if (glue && glue->mode != 0 && !no_glue_tma && !glue_maps(g, *glue, encode, &gm)) gm = GlueMaps{};
     const uint32_t stg_total = 8u * gm.stg_bytes;  // 4 epilogue warps x 2 buffers
     const int mode = glue ? glue->mode : 0;
+    if (mode != 0 && pl_probe_kp(g, main_ch) > 64) return cudaErrorNotSupported;  // glue: KP <= 64
     const uint32_t pf_rows = (mode == 1 && glue->skip) || (mode == 2 && glue->gadd);
     const uint32_t pf_mask = mode == 2 && glue->mask_in;
     const uint32_t pf_slot = pf_rows * 2048u + pf_mask * 128u;  // rows: 16 x 32 fp32, mask: 32 words

@@ -249,12 +249,13 @@ def test_other_dilations_on_tensor_cores(d, bf16_storage, q):
 
 
 @pytest.mark.parametrize("d", [1, 2, 4])
-@pytest.mark.parametrize("c,k", [(15, 15), (64, 64)])
-def test_expanded_rows_long_filters(d, c, k):
-    """d < 8 on the expanded-row tensor-core mode with 4 tap blocks (S = 51), several super-tiles
-    per item and a ragged last tile, vs the oracle on BF16-rounded inputs (AUTO selection)."""
+@pytest.mark.parametrize("c,k,s", [(15, 15, 51), (64, 64, 51), (96, 128, 25)])
+def test_expanded_rows_long_filters(d, c, k, s):
+    """d < 8 on the expanded-row tensor-core mode with several tap blocks, several super-tiles
+    per item and a ragged last tile, vs the oracle on BF16-rounded inputs (AUTO selection).
+    (96, 128): 128-wide filter blocks (single-buffered, one filter group)."""
     rng = oracle.Rng(3000 + 10 * d + c)
-    n, s, q = 2, 51, 1500
+    n, q = 2, 1500
     w_in = q + d * (s - 1)
     x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
     p = cv.ConvParams(c, k, s, d, cv.Precision.Bf16)

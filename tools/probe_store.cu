@@ -51,9 +51,9 @@ int main() {
     CK(cudaMalloc(&out, sizeof(float) * static_cast<size_t>(ITEMS) * ROWS_PER_ITEM * W));
     long long* cyc;
     CK(cudaMalloc(&cyc, 148 * sizeof(long long)));
-    for (int threads : {128, 256, 512})
+    for (int threads : {128})
     for (int mode = 0; mode < 1; ++mode)
-        for (int grid : {148}) {
+        for (int grid : {8, 37, 74, 148}) {
             const int tiles = 5;
             for (int rep = 0; rep < 2; ++rep) {
                 store_probe<<<grid, threads>>>(out, tiles, mode, cyc);
