@@ -192,6 +192,21 @@ ConvGeom xr_geom(ConvGeom g) {
     return g;
 }
 bool xr_ok(const ConvGeom& g) { return (g.dil == 1 || g.dil == 2 || g.dil == 4) && tc_conv_supported(xr_geom(g)); }
+// the same mode with E's rows built in shared memory from natural bf16 rows (pitch padded to 8)
+ConvGeom xr_inline_geom(const ConvGeom& g) {
+    ConvGeom r = pitched(g);
+    r.xr_inline = true;
+    return r;
+}
+// Inline pays when the MMAs per expanded row are many enough to hide the expanders' shared-memory
+// work: 128/(d*G) rows per (tile, block) MMA <= 32. With few taps at d = 1, 2 the TMA-fed row
+// tensor is faster (measured: C = 16, S = 3, d = 1: 60 vs 85 us; C = 64, S = 51, d = 1 bwd-d:
+// 327 vs 259 us).
+bool xr_inline_ok(const ConvGeom& g) {
+    if (g.dil != 1 && g.dil != 2 && g.dil != 4) return false;
+    if (g.dil * ceil_div(g.taps, 16) < 4) return false;
+    return tc_conv_supported(xr_inline_geom(g));
+}
 // backward-weight on expanded rows (d = 1, 2, 4): one tc_wgrad launch over E (rows of x at every
 // d-column start) instead of one launch per phase
 int64_t xr_wgrad_rows(const c1d_desc& d, int64_t q_pad) { return ceil_div(q_pad + d.d * (d.s - 1), d.d) + 16; }
@@ -346,6 +361,13 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
                    align_up(sizeof(float) * static_cast<size_t>(d.k * dp.p * d.c * dp.sp)) + align_up(kws);
         }
         return b + align_up(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, wpd.q_pad));
+    }
+    if (dp.kind == DilPlan::kPhases && xr_inline_ok(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q))) {
+        const ConvGeom g = xr_inline_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
+        size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
+        if (g.in_stride || conv_in_f32)
+            b += align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * (g.in_stride ? g.in_stride : g.in_w)));
+        return b;
     }
     if (dp.kind == DilPlan::kPhases && xr_ok(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q))) {
         const ConvGeom g = xr_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
@@ -615,6 +637,27 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         e = launch_tc_conv(pin, wg, pout, gp, kws, stream);
         if (e == cudaSuccess) e = launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (planes)");
+        return C1D_OK;
+    }
+    if (use_xr && xr_inline_ok(g)) {
+        // d < 8: expanded rows built in shared memory from the natural bf16 rows
+        const ConvGeom gi = xr_inline_geom(g);
+        const uint16_t* in_b = static_cast<const uint16_t*>(in);
+        if (gi.in_stride) {
+            uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * gi.in_stride));
+            e = launch_pad_rows(in, d.in_dtype, tmp, g.n * g.in_ch, g.in_w, gi.in_stride, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
+            in_b = tmp;
+        } else if (d.in_dtype == C1D_DTYPE_F32) {
+            const int64_t count = g.n * g.in_ch * g.in_w;
+            uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(count));
+            e = launch_round_bf16(static_cast<const float*>(in), tmp, count, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
+            in_b = tmp;
+        }
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gi));
+        e = launch_tc_conv(in_b, w_kcs, out, gi, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_conv (expanded rows, inline)");
         return C1D_OK;
     }
     if (use_xr) {

@@ -23,6 +23,9 @@ struct ConvGeom {
     // expanded rows (d = 1, 2, 4): the input is the row tensor E of launch_expand_rows, rows of 8
     // bf16 elements E[n*C + c][r][e] = x[n][c][d*r + e + in_off]; out[q] uses rows q/d + s.
     int64_t xr_rows = 0;  // rows per (item, channel) of E; 0 = natural rows
+    // xr_inline (d = 1, 2, 4): the input stays natural bf16 rows (pitch in_stride or in_w, a
+    // multiple of 8) and the kernel builds E's rows in shared memory (no E tensor in HBM)
+    bool xr_inline = false;
 };
 
 enum WeightMode { kWeightsForward = 0, kWeightsBackwardData = 1 };

@@ -86,6 +86,12 @@ struct Plan {
     int rows_alloc;  // E rows per channel in a stage (n_box * box_rows)
     int box_rows;    // rows per TMA box
     int n_box;       // boxes per channel
+    // inline expansion: the producer loads natural windows (raw_segs 256-column boxes per channel,
+    // from a 16-B aligned start) and warps 2-3 write E's rows into the stage
+    int xin;
+    int rows_stage;       // E rows the MMAs read per channel
+    int raw_segs;         // 256-column boxes per channel window
+    uint32_t raw_stage_bytes;
 };
 
 struct KParams {
@@ -135,15 +141,25 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.tail = 0;
     // E is read as (64 elements = 8 rows, row octets, item x channel) boxes: 128-B inner box rows
     // keep TMA on its fast path (16-B inner rows run at a third of the rate)
-    if (g.xr_rows % 8) return false;
+    if (!g.xr_inline && g.xr_rows % 8) return false;
     const int rows_stage = static_cast<int>(ceil_div(p.t * (kTileQ / p.xr) + kTapsPerBlock * p.g, 8) * 8);
+    p.rows_stage = rows_stage;
     p.box_rows = std::min(256 * 8, rows_stage);
     p.n_box = static_cast<int>(ceil_div(rows_stage, p.box_rows));
     p.rows_alloc = p.n_box * p.box_rows;
+    p.xin = g.xr_inline ? 1 : 0;
+    if (p.xin) {
+        const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
+        if (pitch % 8 || pitch < g.in_w) return false;
+        // window: up to 7 leading columns of alignment + the rows' reach + one 16-B read of slack
+        p.raw_segs = static_cast<int>(ceil_div(7 + (rows_stage - 1) * p.xr + 8 + 8, kSegQ));
+        p.rows_alloc = rows_stage;
+    }
     p.n_seg = 0;
     p.xw = 0;
     p.b_chan_bytes = static_cast<uint32_t>(p.ntot * kTapsPerBlock * 2);
-    const uint32_t per_chan = static_cast<uint32_t>(p.rows_alloc * 16) + p.b_chan_bytes;
+    const uint32_t raw_chan = p.xin ? static_cast<uint32_t>(p.raw_segs * kSegQ * 2) : 0u;
+    const uint32_t per_chan = static_cast<uint32_t>(p.rows_alloc * 16) + p.b_chan_bytes + raw_chan;
     p.cc = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(48 * 1024 / per_chan, 16)));
     p.cc = static_cast<int>(std::min<int64_t>(p.cc, g.in_ch));
     {
@@ -153,7 +169,8 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.x_stage_bytes = static_cast<uint32_t>(p.cc * p.rows_alloc * 16);
     p.w_stage_bytes = static_cast<uint32_t>(p.cc) * p.b_chan_bytes;
     p.tx_stage_bytes = p.tw_stage_bytes = 0;
-    const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes;
+    p.raw_stage_bytes = static_cast<uint32_t>(p.cc) * raw_chan;
+    const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.raw_stage_bytes;
     p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve) / stage));
     if (p.stages < 2) return false;
     p.smem_bytes = static_cast<size_t>(p.stages) * stage + 1024;
@@ -162,7 +179,7 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
 }
 
 bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserve = 0) {
-    if (g.xr_rows > 0) return make_plan_xr(g, pl, main_ch, reserve);
+    if (g.xr_rows > 0 || g.xr_inline) return make_plan_xr(g, pl, main_ch, reserve);
     const bool two_regions = main_ch > 0;
     if (g.dil != 8) return false;
     const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
@@ -569,6 +586,49 @@ __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t
     }
 }
 
+// Inline E rows: rows r0 .. r0+RG-1 of one channel from its natural window (element e of row r =
+// window[K0 + D*r + e], K0 = the window's alignment offset, uniform per super-tile). A group's
+// window words are loaded once; every index is compile-time (one instantiation per D, K0).
+template <int D, int K0>
+__device__ __forceinline__ void expand_group_rows(uint32_t rc, uint32_t xc, int rows, int et) {
+    constexpr int RG = D == 4 ? 4 : 8;                 // rows per group
+    constexpr int NW = ((K0 + D * (RG - 1) + 8 + 7) / 8) * 4;  // 32-bit words loaded
+    for (int r0 = et * RG; r0 < rows; r0 += 64 * RG) {
+        const uint32_t src = rc + static_cast<uint32_t>(D * r0 * 2);  // 16-B aligned (D*r0 % 8 == 0)
+        uint32_t w[NW];
+#pragma unroll
+        for (int i = 0; i < NW; i += 4)
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w[i]), "=r"(w[i + 1]), "=r"(w[i + 2]), "=r"(w[i + 3])
+                         : "r"(src + static_cast<uint32_t>(i * 4)));
+#pragma unroll
+        for (int j = 0; j < RG; ++j) {
+            const int o = K0 + D * j;  // element offset of the row in the loaded words
+            uint32_t v[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                v[i] = (o & 1) ? __funnelshift_r(w[(o >> 1) + i], w[(o >> 1) + i + 1], 16) : w[(o >> 1) + i];
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(xc + static_cast<uint32_t>((r0 + j) * 16)),
+                         "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+                         : "memory");
+        }
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void expand_rows_d(uint32_t rc, uint32_t xc, int rows, int et, int off) {
+    switch (off) {
+        case 0: expand_group_rows<D, 0>(rc, xc, rows, et); break;
+        case 1: expand_group_rows<D, 1>(rc, xc, rows, et); break;
+        case 2: expand_group_rows<D, 2>(rc, xc, rows, et); break;
+        case 3: expand_group_rows<D, 3>(rc, xc, rows, et); break;
+        case 4: expand_group_rows<D, 4>(rc, xc, rows, et); break;
+        case 5: expand_group_rows<D, 5>(rc, xc, rows, et); break;
+        case 6: expand_group_rows<D, 6>(rc, xc, rows, et); break;
+        default: expand_group_rows<D, 7>(rc, xc, rows, et); break;
+    }
+}
+
 // kMode: 0 plain FP32 store, 1 forward glue, 2 backward glue (p.glue.mode); kKPB (modes 1-2): 16-channel
 // blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
 // mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
@@ -580,6 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap om2, const KParams p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t stage_full[kMaxStages], stage_empty[kMaxStages];
+    __shared__ uint64_t raw_full[kMaxStages];  // inline expansion: natural windows landed
     __shared__ uint64_t tmem_full, tmem_empty;
     __shared__ uint32_t tmem_base_s;
     __shared__ float bias_red[4 * 64];  // layer glue: per-quarter bias-gradient sums
@@ -591,6 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* ws_base = smem + static_cast<size_t>(pl.stages) * pl.x_stage_bytes;
     uint8_t* tx_base = ws_base + static_cast<size_t>(pl.stages) * pl.w_stage_bytes;
     uint8_t* tw_base = tx_base + static_cast<size_t>(pl.stages) * pl.tx_stage_bytes;
+    uint8_t* raw_base = tw_base + static_cast<size_t>(pl.stages) * pl.tw_stage_bytes;
     // G: tap blocks the schedule carries between tiles (1 in expanded-row mode: no carry)
     const int G = pl.xr ? 1 : pl.g, T = pl.t, KP = pl.kp;
     const int64_t J = p.tiles_per_item;
@@ -598,7 +660,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < pl.stages; ++s) {
-            mbar_init(&stage_full[s], 1);
+            mbar_init(&stage_full[s], pl.xin ? 2 : 1);  // + the expanders' arrival
+            mbar_init(&raw_full[s], 1);
             mbar_init(&stage_empty[s], 1);
         }
         mbar_init(&tmem_full, 1);
@@ -632,6 +695,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(smem_u32(&stage_empty[stage]), phase ^ 1);
                     t_wait += clock64() - tw0;
                     const uint32_t full = smem_u32(&stage_full[stage]);
+                    if (pl.xin) {
+                        // natural windows from a 16-B aligned start into the raw area (the expanders
+                        // build the E rows), the weights straight into the stage
+                        const uint32_t rf = smem_u32(&raw_full[stage]);
+                        mbar_arrive_expect_tx(rf, static_cast<uint32_t>(ccn * pl.raw_segs * kSegQ * 2));
+                        const int32_t x_al = x_start - (((x_start % 8) + 8) % 8);
+                        const uint32_t raw = smem_u32(raw_base + static_cast<size_t>(stage) * pl.raw_stage_bytes);
+                        for (int c = 0; c < ccn; ++c) {
+                            const int32_t row = static_cast<int32_t>(su.n * p.in_ch + c0 + c);
+                            for (int sg = 0; sg < pl.raw_segs; ++sg)
+                                tma_load_2d(raw + static_cast<uint32_t>((c * pl.raw_segs + sg) * kSegQ * 2), &tmap,
+                                            x_al + sg * kSegQ, row, rf);
+                        }
+                        mbar_arrive_expect_tx(full, static_cast<uint32_t>(ccn) * pl.b_chan_bytes);
+                        const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
+                        bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
+                                 static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
+                        if (++stage == pl.stages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
                     const uint32_t xbytes = pl.xr ? static_cast<uint32_t>(pl.rows_alloc * 16) : static_cast<uint32_t>(nseg * kSegQ * 2);
                     const uint32_t bytes = static_cast<uint32_t>(ccn) * (xbytes + pl.b_chan_bytes) +
                                            (pl.tail ? pl.tail_chunks * pl.cc * 16u + pl.tw_stage_bytes : 0u);
@@ -789,6 +875,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.prof[blockIdx.x * 8 + 2] = t_full;
             p.prof[blockIdx.x * 8 + 3] = t_tmem;
             p.prof[blockIdx.x * 8 + 4] = clock64() - t_begin;
+        }
+    } else if (warp == 2 || warp == 3) {
+        // ------------------------------------------------------------------ E-row expanders
+        // (inline expanded-row mode) row r of a channel = 8 elements from column x_start + d*r
+        // of its natural window: two aligned 16-B reads, a funnel shift, one 16-B write
+        if (pl.xin) {
+            const int et = threadIdx.x - 64;
+            const int d = pl.xr;
+            const uint32_t raw_chan = static_cast<uint32_t>(pl.raw_segs * kSegQ * 2);
+            Cursor cur = make_cursor(p);
+            int stage = 0;
+            uint32_t phase = 0;
+            Super su;
+            while (next_super(cur, J, G, T, &su)) {
+                const int64_t x_start = su.i0 * kTileQ + p.in_off;
+                const int off = static_cast<int>(((x_start % 8) + 8) % 8);
+                for (int ch = 0; ch < n_chunks; ++ch) {
+                    const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - ch * pl.cc));
+                    mbar_wait(smem_u32(&raw_full[stage]), phase);
+                    const uint32_t raw = smem_u32(raw_base + static_cast<size_t>(stage) * pl.raw_stage_bytes);
+                    const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
+                    for (int c = 0; c < ccn; ++c) {
+                        const uint32_t rc = raw + static_cast<uint32_t>(c) * raw_chan;
+                        const uint32_t xc = xs + static_cast<uint32_t>(c * pl.rows_alloc * 16);
+                        if (d == 1)
+                            expand_rows_d<1>(rc, xc, pl.rows_stage, et, off);
+                        else if (d == 2)
+                            expand_rows_d<2>(rc, xc, pl.rows_stage, et, off);
+                        else
+                            expand_rows_d<4>(rc, xc, pl.rows_stage, et, off);
+                    }
+                    fence_async_smem();  // generic-proxy rows -> the tensor core's async proxy
+                    asm volatile("bar.sync 2, 64;" ::: "memory");
+                    if (et == 0) mbar_arrive(smem_u32(&stage_full[stage]));
+                    if (++stage == pl.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------------ epilogue
@@ -1112,7 +1238,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     if (!make_plan(g, &pl, main_ch, extra ? extra + 1024 : 0)) return cudaErrorNotSupported;
     uint32_t stg_off = 0, pf_off = 0;
     if (extra) {
-        const uint32_t stage = pl.x_stage_bytes + pl.w_stage_bytes + pl.tx_stage_bytes + pl.tw_stage_bytes;
+        const uint32_t stage =
+            pl.x_stage_bytes + pl.w_stage_bytes + pl.tx_stage_bytes + pl.tw_stage_bytes + pl.raw_stage_bytes;
         stg_off = (static_cast<uint32_t>(pl.stages) * stage + 127u) & ~127u;
         pf_off = stg_off + stg_total;
         pl.smem_bytes = pf_off + pf_total + 1024;
@@ -1132,7 +1259,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     }
     CUtensorMap tmap;
     CUresult r;
-    if (pl.xr) {  // the row tensor E: (8 elements, rows, item x channel)
+    if (pl.xr && !pl.xin) {  // the row tensor E: (8 elements, rows, item x channel)
         const cuuint64_t dims[3] = {64, static_cast<cuuint64_t>(g.xr_rows / 8), static_cast<cuuint64_t>(g.n * g.in_ch)};
         const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(g.xr_rows) * 16};
         const cuuint32_t box[3] = {64, static_cast<cuuint32_t>(pl.box_rows / 8), 1};
