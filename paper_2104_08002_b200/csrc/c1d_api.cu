@@ -251,11 +251,17 @@ struct SplitConv {
 };
 SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const DilPlan& dp) {
     ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
-    if (dp.kind == DilPlan::kPhases) {  // expanded rows of the split channels when the kernel fits
+    if (dp.kind == DilPlan::kPhases && (g.dil == 1 || g.dil == 2 || g.dil == 4)) {
+        // expanded rows of the split channels: built in shared memory from the natural split rows
+        // (the split quadruples the channels, so a row tensor in HBM would be 4 * 8/d x the input),
+        // else the row tensor
         ConvGeom g4 = g;
         g4.in_ch *= 4;
+        ConvGeom gi = pitched(g4);  // the split rows get an 8-element pitch
+        gi.xr_inline = true;
+        if (tc_conv_supported(gi, g.in_ch)) return SplitConv{gi, g.in_ch};
         g4 = xr_geom(g4);
-        if ((g.dil == 1 || g.dil == 2 || g.dil == 4) && tc_conv_supported(g4, g.in_ch)) return SplitConv{g4, g.in_ch};
+        if (tc_conv_supported(g4, g.in_ch)) return SplitConv{g4, g.in_ch};
     }
     if (dp.kind == DilPlan::kPlanes) g = plane_geom(g, dp);
     if (dp.kind == DilPlan::kPhases) g = phase_geom(g, dp);
@@ -456,7 +462,7 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
     auto step = [&](auto&& launch) {
         if (run && e == cudaSuccess) e = launch();
     };
-    if (dp.kind != DilPlan::kPhases || sc.gs.xr_rows > 0) {
+    if (dp.kind != DilPlan::kPhases || sc.gs.xr_rows > 0 || sc.gs.xr_inline) {
         float* w4 = bump.take<float>(4 * sizeof(float) * kcs);
         float* wg4 = bump.take<float>(4 * sizeof(float) * kcs);
         if (pass == C1D_PASS_FORWARD) {  // c-blocks hi,hi,lo,lo
@@ -466,9 +472,12 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
             step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 4, 1, 0xCu, stream); });
             step([&] { return launch_prep_weights(w4, wg4, 4 * d.k, d.c, d.s, kWeightsBackwardData, false, stream); });
         }
-        const size_t n4 = static_cast<size_t>(g.n * 4 * g.in_ch * g.in_w);
+        const int64_t x4_pitch = sc.gs.xr_inline && sc.gs.in_stride ? sc.gs.in_stride : g.in_w;
+        const size_t n4 = static_cast<size_t>(g.n * 4 * g.in_ch * x4_pitch);
         uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
-        step([&] { return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream); });
+        step([&] {
+            return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream, x4_pitch);
+        });
         if (dp.kind == DilPlan::kPlanes) {
             uint16_t* p4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
             float* pout = bump.take<float>(sizeof(float) * static_cast<size_t>(sc.gs.n * sc.gs.out_ch * sc.gs.out_w));
@@ -476,6 +485,11 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
             step([&] { return launch_to_planes(x4, C1D_DTYPE_BF16, p4, g.n, 4 * g.in_ch, g.in_w, dp.m, stream); });
             step([&] { return launch_tc_conv(p4, wg4, pout, sc.gs, kws, stream, sc.main_ch); });
             step([&] { return launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream); });
+            return e;
+        }
+        if (sc.gs.xr_inline) {  // d < 8: expanded rows built in the kernel from the split rows
+            void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
+            step([&] { return launch_tc_conv(x4, wg4, out, sc.gs, kws, stream, sc.main_ch); });
             return e;
         }
         if (sc.gs.xr_rows > 0) {  // d < 8: expanded rows of the split channels

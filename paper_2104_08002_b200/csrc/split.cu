@@ -23,18 +23,18 @@ namespace c1d {
 // in: [N][C][W] fp32 -> out: [N][R*C][W] bf16 bits, channel block b of `pattern` (bit b: 0 = hi,
 // 1 = lo) for b < R.
 __global__ void split_channels_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n,
-                                      int64_t c, int64_t w, int reps, unsigned pattern) {
-    const int64_t total = n * c * w;
+                                      int64_t c, int64_t w, int reps, unsigned pattern, int64_t wp) {
+    const int64_t total = n * c * wp;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = e % w;
-        const int64_t ch = (e / w) % c;
-        const int64_t item = e / (w * c);
-        const float v = in[e];
+        const int64_t x = e % wp;
+        const int64_t ch = (e / wp) % c;
+        const int64_t item = e / (wp * c);
+        const float v = x < w ? in[(item * c + ch) * w + x] : 0.0f;  // pitch padding: zeros
         const uint16_t hi = fp32_to_bf16_bits(v);
         const uint16_t lo = fp32_to_bf16_bits(v - bf16_bits_to_fp32(hi));
         for (int r = 0; r < reps; ++r) {
             const uint16_t val = ((pattern >> r) & 1u) ? lo : hi;
-            out[((item * reps + r) * c + ch) * w + x] = val;
+            out[((item * reps + r) * c + ch) * wp + x] = val;
         }
     }
 }
@@ -77,8 +77,9 @@ static unsigned blocks_for(int64_t total) {
 }
 
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
-                                  unsigned pattern, cudaStream_t stream) {
-    split_channels_kernel<<<blocks_for(n * c * w), 256, 0, stream>>>(in, out, n, c, w, reps, pattern);
+                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch) {
+    const int64_t wp = w_pitch > 0 ? w_pitch : w;
+    split_channels_kernel<<<blocks_for(n * c * wp), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp);
     note_launch();
     return cudaGetLastError();
 }

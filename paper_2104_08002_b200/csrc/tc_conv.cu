@@ -123,7 +123,7 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.xr = static_cast<int>(g.dil);
     // N = KP per MMA here, so wide filter blocks pay: KP = 128 halves the A-tile re-reads per filter
     // and reads E once (one filter group) — single-buffered, 4 tiles per super-tile
-    p.kp = g.out_ch <= 16 ? 16 : (g.out_ch <= 32 ? 32 : (g.out_ch <= 64 || main_ch > 0 ? 64 : 128));
+    p.kp = g.out_ch <= 16 ? 16 : (g.out_ch <= 32 ? 32 : (g.out_ch <= 64 ? 64 : 128));
     p.kgroups = static_cast<int>(ceil_div(g.out_ch, p.kp));
     p.g = static_cast<int>(ceil_div(g.taps, kTapsPerBlock));
     p.r = static_cast<int>(kTmemCols) / p.kp;
