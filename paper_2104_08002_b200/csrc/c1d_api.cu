@@ -207,6 +207,17 @@ bool xr_inline_ok(const ConvGeom& g) {
     if (g.dil * ceil_div(g.taps, 16) < 4) return false;
     return tc_conv_supported(xr_inline_geom(g));
 }
+// d = 8 on the carry-free direct mode (the expanded-row mode over the natural rows) for more than
+// 64 filters: one 128-wide filter block instead of two carry-mode filter groups that each stream the
+// input (measured, N = 16, Q = 20000: C = K = 128, S = 51 fwd 558 -> 499 us, S = 9 292 -> 181 us;
+// at K <= 64 the carry mode's N = 192-256 MMAs win: config 3 638 vs 938 us)
+bool native_direct(const ConvGeom& g, int64_t main_ch = 0) {
+    if (getenv("C1D_D8_CARRY") != nullptr) return false;  // dev A/B switch
+    if (g.out_ch <= 64 && main_ch == 0) return false;
+    ConvGeom gi = g;
+    gi.xr_inline = true;
+    return tc_conv_supported(gi, main_ch);
+}
 // backward-weight on expanded rows (d = 1, 2, 4): one tc_wgrad launch over E (rows of x at every
 // d-column start) instead of one launch per phase
 int64_t xr_wgrad_rows(const c1d_desc& d, int64_t q_pad) { return ceil_div(q_pad + d.d * (d.s - 1), d.d) + 16; }
@@ -263,12 +274,25 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
         g4 = xr_geom(g4);
         if (tc_conv_supported(g4, g.in_ch)) return SplitConv{g4, g.in_ch};
     }
+    if (dp.kind == DilPlan::kNative) {
+        // two TMEM regions leave the carry mode 256/KP - (G-1) tiles per super-tile (1 at KP = 64,
+        // S = 51), so the carry-free direct mode (4 tiles) runs the split
+        ConvGeom g4 = pitched(g);
+        g4.in_ch *= 4;
+        if (native_direct(g4, g.in_ch)) {
+            g4.xr_inline = true;
+            return SplitConv{g4, g.in_ch};
+        }
+    }
     if (dp.kind == DilPlan::kPlanes) g = plane_geom(g, dp);
     if (dp.kind == DilPlan::kPhases) g = phase_geom(g, dp);
     SplitConv r{g, g.in_ch};
     r.gs.in_ch *= 4;
     return r;
 }
+
+// FP32 split: main-term products per TMEM accumulation chain (error model in resolve())
+constexpr int64_t kMaxSplitTerms = 3300;
 
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
@@ -303,7 +327,8 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
                 tc_wgrad_v3_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q))
                 return true;  // expanded rows
             if (d.w_in % 8 || q % 8) return false;
-            if (dp.kind == DilPlan::kNative) return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q);
+            if (dp.kind == DilPlan::kNative)
+                return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q) || tc_wgrad_supported(d.n, d.c, d.k, d.s, 8, q);
             if (d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, d.c)) return false;
             for (int64_t b = 0; b < dp.p; ++b)
                 if (!tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, ceil_div(d.s - b, dp.m), 8, q)) return false;
@@ -315,9 +340,9 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         // terms accumulate in their own TMEM region, so only the C_in*S main products form the
         // long chain. Keep C_in*S <= kMaxSplitTerms (<= ~6e-6 + 7.6e-6 worst case, 1e-5 bound);
         // longer reductions run on FFMA.
-        constexpr int64_t kMaxSplitTerms = 3300;
         const int64_t cin = pass == C1D_PASS_FORWARD ? d.c : d.k;
-        if (cin * d.s > kMaxSplitTerms) return false;
+        if (cin * d.s > kMaxSplitTerms && !(dp.kind == DilPlan::kNative && cin * d.s <= 2 * kMaxSplitTerms))
+            return false;  // longer chains: two channel halves (native d = 8), else FFMA
         // Small FP32 problems stay on FFMA (exact FP32 products, smooth in the inputs: the reference's
         // finite-difference acceptance checks at eps 1e-3 resolve the split's 1e-6-level error).
         if (dp.kind == DilPlan::kPhases && d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, cin)) return false;
@@ -451,7 +476,7 @@ c1d_status check_device() {
 // FP32 split path of a conv-shaped pass under its dilation plan (see split_conv_geom). With a dry
 // bump only the workspace is sized.
 cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const void* in, const float* w_kcs,
-                           float* out, Bump& bump, cudaStream_t stream) {
+                           float* out, Bump& bump, cudaStream_t stream, int64_t in_item_stride = 0) {
     const DilPlan dp = dil_plan(d, q);
     const ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
     const SplitConv sc = split_conv_geom(d, pass, q, dp);
@@ -476,7 +501,8 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
         const size_t n4 = static_cast<size_t>(g.n * 4 * g.in_ch * x4_pitch);
         uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
         step([&] {
-            return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream, x4_pitch);
+            return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream, x4_pitch,
+                                         in_item_stride);
         });
         if (dp.kind == DilPlan::kPlanes) {
             uint16_t* p4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
@@ -527,6 +553,42 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
     return e;
 }
 
+// FP32 split conv whose main chain C_in*S exceeds kMaxSplitTerms (native d = 8): the reduction
+// channels in two halves (separate launches, hence separate TMEM chains); the second half is added
+// to the first in FP32.
+cudaError_t split_conv_any(const c1d_desc& d, c1d_pass pass, int64_t q, const void* in, const float* w_kcs,
+                           float* out, Bump& bump, cudaStream_t stream) {
+    const bool fwd = pass == C1D_PASS_FORWARD;
+    const int64_t cin = fwd ? d.c : d.k;
+    if (cin * d.s <= kMaxSplitTerms) return split_conv_run(d, pass, q, in, w_kcs, out, bump, stream);
+    const bool run = !bump.dry;
+    const int64_t h0 = (cin + 1) / 2;
+    const int64_t w_in = d.w_in;
+    const int64_t in_w = fwd ? w_in : q;  // width of the reduction-channel rows
+    const int64_t out_elems = fwd ? d.n * d.k * q : d.n * d.c * w_in;
+    float* tmp = bump.take<float>(sizeof(float) * static_cast<size_t>(out_elems));
+    float* wsub = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+    cudaError_t e = cudaSuccess;
+    for (int h = 0; h < 2 && e == cudaSuccess; ++h) {
+        const int64_t c0 = h ? h0 : 0, nh = h ? cin - h0 : h0;
+        c1d_desc dh = d;
+        if (fwd)
+            dh.c = nh;
+        else
+            dh.k = nh;
+        const float* wh = w_kcs + (fwd ? 0 : c0 * d.c * d.s);
+        if (fwd && run)  // channels [c0, c0 + nh) of every filter: a compact [K][nh][S] copy
+            e = cudaMemcpy2DAsync(wsub, sizeof(float) * nh * d.s, w_kcs + c0 * d.s, sizeof(float) * d.c * d.s,
+                                  sizeof(float) * nh * d.s, d.k, cudaMemcpyDeviceToDevice, stream);
+        if (fwd) wh = wsub;
+        const float* inh = run ? static_cast<const float*>(in) + c0 * in_w : nullptr;
+        if (e == cudaSuccess)
+            e = split_conv_run(dh, pass, q, inh, wh, h ? tmp : out, bump, stream, cin * in_w);
+        if (e == cudaSuccess && h == 1 && run) e = launch_add_into(out, tmp, out_elems, stream);
+    }
+    return e;
+}
+
 // FP32 split path of backward-weight: x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the four
 // (k-block, c-block) tiles of the 2K x 2C gradient are summed; under the dilation plans the split
 // operands are relaid out exactly as the BF16 ones.
@@ -541,6 +603,26 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
     const size_t nx = static_cast<size_t>(2 * d.n * d.c * d.w_in), ng = static_cast<size_t>(2 * d.n * d.k * q);
     uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * nx);
     uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * ng);
+    if (dp.kind == DilPlan::kNative && !tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q)) {
+        // 2C or 2K too wide for one launch: three block launches (hi x hi, hi x lo, lo x hi) over
+        // separate hi / lo tensors, summed in a fixed order
+        const size_t kcs = static_cast<size_t>(d.k * d.c * d.s);
+        uint16_t* xl = bump.take<uint16_t>(sizeof(uint16_t) * nx / 2);
+        uint16_t* gl = bump.take<uint16_t>(sizeof(uint16_t) * ng / 2);
+        float* part = bump.take<float>(3 * sizeof(float) * kcs);
+        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, q));
+        uint16_t* xh = x2;  // the first halves of the x2 / g2 buffers hold the hi tensors here
+        uint16_t* gh = g2;
+        step([&] { return launch_split_channels(static_cast<const float*>(x), xh, d.n, d.c, d.w_in, 1, 0x0u, stream); });
+        step([&] { return launch_split_channels(static_cast<const float*>(x), xl, d.n, d.c, d.w_in, 1, 0x1u, stream); });
+        step([&] { return launch_split_channels(static_cast<const float*>(dy), gh, d.n, d.k, q, 1, 0x0u, stream); });
+        step([&] { return launch_split_channels(static_cast<const float*>(dy), gl, d.n, d.k, q, 1, 0x1u, stream); });
+        step([&] { return launch_tc_wgrad(xh, gh, part, kws, d.n, d.c, d.k, d.s, 8, q, stream); });
+        step([&] { return launch_tc_wgrad(xh, gl, part + kcs, kws, d.n, d.c, d.k, d.s, 8, q, stream); });
+        step([&] { return launch_tc_wgrad(xl, gh, part + 2 * kcs, kws, d.n, d.c, d.k, d.s, 8, q, stream); });
+        step([&] { return launch_sum3(part, part + kcs, part + 2 * kcs, dw, static_cast<int64_t>(kcs), stream); });
+        return e;
+    }
     step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, 0x2u, stream); });
     step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, 0x2u, stream); });
     if (dp.kind == DilPlan::kPhases && (d.d == 1 || d.d == 2 || d.d == 4) &&
@@ -594,7 +676,7 @@ size_t split_workspace(const c1d_desc& d, c1d_pass pass, int64_t q) {
     if (pass == C1D_PASS_BACKWARD_WEIGHT)
         split_wgrad_run(d, q, nullptr, nullptr, nullptr, dry, nullptr);
     else
-        split_conv_run(d, pass, q, nullptr, nullptr, nullptr, dry, nullptr);
+        split_conv_any(d, pass, q, nullptr, nullptr, nullptr, dry, nullptr);
     return dry.used;
 }
 
@@ -620,7 +702,7 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     if (st != C1D_OK) return st;
     if (algo == C1D_ALGO_BF16X3) {
         // FP32 via split BF16 operands (split.cu), composed with the dilation plans
-        const cudaError_t e = split_conv_run(d, pass, q, in, w_kcs, out, bump, stream);
+        const cudaError_t e = split_conv_any(d, pass, q, in, w_kcs, out, bump, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (bf16x3)");
         return C1D_OK;
     }
@@ -713,8 +795,10 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
         in_b = tmp;
     }
-    void* kws = bump.take<char>(tc_conv_workspace_bytes(gq));
-    e = launch_tc_conv(in_b, w_kcs, out, gq, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
+    ConvGeom gk = gq;
+    if (!glue && native_direct(gq)) gk.xr_inline = true;  // carry-free direct accumulation (see native_direct)
+    void* kws = bump.take<char>(tc_conv_workspace_bytes(gk));
+    e = launch_tc_conv(in_b, w_kcs, out, gk, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
     if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
     return C1D_OK;
 }
@@ -728,6 +812,8 @@ bool glue_fusable(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo) {
     if (algo != C1D_ALGO_TCGEN05) return false;
     const DilPlan dp = dil_plan(d, q);
     // the glue epilogue handles filter blocks of up to 64 (the expanded-row mode takes KP = 128 above)
+    // native d = 8 keeps the carry mode under glue (any filter count, groups of <= 64); the expanded-row
+    // mode's glue needs filter blocks of <= 64 (it takes 128-wide blocks above)
     return dp.kind == DilPlan::kNative || (dp.kind == DilPlan::kPhases && (pass == C1D_PASS_FORWARD ? d.k : d.c) <= 64);
 }
 struct GlueSizes {

@@ -151,11 +151,16 @@ cudaError_t launch_expand_rows(const void* in, int in_dtype, uint16_t* out, int6
 int64_t tc_conv_xr_rows(const ConvGeom& g);
 
 // FP32-on-tensor-core operand splitting (split.cu)
-// w_pitch: output row pitch (zero-filled past w), default w
+// w_pitch: output row pitch (zero-filled past w), default w; in_item_stride: input elements per
+// item (a channel subset of a wider tensor), default c * w
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
-                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch = 0);
+                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch = 0,
+                                  int64_t in_item_stride = 0);
+cudaError_t launch_add_into(float* out, const float* add, int64_t count, cudaStream_t stream);
 cudaError_t launch_split_weights(const float* w, float* out, int64_t K, int64_t C, int64_t S, int kr, int cr,
                                  unsigned sel, cudaStream_t stream);
+cudaError_t launch_sum3(const float* hh, const float* hl, const float* lh, float* dw, int64_t count,
+                        cudaStream_t stream);
 cudaError_t launch_sum_split_blocks(const float* dw4, float* dw, int64_t K, int64_t C, int64_t S,
                                     cudaStream_t stream);
 

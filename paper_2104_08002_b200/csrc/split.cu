@@ -23,13 +23,14 @@ namespace c1d {
 // in: [N][C][W] fp32 -> out: [N][R*C][W] bf16 bits, channel block b of `pattern` (bit b: 0 = hi,
 // 1 = lo) for b < R.
 __global__ void split_channels_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n,
-                                      int64_t c, int64_t w, int reps, unsigned pattern, int64_t wp) {
+                                      int64_t c, int64_t w, int reps, unsigned pattern, int64_t wp,
+                                      int64_t in_item) {
     const int64_t total = n * c * wp;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t x = e % wp;
         const int64_t ch = (e / wp) % c;
         const int64_t item = e / (wp * c);
-        const float v = x < w ? in[(item * c + ch) * w + x] : 0.0f;  // pitch padding: zeros
+        const float v = x < w ? in[item * in_item + ch * w + x] : 0.0f;  // pitch padding: zeros
         const uint16_t hi = fp32_to_bf16_bits(v);
         const uint16_t lo = fp32_to_bf16_bits(v - bf16_bits_to_fp32(hi));
         for (int r = 0; r < reps; ++r) {
@@ -72,14 +73,23 @@ __global__ void sum_split_blocks_kernel(const float* __restrict__ dw4, float* __
     }
 }
 
+// dw = hh + (hl + lh): the block-launch form of the split backward-weight (same order as
+// sum_split_blocks without the lo x lo term)
+__global__ void sum3_kernel(const float* __restrict__ hh, const float* __restrict__ hl, const float* __restrict__ lh,
+                            float* __restrict__ dw, int64_t count) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        dw[e] = hh[e] + (hl[e] + lh[e]);
+}
+
 static unsigned blocks_for(int64_t total) {
     return static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(total, 256), 16 * num_sms())));
 }
 
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
-                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch) {
+                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch, int64_t in_item_stride) {
     const int64_t wp = w_pitch > 0 ? w_pitch : w;
-    split_channels_kernel<<<blocks_for(n * c * wp), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp);
+    const int64_t si = in_item_stride > 0 ? in_item_stride : c * w;
+    split_channels_kernel<<<blocks_for(n * c * wp), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp, si);
     note_launch();
     return cudaGetLastError();
 }
@@ -94,6 +104,24 @@ cudaError_t launch_split_weights(const float* w, float* out, int64_t K, int64_t 
 cudaError_t launch_sum_split_blocks(const float* dw4, float* dw, int64_t K, int64_t C, int64_t S,
                                     cudaStream_t stream) {
     sum_split_blocks_kernel<<<blocks_for(K * C * S), 256, 0, stream>>>(dw4, dw, K, C, S);
+    note_launch();
+    return cudaGetLastError();
+}
+
+__global__ void add_into_kernel(float* __restrict__ out, const float* __restrict__ add, int64_t count) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x)
+        out[e] += add[e];
+}
+
+cudaError_t launch_add_into(float* out, const float* add, int64_t count, cudaStream_t stream) {
+    add_into_kernel<<<blocks_for(count), 256, 0, stream>>>(out, add, count);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sum3(const float* hh, const float* hl, const float* lh, float* dw, int64_t count,
+                        cudaStream_t stream) {
+    sum3_kernel<<<blocks_for(count), 256, 0, stream>>>(hh, hl, lh, dw, count);
     note_launch();
     return cudaGetLastError();
 }

@@ -117,7 +117,9 @@ struct KParams {
 };
 
 bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve) {
-    if (g.dil != 1 && g.dil != 2 && g.dil != 4) return false;
+    // d = 8 joins as the inline case whose rows are the natural window itself (no expansion)
+    if (g.dil != 1 && g.dil != 2 && g.dil != 4 && !(g.dil == 8 && g.xr_inline)) return false;
+    if (g.dil == 8 && g.in_off % 8) return false;
     if (g.n * g.in_ch >= (int64_t{1} << 31) || g.xr_rows >= (int64_t{1} << 31)) return false;
     Plan p{};
     p.xr = static_cast<int>(g.dil);
@@ -153,7 +155,7 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
         if (pitch % 8 || pitch < g.in_w) return false;
         // window: up to 7 leading columns of alignment + the rows' reach + one 16-B read of slack
         p.raw_segs = static_cast<int>(ceil_div(7 + (rows_stage - 1) * p.xr + 8 + 8, kSegQ));
-        p.rows_alloc = rows_stage;
+        p.rows_alloc = p.xr == 8 ? 0 : rows_stage;  // d = 8: the MMAs read the raw window
     }
     p.n_seg = 0;
     p.xw = 0;
@@ -660,7 +662,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < pl.stages; ++s) {
-            mbar_init(&stage_full[s], pl.xin ? 2 : 1);  // + the expanders' arrival
+            mbar_init(&stage_full[s], pl.xin && pl.xr != 8 ? 2 : 1);  // + the expanders' arrival
             mbar_init(&raw_full[s], 1);
             mbar_init(&stage_empty[s], 1);
         }
@@ -698,8 +700,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (pl.xin) {
                         // natural windows from a 16-B aligned start into the raw area (the expanders
                         // build the E rows), the weights straight into the stage
-                        const uint32_t rf = smem_u32(&raw_full[stage]);
-                        mbar_arrive_expect_tx(rf, static_cast<uint32_t>(ccn * pl.raw_segs * kSegQ * 2));
+                        // (d = 8: the window is the A operand itself, so it completes the stage barrier)
+                        const uint32_t rf = pl.xr == 8 ? full : smem_u32(&raw_full[stage]);
+                        mbar_arrive_expect_tx(rf, static_cast<uint32_t>(ccn * pl.raw_segs * kSegQ * 2) +
+                                                      (pl.xr == 8 ? static_cast<uint32_t>(ccn) * pl.b_chan_bytes : 0u));
                         const int32_t x_al = x_start - (((x_start % 8) + 8) % 8);
                         const uint32_t raw = smem_u32(raw_base + static_cast<size_t>(stage) * pl.raw_stage_bytes);
                         for (int c = 0; c < ccn; ++c) {
@@ -708,7 +712,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 tma_load_2d(raw + static_cast<uint32_t>((c * pl.raw_segs + sg) * kSegQ * 2), &tmap,
                                             x_al + sg * kSegQ, row, rf);
                         }
-                        mbar_arrive_expect_tx(full, static_cast<uint32_t>(ccn) * pl.b_chan_bytes);
+                        if (pl.xr != 8) mbar_arrive_expect_tx(full, static_cast<uint32_t>(ccn) * pl.b_chan_bytes);
                         const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                         bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
                                  static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
@@ -808,7 +812,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (elect_one()) {
                         const uint32_t tile_bytes = static_cast<uint32_t>((kTileQ / pl.xr) * 16);
                         const uint32_t idesc_x = make_idesc(128, static_cast<uint32_t>(KP), kFmtBF16, 1, 0);
-                        uint64_t achan = make_smem_desc(xs, 128, static_cast<uint32_t>(128 / pl.xr), kLayoutNone);
+                        // d = 8 (inline): A is the raw window (its start is 16-B aligned, so no shift)
+                        const uint32_t a_base =
+                            pl.xr == 8 ? smem_u32(raw_base + static_cast<size_t>(stage) * pl.raw_stage_bytes) : xs;
+                        const uint32_t a_chan = pl.xr == 8 ? static_cast<uint32_t>(pl.raw_segs * kSegQ * 2)
+                                                           : static_cast<uint32_t>(pl.rows_alloc * 16);
+                        uint64_t achan = make_smem_desc(a_base, 128, static_cast<uint32_t>(128 / pl.xr), kLayoutNone);
                         uint64_t bchan = make_smem_desc(wsm, 128, 256, kLayoutNone);
                         for (int c = 0; c < ccn; ++c) {
                             // image block b (ascending) holds tap block gb = G-1-b (A rows 16 gb)
@@ -826,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 ablk -= static_cast<uint64_t>(kTapsPerBlock);  // 16 rows x 16 B, in 16-B units
                                 bblk = desc_advance(bblk, static_cast<uint32_t>(KP * 32));
                             }
-                            achan = desc_advance(achan, static_cast<uint32_t>(pl.rows_alloc * 16));
+                            achan = desc_advance(achan, a_chan);
                             bchan = desc_advance(bchan, pl.b_chan_bytes);
                         }
                     }
@@ -880,7 +889,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ------------------------------------------------------------------ E-row expanders
         // (inline expanded-row mode) row r of a channel = 8 elements from column x_start + d*r
         // of its natural window: two aligned 16-B reads, a funnel shift, one 16-B write
-        if (pl.xin) {
+        if (pl.xin && pl.xr != 8) {
             const int et = threadIdx.x - 64;
             const int d = pl.xr;
             const uint32_t raw_chan = static_cast<uint32_t>(pl.raw_segs * kSegQ * 2);
