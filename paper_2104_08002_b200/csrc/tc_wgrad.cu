@@ -350,11 +350,13 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     p.t = 128 / p.cp;
     p.kpw = 16;
     while (p.kpw < k) p.kpw *= 2;
-    p.p = d == 8 ? std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t))) : 1;
+    // dY copies (P > 1) shift by Bq = 8T columns, so their boxes are 8T columns wide; at T = 1 that is a
+    // 16-B box, which TMA moves at ~16 B/clk (too slow to feed the MMAs: C = 128 ran 63% data-starved),
+    // so T = 1 and the expanded rows run without copies and with wide dY boxes
+    p.p = (d == 8 && p.t > 1) ? std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t))) : 1;
     p.n = p.p * p.kpw;
-    p.bq = 8 * p.t;
+    p.bq = 8 * p.t;  // with P = 1 re-chosen per stage size below (64 / 32 / 16 columns)
     if (p.bq > 64) return false;
-    p.swz = p.bq == 64 ? kLayoutSw128 : (p.bq == 32 ? kLayoutSw64 : (p.bq == 16 ? kLayoutSw32 : kLayoutNone));
     p.taps_per_group = p.t * p.p;
     p.groups_total = static_cast<int>(ceil_div(s, p.taps_per_group));
     p.gpc = std::max(1, static_cast<int>(kTmemCols) / p.n);
@@ -399,10 +401,13 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         const int v = e ? atoi(e) : kW2MaxStages;
         return v >= 3 && v <= kW2MaxStages ? v : kW2MaxStages;
     }();
-    const int ks_unit = std::max(1, p.bq / 16);  // K-steps per dY box
     bool ok = false;
     for (int ks = kW2Ks; ks >= 1 && !ok; --ks) {
+        if (p.p == 1) p.bq = (16 * ks) % 64 == 0 ? 64 : ((16 * ks) % 32 == 0 ? 32 : 16);
+        const int ks_unit = std::max(1, p.bq / 16);  // K-steps per dY box
         if (ks % ks_unit || (2 * ks * p.ph) % 4) continue;
+        p.swz = p.bq == 64 ? kLayoutSw128 : (p.bq == 32 ? kLayoutSw64 : (p.bq == 16 ? kLayoutSw32 : kLayoutNone));
+        p.box_bytes = static_cast<uint32_t>(p.kpw * 2 * p.bq);
         p.ks = ks;
         p.stage_q = 16 * p.ks;
         p.kch = 2 * p.ks * p.ph;
