@@ -221,6 +221,11 @@ bool native_direct(const ConvGeom& g, int64_t main_ch = 0) {
 // backward-weight on expanded rows (d = 1, 2, 4): one tc_wgrad launch over E (rows of x at every
 // d-column start) instead of one launch per phase
 int64_t xr_wgrad_rows(const c1d_desc& d, int64_t q_pad) { return ceil_div(q_pad + d.d * (d.s - 1), d.d) + 16; }
+// Loader-built rows vs the HBM row tensor for backward-weight (measured, N = 16, Q = 20000): the
+// loaders win at C = 16 (d = 1: 48 vs 82 us) and tie at d = 1 for C = 64, 128 (the ring, 8 rows per
+// 8 columns, limits both to one K-step per stage); at d = 2, 4 with C >= 64 the row tensor's
+// pipelined cp.async stream is faster (C = 128, d = 2: 2286 vs 3501 us).
+bool xin_wgrad_preferred(const c1d_desc& d) { return d.c <= 32 || d.d == 1; }
 bool xr_wgrad_ok(const c1d_desc& d, int64_t q_pad) {
     return (d.d == 1 || d.d == 2 || d.d == 4) && tc_wgrad_v3_supported(d.n, d.c, d.k, d.s, d.d, q_pad);
 }
@@ -369,6 +374,13 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     // tensor-core paths: BF16 copies of FP32 inputs + kernel workspace
     const bool conv_in_f32 = d.in_dtype == C1D_DTYPE_F32;
     const DilPlan dp = dil_plan(d, q);
+    if (pass == C1D_PASS_BACKWARD_WEIGHT && dp.kind == DilPlan::kPhases && xr_wgrad_ok(d, wgrad_pad(d, q).q_pad) &&
+        xin_wgrad_preferred(d) && tc_wgrad_xin_supported(d.n, d.c, d.k, d.s, d.d, wgrad_pad(d, q).q_pad)) {
+        const WgradPad wpd = wgrad_pad(d, q);
+        return align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad)) +
+               align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * round8(d.w_in))) +
+               align_up(tc_wgrad_xin_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+    }
     if (pass == C1D_PASS_BACKWARD_WEIGHT && dp.kind == DilPlan::kPhases && xr_wgrad_ok(d, wgrad_pad(d, q).q_pad)) {
         const WgradPad wpd = wgrad_pad(d, q);
         return align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad)) +
@@ -966,6 +978,21 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
                         : launch_round_bf16(static_cast<const float*>(dy), tg, d.n * d.k * q, stream);
             if (e != cudaSuccess) return cuda_fail(e, "dy copy");
             g16 = tg;
+        }
+        if (xin_wgrad_preferred(d) && tc_wgrad_xin_supported(d.n, d.c, d.k, d.s, d.d, wpd.q_pad)) {
+            // the loaders build the rows from natural bf16 x (8-element pitch; FP32 rounded once)
+            const int64_t xw = round8(d.w_in);
+            const uint16_t* x16 = static_cast<const uint16_t*>(x);
+            if (xw != d.w_in || d.in_dtype == C1D_DTYPE_F32) {
+                uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * xw));
+                e = launch_pad_rows(x, d.in_dtype, tx, d.n * d.c, d.w_in, xw, stream);
+                if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
+                x16 = tx;
+            }
+            void* kws = bump.take<char>(tc_wgrad_xin_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+            e = launch_tc_wgrad_xin(x16, xw, g16, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, wpd.q_pad, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (expanded rows, inline)");
+            return C1D_OK;
         }
         const int64_t rows = xr_wgrad_rows(d, wpd.q_pad);
         uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * d.c * rows));

@@ -118,6 +118,13 @@ cudaError_t launch_tc_wgrad(const uint16_t* x_bf16, const uint16_t* dy_bf16, flo
                             int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, cudaStream_t stream,
                             int64_t x_w = 0);
 bool tc_wgrad_v3_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+// d = 1, 2, 4 with the expanded rows built by the loaders from natural bf16 x rows (pitch x_w, a
+// multiple of 8 elements covering q + d*(s-1))
+bool tc_wgrad_xin_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+size_t tc_wgrad_xin_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+cudaError_t launch_tc_wgrad_xin(const uint16_t* x_bf16, int64_t x_w, const uint16_t* dy_bf16, float* dw_kcs,
+                                void* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q,
+                                cudaStream_t stream);
 
 // relayout.cu: dilations other than 8 on the dilation-8 tensor-core kernels
 // (O, I, S) -> (O, P*I, S'), S' = ceil(S/m): out[o][b*I + i][t] = w[o][i][b + m*t] (0 past S), P = min(m, S)

@@ -336,11 +336,16 @@ struct W2Plan {
     // column step of d: a tap is one chunk for every d, and 8 columns are ph = 8/d chunks (the
     // K-group stride). dY copies are off (P = 1): their Bq-column shift would need sub-16-B boxes.
     int ph;
+    // inline expansion (d = 1, 2, 4): the loaders stage natural x columns in `raw` (raw_cols per
+    // channel, 16-B cp.async pieces) and write the ring's rows themselves (no row tensor in HBM)
+    int xin, raw_cols;
+    uint32_t raw_bytes;
 };
 
-bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out) {
+bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out, bool xin = false) {
     if (q % 8 != 0 || q < 16) return false;
     if (d != 8 && d != 1 && d != 2 && d != 4) return false;
+    if (xin && d == 8) return false;
     if (c > 128 || k > 128) return false;
     if (n * c >= (int64_t{1} << 31) || n * k >= (int64_t{1} << 31)) return false;
     W2Plan p{};
@@ -416,11 +421,14 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
         p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
         p.stage_bytes = p.y_bytes;
+        p.xin = xin ? 1 : 0;
+        p.raw_cols = xin ? static_cast<int>(ceil_div(static_cast<int64_t>(d) * (p.span + p.kch) + 40, 8) * 8) : 0;
+        p.raw_bytes = xin ? ((static_cast<uint32_t>(p.cp * p.raw_cols * 2) + 1023) & ~1023u) : 0u;  // one of two
         for (int st = max_stages; st >= 3; --st) {
             p.stages = st;
             p.ring = static_cast<int>(ceil_div(2 * p.span + st * p.kch, 4) * 4);
             p.ring_bytes = ((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u;
-            if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes <= kW2SmemBudget) {
+            if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes + 2 * p.raw_bytes <= kW2SmemBudget) {
                 ok = true;
                 break;
             }
@@ -428,7 +436,7 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     }
     if (!ok) return false;
     p.x_bytes = p.ring_bytes;
-    p.smem_bytes = p.ring_bytes + static_cast<size_t>(p.stages) * p.stage_bytes + 1024;
+    p.smem_bytes = p.ring_bytes + static_cast<size_t>(p.stages) * p.stage_bytes + 2 * p.raw_bytes + 1024;
     *out = p;
     return true;
 }
@@ -475,6 +483,57 @@ __device__ __forceinline__ void w2_issue_stage(const W2Issue& w, uint32_t tmem, 
             b += w.b_k;
         }
     }
+}
+
+// Inline rows for the X ring: positions p0 .. p0+RG-1 of channel c (position p = natural columns
+// D*p .. D*p+7 past the stage's first column; raw element K0 + D*(p - p0) of the loaded words).
+template <int D, int K0>
+__device__ __forceinline__ void w2_expand_group(uint32_t rc, int p0, int npos, uint32_t ring_s, int v_pos, int ring,
+                                                int xb, uint32_t chunk_bytes, uint32_t mirror_bytes, int c) {
+    constexpr int RG = D == 4 ? 4 : 8;
+    constexpr int NW = ((K0 + D * (RG - 1) + 8 + 7) / 8) * 4;
+    const uint32_t src = rc + static_cast<uint32_t>(D * p0 * 2);
+    uint32_t w[NW];
+#pragma unroll
+    for (int i = 0; i < NW; i += 4)
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(w[i]), "=r"(w[i + 1]), "=r"(w[i + 2]), "=r"(w[i + 3])
+                     : "r"(src + static_cast<uint32_t>(i * 4)));
+#pragma unroll
+    for (int j = 0; j < RG; ++j) {
+        if (p0 + j >= npos) break;
+        const int o = K0 + D * j;
+        uint32_t v[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            v[i] = (o & 1) ? __funnelshift_r(w[(o >> 1) + i], w[(o >> 1) + i + 1], 16) : w[(o >> 1) + i];
+        int slot = v_pos + p0 + j;
+        if (slot >= ring) slot -= ring;
+        const uint32_t dst = ring_s + static_cast<uint32_t>(slot) * chunk_bytes + static_cast<uint32_t>(c) * 16u;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+                     : "memory");
+        if (slot < xb)
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst + mirror_bytes), "r"(v[0]), "r"(v[1]),
+                         "r"(v[2]), "r"(v[3])
+                         : "memory");
+    }
+}
+
+template <int D>
+__device__ __forceinline__ void w2_expand_d(int off, uint32_t rc, int p0, int npos, uint32_t ring_s, int v_pos, int ring,
+                                            int xb, uint32_t chunk_bytes, uint32_t mirror_bytes, int c) {
+#define W2X(K) w2_expand_group<D, K>(rc, p0, npos, ring_s, v_pos, ring, xb, chunk_bytes, mirror_bytes, c)
+    switch (off) {
+        case 0: W2X(0); break;
+        case 1: W2X(1); break;
+        case 2: W2X(2); break;
+        case 3: W2X(3); break;
+        case 4: W2X(4); break;
+        case 5: W2X(5); break;
+        case 6: W2X(6); break;
+        default: W2X(7); break;
+    }
+#undef W2X
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -636,7 +695,101 @@ __global__ void __launch_bounds__(kThreads, 1)
             p.prof[blockIdx.x * 8 + 4] = clock64() - tb;
         }
     }
-    if (warp == 2 || warp == 3 || warp >= 6) {
+    if ((warp == 2 || warp == 3 || warp >= 6) && pl.xin) {
+        // ---- X loaders, inline expanded rows: the natural columns of a stage's positions land in
+        // one of two `raw` buffers (16-B cp.async pieces, issued one stage ahead), then the loaders
+        // write the ring rows (position p = the 8 elements at column D*p), proxy fence, arrive
+        const int lt = (warp < 4 ? warp - 2 : warp - 4) * 32 + lane;  // 0..127
+        const int d = 8 / pl.ph;
+        const int cshift = __ffs(pl.cp) - 1;
+        const uint32_t ring_s = smem_u32(smem);
+        const uint32_t raw_s0 = ring_s + pl.ring_bytes + static_cast<uint32_t>(pl.stages) * pl.stage_bytes;
+        const uint32_t mirror_bytes = static_cast<uint32_t>(pl.ring) * pl.chunk_bytes;
+        const int pieces_per_c = pl.raw_cols / 8;
+        const int rg = d == 4 ? 4 : 8;
+        // the loaders' stage sequence: (item, first position, positions) per stage
+        struct XStage {
+            int64_t item, first;
+            int n;
+        };
+        int64_t it_cur = kb, it_st = kb, it_seg_end = kb, it_next = 0;
+        bool it_seg_first = true;
+        auto next_stage = [&](XStage* xs) -> bool {
+            if (it_st >= it_seg_end) {  // next item segment
+                it_cur = it_seg_end;
+                if (it_cur >= ke) return false;
+                const int64_t item = it_cur / p.steps_per_item;
+                it_seg_end = imin(ke, (item + 1) * p.steps_per_item);
+                it_st = it_cur;
+                it_seg_first = true;
+            }
+            const int64_t item = it_st / p.steps_per_item;
+            const int64_t q0 = (it_st - item * p.steps_per_item) * 16;
+            xs->item = item;
+            xs->first = it_seg_first ? q0 * pl.ph / 8 + tap0 : it_next;
+            xs->n = it_seg_first ? pl.span + pl.kch : pl.kch;
+            it_seg_first = false;
+            it_next = xs->first + xs->n;
+            it_st += pl.ks;
+            return true;
+        };
+        auto load_raw = [&](const XStage& xs, uint32_t raw_s) {
+            const uint16_t* xi = p.x + xs.item * p.c * p.w_in;
+            const int64_t col0 = (static_cast<int64_t>(d) * xs.first) & ~int64_t{7};
+            for (int i = lt; i < pl.cp * pieces_per_c; i += kLoaderThreads) {
+                const int c = i & (pl.cp - 1), j = i >> cshift;
+                const int64_t col = col0 + 8 * j;
+                const bool valid = c < p.c && col < p.w_in;
+                cp_async16_zfill(raw_s + static_cast<uint32_t>((c * pl.raw_cols + 8 * j) * 2),
+                                 valid ? xi + static_cast<int64_t>(c) * p.w_in + col : p.x, valid);
+            }
+            cp_async_commit();
+        };
+        it_seg_end = kb;
+        it_st = kb;
+        XStage cur_s, nxt_s;
+        bool have = next_stage(&cur_s);
+        if (have) load_raw(cur_s, raw_s0);
+        int stage = 0, rb = 0;
+        uint32_t phase = 0;
+        int v_pos = 0;
+        while (have) {
+            const bool have_next = next_stage(&nxt_s);
+            if (have_next) load_raw(nxt_s, raw_s0 + static_cast<uint32_t>(rb ^ 1) * pl.raw_bytes);
+            mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+            if (have_next)
+                cp_async_wait_group<1>();  // this stage's raw has landed (the next one may be in flight)
+            else
+                cp_async_wait_group<0>();
+            asm volatile("bar.sync 3, 128;" ::: "memory");
+            const uint32_t raw_s = raw_s0 + static_cast<uint32_t>(rb) * pl.raw_bytes;
+            const int64_t cfirst = static_cast<int64_t>(d) * cur_s.first;
+            const int off = static_cast<int>(cfirst & 7);
+            const int ngroups = (cur_s.n + rg - 1) / rg;
+            for (int i = lt; i < pl.cp * ngroups; i += kLoaderThreads) {
+                const int c = i & (pl.cp - 1), g = i >> cshift;
+                const uint32_t rc = raw_s + static_cast<uint32_t>(c * pl.raw_cols * 2);
+                if (d == 1)
+                    w2_expand_d<1>(off, rc, g * rg, cur_s.n, ring_s, v_pos, pl.ring, pl.xb, pl.chunk_bytes, mirror_bytes, c);
+                else if (d == 2)
+                    w2_expand_d<2>(off, rc, g * rg, cur_s.n, ring_s, v_pos, pl.ring, pl.xb, pl.chunk_bytes, mirror_bytes, c);
+                else
+                    w2_expand_d<4>(off, rc, g * rg, cur_s.n, ring_s, v_pos, pl.ring, pl.xb, pl.chunk_bytes, mirror_bytes, c);
+            }
+            fence_async_smem();  // generic-proxy ring rows -> the tensor core
+            mbar_arrive(smem_u32(&full[stage]));
+            asm volatile("bar.sync 3, 128;" ::: "memory");  // raw buffer rb is free again
+            v_pos += cur_s.n;
+            if (v_pos >= pl.ring) v_pos -= pl.ring;
+            if (++stage == pl.stages) {
+                stage = 0;
+                phase ^= 1;
+            }
+            rb ^= 1;
+            cur_s = nxt_s;
+            have = have_next;
+        }
+    } else if (warp == 2 || warp == 3 || warp >= 6) {
         // ---- X loaders (warps 2, 3, 6, 7: the sub-partitions of the TMA and MMA warps stay free
         // of their issue load): 16-byte cp.async pieces straight from the [n][c][w] rows into the
         // q-chunk-major ring. One warp instruction moves 8 channels x 4 chunks: 64 contiguous bytes
@@ -876,6 +1029,25 @@ size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int6
     WPlan p;
     if (!make_wplan(n, c, k, s, d, q, &p)) return 0;
     return sizeof(float) * static_cast<size_t>(p.roles) * p.splits * static_cast<size_t>(k * c * s);
+}
+
+bool tc_wgrad_xin_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    return make_w2plan(n, c, k, s, d, q, &p2, true);
+}
+
+size_t tc_wgrad_xin_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    if (!make_w2plan(n, c, k, s, d, q, &p2, true)) return 0;
+    return sizeof(float) * static_cast<size_t>(p2.grid) * static_cast<size_t>(k * c * s);
+}
+
+cudaError_t launch_tc_wgrad_xin(const uint16_t* x_bf16, int64_t x_w, const uint16_t* dy_bf16, float* dw_kcs,
+                                void* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q,
+                                cudaStream_t stream) {
+    W2Plan p2;
+    if (!make_w2plan(n, c, k, s, d, q, &p2, true)) return cudaErrorNotSupported;
+    return launch_v2(x_bf16, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream, x_w);
 }
 
 bool tc_wgrad_v3_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
