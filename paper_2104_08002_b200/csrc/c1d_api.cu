@@ -298,6 +298,7 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
 
 // FP32 split: main-term products per TMEM accumulation chain (error model in resolve())
 constexpr int64_t kMaxSplitTerms = 3300;
+bool split_wgrad_blocks(const c1d_desc& d);
 
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
@@ -326,14 +327,15 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         const DilPlan dp = dil_plan(d, q);
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {
+            if (split_wgrad_blocks(d))
+                return dp.kind != DilPlan::kPhases || d.algo == C1D_ALGO_BF16X3 || phases_pay_off(dp, d.c);
             if (dp.kind == DilPlan::kPlanes) return tc_wgrad_supported(d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m);
             if (dp.kind == DilPlan::kPhases && d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, d.c)) return false;
             if (dp.kind == DilPlan::kPhases && q % 8 == 0 && (d.d == 1 || d.d == 2 || d.d == 4) &&
                 tc_wgrad_v3_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q))
                 return true;  // expanded rows
             if (d.w_in % 8 || q % 8) return false;
-            if (dp.kind == DilPlan::kNative)
-                return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q) || tc_wgrad_supported(d.n, d.c, d.k, d.s, 8, q);
+            if (dp.kind == DilPlan::kNative) return tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q);
             if (d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, d.c)) return false;
             for (int64_t b = 0; b < dp.p; ++b)
                 if (!tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, ceil_div(d.s - b, dp.m), 8, q)) return false;
@@ -601,6 +603,20 @@ cudaError_t split_conv_any(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
     return e;
 }
 
+// FP32 split backward-weight in three BF16 block passes when [x_hi | x_lo] / [dy_hi | dy_lo] (2C, 2K
+// channels) exceed the single-launch kernels (v3: C, K <= 128) but the BF16 pass runs on (C, K)
+bool split_wgrad_blocks(const c1d_desc& d) {
+    if (d.c * 2 <= 128 && d.k * 2 <= 128) return false;
+    int64_t q = 0;
+    if (validate(&d, &q) != C1D_OK) return false;
+    c1d_desc d16 = d;
+    d16.precision = C1D_PRECISION_BF16;
+    d16.in_dtype = C1D_DTYPE_BF16;
+    d16.algo = C1D_ALGO_TCGEN05;
+    d16.flags = 0;
+    return resolve(d16, C1D_PASS_BACKWARD_WEIGHT, q) == C1D_ALGO_TCGEN05;
+}
+
 // FP32 split path of backward-weight: x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the four
 // (k-block, c-block) tiles of the 2K x 2C gradient are summed; under the dilation plans the split
 // operands are relaid out exactly as the BF16 ones.
@@ -615,23 +631,35 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
     const size_t nx = static_cast<size_t>(2 * d.n * d.c * d.w_in), ng = static_cast<size_t>(2 * d.n * d.k * q);
     uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * nx);
     uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * ng);
-    if (dp.kind == DilPlan::kNative && !tc_wgrad_supported(d.n, 2 * d.c, 2 * d.k, d.s, 8, q)) {
-        // 2C or 2K too wide for one launch: three block launches (hi x hi, hi x lo, lo x hi) over
-        // separate hi / lo tensors, summed in a fixed order
+    if (split_wgrad_blocks(d)) {
+        // 2C or 2K too wide for one launch: three BF16 block passes (hi x hi, hi x lo, lo x hi) on
+        // separate hi / lo tensors through the BF16 tensor-core path (any dilation plan), summed in a
+        // fixed order
         const size_t kcs = static_cast<size_t>(d.k * d.c * d.s);
+        c1d_desc d16 = d;
+        d16.precision = C1D_PRECISION_BF16;
+        d16.in_dtype = C1D_DTYPE_BF16;
+        d16.algo = C1D_ALGO_TCGEN05;
+        d16.flags = 0;
         uint16_t* xl = bump.take<uint16_t>(sizeof(uint16_t) * nx / 2);
         uint16_t* gl = bump.take<uint16_t>(sizeof(uint16_t) * ng / 2);
         float* part = bump.take<float>(3 * sizeof(float) * kcs);
-        void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, q));
+        const size_t inner = workspace_for(d16, C1D_PASS_BACKWARD_WEIGHT, q, C1D_ALGO_TCGEN05);
+        char* iws = bump.take<char>(inner);
         uint16_t* xh = x2;  // the first halves of the x2 / g2 buffers hold the hi tensors here
         uint16_t* gh = g2;
         step([&] { return launch_split_channels(static_cast<const float*>(x), xh, d.n, d.c, d.w_in, 1, 0x0u, stream); });
         step([&] { return launch_split_channels(static_cast<const float*>(x), xl, d.n, d.c, d.w_in, 1, 0x1u, stream); });
         step([&] { return launch_split_channels(static_cast<const float*>(dy), gh, d.n, d.k, q, 1, 0x0u, stream); });
         step([&] { return launch_split_channels(static_cast<const float*>(dy), gl, d.n, d.k, q, 1, 0x1u, stream); });
-        step([&] { return launch_tc_wgrad(xh, gh, part, kws, d.n, d.c, d.k, d.s, 8, q, stream); });
-        step([&] { return launch_tc_wgrad(xh, gl, part + kcs, kws, d.n, d.c, d.k, d.s, 8, q, stream); });
-        step([&] { return launch_tc_wgrad(xl, gh, part + 2 * kcs, kws, d.n, d.c, d.k, d.s, 8, q, stream); });
+        const uint16_t* xs[3] = {xh, xh, xl};
+        const uint16_t* gs[3] = {gh, gl, gh};
+        for (int b = 0; b < 3; ++b)
+            step([&] {
+                const c1d_status st = c1d_backward_weight(&d16, xs[b], gs[b], part + b * kcs, iws, inner,
+                                                          reinterpret_cast<c1d_stream_t>(stream));
+                return st == C1D_OK ? cudaSuccess : cudaErrorUnknown;
+            });
         step([&] { return launch_sum3(part, part + kcs, part + 2 * kcs, dw, static_cast<int64_t>(kcs), stream); });
         return e;
     }

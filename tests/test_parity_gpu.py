@@ -267,14 +267,14 @@ def test_expanded_rows_long_filters(d, c, k, s):
         assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} c={c} {name}")
 
 
-@pytest.mark.parametrize("c,k,s", [(100, 90, 51), (128, 128, 33)])
-def test_fp32_split_long_chains(c, k, s):
+@pytest.mark.parametrize("c,k,s,d", [(100, 90, 51, 8), (128, 128, 33, 8), (100, 72, 9, 1), (128, 96, 9, 16)])
+def test_fp32_split_long_chains(c, k, s, d):
     """FP32 on the tensor cores beyond one accumulation chain's bound (C_in*S > 3300): the conv passes
     run the reduction channels in two halves (separate TMEM chains, summed in FP32), and a split
     backward-weight too wide for one launch (2C or 2K > 128) runs three block launches. The
     reference's 1e-5 bound vs the naive FP32 oracle."""
-    rng = oracle.Rng(4000 + c)
-    n, d, q = 1, 8, 512
+    rng = oracle.Rng(4000 + c + d)
+    n, q = 1, 512
     w_in = q + d * (s - 1)
     x, w, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((k, c, s)), rng.fill_uniform((n, k, q))
     p = cv.ConvParams(c, k, s, d, cv.Precision.Fp32)
