@@ -348,12 +348,14 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         // long chain. Keep C_in*S <= kMaxSplitTerms (<= ~6e-6 + 7.6e-6 worst case, 1e-5 bound);
         // longer reductions run on FFMA.
         const int64_t cin = pass == C1D_PASS_FORWARD ? d.c : d.k;
-        if (cin * d.s > kMaxSplitTerms && !(dp.kind == DilPlan::kNative && cin * d.s <= 2 * kMaxSplitTerms))
-            return false;  // longer chains: two channel halves (native d = 8), else FFMA
+        if (cin * d.s > 2 * kMaxSplitTerms) return false;  // longer chains: FFMA (up to 2x: two channel halves)
         // Small FP32 problems stay on FFMA (exact FP32 products, smooth in the inputs: the reference's
         // finite-difference acceptance checks at eps 1e-3 resolve the split's 1e-6-level error).
         if (dp.kind == DilPlan::kPhases && d.algo != C1D_ALGO_BF16X3 && !phases_pay_off(dp, cin)) return false;
         const SplitConv sc = split_conv_geom(d, pass, q, dp);
+        // the halves read channel subsets through split_channels (not the phase-copy fallback)
+        if (cin * d.s > kMaxSplitTerms && dp.kind == DilPlan::kPhases && sc.gs.xr_rows == 0 && !sc.gs.xr_inline)
+            return false;
         return tc_conv_supported(sc.gs, sc.main_ch);
     }();
     if (d.algo == C1D_ALGO_AUTO) return tc_ok ? C1D_ALGO_TCGEN05 : (split_ok ? C1D_ALGO_BF16X3 : C1D_ALGO_DIRECT);

@@ -267,7 +267,8 @@ def test_expanded_rows_long_filters(d, c, k, s):
         assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} c={c} {name}")
 
 
-@pytest.mark.parametrize("c,k,s,d", [(100, 90, 51, 8), (128, 128, 33, 8), (100, 72, 9, 1), (128, 96, 9, 16)])
+@pytest.mark.parametrize("c,k,s,d", [(100, 90, 51, 8), (128, 128, 33, 8), (100, 72, 9, 1), (128, 96, 9, 16),
+                                     (96, 80, 51, 2), (80, 96, 51, 16)])
 def test_fp32_split_long_chains(c, k, s, d):
     """FP32 on the tensor cores beyond one accumulation chain's bound (C_in*S > 3300): the conv passes
     run the reduction channels in two halves (separate TMEM chains, summed in FP32), and a split
