@@ -109,7 +109,8 @@ C1D_EXPORT c1d_status c1d_output_width(const c1d_desc* desc, int64_t* q_out);
 C1D_EXPORT int64_t c1d_conv_flops(const c1d_desc* desc);
 
 /* Device workspace bytes the pass needs (0 if none). Passing workspace == NULL to a pass makes
- * the library use an internal, lazily grown per-device buffer instead. */
+ * the library use an internal, lazily grown buffer per (device, stream) instead: calls on different
+ * streams never share it; growing it synchronises that stream. */
 C1D_EXPORT c1d_status c1d_workspace_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes);
 
 /* Which kernel family the pass will run for this desc (resolves C1D_ALGO_AUTO). */

@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -42,26 +43,29 @@ c1d_status cuda_fail(cudaError_t e, const char* where) {
     return fail(C1D_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
-// Per-device internal workspace (used when the caller passes workspace == NULL).
+// Internal workspace (used when the caller passes workspace == NULL): one lazily grown buffer per
+// (device, stream), so calls on different streams never share scratch memory; calls on one stream
+// are ordered by the stream itself.
 struct DeviceWorkspace {
     void* ptr = nullptr;
     size_t bytes = 0;
 };
 std::mutex g_ws_mutex;
-std::vector<DeviceWorkspace> g_ws;
+std::map<std::pair<int, cudaStream_t>, DeviceWorkspace> g_ws;
 
-cudaError_t internal_workspace(size_t need, void** out) {
+cudaError_t internal_workspace(size_t need, cudaStream_t stream, void** out) {
     *out = nullptr;
     if (need == 0) return cudaSuccess;
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return e;
     std::lock_guard<std::mutex> lock(g_ws_mutex);
-    if (static_cast<int>(g_ws.size()) <= dev) g_ws.resize(dev + 1);
-    DeviceWorkspace& w = g_ws[dev];
+    DeviceWorkspace& w = g_ws[{dev, stream}];
     if (w.bytes < need) {
         if (w.ptr) {
-            e = cudaDeviceSynchronize();  // in-flight work may still read the old buffer
+            // in-flight work of this stream may still read the old buffer (the legacy default stream
+            // synchronises with the others, so a device-wide sync covers it)
+            e = stream ? cudaStreamSynchronize(stream) : cudaDeviceSynchronize();
             if (e != cudaSuccess) return e;
             cudaFree(w.ptr);
             w.ptr = nullptr;
@@ -464,7 +468,7 @@ struct Bump {
     }
 };
 
-c1d_status acquire_workspace(void* user, size_t user_bytes, size_t need, Bump* out) {
+c1d_status acquire_workspace(void* user, size_t user_bytes, size_t need, Bump* out, cudaStream_t stream) {
     if (user) {
         if (user_bytes < need)
             return fail(C1D_ERR_WORKSPACE, "workspace of " + std::to_string(user_bytes) + " bytes, need " +
@@ -473,7 +477,7 @@ c1d_status acquire_workspace(void* user, size_t user_bytes, size_t need, Bump* o
         return C1D_OK;
     }
     void* p = nullptr;
-    cudaError_t e = internal_workspace(need, &p);
+    cudaError_t e = internal_workspace(need, stream, &p);
     if (e != cudaSuccess) return cuda_fail(e, "internal workspace");
     *out = Bump{static_cast<char*>(p), need};
     return C1D_OK;
@@ -740,7 +744,7 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     const ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
     Bump bump{};
-    st = acquire_workspace(ws, ws_bytes, workspace_for(d, pass, q, algo), &bump);
+    st = acquire_workspace(ws, ws_bytes, workspace_for(d, pass, q, algo), &bump, stream);
     if (st != C1D_OK) return st;
     if (algo == C1D_ALGO_BF16X3) {
         // FP32 via split BF16 operands (split.cu), composed with the dilation plans
@@ -968,7 +972,8 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     const c1d_algo algo = resolve(d, C1D_PASS_BACKWARD_WEIGHT, q);
     if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     Bump bump{};
-    st = acquire_workspace(workspace, workspace_bytes, workspace_for(d, C1D_PASS_BACKWARD_WEIGHT, q, algo), &bump);
+    st = acquire_workspace(workspace, workspace_bytes, workspace_for(d, C1D_PASS_BACKWARD_WEIGHT, q, algo), &bump,
+                           stream);
     if (st != C1D_OK) return st;
     const bool bf16 = is_bf16(d);
     cudaError_t e;
@@ -1113,7 +1118,9 @@ c1d_status c1d_layer_backward_prologue(const float* gin, int64_t gin_w, int64_t 
     if (c1d_status st = check_device(); st != C1D_OK) return st;
     Bump ws{};
     const size_t need = bias_grad ? c1d_layer_backward_workspace(n, k, q) : 0;
-    if (c1d_status st = acquire_workspace(workspace, workspace_bytes, need, &ws); st != C1D_OK) return st;
+    if (c1d_status st = acquire_workspace(workspace, workspace_bytes, need, &ws, reinterpret_cast<cudaStream_t>(stream));
+        st != C1D_OK)
+        return st;
     float* part =
         bias_grad ? ws.take<float>(static_cast<size_t>(n * k * layer_bias_blocks(q)) * sizeof(float)) : nullptr;
     cudaError_t e = launch_layer_bwd_prologue(gin, gin_w, gin_off, gadd, pre, pre_bias, nullptr, n, k, q, relu, gsum, grad_pre,
@@ -1151,7 +1158,7 @@ c1d_status c1d_forward_glued(const c1d_desc* desc, const void* x, const float* w
     if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     const GlueSizes gs = glue_sizes(d, C1D_PASS_FORWARD, q, algo, q);
     Bump bump{};
-    st = acquire_workspace(workspace, workspace_bytes, gs.total(), &bump);
+    st = acquire_workspace(workspace, workspace_bytes, gs.total(), &bump, stream);
     if (st != C1D_OK) return st;
     char* conv_ws = bump.take<char>(gs.conv);
     if (gs.fused) {
@@ -1200,7 +1207,7 @@ c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const f
     if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     const GlueSizes gs = glue_sizes(d, C1D_PASS_BACKWARD_DATA, q, algo, glue->q);
     Bump bump{};
-    st = acquire_workspace(workspace, workspace_bytes, gs.total(), &bump);
+    st = acquire_workspace(workspace, workspace_bytes, gs.total(), &bump, stream);
     if (st != C1D_OK) return st;
     char* conv_ws = bump.take<char>(gs.conv);
     float* part = bump.take<float>(gs.part);
