@@ -128,3 +128,30 @@ def test_fused_glue_matches_torch():
     gpb2 = torch.empty_like(gpb)
     layer_backward_prologue(gin, pad, pre, n, k, q, relu=True, gadd=gadd, grad_pre_bf16=gpb2, pre_bias=bias)
     assert torch.equal(gpb2, gpb)
+
+
+def test_network_step_under_cuda_graph():
+    """The whole training step (C-ABI passes + torch losses) captured in one CUDA graph replays to
+    the eager step's results bit for bit (bench.py --workload network replays it)."""
+    net = ResidualNet(blocks=2, convs_per_block=3, hidden=15, taps=51, dilation=8, seed=5)
+    n, width = 2, 2048
+    pad = net.pad()
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.poisson(torch.full((n, 1, width + 2 * pad), 2.0, device="cuda"), generator=g)
+    target = torch.poisson(torch.full((n, 1, width), 2.0, device="cuda"), generator=g)
+    labels = (torch.rand((n, 1, width), device="cuda", generator=g) < 0.1).float()
+    loss_eager = train_step(net, x, target, labels).item()
+    grads_eager = net.grad_bucket.clone()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        train_step(net, x, target, labels)  # warm this stream's internal workspace
+    s.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        loss_g = train_step(net, x, target, labels)
+    net.grad_bucket.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert loss_g.item() == loss_eager
+    assert torch.equal(net.grad_bucket, grads_eager)
