@@ -48,7 +48,7 @@ constexpr int kTileQ = 128;      // output columns per tile (MMA M)
 constexpr int kSegQ = 256;       // TMA box width in elements
 constexpr int kTapsPerBlock = 16;
 constexpr int kMaxStages = 6;
-constexpr int kThreads = 256;
+
 constexpr int kPfRing = 4;  // layer glue: input blocks in flight per epilogue warp
 constexpr uint32_t kTmemCols = 512;
 
@@ -635,8 +635,8 @@ __device__ __forceinline__ void expand_rows_d(uint32_t rc, uint32_t xc, int rows
 // blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
 // mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
 // and TMA warps, and an all-modes kernel (~30k instructions) ran the epilogue 6x slower.
-template <int kMode, int kKPB>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int kMode, int kKPB, int kEG = 1>
+__global__ void __launch_bounds__(128 + 128 * kEG, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
                    const __grid_constant__ CUtensorMap om0, const __grid_constant__ CUtensorMap om1,
                    const __grid_constant__ CUtensorMap om2, const KParams p) {
@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint64_t raw_full[kMaxStages];  // inline expansion: natural windows landed
     __shared__ uint64_t tmem_full, tmem_empty;
     __shared__ uint32_t tmem_base_s;
-    __shared__ float bias_red[4 * 64];  // layer glue: per-quarter bias-gradient sums
+    __shared__ float bias_red[8 * 64];  // layer glue: per-epilogue-warp bias-gradient sums
 
     const Plan& pl = p.pl;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -927,16 +927,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------------ epilogue
-        const int quarter = warp - 4;  // TMEM lanes 32*quarter .. +31
+        // kEG groups of four warps (the glue variants with narrow filter blocks run two: the glue
+        // is issue-bound); group g stores the CTA's output tiles t with (t - first) % kEG == g, and
+        // group 0 alone carries / zeroes TMEM and signals the MMA warp
+        const int ew = warp - 4;         // epilogue warp 0 .. 4*kEG-1
+        const int egrp = ew >> 2;        // epilogue group
+        const int quarter = ew & 3;      // TMEM lanes 32*quarter .. +31
         const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
         uint32_t z[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) z[j] = 0;
-        for (uint32_t col = 0; col < kTmemCols; col += 16) tmem_st16(lane_base + col, z);
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+        if (egrp == 0) {
+            for (uint32_t col = 0; col < kTmemCols; col += 16) tmem_st16(lane_base + col, z);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+        }
         Cursor cur = make_cursor(p);
         uint32_t tphase = 0;
         Super su;
@@ -954,11 +961,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // in order (the super-tile walk emits every output tile once, in increasing order)
         constexpr int kB = kKPB > 0 ? kKPB : 1;
         const int64_t cta_b = p.total_tiles * blockIdx.x / gridDim.x;
-        const int64_t nblk = (p.total_tiles * (blockIdx.x + 1) / gridDim.x - cta_b) * kB;
+        const int64_t cta_tiles = p.total_tiles * (blockIdx.x + 1) / gridDim.x - cta_b;
+        const int64_t nblk = (cta_tiles > egrp ? (cta_tiles - egrp + kEG - 1) / kEG : 0) * kB;  // this group's blocks
         const bool pf_on = kMode != 0 && (p.pf_rows | p.pf_mask) != 0;
-        const uint32_t pf_base = smem_u32(smem) + p.pf_off + static_cast<uint32_t>(quarter * kPfRing) * p.pf_slot_bytes;
+        const uint32_t pf_base = smem_u32(smem) + p.pf_off + static_cast<uint32_t>(ew * kPfRing) * p.pf_slot_bytes;
         int64_t blk = 0, pf_next = 0;
-        int64_t pf_n = cta_b / p.tiles_per_item, pf_o = cta_b % p.tiles_per_item;  // tile of block pf_next
+        int64_t pf_n = (cta_b + egrp) / p.tiles_per_item, pf_o = (cta_b + egrp) % p.tiles_per_item;  // block pf_next
         int pf_kbi = 0;
         auto pf_issue = [&]() {
             if (pf_next < nblk) {
@@ -966,9 +974,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                               quarter, lane);
                 if (++pf_kbi == kB) {
                     pf_kbi = 0;
-                    if (++pf_o == p.tiles_per_item) {
-                        pf_o = 0;
-                        ++pf_n;
+                    for (int e = 0; e < kEG; ++e) {
+                        if (++pf_o == p.tiles_per_item) {
+                            pf_o = 0;
+                            ++pf_n;
+                        }
                     }
                 }
             }
@@ -989,7 +999,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             return slot;
         };
         uint32_t sbuf = 0;  // layer glue: this warp's staging buffer (0/1) and its shared-memory base
-        const uint32_t wbase = smem_u32(smem) + p.stg_off + static_cast<uint32_t>(quarter) * 2u * p.stg_bytes;
+        const uint32_t wbase = smem_u32(smem) + p.stg_off + static_cast<uint32_t>(ew) * 2u * p.stg_bytes;
         constexpr int kBS = kMode == 2 ? kKPB : 1;
         float bsum[kBS][16];  // layer glue (mode 2): this lane's bias-gradient sums per channel
 #pragma unroll
@@ -998,6 +1008,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int b = 0; b < 16; ++b) bsum[a][b] = 0.0f;
         uint32_t region = 0;  // mirrors the MMA warp's double-buffer region
         const uint32_t used_cols = static_cast<uint32_t>((T + G - 1) * KP);
+        // output tile o of item n belongs to this epilogue group?
+        auto mine = [&](int64_t n, int64_t o) -> bool {
+            return kEG == 1 || (((n * J + o - cta_b) & (kEG - 1)) == egrp);
+        };
         // carry the G-1 partial slots (tcur..tcur+G-2) of `src` into slots 0..G-2 of `dst` (or zero
         // them at a segment end) and zero dst's remaining used slots: dst is then ready
         auto prepare = [&](uint32_t src, uint32_t dst, const Super& s2) {
@@ -1027,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tphase ^= 1;
             tc_fence_after();
             const long long e0 = clock64();
-            if (pl.dbuf) prepare(region, region ^ 256u, su);  // next super-tile may start now
+            if (pl.dbuf && egrp == 0) prepare(region, region ^ 256u, su);  // next super-tile may start now
             const long long e1 = clock64();
             // store the completed outputs (slots 0..tcur-1)
             const int64_t out_w = p.out_w;
@@ -1035,7 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             if constexpr (kMode == 1) {  // fused forward glue instead of the plain store
                 for (int j = 0; j < su.tcur; ++j) {
                     const int64_t o = su.i0 - (G - 1) + j;
-                    if (o < su.j0 || o > su.j1) continue;
+                    if (o < su.j0 || o > su.j1 || !mine(su.n, o)) continue;
                     const int64_t q = o * kTileQ + quarter * 32 + lane;
 #pragma unroll
                     for (int kbi = 0; kbi < kKPB; ++kbi) {
@@ -1057,7 +1071,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else if constexpr (kMode == 2) {  // fused backward glue
                 for (int j = 0; j < su.tcur; ++j) {
                     const int64_t o = su.i0 - (G - 1) + j;
-                    if (o < su.j0 || o > su.j1) continue;
+                    if (o < su.j0 || o > su.j1 || !mine(su.n, o)) continue;
                     const int64_t q = o * kTileQ + quarter * 32 + lane;
 #pragma unroll
                     for (int kbi = 0; kbi < kKPB; ++kbi) {
@@ -1079,7 +1093,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             } else
             for (int j = 0; j < su.tcur; ++j) {
                 const int64_t o = su.i0 - (G - 1) + j;
-                if (o < su.j0 || o > su.j1) continue;  // phantom (warm-up / beyond the segment)
+                if (o < su.j0 || o > su.j1 || !mine(su.n, o)) continue;  // phantom (warm-up / beyond the segment)
                 const int64_t q = o * kTileQ + quarter * 32 + lane;
                 for (int kb = 0; kb < KP; kb += 16) {
                     uint32_t v[16];
@@ -1108,8 +1122,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const long long e2 = clock64();
             e_store += e2 - e1;
+            // both groups are done with this region before group 0 overwrites it (next prepare)
+            if (kEG > 1) asm volatile("bar.sync 4, %0;" ::"n"(128 * kEG) : "memory");
             if (!pl.dbuf) {
-                prepare(0, 0, su);  // in place: carry down, zero the rest, release
+                if (egrp == 0) prepare(0, 0, su);  // in place: carry down, zero the rest, release
                 e_carry += clock64() - e2;
             } else {
                 e_carry += e1 - e0;
@@ -1126,13 +1142,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float t = bsum[kbi][jj];
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
-                    if (lane == 0) bias_red[quarter * 64 + kbi * 16 + jj] = t;
+                    if (lane == 0) bias_red[ew * 64 + kbi * 16 + jj] = t;
                 }
             }
-            asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps
+            asm volatile("bar.sync 1, %0;" ::"n"(128 * kEG) : "memory");  // all epilogue warps
             const int c = threadIdx.x - 128;
             if (c < KP && p.k_begin + c < p.out_ch) {
-                const float t = ((bias_red[c] + bias_red[64 + c]) + bias_red[128 + c]) + bias_red[192 + c];
+                float t = 0.0f;
+                for (int w = 0; w < 4 * kEG; ++w) t += bias_red[w * 64 + c];  // fixed order
                 p.glue.part[(p.k_begin + c) * p.glue.part_stride + blockIdx.x] = t;
             }
         }
@@ -1235,16 +1252,26 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     GlueMaps gm;
     static const bool no_glue_tma = getenv("C1D_NO_GLUE_TMA") != nullptr;  // dev A/B switch
     if (glue && glue->mode != 0 && !no_glue_tma && !glue_maps(g, *glue, encode, &gm)) gm = GlueMaps{};
-    const uint32_t stg_total = 8u * gm.stg_bytes;  // 4 epilogue warps x 2 buffers
     const int mode = glue ? glue->mode : 0;
+    // glue epilogue groups: two for narrow filter blocks (<= 32 filters per launch, the network's
+    // layers), whose glue is issue-bound; one otherwise (register budget at 384 threads)
+    static const bool one_group = getenv("C1D_GLUE_EG1") != nullptr;  // dev A/B switch
+    int eg = (mode != 0 && g.out_ch <= 32 && !one_group) ? 2 : 1;
     if (mode != 0 && pl_probe_kp(g, main_ch) > 64) return cudaErrorNotSupported;  // glue: KP <= 64
     const uint32_t pf_rows = (mode == 1 && glue->skip) || (mode == 2 && glue->gadd);
     const uint32_t pf_mask = mode == 2 && glue->mask_in;
     const uint32_t pf_slot = pf_rows * 2048u + pf_mask * 128u;  // rows: 16 x 32 fp32, mask: 32 words
-    const uint32_t pf_total = 4u * kPfRing * pf_slot;
-    const uint32_t extra = stg_total + pf_total;
+    // staging (epilogue warps x 2 buffers) and prefetch rings scale with the epilogue warps; a
+    // second group that leaves too few pipeline stages falls back to one
+    uint32_t stg_total = 0, pf_total = 0, extra = 0;
     Plan pl;
-    if (!make_plan(g, &pl, main_ch, extra ? extra + 1024 : 0)) return cudaErrorNotSupported;
+    for (;; eg = 1) {
+        stg_total = 4u * eg * 2u * gm.stg_bytes;
+        pf_total = 4u * eg * kPfRing * pf_slot;
+        extra = stg_total + pf_total;
+        if (make_plan(g, &pl, main_ch, extra ? extra + 1024 : 0)) break;
+        if (eg == 1) return cudaErrorNotSupported;
+    }
     uint32_t stg_off = 0, pf_off = 0;
     if (extra) {
         const uint32_t stage =
@@ -1300,9 +1327,14 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-    auto kernel = tc_conv_kernel<0, 0>;
-    if (mode == 1) kernel = pl.kp == 16 ? tc_conv_kernel<1, 1> : (pl.kp == 32 ? tc_conv_kernel<1, 2> : tc_conv_kernel<1, 4>);
-    if (mode == 2) kernel = pl.kp == 16 ? tc_conv_kernel<2, 1> : (pl.kp == 32 ? tc_conv_kernel<2, 2> : tc_conv_kernel<2, 4>);
+    auto kernel = tc_conv_kernel<0, 0, 1>;
+    if (mode == 1)
+        kernel = pl.kp == 16 ? (eg == 2 ? tc_conv_kernel<1, 1, 2> : tc_conv_kernel<1, 1, 1>)
+               : (pl.kp == 32 ? (eg == 2 ? tc_conv_kernel<1, 2, 2> : tc_conv_kernel<1, 2, 1>) : tc_conv_kernel<1, 4, 1>);
+    if (mode == 2)
+        kernel = pl.kp == 16 ? (eg == 2 ? tc_conv_kernel<2, 1, 2> : tc_conv_kernel<2, 1, 1>)
+               : (pl.kp == 32 ? (eg == 2 ? tc_conv_kernel<2, 2, 2> : tc_conv_kernel<2, 2, 1>) : tc_conv_kernel<2, 4, 1>);
+    const int threads = 128 + 128 * eg;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
     if (e != cudaSuccess) return e;
@@ -1344,7 +1376,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         kp.k_begin = kg * pl.kp;
         kp.bimg = img + static_cast<size_t>(kg) * g.in_ch * (pl.b_chan_bytes / 2);
         kp.bimg_tail = img_tail + static_cast<size_t>(kg) * n_chunks * (pl.tw_stage_bytes / 2);
-        kernel<<<grid, kThreads, pl.smem_bytes, stream>>>(tmap, tmap_tail, gm.slots & 1u ? gm.m[0] : tmap,
+        kernel<<<grid, threads, pl.smem_bytes, stream>>>(tmap, tmap_tail, gm.slots & 1u ? gm.m[0] : tmap,
                                                           gm.slots & 2u ? gm.m[1] : tmap,
                                                           gm.slots & 4u ? gm.m[2] : tmap, kp);
         note_launch();
