@@ -44,6 +44,9 @@ CASES = [
     (16, 16, 17, 2, cv.Precision.Bf16, True, None),     # phase rewrite or FFMA
     (6, 6, 5, 8, cv.Precision.Fp32, False, False),      # FP32: conv + separate glue pass
     (8, 8, 7, 3, cv.Precision.Bf16, True, False),       # FFMA path
+    (96, 40, 17, 4, cv.Precision.Bf16, False, None),    # expanded rows (fused forward, 96-wide backward)
+    (40, 100, 9, 8, cv.Precision.Bf16, True, None),     # carry mode, two filter groups under glue
+    (128, 128, 9, 1, cv.Precision.Bf16, True, None),    # 128-wide expanded rows: conv + glue pass
 ]
 
 
