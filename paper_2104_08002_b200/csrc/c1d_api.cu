@@ -218,6 +218,9 @@ bool xr_inline_ok(const ConvGeom& g) {
 bool native_direct(const ConvGeom& g, int64_t main_ch = 0) {
     if (getenv("C1D_D8_CARRY") != nullptr) return false;  // dev A/B switch
     if (g.out_ch <= 64 && main_ch == 0) return false;
+    // split FP32 (two TMEM regions): only when the carry mode would run tiny super-tiles (FP32
+    // config 1, C = K = 15, keeps 8 tiles per super-tile in the carry mode: 99 vs 144 us)
+    if (g.out_ch <= 64 && main_ch > 0 && tc_conv_carry_tiles(g, main_ch) >= 4) return false;
     ConvGeom gi = g;
     gi.xr_inline = true;
     return tc_conv_supported(gi, main_ch);

@@ -102,6 +102,8 @@ struct TcConvPlan;
 // main_ch > 0 (split-FP32 mode): input channels >= main_ch accumulate into a second TMEM region
 // that the epilogue adds to the first, so the long accumulation chain only carries the main term.
 bool tc_conv_supported(const ConvGeom& g, int64_t main_ch = 0);
+// input tiles per super-tile of the carry mode (d = 8, natural rows) for this geometry, 0 if none
+int tc_conv_carry_tiles(const ConvGeom& g, int64_t main_ch = 0);
 size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch = 0);
 // wg: (o, i, s) weights of the forward-shaped problem, or with w_bwd_raw the caller's KCS weights of
 // a backward-data pass (transposed and tap-reversed while packing).

@@ -1228,6 +1228,14 @@ int64_t tc_conv_xr_rows(const ConvGeom& g) {
     return ceil_div(g.out_w, kTileQ) * (kTileQ / g.dil) + kTapsPerBlock * ceil_div(g.taps, kTapsPerBlock) + 8;
 }
 
+int tc_conv_carry_tiles(const ConvGeom& g, int64_t main_ch) {
+    Plan pl;
+    ConvGeom gc = g;
+    gc.xr_inline = false;
+    gc.xr_rows = 0;
+    return make_plan(gc, &pl, main_ch) ? pl.t : 0;
+}
+
 int pl_probe_kp(const ConvGeom& g, int64_t main_ch) {
     Plan pl;
     return make_plan(g, &pl, main_ch) ? pl.kp : 0;

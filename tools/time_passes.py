@@ -1,6 +1,6 @@
 """Dev timing tool: CUDA-event time of each pass at a BASELINE config (inputs resident in HBM).
 
-usage: python tools/time_passes.py [cfg ...]   cfg in {1,2,3}
+usage: python tools/time_passes.py [cfg ...]   cfg in {1,2,3,33}  (33: config 3 in FP32)
 """
 import os
 import sys
@@ -14,6 +14,7 @@ CFGS = {
     1: dict(n=4, c=15, k=15, s=51, d=8, q=60000, prec=cv.Precision.Fp32),
     2: dict(n=16, c=15, k=15, s=51, d=8, q=60000, prec=cv.Precision.Bf16),
     3: dict(n=32, c=64, k=64, s=51, d=8, q=60000, prec=cv.Precision.Bf16),
+    33: dict(n=32, c=64, k=64, s=51, d=8, q=60000, prec=cv.Precision.Fp32),
 }
 
 
