@@ -107,3 +107,27 @@ def test_packed_weight_layout_checks():
     assert torch.equal(pb.data[0], w[:, :, 3].t())
     with pytest.raises(cv.ShapeMismatch):
         cv._weights_kcs(pb, cv.ConvParams(2, 3, 4, 1), cv.WeightLayout.ForwardSKC)
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The ctypes mirrors (_lib.Desc / FwdGlue / BwdGlue) have the C structs' size and field offsets
+    (compiled against include/c1d.h with the host compiler)."""
+    structs = {"c1d_desc": L.Desc, "c1d_fwd_glue": L.FwdGlue, "c1d_bwd_glue": L.BwdGlue}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{L.HEADER_PATH}"', "int main(void) {"]
+    for cname, py in structs.items():
+        lines.append(f'  printf("{cname} size %zu\\n", sizeof({cname}));')
+        for fname, _ in py._fields_:
+            lines.append(f'  printf("{cname} {fname} %zu\\n", offsetof({cname}, {fname}));')
+    lines.append("  return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.run(["gcc", "-std=c11", "-o", str(exe), str(src)], check=True)
+    got = {}
+    for line in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.splitlines():
+        cname, field, val = line.split()
+        got[(cname, field)] = int(val)
+    for cname, py in structs.items():
+        assert got[(cname, "size")] == C.sizeof(py), cname
+        for fname, _ in py._fields_:
+            assert got[(cname, fname)] == getattr(py, fname).offset, (cname, fname)
