@@ -92,7 +92,22 @@ struct Plan {
     int rows_stage;       // E rows the MMAs read per channel
     int raw_segs;         // 256-column boxes per channel window
     uint32_t raw_stage_bytes;
+    // Resident weights: when the whole B image of a launch is small (narrow layers, e.g. C = K = 15:
+    // 30 KB), it is loaded once per CTA into the front of shared memory instead of with every stage
+    uint32_t wres_bytes;  // 0 = weights streamed per stage
 };
+
+constexpr uint32_t kWresMax = 64 * 1024;
+
+// Resident-weight decision for a plan whose b_chan_bytes / cc are set (stages are sized afterwards)
+inline bool want_wres(const ConvGeom& g, uint32_t b_chan_bytes, bool allow) {
+    return allow && static_cast<uint64_t>(g.in_ch) * b_chan_bytes <= kWresMax && getenv("C1D_NO_WRES") == nullptr;
+}
+inline void plan_wres(const ConvGeom& g, Plan* p, bool allow) {
+    const uint64_t img = static_cast<uint64_t>(g.in_ch) * p->b_chan_bytes;
+    p->wres_bytes = want_wres(g, p->b_chan_bytes, allow) ? static_cast<uint32_t>((img + 1023) & ~1023ull) : 0u;
+    if (p->wres_bytes) p->w_stage_bytes = 0;
+}
 
 struct KParams {
     int64_t n_items, in_ch, in_w, out_ch, out_w, in_off;
@@ -116,7 +131,7 @@ struct KParams {
     uint32_t pf_off, pf_slot_bytes, pf_rows, pf_mask;
 };
 
-bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve) {
+bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve, bool allow_wres = true) {
     // d = 8 joins as the inline case whose rows are the natural window itself (no expansion)
     if (g.dil != 1 && g.dil != 2 && g.dil != 4 && !(g.dil == 8 && g.xr_inline)) return false;
     if (g.dil == 8 && g.in_off % 8) return false;
@@ -161,7 +176,8 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.xw = 0;
     p.b_chan_bytes = static_cast<uint32_t>(p.ntot * kTapsPerBlock * 2);
     const uint32_t raw_chan = p.xin ? static_cast<uint32_t>(p.raw_segs * kSegQ * 2) : 0u;
-    const uint32_t per_chan = static_cast<uint32_t>(p.rows_alloc * 16) + p.b_chan_bytes + raw_chan;
+    const bool wres = want_wres(g, p.b_chan_bytes, allow_wres);
+    const uint32_t per_chan = static_cast<uint32_t>(p.rows_alloc * 16) + (wres ? 0u : p.b_chan_bytes) + raw_chan;
     p.cc = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(48 * 1024 / per_chan, 16)));
     p.cc = static_cast<int>(std::min<int64_t>(p.cc, g.in_ch));
     {
@@ -172,16 +188,17 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.w_stage_bytes = static_cast<uint32_t>(p.cc) * p.b_chan_bytes;
     p.tx_stage_bytes = p.tw_stage_bytes = 0;
     p.raw_stage_bytes = static_cast<uint32_t>(p.cc) * raw_chan;
+    plan_wres(g, &p, allow_wres);
     const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.raw_stage_bytes;
-    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve) / stage));
-    if (p.stages < 2) return false;
-    p.smem_bytes = static_cast<size_t>(p.stages) * stage + 1024;
+    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve - p.wres_bytes) / stage));
+    if (p.stages < 2) return p.wres_bytes ? make_plan_xr(g, pl, main_ch, reserve, false) : false;
+    p.smem_bytes = p.wres_bytes + static_cast<size_t>(p.stages) * stage + 1024;
     *pl = p;
     return true;
 }
 
-bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserve = 0) {
-    if (g.xr_rows > 0 || g.xr_inline) return make_plan_xr(g, pl, main_ch, reserve);
+bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserve = 0, bool allow_wres = true) {
+    if (g.xr_rows > 0 || g.xr_inline) return make_plan_xr(g, pl, main_ch, reserve, allow_wres);
     const bool two_regions = main_ch > 0;
     if (g.dil != 8) return false;
     const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
@@ -208,7 +225,8 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     p.n_seg = static_cast<int>(ceil_div(p.t * kTileQ + 8 * (kTapsPerBlock - 1), kSegQ));
     p.xw = p.n_seg * kSegQ;
     p.b_chan_bytes = static_cast<uint32_t>(p.ntot * kTapsPerBlock * 2);
-    const uint32_t per_chan = static_cast<uint32_t>(p.xw * 2) + p.b_chan_bytes;
+    const bool wres = want_wres(g, p.b_chan_bytes, allow_wres);
+    const uint32_t per_chan = static_cast<uint32_t>(p.xw * 2) + (wres ? 0u : p.b_chan_bytes);
     p.cc = static_cast<int>(std::max<uint32_t>(1, std::min<uint32_t>(48 * 1024 / per_chan, 16)));
     p.cc = static_cast<int>(std::min<int64_t>(p.cc, g.in_ch));
     {
@@ -230,10 +248,11 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     p.w_stage_bytes = static_cast<uint32_t>(p.cc) * p.b_chan_bytes;
     p.tx_stage_bytes = p.tail ? ((static_cast<uint32_t>(p.tail_chunks * p.cc * 16) + 1023) & ~1023u) : 0;
     p.tw_stage_bytes = p.tail ? static_cast<uint32_t>(p.kp * kTapsPerBlock * 2) : 0;
+    plan_wres(g, &p, allow_wres);
     const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.tx_stage_bytes + p.tw_stage_bytes;
-    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve) / stage));
-    if (p.stages < 2) return false;
-    p.smem_bytes = static_cast<size_t>(p.stages) * stage + 1024;
+    p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve - p.wres_bytes) / stage));
+    if (p.stages < 2) return p.wres_bytes ? make_plan(g, pl, main_ch, reserve, false) : false;
+    p.smem_bytes = p.wres_bytes + static_cast<size_t>(p.stages) * stage + 1024;
     *pl = p;
     return true;
 }
@@ -293,6 +312,8 @@ __global__ void pack_images_kernel(const float* __restrict__ w, int bwd_raw, uin
 // (n, j0..j1) it walks input tiles j0 .. j1+G-1 in super-tiles of up to T tiles. Input tile
 // i0+t of a super-tile writes output tiles i0+t-G+1 .. i0+t, which live at TMEM slots t..t+G-1
 // (slot j <-> output i0-(G-1)+j, KP columns per slot): every MMA is one contiguous N = G*KP run.
+constexpr int kProfSlots = 16;  // C1D_PROFILE counters per CTA
+
 struct Cursor {
     int64_t cur, end;         // flattened output-tile cursor
     int64_t n, j0, j1;        // current segment
@@ -643,15 +664,18 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t stage_full[kMaxStages], stage_empty[kMaxStages];
     __shared__ uint64_t raw_full[kMaxStages];  // inline expansion: natural windows landed
-    __shared__ uint64_t tmem_full, tmem_empty;
+    // double-buffered TMEM: tmem_empty / tmem_empty2 release region 0 / 1 (stores done, non-carry
+    // slots zeroed); carry_full publishes the G-1 carried slots of the next super-tile
+    __shared__ uint64_t tmem_full, tmem_empty, tmem_empty2, carry_full, wres_full;
     __shared__ uint32_t tmem_base_s;
     __shared__ float bias_red[8 * 64];  // layer glue: per-epilogue-warp bias-gradient sums
 
     const Plan& pl = p.pl;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-    uint8_t* xs_base = smem;
-    uint8_t* ws_base = smem + static_cast<size_t>(pl.stages) * pl.x_stage_bytes;
+    const uint32_t wres_s = smem_u32(smem);  // resident weights (pl.wres_bytes), then the stages
+    uint8_t* xs_base = smem + pl.wres_bytes;
+    uint8_t* ws_base = xs_base + static_cast<size_t>(pl.stages) * pl.x_stage_bytes;
     uint8_t* tx_base = ws_base + static_cast<size_t>(pl.stages) * pl.w_stage_bytes;
     uint8_t* tw_base = tx_base + static_cast<size_t>(pl.stages) * pl.tx_stage_bytes;
     uint8_t* raw_base = tw_base + static_cast<size_t>(pl.stages) * pl.tw_stage_bytes;
@@ -668,6 +692,9 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         }
         mbar_init(&tmem_full, 1);
         mbar_init(&tmem_empty, 4);  // one arrival per epilogue warp
+        mbar_init(&tmem_empty2, 4);
+        mbar_init(&carry_full, 4);
+        mbar_init(&wres_full, 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base_s);
@@ -675,6 +702,10 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    if (p.prof && threadIdx.x == 0) {
+        p.prof[blockIdx.x * kProfSlots + 8] = globaltimer_ns();
+        p.prof[blockIdx.x * kProfSlots + 10] = clock64();
+    }
 
     if (warp == 0) {
         // ------------------------------------------------------------------ TMA producer
@@ -687,6 +718,13 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             int stage = 0;
             uint32_t phase = 0;
             Super su;
+            const uint32_t wchan = pl.wres_bytes ? 0u : pl.b_chan_bytes;  // weight bytes per channel and stage
+            if (pl.wres_bytes) {
+                const uint32_t wbytes = static_cast<uint32_t>(p.in_ch) * pl.b_chan_bytes;
+                mbar_arrive_expect_tx(smem_u32(&wres_full), wbytes);
+                for (uint32_t o = 0; o < wbytes; o += 32768u)
+                    bulk_g2s(wres_s + o, p.bimg + o / 2, wbytes - o < 32768u ? wbytes - o : 32768u, smem_u32(&wres_full));
+            }
             while (next_super(cur, J, G, T, &su)) {
                 const int32_t x_start = static_cast<int32_t>(su.i0 * kTileQ + p.in_off);
                 const int nseg = static_cast<int>(ceil_div(su.tcur * kTileQ + 8 * (kTapsPerBlock - 1), kSegQ));
@@ -703,7 +741,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                         // (d = 8: the window is the A operand itself, so it completes the stage barrier)
                         const uint32_t rf = pl.xr == 8 ? full : smem_u32(&raw_full[stage]);
                         mbar_arrive_expect_tx(rf, static_cast<uint32_t>(ccn * pl.raw_segs * kSegQ * 2) +
-                                                      (pl.xr == 8 ? static_cast<uint32_t>(ccn) * pl.b_chan_bytes : 0u));
+                                                      (pl.xr == 8 ? static_cast<uint32_t>(ccn) * wchan : 0u));
                         const int32_t x_al = x_start - (((x_start % 8) + 8) % 8);
                         const uint32_t raw = smem_u32(raw_base + static_cast<size_t>(stage) * pl.raw_stage_bytes);
                         for (int c = 0; c < ccn; ++c) {
@@ -712,10 +750,12 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                                 tma_load_2d(raw + static_cast<uint32_t>((c * pl.raw_segs + sg) * kSegQ * 2), &tmap,
                                             x_al + sg * kSegQ, row, rf);
                         }
-                        if (pl.xr != 8) mbar_arrive_expect_tx(full, static_cast<uint32_t>(ccn) * pl.b_chan_bytes);
-                        const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
-                        bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
-                                 static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
+                        if (pl.xr != 8) mbar_arrive_expect_tx(full, static_cast<uint32_t>(ccn) * wchan);
+                        if (wchan) {
+                            const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
+                            bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
+                                     static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
+                        }
                         if (++stage == pl.stages) {
                             stage = 0;
                             phase ^= 1;
@@ -723,7 +763,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                         continue;
                     }
                     const uint32_t xbytes = pl.xr ? static_cast<uint32_t>(pl.rows_alloc * 16) : static_cast<uint32_t>(nseg * kSegQ * 2);
-                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (xbytes + pl.b_chan_bytes) +
+                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (xbytes + wchan) +
                                            (pl.tail ? pl.tail_chunks * pl.cc * 16u + pl.tw_stage_bytes : 0u);
                     mbar_arrive_expect_tx(full, bytes);
                     const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
@@ -743,9 +783,11 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                                             x_start + sg * kSegQ, row, full);
                         }
                     }
-                    const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
-                    bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
-                             static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
+                    if (wchan) {
+                        const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
+                        bulk_g2s(wsm, p.bimg + static_cast<size_t>(c0) * (pl.b_chan_bytes / 2),
+                                 static_cast<uint32_t>(ccn) * pl.b_chan_bytes, full);
+                    }
                     if (pl.tail) {
                         // q-chunk-major box of the stage's cc channels over the same input tiles
                         // (tap block G-1 of input tile p lands on output slot t, like block 0 of B)
@@ -767,15 +809,15 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                 }
             }
             if (p.prof) {
-                p.prof[blockIdx.x * 8 + 0] = t_wait;
-                p.prof[blockIdx.x * 8 + 1] = clock64() - t_begin;
+                p.prof[blockIdx.x * kProfSlots + 0] = t_wait;
+                p.prof[blockIdx.x * kProfSlots + 1] = clock64() - t_begin;
             }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------------ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps descriptors in
         // uniform registers); one elected lane issues each tcgen05 instruction.
-        long long t_full = 0, t_tmem = 0;
+        long long t_full = 0, t_tmem = 0, t_full_first = -1, n_super = 0;
         const long long t_begin = clock64();
         Cursor cur = make_cursor(p);
         int stage = 0;
@@ -787,13 +829,29 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         const uint32_t main_slot = pl.tail ? static_cast<uint32_t>(KP) : 0u;       // D column offset
         const uint32_t main_brow = pl.tail ? static_cast<uint32_t>(KP) * 32u : 0u;  // skip block 0 of B
         uint32_t region = 0;  // TMEM region of the current super-tile (double buffering)
+        uint32_t rphase[2] = {0u, 0u}, cphase = 0;
+        if (pl.wres_bytes) {
+            mbar_wait(smem_u32(&wres_full), 0);
+            tc_fence_after();
+        }
+        bool first_super = true;
         Super su;
         while (next_super(cur, J, G, T, &su)) {
             const long long ts0 = clock64();
-            mbar_wait(smem_u32(&tmem_empty), tphase);
-            tphase ^= 1;
+            if (pl.dbuf) {
+                const int ri = region ? 1 : 0;
+                mbar_wait(smem_u32(ri ? &tmem_empty2 : &tmem_empty), rphase[ri]);
+                rphase[ri] ^= 1u;
+            } else {
+                mbar_wait(smem_u32(&tmem_empty), tphase);
+                tphase ^= 1;
+            }
             t_tmem += clock64() - ts0;
             tc_fence_after();
+            // double buffering: tiles t >= G-1 do not touch the carried slots 0..G-2, so the first
+            // stage issues them before waiting for the epilogue's carry (the carry overlaps MMAs)
+            bool need_carry = pl.dbuf && G > 1 && !first_super;
+            first_super = false;
             const uint32_t rtmem = tmem + region;
             for (int ch = 0; ch < n_chunks; ++ch) {
                 const int c0 = ch * pl.cc;
@@ -803,7 +861,8 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                 t_full += clock64() - tf0;
                 tc_fence_after();
                 const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
-                const uint32_t wsm = smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
+                const uint32_t wsm = pl.wres_bytes ? wres_s + static_cast<uint32_t>(c0) * pl.b_chan_bytes
+                                                   : smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
                 const uint64_t a0 = make_smem_desc(xs, 128, 16, kLayoutNone);
                 const uint64_t b0 = make_smem_desc(wsm + main_brow, 128, 256, kLayoutNone);
                 if (pl.xr) {
@@ -839,21 +898,38 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                             bchan = desc_advance(bchan, pl.b_chan_bytes);
                         }
                     }
-                } else if (elect_one()) {
-                    uint64_t bdesc = b0;
-                    uint64_t achan = a0;
-                    for (int c = 0; c < ccn; ++c) {
-                        uint64_t adesc = achan;
-                        uint32_t dcol = rtmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u) + main_slot;
-                        for (int t = 0; t < su.tcur; ++t) {
-                            mma_bf16_ss(dcol, adesc, bdesc, idesc, 1);
-                            adesc = desc_advance(adesc, static_cast<uint32_t>(kTileQ * 2));
-                            dcol += static_cast<uint32_t>(KP);
+                } else {
+                    const int tsplit = need_carry ? (su.tcur < G - 1 ? su.tcur : G - 1) : 0;
+                    // main MMAs of input tiles [t0, t1) for every channel of the stage
+                    auto issue_tiles = [&](int t0, int t1) {
+                        uint64_t bdesc = b0;
+                        uint64_t achan = desc_advance(a0, static_cast<uint32_t>(t0 * kTileQ * 2));
+                        for (int c = 0; c < ccn; ++c) {
+                            uint64_t adesc = achan;
+                            uint32_t dcol = rtmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u) + main_slot +
+                                            static_cast<uint32_t>(t0 * KP);
+                            for (int t = t0; t < t1; ++t) {
+                                mma_bf16_ss(dcol, adesc, bdesc, idesc, 1);
+                                adesc = desc_advance(adesc, static_cast<uint32_t>(kTileQ * 2));
+                                dcol += static_cast<uint32_t>(KP);
+                            }
+                            bdesc = desc_advance(bdesc, pl.b_chan_bytes);
+                            achan = desc_advance(achan, static_cast<uint32_t>(pl.xw * 2));
                         }
-                        bdesc = desc_advance(bdesc, pl.b_chan_bytes);
-                        achan = desc_advance(achan, static_cast<uint32_t>(pl.xw * 2));
+                    };
+                    if (elect_one()) issue_tiles(tsplit, su.tcur);
+                    __syncwarp();
+                    if (need_carry) {
+                        const long long tc0 = clock64();
+                        mbar_wait(smem_u32(&carry_full), cphase);
+                        cphase ^= 1u;
+                        t_tmem += clock64() - tc0;
+                        tc_fence_after();
+                        need_carry = false;
+                        if (elect_one()) issue_tiles(0, tsplit);
+                        __syncwarp();
                     }
-                    if (pl.tail) {
+                    if (pl.tail && elect_one()) {
                         // A[m][k = r*cc + c] = x[c][q0 + m + 8r] (tap 16(G-1) + r): MN-major, K rows
                         // 16 B apart (contiguous), M groups of 8 columns one q-chunk (cc*16 B) apart
                         const uint32_t tx = smem_u32(tx_base + static_cast<size_t>(stage) * pl.tx_stage_bytes);
@@ -879,11 +955,15 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             if (elect_one()) mma_commit(smem_u32(&tmem_full));
             __syncwarp();
             if (pl.dbuf) region ^= 256u;
+            if (t_full_first < 0) t_full_first = t_full + t_tmem;
+            ++n_super;
         }
         if (p.prof && lane == 0) {
-            p.prof[blockIdx.x * 8 + 2] = t_full;
-            p.prof[blockIdx.x * 8 + 3] = t_tmem;
-            p.prof[blockIdx.x * 8 + 4] = clock64() - t_begin;
+            p.prof[blockIdx.x * kProfSlots + 2] = t_full;
+            p.prof[blockIdx.x * kProfSlots + 3] = t_tmem;
+            p.prof[blockIdx.x * kProfSlots + 4] = clock64() - t_begin;
+            p.prof[blockIdx.x * kProfSlots + 12] = t_full_first;
+            p.prof[blockIdx.x * kProfSlots + 13] = n_super;
         }
     } else if (warp == 2 || warp == 3) {
         // ------------------------------------------------------------------ E-row expanders
@@ -942,7 +1022,10 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
+            if (lane == 0) {
+                mbar_arrive(smem_u32(&tmem_empty));
+                if (pl.dbuf) mbar_arrive(smem_u32(&tmem_empty2));  // both regions start zeroed
+            }
         }
         Cursor cur = make_cursor(p);
         uint32_t tphase = 0;
@@ -1036,12 +1119,42 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tmem_empty));
         };
+        // double buffering: carry the G-1 partial slots of `region` into slots 0..G-2 of the other
+        // region (zeros at a segment end) and publish them; the other region's remaining slots were
+        // zeroed when it was released
+        auto carry_out = [&](const Super& s2) {
+            for (int j = 0; j < G - 1; ++j) {
+                for (int kb = 0; kb < KP; kb += 16) {
+                    uint32_t v[16];
+                    if (!s2.last_in_segment) {
+                        tmem_ld16(lane_base + region + static_cast<uint32_t>((s2.tcur + j) * KP + kb), v);
+                        tmem_ld_wait();
+                        tmem_st16(lane_base + (region ^ 256u) + static_cast<uint32_t>(j * KP + kb), v);
+                    } else {
+                        tmem_st16(lane_base + (region ^ 256u) + static_cast<uint32_t>(j * KP + kb), z);
+                    }
+                }
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&carry_full));
+        };
+        // double buffering: zero the non-carry slots of `region` after its stores, then release it
+        auto release = [&]() {
+            for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < used_cols; col += 16)
+                tmem_st16(lane_base + region + col, z);
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(region ? &tmem_empty2 : &tmem_empty));
+        };
         while (next_super(cur, J, G, T, &su)) {
             mbar_wait_sleep(smem_u32(&tmem_full), tphase, 256);
             tphase ^= 1;
             tc_fence_after();
             const long long e0 = clock64();
-            if (pl.dbuf && egrp == 0) prepare(region, region ^ 256u, su);  // next super-tile may start now
+            if (pl.dbuf && egrp == 0) carry_out(su);  // the next super-tile's carry-dependent tiles may start
             const long long e1 = clock64();
             // store the completed outputs (slots 0..tcur-1)
             const int64_t out_w = p.out_w;
@@ -1128,7 +1241,9 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                 if (egrp == 0) prepare(0, 0, su);  // in place: carry down, zero the rest, release
                 e_carry += clock64() - e2;
             } else {
+                if (egrp == 0) release();
                 e_carry += e1 - e0;
+                e_zero += clock64() - e2;
                 region ^= 256u;
             }
         }
@@ -1154,9 +1269,11 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             }
         }
         if (p.prof && threadIdx.x == 128) {
-            p.prof[blockIdx.x * 8 + 5] = e_store;
-            p.prof[blockIdx.x * 8 + 6] = e_carry;
-            p.prof[blockIdx.x * 8 + 7] = e_zero;
+            p.prof[blockIdx.x * kProfSlots + 5] = e_store;
+            p.prof[blockIdx.x * kProfSlots + 6] = e_carry;
+            p.prof[blockIdx.x * kProfSlots + 7] = e_zero;
+            p.prof[blockIdx.x * kProfSlots + 9] = globaltimer_ns();
+            p.prof[blockIdx.x * kProfSlots + 11] = clock64();
         }
     }
     tc_fence_before();
@@ -1284,7 +1401,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     if (extra) {
         const uint32_t stage =
             pl.x_stage_bytes + pl.w_stage_bytes + pl.tx_stage_bytes + pl.tw_stage_bytes + pl.raw_stage_bytes;
-        stg_off = (static_cast<uint32_t>(pl.stages) * stage + 127u) & ~127u;
+        stg_off = (pl.wres_bytes + static_cast<uint32_t>(pl.stages) * stage + 127u) & ~127u;
         pf_off = stg_off + stg_total;
         pl.smem_bytes = pf_off + pf_total + 1024;
     }
@@ -1377,8 +1494,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     }
     static const bool profile = getenv("C1D_PROFILE") != nullptr;
     if (profile) {
-        cudaMalloc(&kp.prof, sizeof(unsigned long long) * 8 * grid);
-        cudaMemset(kp.prof, 0, sizeof(unsigned long long) * 8 * grid);
+        cudaMalloc(&kp.prof, sizeof(unsigned long long) * kProfSlots * grid);
+        cudaMemset(kp.prof, 0, sizeof(unsigned long long) * kProfSlots * grid);
     }
     for (int kg = 0; kg < pl.kgroups; ++kg) {
         kp.k_begin = kg * pl.kp;
@@ -1396,13 +1513,25 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         if (e != cudaSuccess) return e;
     }
     if (profile) {
-        std::vector<unsigned long long> h(8 * grid);
+        std::vector<unsigned long long> h(kProfSlots * grid);
         cudaMemcpy(h.data(), kp.prof, h.size() * 8, cudaMemcpyDeviceToHost);
-        double a[8] = {0};
-        for (int b = 0; b < grid; ++b)
-            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[b * 8 + i]) / grid;
-        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f | epilogue store %.0f carry %.0f zero %.0f (cycles, CTA avg)\n",
-                a[0], a[1], a[2], a[3], a[4], a[5], a[6], a[7]);
+        double a[8] = {0}, mma_max = 0;
+        unsigned long long t0 = ~0ull, t1 = 0, t1_min = ~0ull;
+        double mhz = 0, cta_us = 0, first = 0, nsup = 0;
+        for (int b = 0; b < grid; ++b) {
+            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[b * kProfSlots + i]) / grid;
+            mma_max = std::max(mma_max, static_cast<double>(h[b * kProfSlots + 4]));
+            t0 = std::min(t0, h[b * kProfSlots + 8]);
+            t1 = std::max(t1, h[b * kProfSlots + 9]);
+            t1_min = std::min(t1_min, h[b * kProfSlots + 9]);
+            const double dt = static_cast<double>(h[b * kProfSlots + 9] - h[b * kProfSlots + 8]);
+            mhz += static_cast<double>(h[b * kProfSlots + 11] - h[b * kProfSlots + 10]) / dt * 1e3 / grid;
+            cta_us += dt * 1e-3 / grid;
+            first += static_cast<double>(h[b * kProfSlots + 12]) / grid;
+            nsup += static_cast<double>(h[b * kProfSlots + 13]) / grid;
+        }
+        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f (max %.0f) | epilogue store %.0f carry %.0f zero %.0f (cycles, CTA avg) | span %.1f us, first CTA done %.1f us, CTA avg %.1f us at %.0f MHz | mma waits in super-tile 1: %.0f, super-tiles %.1f\n",
+                a[0], a[1], a[2], a[3], a[4], mma_max, a[5], a[6], a[7], (t1 - t0) * 1e-3, (t1_min - t0) * 1e-3, cta_us, mhz, first, nsup);
         cudaFree(kp.prof);
     }
     return cudaSuccess;

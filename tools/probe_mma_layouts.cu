@@ -5,6 +5,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "../paper_2104_08002_b200/csrc/sm100.cuh"
 
@@ -30,7 +31,10 @@ struct Cfg {
     int unroll;               // issue 8 K-steps straight-line (no address wrap)
     int rnd;                  // random operands (else zeros)
     int d_step;               // TMEM column advance per K-step (unrolled mode), wraps at 512-N
+    int g_dcol;               // TMEM column advance between accumulators (0: N, disjoint)
+    int a_tmem;               // A operand from TMEM columns [384 + 8g, ...) instead of shared memory
 };
+
 
 __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long* cyc, int bg, const uint4* gsrc,
                                                     volatile int* stop) {
@@ -97,9 +101,14 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
 #pragma unroll 1
-                    for (int g = 0; g < c.nacc; ++g)
-                        mma_bf16_ss(tmem_s + dc + g * c.n, desc_advance(a0, u * c.a_step + g * c.g_step),
-                                    desc_advance(b0, u * c.b_step), idesc, 1u);
+                    for (int g = 0; g < c.nacc; ++g) {
+                        if (c.a_tmem)
+                            mma_bf16_ts(tmem_s + dc + g * (c.g_dcol ? c.g_dcol : c.n), tmem_s + 384 + 8 * (g & 7),
+                                        desc_advance(b0, u * c.b_step), idesc, 1u);
+                        else
+                            mma_bf16_ss(tmem_s + dc + g * (c.g_dcol ? c.g_dcol : c.n), desc_advance(a0, u * c.a_step + g * c.g_step),
+                                        desc_advance(b0, u * c.b_step), idesc, 1u);
+                    }
                     dc += c.d_step;
                     if (dc > dwrap) dc = 0;
                 }
@@ -153,6 +162,40 @@ int main() {
         {"UNROLLED N=112 1 acc", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 1},
         {"UNROLLED N=128 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 128, 2048, 2048, 1, 0, 1},
         {"UNROLLED N=64 1 acc", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 64, 2048, 2048, 1, 0, 1},
+        // small-N forward row-tap MMAs (C = K = 15 shapes): does a disjoint accumulator per MMA beat the chain?
+        {"SMALLN N=64 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 512, 8192, 1, 0, 1, 1, 0},
+        {"SMALLN N=64 D+64", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 512, 8192, 1, 0, 1, 1, 64},
+        {"SMALLN N=64 D+16 (overlap)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 512, 8192, 1, 0, 1, 1, 16},
+        {"SMALLN N=48 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 48, 512, 8192, 1, 0, 1, 1, 0},
+        {"SMALLN N=48 D+16 (overlap)", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 48, 512, 8192, 1, 0, 1, 1, 16},
+        {"SMALLN N=48 D+48", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 48, 512, 8192, 1, 0, 1, 1, 48},
+        {"SMALLN N=32 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 32, 512, 8192, 1, 0, 1, 1, 0},
+        {"SMALLN N=32 D+32", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 32, 512, 8192, 1, 0, 1, 1, 32},
+        {"SMALLN N=16 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 512, 8192, 1, 0, 1, 1, 0},
+        {"SMALLN N=16 D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 512, 8192, 1, 0, 1, 1, 16},
+        {"SMALLN N=16 4acc D+64", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 512, 8192, 4, 512, 1, 1, 64},
+        {"SMALLN N=64 4acc D+256", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 512, 8192, 4, 512, 1, 1, 256},
+        {"SMALLN carry N=48 8acc A+256 D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 48, 2048, 8192, 8, 256, 1, 1, 0, 16},
+        {"SMALLN carry N=48 8acc A+256 D+48", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 48, 2048, 8192, 8, 256, 1, 1, 0, 48},
+        {"SMALLN carry N=64 8acc A+256 D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 2048, 8192, 8, 256, 1, 1, 0, 16},
+        {"SMALLN carry N=64 4acc A+256 D+64", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 2048, 8192, 4, 256, 1, 1, 0, 64},
+        {"SMALLN carry N=16 8acc A+256 D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 2048, 8192, 8, 256, 1, 1, 0, 16},
+        {"SMALLN carry N=32 8acc A+256 D+32", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 32, 2048, 8192, 8, 256, 1, 1, 0, 32},
+        {"SMALLN carry N=16 8acc A+256 sameD", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 2048, 8192, 8, 256, 1, 1, 0, 0},
+        {"SMALLN Bsame N=64 1acc A+256", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 1, 1, 0},
+        {"SMALLN Bsame N=16 1acc A+256", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 256, 0, 1, 0, 1, 1, 0},
+        {"SMALLN Bsame N=16 1acc D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 256, 0, 1, 0, 1, 1, 16},
+        {"SMALLN TMEM-A N=16 8acc", 128, 16, kLayoutNone, 0, 128, 256, kLayoutNone, 16, 2048, 8192, 8, 256, 1, 1, 0, 16, 1},
+        {"SMALLN TMEM-A N=48 8acc D+16", 128, 16, kLayoutNone, 0, 128, 256, kLayoutNone, 48, 2048, 8192, 8, 256, 1, 1, 0, 16, 1},
+        {"SMALLN TMEM-A N=64 4acc", 128, 16, kLayoutNone, 0, 128, 256, kLayoutNone, 64, 2048, 8192, 4, 256, 1, 1, 0, 64, 1},
+        {"SMALLN TMEM-A N=128 2acc", 128, 16, kLayoutNone, 0, 128, 256, kLayoutNone, 128, 2048, 8192, 2, 256, 1, 1, 0, 128, 1},
+        {"SMALLN GEMM-A SW128 N=16 8acc", 16, 1024, kLayoutSw128, 0, 128, 256, kLayoutNone, 16, 32, 8192, 8, 16384, 1, 1, 0, 16},
+        {"SMALLN GEMM-A SW128 N=48 8acc", 16, 1024, kLayoutSw128, 0, 128, 256, kLayoutNone, 48, 32, 8192, 8, 16384, 1, 1, 0, 16},
+        {"SMALLN N=128 2acc D+128", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 2048, 8192, 2, 256, 1, 1, 0, 128},
+        {"SMALLN N=256 2acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 2048, 8192, 2, 256, 1, 1, 0, 0},
+        {"SMALLN N=128 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 0},
+        {"SMALLN N=128 D+128", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 128},
+        {"SMALLN N=256 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512, 8192, 1, 0, 1, 1, 0},
         {"wgrad A | B SW32, 4 acc N=128", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 128, 2048, 2048, 4, 8192},
         {"GEMM SW128, 1 acc N=256", 16, 1024, kLayoutSw128, 0, 16, 1024, kLayoutSw128, 256, 32, 32, 1, 0},
         {"wgrad A | B SW32 N=128", 1024, 128, kLayoutNone, 0, 16, 256, kLayoutSw32, 128, 2048, 2048, 2, 8192},
@@ -168,9 +211,12 @@ int main() {
     CK(cudaMalloc(&gsrc, (size_t(1) << 22) * 16));
     CK(cudaMemset(gsrc, 0, (size_t(1) << 22) * 16));
     const char* bgname[] = {"", " +st.shared bg", " +cp.async bg"};
+    const char* only = getenv("PROBE_ONLY");
     for (const Cfg& c : cfgs)
       for (int bg = 0; bg < 3; ++bg) {
         if (bg && !c.unroll) continue;
+        if (only && !strstr(c.name, only)) continue;
+        if (only && bg) continue;
         for (int grid : {148}) {
             mma_probe<<<grid, 128, 161 * 1024>>>(c, ksteps, cyc, bg, gsrc, nullptr);
             CK(cudaDeviceSynchronize());
