@@ -95,6 +95,11 @@ struct Plan {
     // Resident weights: when the whole B image of a launch is small (narrow layers, e.g. C = K = 15:
     // 30 KB), it is loaded once per CTA into the front of shared memory instead of with every stage
     uint32_t wres_bytes;  // 0 = weights streamed per stage
+    // Natural mode: a stage's cc channel windows as ONE 3-D TMA box (256 columns, n_seg segments,
+    // cc rows) through an overlapping view whose segment stride is 512 B, instead of cc * n_seg
+    // single-row boxes (each TMA box costs the producer ~100 cycles); only for windows inside
+    // [0, in_w), since the view's bounds are checked per dimension (edge windows keep the 2-D boxes)
+    int xbox3;
 };
 
 constexpr uint32_t kWresMax = 64 * 1024;
@@ -711,7 +716,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         // ------------------------------------------------------------------ TMA producer
         if (lane == 0) {
             prefetch_tmap(&tmap);
-            if (pl.tail) prefetch_tmap(&tmap_tail);
+            if (pl.tail || pl.xbox3) prefetch_tmap(&tmap_tail);
             long long t_wait = 0;
             const long long t_begin = clock64();
             Cursor cur = make_cursor(p);
@@ -762,8 +767,10 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                         }
                         continue;
                     }
+                    const bool box3 = pl.xbox3 && x_start >= 0 && x_start + pl.xw <= p.in_w;
                     const uint32_t xbytes = pl.xr ? static_cast<uint32_t>(pl.rows_alloc * 16) : static_cast<uint32_t>(nseg * kSegQ * 2);
-                    const uint32_t bytes = static_cast<uint32_t>(ccn) * (xbytes + wchan) +
+                    const uint32_t bytes = (box3 ? static_cast<uint32_t>(pl.cc * pl.xw * 2) + static_cast<uint32_t>(ccn) * wchan
+                                                 : static_cast<uint32_t>(ccn) * (xbytes + wchan)) +
                                            (pl.tail ? pl.tail_chunks * pl.cc * 16u + pl.tw_stage_bytes : 0u);
                     mbar_arrive_expect_tx(full, bytes);
                     const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
@@ -775,6 +782,8 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                                 tma_load_3d(xs + static_cast<uint32_t>((c * pl.rows_alloc + b * pl.box_rows) * 16), &tmap,
                                             0, (r0 + b * pl.box_rows) / 8, row, full);
                         }
+                    } else if (box3) {
+                        tma_load_3d(xs, &tmap_tail, x_start, 0, static_cast<int32_t>(su.n * p.in_ch + c0), full);
                     } else {
                         for (int c = 0; c < ccn; ++c) {
                             const int32_t row = static_cast<int32_t>(su.n * p.in_ch + c0 + c);
@@ -1438,7 +1447,26 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
-    CUtensorMap tmap_tail = tmap;  // unused unless pl.tail
+    CUtensorMap tmap_tail = tmap;  // unused unless pl.tail / pl.xbox3
+    pl.xbox3 = 0;
+    static const bool no_box3 = getenv("C1D_NO_BOX3") != nullptr;  // dev A/B switch
+    if (!pl.tail && !pl.xr && !no_box3 && pl.n_seg * kSegQ == pl.xw) {
+        // overlapping view: element (i, j, row) at row*pitch + i + 256 j (see Plan::xbox3)
+        const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
+        const cuuint64_t d3[3] = {static_cast<cuuint64_t>(g.in_w), static_cast<cuuint64_t>(pl.n_seg),
+                                  static_cast<cuuint64_t>(g.n * g.in_ch)};
+        const cuuint64_t s3[2] = {static_cast<cuuint64_t>(kSegQ) * 2, static_cast<cuuint64_t>(pitch) * 2};
+        const cuuint32_t b3[3] = {static_cast<cuuint32_t>(kSegQ), static_cast<cuuint32_t>(pl.n_seg),
+                                  static_cast<cuuint32_t>(pl.cc)};
+        const cuuint32_t e3[3] = {1, 1, 1};
+        if (pl.cc * pl.xw * 2 <= static_cast<int>(pl.x_stage_bytes) &&
+            encode(&tmap_tail, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(in_bf16), d3, s3, b3, e3,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            pl.xbox3 = 1;
+        else
+            tmap_tail = tmap;
+    }
     if (pl.tail) {
         // the input as (8 columns, channel, q-chunk, item): element (e, c, u, n) at ((n*C + c)*pitch + 8u + e)
         const int64_t pitch = g.in_stride ? g.in_stride : g.in_w;
