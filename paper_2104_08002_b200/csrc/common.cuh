@@ -1,7 +1,9 @@
 // common.cuh — shared device helpers for the conv1d kernels.
 #pragma once
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_runtime.h>
+#include <utility>
 
 namespace c1d {
 
@@ -50,5 +52,36 @@ __device__ __forceinline__ float load_as_float<uint16_t>(const uint16_t* p, int6
 }
 
 __host__ __device__ constexpr int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- programmatic dependent launch (PDL) ------------------------------------------------------
+// The hot kernels launch with programmatic stream serialization: a kernel's CTAs may become
+// resident while the previous kernel in the stream is finishing, run their prologue (barrier
+// init, TMEM allocation, tensor-map prefetch), and block in pdl_wait() until that kernel has
+// completed and its memory is visible. Every kernel launched through launch_pdl() calls
+// pdl_wait() before its first global-memory access; pdl_trigger() lets the next kernel start
+// launching (its own pdl_wait() still waits for this kernel's completion).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    static const bool on = getenv("C1D_NO_PDL") == nullptr;  // dev A/B switch
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 }  // namespace c1d

@@ -285,6 +285,8 @@ __global__ void pack_images_kernel(const float* __restrict__ w, int bwd_raw, uin
     const int64_t main_total = static_cast<int64_t>(kgroups) * in_ch * per_chan;
     const int64_t per_tail = static_cast<int64_t>(kp) * kTapsPerBlock;
     const int64_t total = main_total + (tail ? static_cast<int64_t>(kgroups) * chunks * per_tail : 0);
+    pdl_trigger();
+    pdl_wait();
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         if (e < main_total) {
             const int64_t r = e % kTapsPerBlock;
@@ -707,6 +709,9 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    // PDL: everything above overlapped the previous kernel; global memory only from here on
+    pdl_trigger();
+    pdl_wait();
     if (p.prof && threadIdx.x == 0) {
         p.prof[blockIdx.x * kProfSlots + 8] = globaltimer_ns();
         p.prof[blockIdx.x * kProfSlots + 10] = clock64();
@@ -1421,10 +1426,10 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         const int64_t total = static_cast<int64_t>(pl.kgroups) *
                               (g.in_ch * pl.ntot + (pl.tail ? n_chunks * pl.kp : 0)) * kTapsPerBlock;
         const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
-        pack_images_kernel<<<blocks, 256, 0, stream>>>(wg, w_bwd_raw ? 1 : 0, img, img_tail, g.out_ch, g.in_ch, g.taps,
-                                                       pl.kp, pl.g, pl.kgroups, pl.cc, pl.tail, n_chunks);
         note_launch();
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(pack_images_kernel, dim3(blocks), dim3(256), 0, stream, wg, w_bwd_raw ? 1 : 0, img,
+                                   img_tail, static_cast<int64_t>(g.out_ch), static_cast<int64_t>(g.in_ch),
+                                   static_cast<int64_t>(g.taps), pl.kp, pl.g, pl.kgroups, pl.cc, pl.tail, n_chunks);
         if (e != cudaSuccess) return e;
     }
     CUtensorMap tmap;
@@ -1529,11 +1534,9 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         kp.k_begin = kg * pl.kp;
         kp.bimg = img + static_cast<size_t>(kg) * g.in_ch * (pl.b_chan_bytes / 2);
         kp.bimg_tail = img_tail + static_cast<size_t>(kg) * n_chunks * (pl.tw_stage_bytes / 2);
-        kernel<<<grid, threads, pl.smem_bytes, stream>>>(tmap, tmap_tail, gm.slots & 1u ? gm.m[0] : tmap,
-                                                          gm.slots & 2u ? gm.m[1] : tmap,
-                                                          gm.slots & 4u ? gm.m[2] : tmap, kp);
+        e = launch_pdl(kernel, dim3(grid), dim3(threads), pl.smem_bytes, stream, tmap, tmap_tail,
+                       gm.slots & 1u ? gm.m[0] : tmap, gm.slots & 2u ? gm.m[1] : tmap, gm.slots & 4u ? gm.m[2] : tmap, kp);
         note_launch();
-        e = cudaGetLastError();
         if (e != cudaSuccess) return e;
     }
     if (kp.glue.mode == 2 && kp.glue.bias_grad) {

@@ -568,6 +568,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    // PDL: everything above overlapped the previous kernel; global memory only from here on (no
+    // early trigger: the reduce's many small CTAs would sit on the SMs beside this kernel)
+    pdl_wait();
     const int64_t back = static_cast<int64_t>(pl.p - 1) * pl.bq;  // dY history columns per stage
 
     if (warp == 0) {
@@ -903,6 +906,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
                                                             int64_t K, int64_t C, int64_t S, const W2Plan pl) {
     __shared__ float red[4][64];
+    pdl_trigger();
+    pdl_wait();
     const int64_t count = K * C * S;
     const int64_t e = static_cast<int64_t>(blockIdx.x) * 64 + (threadIdx.x % 64);
     const int quarter = threadIdx.x / 64;
@@ -985,9 +990,8 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * pl.grid);
         cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * pl.grid);
     }
-    tc_wgrad2_kernel<<<pl.grid, kThreads, pl.smem_bytes, stream>>>(ymap, wp);
+    e = launch_pdl(tc_wgrad2_kernel, dim3(pl.grid), dim3(kThreads), pl.smem_bytes, stream, ymap, wp);
     note_launch();
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (profile) {
         std::vector<unsigned long long> h(8 * pl.grid);
@@ -1010,9 +1014,10 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         cudaFree(wp.prof);
     }
     const int64_t count = k * c * s;
-    wgrad2_reduce_kernel<<<static_cast<unsigned>(ceil_div(count, 64)), 256, 0, stream>>>(wp.part, dw_kcs, k, c, s, pl);
     note_launch();
-    return cudaGetLastError();
+    return launch_pdl(wgrad2_reduce_kernel, dim3(static_cast<unsigned>(ceil_div(count, 64))), dim3(256), 0, stream,
+                      static_cast<const float*>(wp.part), dw_kcs, static_cast<int64_t>(k), static_cast<int64_t>(c),
+                      static_cast<int64_t>(s), pl);
 }
 }  // namespace
 

@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
         const uint32_t idesc = make_idesc(128, c.n, kFmtBF16, c.a_mn, 0);
         const uint64_t a0 = make_smem_desc(sa, c.a_lbo, c.a_sbo, c.a_layout);
         const uint64_t b0 = make_smem_desc(sb, c.b_lbo, c.b_sbo, c.b_layout);
+        const uint32_t tb = tmem_s;  // register copy: a shared load between MMAs waits for them
         const long long t0 = clock64();
         uint32_t ao = 0, bo = 0;
         if (c.unroll) {
@@ -103,10 +104,10 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
 #pragma unroll 1
                     for (int g = 0; g < c.nacc; ++g) {
                         if (c.a_tmem)
-                            mma_bf16_ts(tmem_s + dc + g * (c.g_dcol ? c.g_dcol : c.n), tmem_s + 384 + 8 * (g & 7),
+                            mma_bf16_ts(tb + dc + g * (c.g_dcol ? c.g_dcol : c.n), tb + 384 + 8 * (g & 7),
                                         desc_advance(b0, u * c.b_step), idesc, 1u);
                         else
-                            mma_bf16_ss(tmem_s + dc + g * (c.g_dcol ? c.g_dcol : c.n), desc_advance(a0, u * c.a_step + g * c.g_step),
+                            mma_bf16_ss(tb + dc + g * (c.g_dcol ? c.g_dcol : c.n), desc_advance(a0, u * c.a_step + g * c.g_step),
                                         desc_advance(b0, u * c.b_step), idesc, 1u);
                     }
                     dc += c.d_step;
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
         for (int k = 0; k < ksteps; ++k) {
 #pragma unroll 1
             for (int g = 0; g < c.nacc; ++g)
-                mma_bf16_ss(tmem_s + g * c.n, desc_advance(a0, ao + g * c.g_step), desc_advance(b0, bo), idesc,
+                mma_bf16_ss(tb + g * c.n, desc_advance(a0, ao + g * c.g_step), desc_advance(b0, bo), idesc,
                             k > 0 ? 1u : 0u);
             ao += c.a_step;
             if (ao >= 32768) ao -= 32768;
@@ -193,6 +194,15 @@ int main() {
         {"SMALLN GEMM-A SW128 N=48 8acc", 16, 1024, kLayoutSw128, 0, 128, 256, kLayoutNone, 48, 32, 8192, 8, 16384, 1, 1, 0, 16},
         {"SMALLN N=128 2acc D+128", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 2048, 8192, 2, 256, 1, 1, 0, 128},
         {"SMALLN N=256 2acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 2048, 8192, 2, 256, 1, 1, 0, 0},
+        {"WG N=112 A CP16 | B SW128, 1acc", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 1, 1, 0},
+        {"WG N=112 A CP16 | B SW128, 4 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 1, 1, 112},
+        {"WG N=112 A CP16 | B none, 4 copies", 256, 128, kLayoutNone, 0, 128, 256, kLayoutNone, 112, 512, 256, 1, 0, 1, 1, 112},
+        {"WG N=64 A CP16 | B SW128, 4 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 64, 512, 32, 1, 0, 1, 1, 64},
+        {"WG N=128 A CP16 | B SW128, 3 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 128, 512, 32, 1, 0, 1, 1, 128},
+        {"WG N=224 A CP16 | B SW128, 2 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 224, 512, 32, 1, 0, 1, 1, 224},
+        {"WG N=112 2 groups (A+1024) 2 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 2, 1024, 1, 1, 224},
+        {"SMALLN carry N=64 1acc unrolled D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 1, 1, 16},
+        {"SMALLN carry N=64 1acc unrolled same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 1, 1, 0},
         {"SMALLN N=128 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 0},
         {"SMALLN N=128 D+128", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 128},
         {"SMALLN N=256 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512, 8192, 1, 0, 1, 1, 0},
