@@ -37,7 +37,7 @@ constexpr int kMaxStages = 4;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kLoaderThreads = 128;  // v3: warps 2, 3, 6, 7 stream X into the ring
 constexpr int kW2MaxStages = 6;
-constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage
+constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage (the default cap)
 constexpr uint32_t kW2SmemBudget = 222 * 1024;  // v3 ring + stages (227 KB max per CTA, minus static + alignment)  // v3: warps 4-7 load X before running the epilogue
 
 struct WPlan {
@@ -407,7 +407,14 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         return v >= 3 && v <= kW2MaxStages ? v : kW2MaxStages;
     }();
     bool ok = false;
-    for (int ks = kW2Ks; ks >= 1 && !ok; --ks) {
+    // narrow plans (one tap group per CTA) take 32-K-step stages: half the per-stage overhead (barrier
+    // waits, commits, ring bookkeeping) and fewer re-loaded dY history boxes per new column
+    static const int ks_env = [] {  // C1D_W2_KS: dev override of the K-steps per stage
+        const char* e = getenv("C1D_W2_KS");
+        return e ? atoi(e) : 0;
+    }();
+    const int ks_max = ks_env > 0 ? std::min(ks_env, 32) : (p.gpc == 1 && p.p > 1 ? 32 : kW2Ks);
+    for (int ks = ks_max; ks >= 1 && !ok; --ks) {
         if (p.p == 1) p.bq = (16 * ks) % 64 == 0 ? 64 : ((16 * ks) % 32 == 0 ? 32 : 16);
         const int ks_unit = std::max(1, p.bq / 16);  // K-steps per dY box
         if (ks % ks_unit || (2 * ks * p.ph) % 4) continue;
@@ -456,10 +463,34 @@ struct W2Params {
 struct W2Issue {
     uint32_t idesc, a_ks, a_g, b_k, b_box, copy_stride, cmask;
     int per_box, n, copies;
+    uint32_t b_off[9];  // B descriptor offset (16-B units) of K-step ks of an 8-step block (8: the next block)
 };
 template <int G>
 __device__ __forceinline__ void w2_issue_stage(const W2Issue& w, uint32_t tmem, uint64_t a, uint64_t b, int k0,
                                                int nks, int g_count) {
+    if (G > 0 && nks % 8 == 0) {
+        // full stage, straight line: every K-step's descriptors come from the stage base with
+        // independent adds (no loop-carried chain), so the issuing thread keeps up with the
+        // tensor pipe; a rolled loop's dependent uniform-datapath chain cost ~90-130 cycles per
+        // K-step (tools/probe_mma_layouts.cu: STRAIGHT vs loop rows)
+#pragma unroll 1
+        for (int blk = 0; blk < nks; blk += 8) {
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+            const uint32_t kk = static_cast<uint32_t>(k0 + blk + ks);
+            const uint32_t d0 = tmem + (kk & w.cmask) * w.copy_stride;
+            const uint32_t acc = kk >= static_cast<uint32_t>(w.copies) ? 1u : 0u;
+            const uint64_t ak = a + static_cast<uint64_t>(static_cast<uint32_t>(ks) * w.a_ks);
+            const uint64_t bk = b + static_cast<uint64_t>(w.b_off[ks]);
+#pragma unroll
+            for (int g = 0; g < (G > 0 ? G : 1); ++g)
+                mma_bf16_ss(d0 + static_cast<uint32_t>(g * w.n), ak + static_cast<uint64_t>(g * w.a_g), bk, w.idesc, acc);
+        }
+        a += static_cast<uint64_t>(8u * w.a_ks);
+        b += static_cast<uint64_t>(w.b_off[8]);
+        }
+        return;
+    }
     int inbox = 0;
 #pragma unroll 1
     for (int ks = 0; ks < nks; ++ks) {
@@ -614,7 +645,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // plain core-matrix layout with K-chunks one box apart.
         const uint32_t b_sbo = pl.bq == 8 ? 128u : 16u * static_cast<uint32_t>(pl.bq);
         const uint32_t b_lbo = pl.bq == 8 ? pl.box_bytes : 16u;
-        long long tf_sum = 0;
+        long long tf_sum = 0, ti_sum = 0, tc_sum = 0;
         const long long tb = clock64();
         int stage = 0;
         uint32_t phase = 0;
@@ -637,6 +668,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         wi.cmask = static_cast<uint32_t>(pl.copies - 1);
         wi.n = pl.n;
         wi.copies = pl.copies;
+#pragma unroll
+        for (int ks = 0; ks < 9; ++ks)
+            wi.b_off[ks] = static_cast<uint32_t>(ks / wi.per_box) * (wi.b_box + static_cast<uint32_t>(wi.per_box - 1) * wi.b_k) +
+                           static_cast<uint32_t>(ks % wi.per_box) * wi.b_k;
         int kdone = 0;  // K-steps issued so far (accumulator copy rotation)
         // ring bookkeeping mirrors the loaders': a segment (item) starts a fresh window of
         // span + kch chunks at v_pos; each later stage appends kch chunks and the window start
@@ -670,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t by0 = make_smem_desc(smem_u32(sbase), b_lbo, b_sbo, pl.swz);
                 // One elected lane issues the whole stage. The ring mirror keeps every address of
                 // the stage wrap-free, so a full stage is a straight-line run of MMAs.
+                const long long ti = clock64();
                 if (elect_one()) {
                     const uint64_t a_st = desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
                     switch (g_count) {
@@ -682,8 +718,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 kdone += nks;
                 __syncwarp();
+                const long long tc = clock64();
+                ti_sum += tc - ti;
                 if (elect_one()) mma_commit(smem_u32(&empty[stage]));
                 __syncwarp();
+                tc_sum += clock64() - tc;
                 if (++stage == pl.stages) {
                     stage = 0;
                     phase ^= 1;
@@ -695,6 +734,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         if (p.prof && lane == 0) {
             p.prof[blockIdx.x * 8 + 2] = tf_sum;
+            p.prof[blockIdx.x * 8 + 3] = ti_sum;
+            p.prof[blockIdx.x * 8 + 5] = tc_sum;
             p.prof[blockIdx.x * 8 + 4] = clock64() - tb;
         }
     }
@@ -1000,8 +1041,8 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         for (int bb = 0; bb < pl.grid; ++bb)
             for (int i2 = 0; i2 < 8; ++i2) acc[i2] += static_cast<double>(h[bb * 8 + i2]) / pl.grid;
         fprintf(stderr, "[tc_wgrad3 prof] T=%d P=%d N=%d gpc=%d roles=%d ks=%d stages=%d span=%d ring=%d nbox=%d copies=%d xb=%d | "
-                "producer wait_empty %.0f / total %.0f | mma wait_full %.0f total %.0f\n",
-                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.span, pl.ring, pl.nbox, pl.copies, pl.xb, acc[0], acc[1], acc[2], acc[4]);
+                "producer wait_empty %.0f / total %.0f | mma wait_full %.0f issue %.0f commit %.0f total %.0f\n",
+                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.span, pl.ring, pl.nbox, pl.copies, pl.xb, acc[0], acc[1], acc[2], acc[3], acc[5], acc[4]);
         for (int r = 0; r < pl.roles; ++r) {
             unsigned long long mx = 0, wf = 0;
             for (int bb = pl.role_cta_begin[r]; bb < pl.role_cta_begin[r + 1]; ++bb) {

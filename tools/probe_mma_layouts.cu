@@ -95,7 +95,19 @@ __global__ void __launch_bounds__(128, 1) mma_probe(Cfg c, int ksteps, long long
         const uint32_t tb = tmem_s;  // register copy: a shared load between MMAs waits for them
         const long long t0 = clock64();
         uint32_t ao = 0, bo = 0;
-        if (c.unroll) {
+        if (c.unroll == 2) {
+            // straight line: 8 MMAs per iteration, descriptors from running adds, D cycles over
+            // 4 accumulators d_step apart
+            for (int k = 0; k < ksteps; k += 8) {
+                uint64_t a = a0, b = b0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    mma_bf16_ss(tb + static_cast<uint32_t>((u & 3) * c.d_step), a, b, idesc, 1u);
+                    a += static_cast<uint64_t>(c.a_step >> 4);
+                    b += static_cast<uint64_t>(c.b_step >> 4);
+                }
+            }
+        } else if (c.unroll) {
             const uint32_t dwrap = 512 - c.n;
             uint32_t dc = 0;
             for (int k = 0; k < ksteps; k += 8) {
@@ -203,6 +215,14 @@ int main() {
         {"WG N=112 2 groups (A+1024) 2 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 2, 1024, 1, 1, 224},
         {"SMALLN carry N=64 1acc unrolled D+16", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 1, 1, 16},
         {"SMALLN carry N=64 1acc unrolled same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 1, 1, 0},
+        {"STRAIGHT N=64 4 acc, A+256 B same", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 2, 1, 64},
+        {"STRAIGHT N=64 4 acc, A+256 B+2048", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 2048, 1, 0, 2, 1, 64},
+        {"STRAIGHT N=64 same D, A+256 B same", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 64, 256, 0, 1, 0, 2, 1, 0},
+        {"STRAIGHT N=16 4 acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 16, 256, 0, 1, 0, 2, 1, 16},
+        {"STRAIGHT N=128 4 acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 256, 0, 1, 0, 2, 1, 128},
+        {"STRAIGHT N=256 2 acc", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 256, 0, 1, 0, 2, 1, 0},
+        {"STRAIGHT WG N=112 4 copies", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 2, 1, 112},
+        {"STRAIGHT WG N=112 same D", 256, 128, kLayoutNone, 0, 16, 1024, kLayoutSw128, 112, 512, 32, 1, 0, 2, 1, 0},
         {"SMALLN N=128 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 0},
         {"SMALLN N=128 D+128", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 128, 512, 8192, 1, 0, 1, 1, 128},
         {"SMALLN N=256 same D", 128, 16, kLayoutNone, 1, 128, 256, kLayoutNone, 256, 512, 8192, 1, 0, 1, 1, 0},
@@ -226,7 +246,7 @@ int main() {
       for (int bg = 0; bg < 3; ++bg) {
         if (bg && !c.unroll) continue;
         if (only && !strstr(c.name, only)) continue;
-        if (only && bg) continue;
+        if (only && bg && !getenv("PROBE_BG")) continue;
         for (int grid : {148}) {
             mma_probe<<<grid, 128, 161 * 1024>>>(c, ksteps, cyc, bg, gsrc, nullptr);
             CK(cudaDeviceSynchronize());
