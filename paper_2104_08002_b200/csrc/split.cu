@@ -21,21 +21,53 @@
 namespace c1d {
 
 // in: [N][C][W] fp32 -> out: [N][R*C][W] bf16 bits, channel block b of `pattern` (bit b: 0 = hi,
-// 1 = lo) for b < R.
+// 1 = lo) for b < R. One row (item, channel) per blockIdx.y step; each thread splits 8 consecutive
+// columns and writes them as one 16-B store per block when wp is a multiple of 8 (output rows then
+// 16-B aligned); rows whose input start is 16-B aligned read two float4s.
 __global__ void split_channels_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n,
                                       int64_t c, int64_t w, int reps, unsigned pattern, int64_t wp,
                                       int64_t in_item) {
-    const int64_t total = n * c * wp;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t x = e % wp;
-        const int64_t ch = (e / wp) % c;
-        const int64_t item = e / (wp * c);
-        const float v = x < w ? in[item * in_item + ch * w + x] : 0.0f;  // pitch padding: zeros
-        const uint16_t hi = fp32_to_bf16_bits(v);
-        const uint16_t lo = fp32_to_bf16_bits(v - bf16_bits_to_fp32(hi));
-        for (int r = 0; r < reps; ++r) {
-            const uint16_t val = ((pattern >> r) & 1u) ? lo : hi;
-            out[((item * reps + r) * c + ch) * wp + x] = val;
+    for (int64_t row = blockIdx.y; row < n * c; row += gridDim.y) {
+        const int64_t item = row / c, ch = row - item * c;
+        const float* src = in + item * in_item + ch * w;
+        const bool vec = ((reinterpret_cast<uintptr_t>(src) & 15u) == 0);
+        const bool vout = (wp % 8) == 0 && (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
+        for (int64_t x0 = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * 8; x0 < wp;
+             x0 += static_cast<int64_t>(gridDim.x) * blockDim.x * 8) {
+            float v[8];
+            if (vec && x0 + 8 <= w) {
+                const float4 a = __ldg(reinterpret_cast<const float4*>(src + x0));
+                const float4 b = __ldg(reinterpret_cast<const float4*>(src + x0 + 4));
+                v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+                v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = x0 + j < w ? __ldg(src + x0 + j) : 0.0f;  // pitch padding: zeros
+            }
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint16_t h[2], l[2];
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    h[e] = fp32_to_bf16_bits(v[2 * j + e]);
+                    l[e] = fp32_to_bf16_bits(v[2 * j + e] - bf16_bits_to_fp32(h[e]));
+                }
+                hi[j] = static_cast<uint32_t>(h[0]) | (static_cast<uint32_t>(h[1]) << 16);
+                lo[j] = static_cast<uint32_t>(l[0]) | (static_cast<uint32_t>(l[1]) << 16);
+            }
+            for (int r = 0; r < reps; ++r) {
+                const bool is_lo = (pattern >> r) & 1u;
+                uint16_t* dst = out + ((item * reps + r) * c + ch) * wp + x0;
+                if (vout) {
+                    *reinterpret_cast<uint4*>(dst) =
+                        is_lo ? make_uint4(lo[0], lo[1], lo[2], lo[3]) : make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                } else {  // unpadded odd-width rows: element stores
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        if (x0 + j < wp) dst[j] = static_cast<uint16_t>((is_lo ? lo[j / 2] : hi[j / 2]) >> (16 * (j % 2)));
+                }
+            }
         }
     }
 }
@@ -89,7 +121,10 @@ cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int
                                   unsigned pattern, cudaStream_t stream, int64_t w_pitch, int64_t in_item_stride) {
     const int64_t wp = w_pitch > 0 ? w_pitch : w;
     const int64_t si = in_item_stride > 0 ? in_item_stride : c * w;
-    split_channels_kernel<<<blocks_for(n * c * wp), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp, si);
+    const int64_t rows = n * c;
+    const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(wp, 8 * 256), 64)));
+    const unsigned gy = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(rows, 65535)));
+    split_channels_kernel<<<dim3(gx, gy), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp, si);
     note_launch();
     return cudaGetLastError();
 }
