@@ -166,7 +166,14 @@ def _weights_kcs(w, p: ConvParams, want: WeightLayout) -> torch.Tensor:
         if (w.c, w.k, w.s) != (p.channels, p.filters, p.taps):
             raise ShapeMismatch(f"packed weights are S={w.s} K={w.k} C={w.c}, conv params say "
                                 f"S={p.taps} K={p.filters} C={p.channels}")
-        w = unpack_weights(w)
+        # the natural KCS copy is cached on the PackedWeights object and rebuilt whenever its data
+        # tensor is replaced or modified in place (torch bumps the tensor's version counter)
+        key = (w.data.data_ptr(), w.data._version, w.data.device)
+        cached = w.__dict__.get("_kcs")
+        if cached is None or cached[0] != key:
+            cached = (key, _dev_f32(unpack_weights(w)))
+            w.__dict__["_kcs"] = cached
+        w = cached[1]
     if tuple(w.shape) != (p.filters, p.channels, p.taps):
         raise ShapeMismatch(f"weights are {tuple(w.shape)}, conv params say K={p.filters} C={p.channels} S={p.taps}")
     return _dev_f32(w)
