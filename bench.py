@@ -202,10 +202,15 @@ def main_arm(args):
         if st != 0:
             raise RuntimeError(f"c1d error {st}: {lib.c1d_last_error_message().decode()}")
 
-    def step_device():
-        chk(lib.c1d_forward(C.byref(desc), x.data_ptr(), w.data_ptr(), y.data_ptr(), None, 0, sp))
-        chk(lib.c1d_backward_data(C.byref(desc), dy.data_ptr(), w.data_ptr(), dx.data_ptr(), None, 0, sp))
-        chk(lib.c1d_backward_weight(C.byref(desc), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), None, 0, sp))
+    def step_device(mark=None):
+        # mark: (pass name, event pair) bracketing that pass inside the timed region
+        for name, fn in pass_fns.items():
+            if mark is not None and mark[0] == name:
+                mark[1].record(stream)
+                fn()
+                mark[2].record(stream)
+            else:
+                fn()
         if world > 1:
             dist.all_reduce(dw)
 
@@ -220,7 +225,7 @@ def main_arm(args):
     for _ in range(max(args.warmup, 3)):
         step_device()
     torch.cuda.synchronize()
-    per_pass = {}
+    per_pass = {}  # each pass timed alone (3 launches, median): burst-clock numbers
     for name, fn in pass_fns.items():
         evs = []
         for _ in range(3):
@@ -242,13 +247,19 @@ def main_arm(args):
         dist.barrier()
     torch.cuda.synchronize()
     launches0 = lib.c1d_launch_count()
+    # the dominant pass (longest alone) is bracketed by events in every timed step: its average
+    # duration inside the long run is the roofline's achieved rate (sustained-clock conditions)
+    dom = max(per_pass, key=lambda kname: per_pass[kname]["ms"])
+    marks = [(dom, torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+             for _ in range(args.steps)]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    for _ in range(args.steps):
-        step_device()
+    for i in range(args.steps):
+        step_device(marks[i])
     e1.record(stream)
     torch.cuda.synchronize()
     launches = lib.c1d_launch_count() - launches0
+    dom_ms = sum(m[1].elapsed_time(m[2]) for m in marks) / len(marks)
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
@@ -298,17 +309,23 @@ def main_arm(args):
             peaks = json.load(f)
     except OSError:
         pass
-    dom = max(per_pass, key=lambda kname: per_pass[kname]["ms"])
-    peak = peaks.get("bf16_tflops", 1590.0)
+    # a kernel timed inside a long step: the sustained bf16 peak is the denominator
+    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 1590.0))
+    peak_burst = peaks.get("bf16_tflops", 1590.0)
+    dom_tflops = flops_per_pass() / (dom_ms * 1e-3) / 1e12
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             traffic = json.load(f).get(dom)
     except (OSError, ValueError):
         pass
-    roofline = {"bound": "tensor", "kernel": dom, "achieved": per_pass[dom]["tflops"], "peak": peak,
-                "unit": "TFLOP/s", "frac": per_pass[dom]["tflops"] / peak, "traffic": traffic,
-                "peak_source": "MEASURED_PEAKS.json bf16_tflops (burst; kernel timed alone)" if peaks
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": dom_tflops, "peak": peak,
+                "unit": "TFLOP/s", "frac": dom_tflops / peak, "traffic": traffic,
+                "avg_launch_ms": dom_ms, "launches_timed": len(marks),
+                "alone": {"achieved": per_pass[dom]["tflops"], "peak_burst": peak_burst,
+                          "frac": per_pass[dom]["tflops"] / peak_burst},
+                "peak_source": ("MEASURED_PEAKS.json bf16_tflops_sustained (kernel timed inside the long timed "
+                                "region); 'alone' = the same kernel timed alone vs the burst peak") if peaks
                 else "fallback 1590 TFLOP/s (B200_PROFILING.md)"}
 
     # ---- CPU baseline (rank 0, N=1 only): reference on a bounded sample
@@ -333,7 +350,7 @@ def main_arm(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) x/dy, Kaiming-uniform w)",
             "config": config_block({"parallelism": f"dp{world}" + (" (NCCL all-reduce of dW)" if world > 1 else "")}),
             "passes": per_pass,
-            "frac_of_peak_step": value / world / peak,
+            "frac_of_peak_step": value / world / peak,  # vs the sustained peak
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
