@@ -891,7 +891,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         cp_async_wait_group<0>();
     }
     if (warp >= 4) {
-        // ---- epilogue: D rows (t, c) x columns (p', k) -> partial[cta][k][c][tap]
+        // ---- epilogue: D rows (t, c) x columns (p', k) -> partial[cta][k][tap][c] (c fastest: a
+        // warp's 32 lanes are consecutive channels, so every store is coalesced)
         const int quarter = warp - 4;
         const int row = quarter * 32 + lane;
         const int t = row / pl.cp, c = row % pl.cp;
@@ -929,7 +930,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int col = cb + j;
                         const int pp = col / pl.kpw, kk = col % pl.kpw;
                         const int64_t tap = sgrp + static_cast<int64_t>(pl.t) * (pl.p - 1 - pp);
-                        if (kk < p.k && tap < p.s) dst[(static_cast<int64_t>(kk) * p.c + c) * p.s + tap] = __uint_as_float(v[j]);
+                        if (kk < p.k && tap < p.s) dst[(static_cast<int64_t>(kk) * p.s + tap) * p.c + c] = __uint_as_float(v[j]);
                     }
                 }
             }
@@ -941,9 +942,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
 }
 
-// dw[e] = sum over the role's CTAs (ascending) of part[cta][e]. A block covers 64 outputs x 4
-// CTA quarters: each thread sums its quarter of the CTAs in order (all loads in flight), then the
-// four quarter sums are added in order (fixed shape, deterministic).
+// dw = sum over the role's CTAs (ascending) of part[cta][e], e = (k*S + s)*C + c in the partials'
+// (k, tap, channel) order (coalesced reads); the sum lands at dw[(k*C + c)*S + s] (KCS). A block
+// covers 64 outputs x 4 CTA quarters: each thread sums its quarter of the CTAs in order (all loads
+// in flight), then the four quarter sums are added in order (fixed shape, deterministic).
 __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
                                                             int64_t K, int64_t C, int64_t S, const W2Plan pl) {
     __shared__ float red[4][64];
@@ -954,7 +956,7 @@ __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restr
     const int quarter = threadIdx.x / 64;
     float v = 0.0f;
     if (e < count) {
-        const int64_t s = e % S;
+        const int64_t s = (e / C) % S;
         const int role = static_cast<int>(s / (static_cast<int64_t>(pl.gpc) * pl.taps_per_group));
         const int b0 = pl.role_cta_begin[role], b1 = pl.role_cta_begin[role + 1];
         const int n = b1 - b0;
@@ -968,7 +970,10 @@ __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restr
     }
     red[quarter][threadIdx.x % 64] = v;
     __syncthreads();
-    if (threadIdx.x < 64 && e < count) dw[e] = ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+    if (threadIdx.x < 64 && e < count) {
+        const int64_t c = e % C, s = (e / C) % S, k = e / (C * S);
+        dw[(k * C + c) * S + s] = ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
+    }
 }
 
 }  // namespace
