@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp >= 4) {
-        // epilogue: D rows (t, c) x columns (g, k) -> partial[role-split][k][c][tap]
+        // epilogue: D rows (t, c) x columns (g, k) -> partial[role-split][k][tap][c] (channel-fastest:
+        // coalesced stores)
         if (g_count > 0) {
             const int quarter = warp - 4;
             const int row = quarter * 32 + lane;
@@ -274,7 +275,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
                             const int64_t kk = kb2 + j;
-                            if (kk < p.k) dst[(kk * p.c + c) * p.s + tap] = __uint_as_float(v[j]);
+                            if (kk < p.k) dst[(kk * p.s + tap) * p.c + c] = __uint_as_float(v[j]);
                         }
                     }
                 }
@@ -287,17 +288,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
 }
 
-// dw[k][c][s] = sum over the splits of the role owning tap s, in ascending split order.
+// dw[k][c][s] = sum over the splits of the role owning tap s, in ascending split order; e walks the
+// partials' (k, tap, channel) order (coalesced reads).
 __global__ void wgrad_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw, int64_t K, int64_t C,
                                     int64_t S, int t, int gmax, int splits) {
     const int64_t count = K * C * S;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = e % S;
+        const int64_t c = e % C, s = (e / C) % S, k = e / (C * S);
         const int role = static_cast<int>(s / (static_cast<int64_t>(gmax) * t));
         const float* src = part + static_cast<int64_t>(role) * splits * count + e;
         float v = 0.0f;
         for (int sp = 0; sp < splits; ++sp) v += src[static_cast<int64_t>(sp) * count];
-        dw[e] = v;
+        dw[(k * C + c) * S + s] = v;
     }
 }
 
