@@ -1228,6 +1228,16 @@ c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const f
         lg.bias_grad = glue->bias_grad;
         return conv_pass(desc, C1D_PASS_BACKWARD_DATA, dy, w_kcs, nullptr, conv_ws, gs.conv, stream, &lg);
     }
+    if (d.s == 1 && d.precision == C1D_PRECISION_FP32 && d.in_dtype == C1D_DTYPE_F32 && algo == C1D_ALGO_DIRECT &&
+        d.k <= 16 && glue->off == 0 && glue->q == q && d.w_in == q) {
+        // 1-tap FP32 backward-data (the network's heads): the glue pass computes the few-filter
+        // sum itself, in the pointwise kernel's order, instead of reading an FP32 dx scratch tensor
+        const cudaError_t e = launch_layer_bwd_prologue(nullptr, q, 0, glue->gadd, nullptr, nullptr, glue->mask, d.n, d.c,
+                                                        q, glue->mask != nullptr, glue->gsum, glue->grad_pre,
+                                                        glue->grad_pre_bf16, glue->bias_grad, part, stream,
+                                                        static_cast<const float*>(dy), w_kcs, static_cast<int>(d.k));
+        return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_backward_prologue (1-tap)");
+    }
     float* dx = bump.take<float>(gs.scratch);
     st = conv_pass(desc, C1D_PASS_BACKWARD_DATA, dy, w_kcs, dx, conv_ws, gs.conv, stream);
     if (st != C1D_OK) return st;

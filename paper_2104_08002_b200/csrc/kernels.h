@@ -57,7 +57,8 @@ cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t g
                                       const float* pre, const float* pre_bias, const uint32_t* mask, int64_t n,
                                       int64_t k, int64_t q, int relu, float* gsum,
                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
-                                      cudaStream_t stream);
+                                      cudaStream_t stream, const float* pw_dy = nullptr,
+                                      const float* pw_w = nullptr, int pw_k = 0);
 // bias_grad[c] = fixed-order sum of part[(i*k + c)*nbx + b] over items i < n and blocks b < nbx
 cudaError_t launch_bias_grad_reduce(const float* part, float* bias_grad, int64_t n, int64_t k, int64_t nbx,
                                     cudaStream_t stream);

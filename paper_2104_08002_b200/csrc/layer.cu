@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
     const float* __restrict__ gin, int64_t gin_w, int64_t gin_off, const float* __restrict__ gadd,
     const float* __restrict__ pre, const float* __restrict__ pre_bias, const uint32_t* __restrict__ mask, int64_t k,
     int64_t q, int relu, float* __restrict__ gsum, float* __restrict__ grad_pre,
-    uint16_t* __restrict__ grad_pre_bf16, float* __restrict__ part, bool vec) {
+    uint16_t* __restrict__ grad_pre_bf16, float* __restrict__ part, bool vec, const float* __restrict__ pw_dy,
+    const float* __restrict__ pw_w, int pw_k) {
     __shared__ float red[kEltThreads / 32];
     const int64_t row = blockIdx.y;
     const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
@@ -117,7 +118,42 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
         const bool v4 = vec && cnt == kEltPerThread;
         const float* gi = gin + row * gin_w + gin_off + x0;
         float g[4], ad[4] = {0.f, 0.f, 0.f, 0.f}, pr[4] = {1.f, 1.f, 1.f, 1.f};
-        if (v4) {
+        if (pw_dy) {
+            // gin = the 1-tap backward-data of pw_k filters computed here (the FP32 pointwise
+            // conv's order: fmaf over the filters from 0), instead of read from a scratch tensor
+            const int64_t item = row / k, ch = row % k;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) g[j] = 0.0f;
+            for (int f = 0; f < pw_k; ++f) {
+                const float wv = __ldg(pw_w + f * k + ch);
+                const float* src = pw_dy + (item * pw_k + f) * q + x0;
+                float dv[4];
+                if (v4) {  // q % 4 == 0 and 16-B aligned rows (launcher's vec flag)
+                    const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+                    dv[0] = t.x, dv[1] = t.y, dv[2] = t.z, dv[3] = t.w;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dv[j] = j < cnt ? __ldg(src + j) : 0.0f;
+                }
+#pragma unroll
+                for (int j = 0; j < 4; ++j) g[j] = fmaf(wv, dv[j], g[j]);
+            }
+            if (v4) {
+                if (gadd) {
+                    const float4 t = *reinterpret_cast<const float4*>(gadd + row * q + x0);
+                    ad[0] = t.x, ad[1] = t.y, ad[2] = t.z, ad[3] = t.w;
+                }
+                if (relu && !mask) {
+                    const float4 t = *reinterpret_cast<const float4*>(pre + row * q + x0);
+                    pr[0] = t.x, pr[1] = t.y, pr[2] = t.z, pr[3] = t.w;
+                }
+            } else {
+                if (gadd)
+                    for (int j = 0; j < cnt; ++j) ad[j] = gadd[row * q + x0 + j];
+                if (relu && !mask)
+                    for (int j = 0; j < cnt; ++j) pr[j] = pre[row * q + x0 + j];
+            }
+        } else if (v4) {
             const float4 t = *reinterpret_cast<const float4*>(gi);
             g[0] = t.x, g[1] = t.y, g[2] = t.z, g[3] = t.w;
             if (gadd) {
@@ -224,18 +260,18 @@ cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t g
                                       const float* pre, const float* pre_bias, const uint32_t* mask, int64_t n,
                                       int64_t k, int64_t q, int relu, float* gsum,
                                       float* grad_pre, uint16_t* grad_pre_bf16, float* bias_grad, float* part,
-                                      cudaStream_t stream) {
+                                      cudaStream_t stream, const float* pw_dy, const float* pw_w, int pw_k) {
     if (n * k == 0 || q == 0) return cudaSuccess;
     if (n * k > 65535) return cudaErrorInvalidValue;
-    const bool vec = (q % 4 == 0) && (gin_w % 4 == 0) && (gin_off % 4 == 0) && aligned16(gin) &&
+    const bool vec = (q % 4 == 0) && (gin_w % 4 == 0) && (gin_off % 4 == 0) && (pw_dy ? aligned16(pw_dy) : aligned16(gin)) &&
                      (!gadd || aligned16(gadd)) && (!pre || aligned16(pre)) && (!gsum || aligned16(gsum)) &&
                      (!grad_pre || aligned16(grad_pre)) &&
                      (!grad_pre_bf16 || (reinterpret_cast<uintptr_t>(grad_pre_bf16) & 7u) == 0);
     const int64_t nbx = layer_bias_blocks(q);
     const dim3 grid(static_cast<unsigned>(nbx), static_cast<unsigned>(n * k));
     bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, pre_bias, mask, k, q, relu, gsum,
-                                                          grad_pre,
-                                                          grad_pre_bf16, bias_grad ? part : nullptr, vec);
+                                                          grad_pre, grad_pre_bf16, bias_grad ? part : nullptr, vec,
+                                                          pw_dy, pw_w, pw_k);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || !bias_grad) return e;

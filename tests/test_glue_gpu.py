@@ -47,6 +47,7 @@ CASES = [
     (96, 40, 17, 4, cv.Precision.Bf16, False, None),    # expanded rows (fused forward, 96-wide backward)
     (40, 100, 9, 8, cv.Precision.Bf16, True, None),     # carry mode, two filter groups under glue
     (128, 128, 9, 1, cv.Precision.Bf16, True, None),    # 128-wide expanded rows: conv + glue pass
+    (15, 2, 1, 1, cv.Precision.Fp32, False, False),     # config-5 heads: 1-tap FP32 (backward glue computes dx)
 ]
 
 
