@@ -75,12 +75,23 @@ typedef enum c1d_algo {
     C1D_ALGO_DIRECT = 1,  /* CUDA-core FFMA direct convolution, any shape */
     C1D_ALGO_TCGEN05 = 2, /* tcgen05.mma BF16 tensor-core kernels (TMEM accumulators) */
     C1D_ALGO_BF16X3 = 3   /* FP32 precision on the tcgen05 kernels: operands split into bf16 hi+lo
-                             parts (3 partial products per term, FP32 accumulation in TMEM) */
+                             parts, v = hi + lo; the hi*hi, hi*lo, lo*hi and lo*lo partial
+                             products accumulate in FP32 in TMEM (4 BF16 products per term) */
 } c1d_algo;
 
 typedef enum c1d_pass { C1D_PASS_FORWARD = 0, C1D_PASS_BACKWARD_DATA = 1, C1D_PASS_BACKWARD_WEIGHT = 2 } c1d_pass;
 
 #define C1D_FLAG_STRICT_BF16_DIMS 0x1u
+/* Accumulation accuracy. The tensor cores accumulate FP32 into TMEM with a consistent shrink toward
+ * zero of ~1.2e-9 (norm-relative) per accumulated product, so one accumulator over a long reduction
+ * drifts: BASELINE config 3 backward-weight sums 1.92M products per dW entry, and a single chain per
+ * CTA (52k products) lands at ~6e-5 from the FP32-on-rounded result, inside the reference's BF16
+ * bound (1e-2, acceptance.cpp:526) but not its FP32 one (1e-5). With this flag every chain is capped
+ * at ~4096 products (backward-weight restarts its accumulators and sums the segments in a fixed
+ * order; conv-shaped passes with C_in*S > 4096 split their channels over two TMEM regions): ~4e-6
+ * at config 3, at some cost in time (config-3 backward-weight ~+45%). FP32 precision always runs
+ * this way. */
+#define C1D_FLAG_EXACT_ACCUM 0x2u
 
 /* Mirrors conv1d::ConvParams (conv.hpp:18-25) plus the tensor sizes the reference reads from
  * its Tensor3D arguments. */
@@ -110,8 +121,15 @@ C1D_EXPORT int64_t c1d_conv_flops(const c1d_desc* desc);
 
 /* Device workspace bytes the pass needs (0 if none). Passing workspace == NULL to a pass makes
  * the library use an internal, lazily grown buffer per (device, stream) instead: calls on different
- * streams never share it; growing it synchronises that stream. */
+ * streams never share it. An outgrown buffer is retired, never freed behind the caller's back
+ * (CUDA graphs captured on that stream keep its address), and growing never synchronises, so it
+ * is legal under stream capture. c1d_release_workspace frees them. */
 C1D_EXPORT c1d_status c1d_workspace_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes);
+
+/* Frees the internal workspace buffers (current and retired) of `stream` on the current device,
+ * after synchronising the stream. Call it when a stream is destroyed, and only once no captured
+ * CUDA graph that used the stream's internal workspace will be replayed again. */
+C1D_EXPORT c1d_status c1d_release_workspace(c1d_stream_t stream);
 
 /* Which kernel family the pass will run for this desc (resolves C1D_ALGO_AUTO). */
 C1D_EXPORT c1d_status c1d_selected_algo(const c1d_desc* desc, c1d_pass pass, c1d_algo* algo);
@@ -209,6 +227,29 @@ C1D_EXPORT c1d_status c1d_forward_glued(const c1d_desc* desc, const void* x, con
 C1D_EXPORT c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const float* w_kcs,
                                               const c1d_bwd_glue* glue, void* workspace, size_t workspace_bytes,
                                               c1d_stream_t stream);
+/* ---- The training step around the conv layers (BASELINE config 5) ----
+ * Seeded input samplers (new: the reference's Rng has none). Element i draws from its own
+ * splitmix64 stream (state = mix64(seed ^ mix64(i + golden)), uniform = (next >> 11) * 2^-53), so
+ * the values do not depend on the launch shape or on how a batch is split:
+ *   Poisson(lambda): Knuth's product of uniforms, the smallest k with u_0*...*u_k <= exp(-lambda)
+ *   Bernoulli(p):    1 if u < p else 0                                                     */
+C1D_EXPORT c1d_status c1d_fill_poisson(float* out, int64_t count, double lambda, uint64_t seed, c1d_stream_t stream);
+C1D_EXPORT c1d_status c1d_fill_bernoulli(float* out, int64_t count, double p, uint64_t seed, c1d_stream_t stream);
+/* mse_loss + bce_with_logits (train.cpp:106-135) in one pass over n items x width columns:
+ *   pred(i, x) = pred[i*in_stride + x], logits likewise; target / labels contiguous (n, width)
+ *   loss3[0] = mean((pred - target)^2), loss3[1] = mean(softplus(l) - m*l) (stable form),
+ *   loss3[2] = loss3[0] + bce_weight * loss3[1]      (double, on the device; deterministic)
+ *   grad_pred(i, x)   = float(2*(pred - target)/count)                 (optional)
+ *   grad_logits(i, x) = bce_weight * float((sigmoid(l) - m)/count)    (optional; stride grad_stride)
+ * workspace: c1d_loss_workspace_size() bytes, not shared by concurrent calls. */
+C1D_EXPORT size_t c1d_loss_workspace_size(void);
+C1D_EXPORT c1d_status c1d_mse_bce_loss(const float* pred, const float* logits, int64_t in_stride, const float* target,
+                                       const float* labels, int64_t n, int64_t width, float bce_weight,
+                                       float* grad_pred, float* grad_logits, int64_t grad_stride, double* loss3,
+                                       void* workspace, size_t workspace_bytes, c1d_stream_t stream);
+/* params[i] -= lr * grads[i] in float (sgd_step, train.cpp:137-141); lr must be positive. */
+C1D_EXPORT c1d_status c1d_sgd_update(float* params, const float* grads, int64_t count, float lr, c1d_stream_t stream);
+
 /* Number of kernels this library has launched since load (instrumentation for benchmarks). */
 C1D_EXPORT uint64_t c1d_launch_count(void);
 

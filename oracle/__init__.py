@@ -364,3 +364,132 @@ class Ref:
             raise ValueError(kind)
         finally:
             self.lib.ref_rng_free(r)
+
+
+class RefNet:
+    """The reference's DemoNet (proj/src/train.cpp:257-353) through oracle/_ref: the network the
+    GPU ResidualNet(convs_per_block=1) is pinned to. TEST INFRASTRUCTURE ONLY."""
+
+    def __init__(self, blocks: int, hidden: int, taps: int = 51, dilation: int = 8, precision: int = 0,
+                 seed: int = 1, ref: "Ref | None" = None):
+        self.ref = ref or Ref()
+        L = self.ref.lib
+        L.ref_demonet_new.restype = C.c_void_p
+        L.ref_demonet_new.argtypes = [C.c_int, I64, I64, I64, C.c_int, C.c_uint64]
+        L.ref_demonet_free.argtypes = [C.c_void_p]
+        L.ref_demonet_layer_precision.argtypes = [C.c_void_p, C.c_int]
+        L.ref_demonet_param_count.restype = I64
+        L.ref_demonet_param_count.argtypes = [C.c_void_p]
+        L.ref_demonet_gather_params.argtypes = [C.c_void_p, _f32p]
+        L.ref_demonet_scatter_params.argtypes = [C.c_void_p, _f32p, I64]
+        L.ref_demonet_gather_grads.argtypes = [C.c_void_p, _f32p]
+        L.ref_demonet_forward.argtypes = [C.c_void_p, _f32p, I64, I64, C.c_int, _f32p, _f32p]
+        L.ref_demonet_train_step.argtypes = [C.c_void_p, _f32p, _f32p, _f32p, I64, I64, I64, C.c_float, C.c_int,
+                                             C.POINTER(C.c_double)]
+        L.ref_demonet_step.argtypes = [C.c_void_p, C.c_float]
+        self.L = L
+        self.blocks, self.taps, self.dilation = blocks, taps, dilation
+        self.h = L.ref_demonet_new(blocks, hidden, taps, dilation, precision, seed)
+        if not self.h:
+            raise RuntimeError("DemoNet construction failed")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_demonet_free(self.h)
+            self.h = None
+
+    def pad(self) -> int:
+        return self.dilation * (self.taps - 1) // 2
+
+    def layer_precisions(self) -> list[int]:
+        return [self.L.ref_demonet_layer_precision(self.h, i) for i in range(self.blocks + 3)]
+
+    def params(self) -> np.ndarray:
+        out = np.empty(self.L.ref_demonet_param_count(self.h), dtype=np.float32)
+        self.L.ref_demonet_gather_params(self.h, out)
+        return out
+
+    def set_params(self, flat) -> None:
+        flat = _f32(flat).reshape(-1)
+        if self.L.ref_demonet_scatter_params(self.h, flat, flat.size) != 0:
+            raise ValueError("scatter_params rejected the vector")
+
+    def grads(self) -> np.ndarray:
+        out = np.empty(self.L.ref_demonet_param_count(self.h), dtype=np.float32)
+        self.L.ref_demonet_gather_grads(self.h, out)
+        return out
+
+    def forward(self, x_padded, threads: int = 1):
+        x = _f32(x_padded)
+        n, _, wp = x.shape
+        width = wp - 2 * self.pad()
+        pred = np.empty((n, 1, width), dtype=np.float32)
+        logits = np.empty((n, 1, width), dtype=np.float32)
+        rc = self.L.ref_demonet_forward(self.h, x.reshape(-1), n, wp, threads, pred.reshape(-1), logits.reshape(-1))
+        if rc:
+            raise RuntimeError(f"DemoNet forward failed ({rc})")
+        return pred, logits
+
+    def train_step(self, x_padded, clean, mask, bce_weight: float = 1.0, threads: int = 1) -> float:
+        x, y, m = _f32(x_padded), _f32(clean), _f32(mask)
+        n, _, wp = x.shape
+        loss = C.c_double(0.0)
+        rc = self.L.ref_demonet_train_step(self.h, x.reshape(-1), y.reshape(-1), m.reshape(-1), n, wp, y.shape[2],
+                                           bce_weight, threads, C.byref(loss))
+        if rc:
+            raise RuntimeError(f"DemoNet train_step failed ({rc})")
+        return loss.value
+
+    def step(self, lr: float) -> None:
+        self.L.ref_demonet_step(self.h, lr)
+
+
+def ref_losses(ref: "Ref", pred, target, logits, labels):
+    """mse_loss / bce_with_logits of the reference (train.cpp:106-135): (mse, g_mse, bce, g_bce)."""
+    L = ref.lib
+    for name in ("ref_mse_loss", "ref_bce_with_logits"):
+        fn = getattr(L, name)
+        fn.restype = C.c_double
+        fn.argtypes = [_f32p, _f32p, I64, _f32p]
+    a, b, c, d = (_f32(v).reshape(-1) for v in (pred, target, logits, labels))
+    ga, gc = np.empty_like(a), np.empty_like(c)
+    mse = L.ref_mse_loss(a, b, a.size, ga)
+    bce = L.ref_bce_with_logits(c, d, c.size, gc)
+    return mse, ga, bce, gc
+
+
+def ref_auroc(ref: "Ref", scores, labels) -> float:
+    """auroc of the reference (train.cpp:143-171): rank statistic, ties averaged."""
+    L = ref.lib
+    L.ref_auroc.restype = C.c_double
+    L.ref_auroc.argtypes = [_f32p, _f32p, I64]
+    a, b = _f32(scores).reshape(-1), _f32(labels).reshape(-1)
+    return L.ref_auroc(a, b, a.size)
+
+
+def ref_synthetic_dataset(ref: "Ref", seed: int, count: int, width: int):
+    """generate_synthetic_dataset of the reference (train.cpp:62-98): (noisy, clean, mask)."""
+    L = ref.lib
+    L.ref_synthetic_dataset.argtypes = [C.c_uint64, I64, I64, _f32p, _f32p, _f32p]
+    out = [np.empty((count, 1, width), dtype=np.float32) for _ in range(3)]
+    rc = L.ref_synthetic_dataset(seed, count, width, *(o.reshape(-1) for o in out))
+    if rc:
+        raise RuntimeError(f"generate_synthetic_dataset failed ({rc})")
+    return tuple(out)
+
+
+def sample_poisson(count: int, lam: float, seed: int) -> np.ndarray:
+    """The device sampler's per-element splitmix64 Poisson draw (c1d_fill_poisson), restated."""
+    out = np.empty(count, dtype=np.float32)
+    _lib.orc_sample_poisson.argtypes = [_f32p, I64, C.c_double, C.c_uint64]
+    _lib.orc_sample_poisson(out, count, lam, seed)
+    return out
+
+
+def sample_bernoulli(count: int, p: float, seed: int) -> np.ndarray:
+    """The device sampler's Bernoulli draw (c1d_fill_bernoulli), restated."""
+    out = np.empty(count, dtype=np.float32)
+    _lib.orc_sample_bernoulli.argtypes = [_f32p, I64, C.c_double, C.c_uint64]
+    _lib.orc_sample_bernoulli(out, count, p, seed)
+    return out
+

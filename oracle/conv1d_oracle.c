@@ -106,6 +106,38 @@ void orc_fill_bernoulli(orc_rng* r, float* out, int64_t n, double p) {
     for (int64_t i = 0; i < n; ++i) out[i] = orc_rng_next_double(r) < p ? 1.0f : 0.0f;
 }
 
+/* Counter-based samplers of the device path (paper_2104_08002_b200/csrc/train.cu, c1d.h
+ * c1d_fill_poisson / c1d_fill_bernoulli), restated for bit-exact checks: element i owns the
+ * splitmix64 stream state = mix64(seed ^ mix64(i + golden)). New code, no reference counterpart. */
+static uint64_t orc_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+static double orc_splitmix_next(uint64_t* s) {
+    *s += 0x9E3779B97F4A7C15ull;
+    return (double)(orc_mix64(*s) >> 11) * 0x1.0p-53;
+}
+void orc_sample_poisson(float* out, int64_t n, double lambda, uint64_t seed) {
+    const double limit = exp(-lambda);
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t st = orc_mix64(seed ^ orc_mix64((uint64_t)i + 0x9E3779B97F4A7C15ull));
+        double prod = orc_splitmix_next(&st);
+        uint32_t k = 0;
+        while (prod > limit) {
+            ++k;
+            prod *= orc_splitmix_next(&st);
+        }
+        out[i] = (float)k;
+    }
+}
+void orc_sample_bernoulli(float* out, int64_t n, double p, uint64_t seed) {
+    for (int64_t i = 0; i < n; ++i) {
+        uint64_t st = orc_mix64(seed ^ orc_mix64((uint64_t)i + 0x9E3779B97F4A7C15ull));
+        out[i] = orc_splitmix_next(&st) < p ? 1.0f : 0.0f;
+    }
+}
+
 /* ---------------------------------------------------------------- bf16 (bf16.hpp:20-42) */
 uint16_t orc_fp32_to_bf16(float x) {
     uint32_t u;

@@ -10,6 +10,9 @@
 //   norm_rel_error                                                    proj/src/reference.cpp:151-162
 //   measure_kernel (the reference timing method)                      proj/src/bench.cpp:172-234
 //   Rng / fp32_to_bf16                                                proj/include/conv1d/{rng,bf16}.hpp
+//   DemoNet forward / backward / train_step, gather/scatter params    proj/src/train.cpp:257-353
+//   mse_loss / bce_with_logits / sgd_step / auroc                     proj/src/train.cpp:106-171
+//   generate_synthetic_dataset                                        proj/src/train.cpp:62-98
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -22,6 +25,7 @@
 #include "conv1d/reference.hpp"
 #include "conv1d/rng.hpp"
 #include "conv1d/tensor.hpp"
+#include "conv1d/train.hpp"
 
 using namespace conv1d;
 
@@ -189,6 +193,78 @@ int64_t ref_parse_csv_count(const char* path) {
     } catch (const std::exception&) {
         return -1;
     }
+}
+
+// ---- the reference network (train.cpp), for pinning the GPU network step ----
+void* ref_demonet_new(int blocks, int64_t hidden, int64_t taps, int64_t dilation, int precision, uint64_t seed) {
+    try {
+        return new DemoNet(blocks, hidden, taps, dilation, precision == 1 ? Precision::Bf16 : Precision::Fp32,
+                           seed);
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+void ref_demonet_free(void* h) { delete static_cast<DemoNet*>(h); }
+// precision actually used by layer i (make_layer's even-dims rule, train.cpp:233-239): 0 FP32, 1 BF16
+int ref_demonet_layer_precision(void* h, int i) {
+    auto layers = static_cast<DemoNet*>(h)->layers();
+    if (i < 0 || i >= static_cast<int>(layers.size())) return -1;
+    return layers[static_cast<size_t>(i)]->p.precision == Precision::Bf16 ? 1 : 0;
+}
+int64_t ref_demonet_param_count(void* h) { return static_cast<int64_t>(gather_params(*static_cast<DemoNet*>(h)).size()); }
+void ref_demonet_gather_params(void* h, float* out) {
+    const std::vector<float> v = gather_params(*static_cast<DemoNet*>(h));
+    std::memcpy(out, v.data(), sizeof(float) * v.size());
+}
+int ref_demonet_scatter_params(void* h, const float* in, int64_t count) {
+    return guarded([&] { scatter_params(*static_cast<DemoNet*>(h), {in, static_cast<size_t>(count)}); });
+}
+void ref_demonet_gather_grads(void* h, float* out) {
+    const std::vector<float> v = gather_grads(*static_cast<DemoNet*>(h));
+    std::memcpy(out, v.data(), sizeof(float) * v.size());
+}
+// forward only: pred and logits, each (n, 1, width_padded - 2*pad)
+int ref_demonet_forward(void* h, const float* x, int64_t n, int64_t w_padded, int threads, float* pred,
+                        float* logits) {
+    return guarded([&] {
+        const DemoNet::Output o = static_cast<DemoNet*>(h)->forward(make_tensor(x, n, 1, w_padded), threads);
+        std::memcpy(pred, o.pred.data.data(), sizeof(float) * o.pred.data.size());
+        std::memcpy(logits, o.logits.data.data(), sizeof(float) * o.logits.data.size());
+    });
+}
+// one train_step (forward, mse + bce_weight*bce, full backward; gradients left in the layers)
+int ref_demonet_train_step(void* h, const float* x, const float* clean, const float* mask, int64_t n,
+                           int64_t w_padded, int64_t width, float bce_weight, int threads, double* loss) {
+    return guarded([&] {
+        *loss = train_step(*static_cast<DemoNet*>(h), make_tensor(x, n, 1, w_padded), make_tensor(clean, n, 1, width),
+                           make_tensor(mask, n, 1, width), bce_weight, threads);
+    });
+}
+void ref_demonet_step(void* h, float lr) { static_cast<DemoNet*>(h)->step(lr); }
+
+double ref_mse_loss(const float* pred, const float* target, int64_t count, float* grad) {
+    const LossResult r = mse_loss({pred, static_cast<size_t>(count)}, {target, static_cast<size_t>(count)});
+    std::memcpy(grad, r.grad.data(), sizeof(float) * r.grad.size());
+    return r.value;
+}
+double ref_bce_with_logits(const float* logits, const float* mask, int64_t count, float* grad) {
+    const LossResult r = bce_with_logits({logits, static_cast<size_t>(count)}, {mask, static_cast<size_t>(count)});
+    std::memcpy(grad, r.grad.data(), sizeof(float) * r.grad.size());
+    return r.value;
+}
+void ref_sgd_step(float* params, const float* grads, int64_t count, float lr) {
+    sgd_step({params, static_cast<size_t>(count)}, {grads, static_cast<size_t>(count)}, lr);
+}
+double ref_auroc(const float* scores, const float* labels, int64_t count) {
+    return auroc({scores, static_cast<size_t>(count)}, {labels, static_cast<size_t>(count)});
+}
+int ref_synthetic_dataset(uint64_t seed, int64_t count, int64_t width, float* noisy, float* clean, float* mask) {
+    return guarded([&] {
+        const SyntheticDataset ds = generate_synthetic_dataset(seed, count, width);
+        std::memcpy(noisy, ds.noisy.data.data(), sizeof(float) * ds.noisy.data.size());
+        std::memcpy(clean, ds.clean.data.data(), sizeof(float) * ds.clean.data.size());
+        std::memcpy(mask, ds.mask.data.data(), sizeof(float) * ds.mask.data.size());
+    });
 }
 
 }  // extern "C"

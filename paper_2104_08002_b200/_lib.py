@@ -18,6 +18,7 @@ PASS_FORWARD, PASS_BACKWARD_DATA, PASS_BACKWARD_WEIGHT = 0, 1, 2
 ALGO_AUTO, ALGO_DIRECT, ALGO_TCGEN05, ALGO_BF16X3 = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16 = 0, 1
 FLAG_STRICT_BF16_DIMS = 0x1
+FLAG_EXACT_ACCUM = 0x2
 
 
 class Desc(C.Structure):
@@ -111,6 +112,8 @@ def lib() -> C.CDLL:
     L.c1d_round_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     L.c1d_round_bf16.restype = C.c_int
     L.c1d_launch_count.restype = C.c_uint64
+    L.c1d_release_workspace.argtypes = [C.c_void_p]
+    L.c1d_release_workspace.restype = C.c_int
     i64, vp = C.c_int64, C.c_void_p
     L.c1d_layer_forward_epilogue.argtypes = [vp, vp, vp, i64, i64, i64, C.c_int, C.c_int, vp, vp, i64, vp]
     L.c1d_layer_forward_epilogue.restype = C.c_int
@@ -125,5 +128,14 @@ def lib() -> C.CDLL:
     L.c1d_forward_glued.restype = C.c_int
     L.c1d_backward_data_glued.argtypes = [P(Desc), vp, vp, P(BwdGlue), vp, C.c_size_t, vp]
     L.c1d_backward_data_glued.restype = C.c_int
+    L.c1d_fill_poisson.argtypes = [vp, i64, C.c_double, C.c_uint64, vp]
+    L.c1d_fill_poisson.restype = C.c_int
+    L.c1d_fill_bernoulli.argtypes = [vp, i64, C.c_double, C.c_uint64, vp]
+    L.c1d_fill_bernoulli.restype = C.c_int
+    L.c1d_loss_workspace_size.restype = C.c_size_t
+    L.c1d_mse_bce_loss.argtypes = [vp, vp, i64, vp, vp, i64, i64, C.c_float, vp, vp, i64, vp, vp, C.c_size_t, vp]
+    L.c1d_mse_bce_loss.restype = C.c_int
+    L.c1d_sgd_update.argtypes = [vp, vp, i64, C.c_float, vp]
+    L.c1d_sgd_update.restype = C.c_int
     _lib = L
     return L

@@ -114,10 +114,12 @@ ALGO_NAMES = {v: k for k, v in _ALGOS.items()}
 
 
 def make_desc(p: ConvParams, n: int, w_in: int, in_dtype: int = L.DTYPE_F32, algo: str = "auto",
-              strict: bool = False) -> L.Desc:
+              strict: bool = False, exact: bool = False) -> L.Desc:
+    """exact: C1D_FLAG_EXACT_ACCUM (BF16 accumulation chains capped at ~4096 products; FP32
+    precision always runs that way)."""
+    flags = (L.FLAG_STRICT_BF16_DIMS if strict else 0) | (L.FLAG_EXACT_ACCUM if exact else 0)
     return L.Desc(n=n, c=p.channels, k=p.filters, s=p.taps, d=p.dilation, w_in=w_in, precision=int(p.precision),
-                  in_dtype=in_dtype, algo=_ALGOS[algo], flags=L.FLAG_STRICT_BF16_DIMS if strict else 0,
-                  block_w=p.block_w)
+                  in_dtype=in_dtype, algo=_ALGOS[algo], flags=flags, block_w=p.block_w)
 
 
 # ----------------------------------------------------------------------------- geometry
@@ -193,13 +195,29 @@ def _dev_input(t: torch.Tensor) -> tuple[torch.Tensor, int]:
     return t.to(torch.float32).contiguous(), L.DTYPE_F32
 
 
-def _stream() -> int:
-    return torch.cuda.current_stream().cuda_stream
+def _stream(t: torch.Tensor | None = None) -> int:
+    """The current stream of the tensors' device (not of the current device)."""
+    return torch.cuda.current_stream(t.device if t is not None else None).cuda_stream
+
+
+def _check_out(out: torch.Tensor, shape: tuple, like: torch.Tensor) -> torch.Tensor:
+    """A caller-supplied output must be exactly what the kernels write: contiguous float32 of the
+    pass's output shape on the inputs' device (anything else would be written out of bounds)."""
+    if tuple(out.shape) != tuple(shape):
+        raise ShapeMismatch(f"out has shape {tuple(out.shape)}, the pass writes {tuple(shape)}")
+    if out.dtype != torch.float32:
+        raise ShapeMismatch(f"out must be float32, got {out.dtype}")
+    if not out.is_contiguous():
+        raise ShapeMismatch("out must be contiguous")
+    if out.device != like.device:
+        raise ShapeMismatch(f"out is on {out.device}, the inputs on {like.device}")
+    return out
 
 
 # ----------------------------------------------------------------------------- passes
 def conv1d_forward(inp: torch.Tensor, w, p: ConvParams, threads: int = 1, *, algo: str = "auto",
-                   strict: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+                   strict: bool = False, exact: bool = False,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
     """Forward pass (conv.cpp:165-191): out(n,k,q) = sum_c sum_s in(n,c,q+d*s) * w(k,c,s)."""
     if inp.dim() != 3:
         raise ShapeMismatch("input must be (N, C, W)")
@@ -208,17 +226,21 @@ def conv1d_forward(inp: torch.Tensor, w, p: ConvParams, threads: int = 1, *, alg
         raise ShapeMismatch(f"input has {c} channels, conv expects {p.channels}")
     wk = _weights_kcs(w, p, WeightLayout.ForwardSKC)
     x, dt = _dev_input(inp)
-    desc = make_desc(p, n, w_in, dt, algo, strict)
+    desc = make_desc(p, n, w_in, dt, algo, strict, exact)
     q = C.c_int64(0)
     _check(L.lib().c1d_output_width(C.byref(desc), C.byref(q)))
+    if wk.device != x.device:
+        raise ShapeMismatch(f"weights are on {wk.device}, the input on {x.device}")
     if out is None:
         out = torch.empty((n, p.filters, q.value), dtype=torch.float32, device=x.device)
-    _check(L.lib().c1d_forward(C.byref(desc), x.data_ptr(), wk.data_ptr(), out.data_ptr(), None, 0, _stream()))
+    _check_out(out, (n, p.filters, q.value), x)
+    _check(L.lib().c1d_forward(C.byref(desc), x.data_ptr(), wk.data_ptr(), out.data_ptr(), None, 0, _stream(x)))
     return out
 
 
 def conv1d_backward_data(grad_out: torch.Tensor, w, p: ConvParams, threads: int = 1, *, algo: str = "auto",
-                         strict: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+                         strict: bool = False, exact: bool = False,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
     """Backward-data pass (conv.cpp:193-227): gradient w.r.t. the padded input, width Q + d(S-1)."""
     if grad_out.dim() != 3:
         raise ShapeMismatch("grad_out must be (N, K, Q)")
@@ -228,16 +250,20 @@ def conv1d_backward_data(grad_out: torch.Tensor, w, p: ConvParams, threads: int 
     wk = _weights_kcs(w, p, WeightLayout.BackwardSCK)
     g, dt = _dev_input(grad_out)
     w_in = q + p.dilation * (p.taps - 1)
-    desc = make_desc(p, n, w_in, dt, algo, strict)
+    desc = make_desc(p, n, w_in, dt, algo, strict, exact)
+    if wk.device != g.device:
+        raise ShapeMismatch(f"weights are on {wk.device}, grad_out on {g.device}")
     if out is None:
         out = torch.empty((n, p.channels, w_in), dtype=torch.float32, device=g.device)
+    _check_out(out, (n, p.channels, w_in), g)
     _check(L.lib().c1d_backward_data(C.byref(desc), g.data_ptr(), wk.data_ptr(), out.data_ptr(), None, 0,
-                                     _stream()))
+                                     _stream(g)))
     return out
 
 
 def conv1d_backward_weight(grad_out: torch.Tensor, inp: torch.Tensor, p: ConvParams, threads: int = 1, *,
-                           algo: str = "auto", strict: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+                           algo: str = "auto", strict: bool = False, exact: bool = False,
+                   out: torch.Tensor | None = None) -> torch.Tensor:
     """Backward-weight pass (conv.cpp:229-326): grad_w(k,c,s) = sum_n sum_q in(n,c,q+d*s) grad_out(n,k,q)."""
     if grad_out.dim() != 3 or inp.dim() != 3:
         raise ShapeMismatch("tensors must be rank 3")
@@ -254,11 +280,14 @@ def conv1d_backward_weight(grad_out: torch.Tensor, inp: torch.Tensor, p: ConvPar
     if dt_g != dt_x:  # one storage dtype per call
         g, x = g.to(torch.float32), x.to(torch.float32)
         dt_g = dt_x = L.DTYPE_F32
-    desc = make_desc(p, n, w_in, dt_x, algo, strict)
+    if g.device != x.device:
+        raise ShapeMismatch(f"grad_out is on {g.device}, the input on {x.device}")
+    desc = make_desc(p, n, w_in, dt_x, algo, strict, exact)
     if out is None:
         out = torch.empty((k, c, p.taps), dtype=torch.float32, device=x.device)
+    _check_out(out, (k, c, p.taps), x)
     _check(L.lib().c1d_backward_weight(C.byref(desc), x.data_ptr(), g.data_ptr(), out.data_ptr(), None, 0,
-                                       _stream()))
+                                       _stream(x)))
     return out
 
 
@@ -266,7 +295,7 @@ def round_bf16(t: torch.Tensor) -> torch.Tensor:
     """Reference-exact RNE fp32 -> bf16 (bf16.hpp:29-40) on the device; returns a bfloat16 tensor."""
     src = _dev_f32(t)
     out = torch.empty(src.shape, dtype=torch.bfloat16, device=src.device)
-    _check(L.lib().c1d_round_bf16(src.data_ptr(), out.data_ptr(), src.numel(), _stream()))
+    _check(L.lib().c1d_round_bf16(src.data_ptr(), out.data_ptr(), src.numel(), _stream(src)))
     return out
 
 
@@ -278,10 +307,18 @@ def selected_algo(p: ConvParams, n: int, w_in: int, pass_: int, in_dtype: int = 
 
 
 def workspace_size(p: ConvParams, n: int, w_in: int, pass_: int, in_dtype: int = L.DTYPE_BF16,
-                   algo: str = "auto") -> int:
+                   algo: str = "auto", exact: bool = False) -> int:
     b = C.c_size_t(0)
-    _check(L.lib().c1d_workspace_size(C.byref(make_desc(p, n, w_in, in_dtype, algo)), pass_, C.byref(b)))
+    _check(L.lib().c1d_workspace_size(C.byref(make_desc(p, n, w_in, in_dtype, algo, exact=exact)), pass_,
+                                      C.byref(b)))
     return b.value
+
+
+def release_workspace(stream: torch.cuda.Stream | None = None) -> None:
+    """Free the library's internal workspace of `stream` (default: the current stream); only once
+    no CUDA graph captured on that stream will be replayed again (c1d_release_workspace)."""
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(L.lib().c1d_release_workspace(s.cuda_stream))
 
 
 def launch_count() -> int:

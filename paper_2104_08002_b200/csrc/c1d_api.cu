@@ -21,6 +21,18 @@ namespace c1d {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(static_cast<uint64_t>(n), std::memory_order_relaxed); }
 
+namespace {
+thread_local std::string t_last_error;
+}
+void set_last_error(const char* msg) { t_last_error = msg; }
+
+namespace {
+thread_local bool t_exact = false;
+}
+bool exact_accum() { return t_exact; }
+ExactAccumScope::ExactAccumScope(bool on) : saved(t_exact) { t_exact = on; }
+ExactAccumScope::~ExactAccumScope() { t_exact = saved; }
+
 int num_sms() {
     static int sms = [] {
         int dev = 0, v = 148;
@@ -31,8 +43,6 @@ int num_sms() {
 }
 
 namespace {
-
-thread_local std::string t_last_error;
 
 c1d_status fail(c1d_status st, const std::string& msg) {
     t_last_error = msg;
@@ -45,10 +55,14 @@ c1d_status cuda_fail(cudaError_t e, const char* where) {
 
 // Internal workspace (used when the caller passes workspace == NULL): one lazily grown buffer per
 // (device, stream), so calls on different streams never share scratch memory; calls on one stream
-// are ordered by the stream itself.
+// are ordered by the stream itself. A buffer that is outgrown is RETIRED, not freed: CUDA graphs
+// captured earlier on that stream keep its address, so it stays allocated until the caller
+// releases the stream's buffers (c1d_release_workspace). Growing never synchronises, so it is legal
+// during stream capture (the allocation itself runs in relaxed capture mode).
 struct DeviceWorkspace {
     void* ptr = nullptr;
     size_t bytes = 0;
+    std::vector<void*> retired;
 };
 std::mutex g_ws_mutex;
 std::map<std::pair<int, cudaStream_t>, DeviceWorkspace> g_ws;
@@ -62,25 +76,41 @@ cudaError_t internal_workspace(size_t need, cudaStream_t stream, void** out) {
     std::lock_guard<std::mutex> lock(g_ws_mutex);
     DeviceWorkspace& w = g_ws[{dev, stream}];
     if (w.bytes < need) {
-        if (w.ptr) {
-            // in-flight work of this stream may still read the old buffer (the legacy default stream
-            // synchronises with the others, so a device-wide sync covers it)
-            e = stream ? cudaStreamSynchronize(stream) : cudaDeviceSynchronize();
-            if (e != cudaSuccess) return e;
-            cudaFree(w.ptr);
-            w.ptr = nullptr;
-            w.bytes = 0;
-        }
         const size_t grow = need + need / 4;
-        e = cudaMalloc(&w.ptr, grow);
+        void* p = nullptr;
+        cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+        cudaThreadExchangeStreamCaptureMode(&mode);
+        e = cudaMalloc(&p, grow);
+        cudaThreadExchangeStreamCaptureMode(&mode);
         if (e != cudaSuccess) return e;
+        if (w.ptr) w.retired.push_back(w.ptr);
+        w.ptr = p;
         w.bytes = grow;
     }
     *out = w.ptr;
     return cudaSuccess;
 }
 
+// Frees the internal buffers of (current device, stream) after the stream drains. The caller
+// guarantees that no captured graph which used them will be replayed again.
+cudaError_t release_internal_workspace(cudaStream_t stream) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(g_ws_mutex);
+    auto it = g_ws.find({dev, stream});
+    if (it == g_ws.end()) return cudaSuccess;
+    e = stream ? cudaStreamSynchronize(stream) : cudaDeviceSynchronize();
+    if (e != cudaSuccess) return e;
+    for (void* p : it->second.retired) cudaFree(p);
+    if (it->second.ptr) cudaFree(it->second.ptr);
+    g_ws.erase(it);
+    return cudaSuccess;
+}
+
 bool is_bf16(const c1d_desc& d) { return d.precision == C1D_PRECISION_BF16; }
+// FP32 precision always caps its accumulation chains (the reference's 1e-5 bound); BF16 on request
+bool exact_for(const c1d_desc& d) { return !is_bf16(d) || (d.flags & C1D_FLAG_EXACT_ACCUM); }
 
 c1d_status validate(const c1d_desc* desc, int64_t* q_out) {
     if (!desc) return fail(C1D_ERR_INVALID_ARGUMENT, "desc is NULL");
@@ -225,6 +255,36 @@ bool native_direct(const ConvGeom& g, int64_t main_ch = 0) {
     gi.xr_inline = true;
     return tc_conv_supported(gi, main_ch);
 }
+// BF16 reduction chains: the tensor core's FP32 accumulation into one TMEM accumulator drifts by
+// ~1.2e-9 (norm-relative) per accumulated product, always toward zero (measured: got/true - 1 =
+// -6.4e-5 for both signs at 52k products), so a chain of C_in*S products much past ~4k leaves 1e-5
+// (C = 160, S = 51: 1.07e-5; the reference's RN FP32 accumulation gives 2.5e-6 there). Under
+// C1D_FLAG_EXACT_ACCUM longer reductions run as two chains: the channel halves accumulate in two
+// TMEM regions that the epilogue adds in FP32 (the split-FP32 machinery's main_ch).
+constexpr int64_t kMaxBf16Chain = 4096;
+struct ChainPlan {
+    ConvGeom g;
+    int64_t main_ch;
+};
+// native d = 8, no glue: carry mode, or the carry-free direct mode for > 64 filters or two chains
+ChainPlan native_choice(const ConvGeom& gq) {
+    if (exact_accum() && gq.in_ch * gq.taps > kMaxBf16Chain) {
+        const int64_t half = (gq.in_ch + 1) / 2;
+        ConvGeom gd = gq;
+        gd.xr_inline = native_direct(gq, half);
+        if (tc_conv_supported(gd, half)) return ChainPlan{gd, half};
+    }
+    ConvGeom gk = gq;
+    gk.xr_inline = native_direct(gq);
+    return ChainPlan{gk, 0};
+}
+// expanded-row geometries (d < 8): the same mode with two chains when the reduction is long
+int64_t xr_main_ch(const ConvGeom& gx) {
+    if (!exact_accum() || gx.in_ch * gx.taps <= kMaxBf16Chain) return 0;
+    const int64_t half = (gx.in_ch + 1) / 2;
+    return tc_conv_supported(gx, half) ? half : 0;
+}
+
 // backward-weight on expanded rows (d = 1, 2, 4): one tc_wgrad launch over E (rows of x at every
 // d-column start) instead of one launch per phase
 int64_t xr_wgrad_rows(const c1d_desc& d, int64_t q_pad) { return ceil_div(q_pad + d.d * (d.s - 1), d.d) + 16; }
@@ -279,7 +339,7 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
         // (the split quadruples the channels, so a row tensor in HBM would be 4 * 8/d x the input),
         // else the row tensor
         ConvGeom g4 = g;
-        g4.in_ch *= 4;
+        g4.in_ch *= kSplitBlocks;
         ConvGeom gi = pitched(g4);  // the split rows get an 8-element pitch
         gi.xr_inline = true;
         if (tc_conv_supported(gi, g.in_ch)) return SplitConv{gi, g.in_ch};
@@ -290,7 +350,7 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
         // two TMEM regions leave the carry mode 256/KP - (G-1) tiles per super-tile (1 at KP = 64,
         // S = 51), so the carry-free direct mode (4 tiles) runs the split
         ConvGeom g4 = pitched(g);
-        g4.in_ch *= 4;
+        g4.in_ch *= kSplitBlocks;
         if (native_direct(g4, g.in_ch)) {
             g4.xr_inline = true;
             return SplitConv{g4, g.in_ch};
@@ -299,7 +359,7 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
     if (dp.kind == DilPlan::kPlanes) g = plane_geom(g, dp);
     if (dp.kind == DilPlan::kPhases) g = phase_geom(g, dp);
     SplitConv r{g, g.in_ch};
-    r.gs.in_ch *= 4;
+    r.gs.in_ch *= kSplitBlocks;
     return r;
 }
 
@@ -418,14 +478,14 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     }
     if (dp.kind == DilPlan::kPhases && xr_inline_ok(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q))) {
         const ConvGeom g = xr_inline_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
-        size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
+        size_t b = wbytes + align_up(std::max(tc_conv_workspace_bytes(g), tc_conv_workspace_bytes(g, xr_main_ch(g))));
         if (g.in_stride || conv_in_f32)
             b += align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * (g.in_stride ? g.in_stride : g.in_w)));
         return b;
     }
     if (dp.kind == DilPlan::kPhases && xr_ok(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q))) {
         const ConvGeom g = xr_geom(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
-        return wbytes + align_up(tc_conv_workspace_bytes(g)) +
+        return wbytes + align_up(std::max(tc_conv_workspace_bytes(g), tc_conv_workspace_bytes(g, xr_main_ch(g)))) +
                align_up(sizeof(uint16_t) * 8 * static_cast<size_t>(g.n * g.in_ch * g.xr_rows));
     }
     if (dp.kind == DilPlan::kPhases) {
@@ -436,7 +496,10 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     }
     if (dp.kind == DilPlan::kNative) {
         const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
-        size_t b = wbytes + align_up(tc_conv_workspace_bytes(g));
+        // conv_pass runs the carry mode (glued calls) or native_choice's plan: size for the larger
+        const ChainPlan cp = native_choice(g);
+        const size_t kws = std::max(tc_conv_workspace_bytes(g), tc_conv_workspace_bytes(cp.g, cp.main_ch));
+        size_t b = wbytes + align_up(kws);
         if (g.in_stride || conv_in_f32)
             b += align_up(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * (g.in_stride ? g.in_stride : g.in_w)));
         return b;
@@ -458,12 +521,16 @@ struct Bump {
     size_t left;
     bool dry = false;  // sizing pass: only count (used by workspace_for for the composed paths)
     size_t used = 0;
+    bool overflow = false;  // a take() did not fit: the plan's sizing and its run disagree
     template <typename T>
     T* take(size_t bytes) {
         bytes = align_up(bytes);
         used += bytes;
         if (dry) return reinterpret_cast<T*>(alignof(T));  // never dereferenced
-        if (bytes > left) return nullptr;
+        if (bytes > left) {
+            overflow = true;
+            return nullptr;
+        }
         T* r = reinterpret_cast<T*>(p);
         p += bytes;
         left -= bytes;
@@ -484,6 +551,11 @@ c1d_status acquire_workspace(void* user, size_t user_bytes, size_t need, Bump* o
     if (e != cudaSuccess) return cuda_fail(e, "internal workspace");
     *out = Bump{static_cast<char*>(p), need};
     return C1D_OK;
+}
+
+// a bump.take() of a running plan did not fit the workspace its sizing pass computed
+c1d_status workspace_overflow() {
+    return fail(C1D_ERR_WORKSPACE, "workspace too small for the selected plan (internal sizing mismatch)");
 }
 
 c1d_status check_device() {
@@ -508,30 +580,32 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
     const int mode = pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData;
     cudaError_t e = cudaSuccess;
     auto step = [&](auto&& launch) {
-        if (run && e == cudaSuccess) e = launch();
+        if (run && e == cudaSuccess) e = bump.overflow ? cudaErrorInvalidValue : launch();
     };
     if (dp.kind != DilPlan::kPhases || sc.gs.xr_rows > 0 || sc.gs.xr_inline) {
-        float* w4 = bump.take<float>(4 * sizeof(float) * kcs);
-        float* wg4 = bump.take<float>(4 * sizeof(float) * kcs);
-        if (pass == C1D_PASS_FORWARD) {  // c-blocks hi,hi,lo,lo
-            step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 1, 4, 0xCu, stream); });
-            step([&] { return launch_prep_weights(w4, wg4, d.k, 4 * d.c, d.s, kWeightsForward, false, stream); });
-        } else {  // k-blocks hi,hi,lo,lo, then the bwd-d transpose
-            step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 4, 1, 0xCu, stream); });
-            step([&] { return launch_prep_weights(w4, wg4, 4 * d.k, d.c, d.s, kWeightsBackwardData, false, stream); });
+        float* w4 = bump.take<float>(kSplitBlocks * sizeof(float) * kcs);
+        float* wg4 = bump.take<float>(kSplitBlocks * sizeof(float) * kcs);
+        if (pass == C1D_PASS_FORWARD) {  // c-blocks of the weight parts (kSplitW)
+            step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, 1, kSplitBlocks, kSplitW, stream); });
+            step([&] { return launch_prep_weights(w4, wg4, d.k, kSplitBlocks * d.c, d.s, kWeightsForward, false, stream); });
+        } else {  // k-blocks of the weight parts, then the bwd-d transpose
+            step([&] { return launch_split_weights(w_kcs, w4, d.k, d.c, d.s, kSplitBlocks, 1, kSplitW, stream); });
+            step([&] {
+                return launch_prep_weights(w4, wg4, kSplitBlocks * d.k, d.c, d.s, kWeightsBackwardData, false, stream);
+            });
         }
         const int64_t x4_pitch = sc.gs.xr_inline && sc.gs.in_stride ? sc.gs.in_stride : g.in_w;
-        const size_t n4 = static_cast<size_t>(g.n * 4 * g.in_ch * x4_pitch);
+        const size_t n4 = static_cast<size_t>(g.n * kSplitBlocks * g.in_ch * x4_pitch);
         uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
         step([&] {
-            return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, 4, 0xAu, stream, x4_pitch,
+            return launch_split_channels(static_cast<const float*>(in), x4, g.n, g.in_ch, g.in_w, kSplitBlocks, kSplitX, stream, x4_pitch,
                                          in_item_stride);
         });
         if (dp.kind == DilPlan::kPlanes) {
             uint16_t* p4 = bump.take<uint16_t>(sizeof(uint16_t) * n4);
             float* pout = bump.take<float>(sizeof(float) * static_cast<size_t>(sc.gs.n * sc.gs.out_ch * sc.gs.out_w));
             void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
-            step([&] { return launch_to_planes(x4, C1D_DTYPE_BF16, p4, g.n, 4 * g.in_ch, g.in_w, dp.m, stream); });
+            step([&] { return launch_to_planes(x4, C1D_DTYPE_BF16, p4, g.n, kSplitBlocks * g.in_ch, g.in_w, dp.m, stream); });
             step([&] { return launch_tc_conv(p4, wg4, pout, sc.gs, kws, stream, sc.main_ch); });
             step([&] { return launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream); });
             return e;
@@ -542,10 +616,10 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
             return e;
         }
         if (sc.gs.xr_rows > 0) {  // d < 8: expanded rows of the split channels
-            uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(g.n * 4 * g.in_ch * sc.gs.xr_rows));
+            uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(g.n * kSplitBlocks * g.in_ch * sc.gs.xr_rows));
             void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
             step([&] {
-                return launch_expand_rows(x4, C1D_DTYPE_BF16, ex, g.n * 4 * g.in_ch, g.in_w, g.dil, g.in_off, sc.gs.xr_rows,
+                return launch_expand_rows(x4, C1D_DTYPE_BF16, ex, g.n * kSplitBlocks * g.in_ch, g.in_w, g.dil, g.in_off, sc.gs.xr_rows,
                                           stream);
             });
             step([&] { return launch_tc_conv(ex, wg4, out, sc.gs, kws, stream, sc.main_ch); });
@@ -559,19 +633,19 @@ cudaError_t split_conv_run(const c1d_desc& d, c1d_pass pass, int64_t q, const vo
     const int64_t O = g.out_ch, I = g.in_ch, PI = dp.p * g.in_ch;
     float* wg = bump.take<float>(sizeof(float) * kcs);
     float* wph = bump.take<float>(sizeof(float) * static_cast<size_t>(O * PI * dp.sp));
-    float* wg4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(O * PI * dp.sp));
+    float* wg4 = bump.take<float>(kSplitBlocks * sizeof(float) * static_cast<size_t>(O * PI * dp.sp));
     step([&] { return launch_prep_weights(w_kcs, wg, d.k, d.c, d.s, mode, false, stream); });
     step([&] { return launch_phase_split_weights(wg, wph, O, I, d.s, dp.m, dp.p, stream); });
-    step([&] { return launch_split_weights(wph, wg4, O, PI, dp.sp, 1, 4, 0xCu, stream); });
+    step([&] { return launch_split_weights(wph, wg4, O, PI, dp.sp, 1, kSplitBlocks, kSplitW, stream); });
     const PhaseCopy pc = phase_copy(g);
     const int64_t W2 = sc.gs.in_w;
     float* cp = bump.take<float>(sizeof(float) * static_cast<size_t>(g.n * PI * W2));
-    uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * 4 * PI * W2));
+    uint16_t* x4 = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * kSplitBlocks * PI * W2));
     void* kws = bump.take<char>(tc_conv_workspace_bytes(sc.gs, sc.main_ch));
     step([&] {
         return launch_shift_copies_f32(static_cast<const float*>(in), cp, g.n, I, g.in_w, dp.p, pc.base, d.d, W2, stream);
     });
-    step([&] { return launch_split_channels(cp, x4, g.n, PI, W2, 4, 0xAu, stream); });
+    step([&] { return launch_split_channels(cp, x4, g.n, PI, W2, kSplitBlocks, kSplitX, stream); });
     step([&] { return launch_tc_conv(x4, wg4, out, sc.gs, kws, stream, sc.main_ch); });
     return e;
 }
@@ -626,97 +700,122 @@ bool split_wgrad_blocks(const c1d_desc& d) {
     return resolve(d16, C1D_PASS_BACKWARD_WEIGHT, q) == C1D_ALGO_TCGEN05;
 }
 
-// FP32 split path of backward-weight: x' = [x_hi | x_lo] (2C), dy' = [dy_hi | dy_lo] (2K); the four
-// (k-block, c-block) tiles of the 2K x 2C gradient are summed; under the dilation plans the split
-// operands are relaid out exactly as the BF16 ones.
+// FP32 split path of backward-weight, three-level split v = hi + mid + lo (split.cu): two launches
+// of the (2C, 2K) problem under the dilation plan,
+//   A: x' = [x_hi | x_mid], dy' = [dy_hi | dy_mid]      B: x' = [x_hi | x_lo], dy' = [dy_lo | dy_hi]
+// whose 2x2 block results combine as hh + (hm + (mh + (hl + (lh + (mm + ll))))) (sum_split3). Under the
+// dilation plans the split operands are relaid out exactly as the BF16 ones.
 cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const void* dy, float* dw, Bump& bump,
                             cudaStream_t stream) {
     const DilPlan dp = dil_plan(d, q);
     const bool run = !bump.dry;
     cudaError_t e = cudaSuccess;
     auto step = [&](auto&& launch) {
-        if (run && e == cudaSuccess) e = launch();
+        if (run && e == cudaSuccess) e = bump.overflow ? cudaErrorInvalidValue : launch();
     };
     const size_t nx = static_cast<size_t>(2 * d.n * d.c * d.w_in), ng = static_cast<size_t>(2 * d.n * d.k * q);
-    uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * nx);
-    uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * ng);
+    const size_t kcs = static_cast<size_t>(d.k * d.c * d.s);
     if (split_wgrad_blocks(d)) {
-        // 2C or 2K too wide for one launch: three BF16 block passes (hi x hi, hi x lo, lo x hi) on
-        // separate hi / lo tensors through the BF16 tensor-core path (any dilation plan), summed in a
-        // fixed order
-        const size_t kcs = static_cast<size_t>(d.k * d.c * d.s);
+        // 2C or 2K too wide for one launch: six BF16 block passes (dy part x x part: hh, hm, mh, hl,
+        // lh, mm) on separate part tensors through the BF16 tensor-core path (any dilation plan),
+        // summed in a fixed order
         c1d_desc d16 = d;
         d16.precision = C1D_PRECISION_BF16;
         d16.in_dtype = C1D_DTYPE_BF16;
         d16.algo = C1D_ALGO_TCGEN05;
-        d16.flags = 0;
-        uint16_t* xl = bump.take<uint16_t>(sizeof(uint16_t) * nx / 2);
-        uint16_t* gl = bump.take<uint16_t>(sizeof(uint16_t) * ng / 2);
-        float* part = bump.take<float>(3 * sizeof(float) * kcs);
+        d16.flags = C1D_FLAG_EXACT_ACCUM;  // the FP32 result keeps its capped chains
+        uint16_t* xp[3];
+        uint16_t* gp[3];
+        for (int i = 0; i < 3; ++i) xp[i] = bump.take<uint16_t>(sizeof(uint16_t) * nx / 2);
+        for (int i = 0; i < 3; ++i) gp[i] = bump.take<uint16_t>(sizeof(uint16_t) * ng / 2);
+        float* part = bump.take<float>(6 * sizeof(float) * kcs);
         const size_t inner = workspace_for(d16, C1D_PASS_BACKWARD_WEIGHT, q, C1D_ALGO_TCGEN05);
         char* iws = bump.take<char>(inner);
-        uint16_t* xh = x2;  // the first halves of the x2 / g2 buffers hold the hi tensors here
-        uint16_t* gh = g2;
-        step([&] { return launch_split_channels(static_cast<const float*>(x), xh, d.n, d.c, d.w_in, 1, 0x0u, stream); });
-        step([&] { return launch_split_channels(static_cast<const float*>(x), xl, d.n, d.c, d.w_in, 1, 0x1u, stream); });
-        step([&] { return launch_split_channels(static_cast<const float*>(dy), gh, d.n, d.k, q, 1, 0x0u, stream); });
-        step([&] { return launch_split_channels(static_cast<const float*>(dy), gl, d.n, d.k, q, 1, 0x1u, stream); });
-        const uint16_t* xs[3] = {xh, xh, xl};
-        const uint16_t* gs[3] = {gh, gl, gh};
-        for (int b = 0; b < 3; ++b)
+        for (unsigned i = 0; i < 3; ++i) {
+            step([&] { return launch_split_channels(static_cast<const float*>(x), xp[i], d.n, d.c, d.w_in, 1, i, stream); });
+            step([&] { return launch_split_channels(static_cast<const float*>(dy), gp[i], d.n, d.k, q, 1, i, stream); });
+        }
+        const int pairs[6][2] = {{0, 0}, {0, 1}, {1, 0}, {0, 2}, {2, 0}, {1, 1}};  // (dy part, x part)
+        for (int b = 0; b < 6; ++b)
             step([&] {
-                const c1d_status st = c1d_backward_weight(&d16, xs[b], gs[b], part + b * kcs, iws, inner,
-                                                          reinterpret_cast<c1d_stream_t>(stream));
+                const c1d_status st = c1d_backward_weight(&d16, xp[pairs[b][1]], gp[pairs[b][0]], part + b * kcs, iws,
+                                                          inner, reinterpret_cast<c1d_stream_t>(stream));
                 return st == C1D_OK ? cudaSuccess : cudaErrorUnknown;
             });
-        step([&] { return launch_sum3(part, part + kcs, part + 2 * kcs, dw, static_cast<int64_t>(kcs), stream); });
+        step([&] { return launch_sum6(part, dw, static_cast<int64_t>(kcs), stream); });
         return e;
     }
-    step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, 0x2u, stream); });
-    step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, 0x2u, stream); });
+    uint16_t* x2 = bump.take<uint16_t>(sizeof(uint16_t) * nx);
+    uint16_t* g2 = bump.take<uint16_t>(sizeof(uint16_t) * ng);
+    const unsigned pat_x[2] = {kSplitHM, kSplitHL3}, pat_g[2] = {kSplitHM, kSplitL3H};
+    auto split_pass = [&](int pass) {
+        step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, pat_x[pass], stream); });
+        step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[pass], stream); });
+    };
     if (dp.kind == DilPlan::kPhases && (d.d == 1 || d.d == 2 || d.d == 4) &&
         tc_wgrad_v3_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q)) {
-        // expanded rows of the split x, one launch
+        // expanded rows of the split x, one launch per split pass
         const int64_t rows = xr_wgrad_rows(d, q);
         uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(2 * d.n * d.c * rows));
-        float* dw4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+        float* dw4[2] = {bump.take<float>(4 * sizeof(float) * kcs), bump.take<float>(4 * sizeof(float) * kcs)};
         void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q));
-        step([&] { return launch_expand_rows(x2, C1D_DTYPE_BF16, ex, 2 * d.n * d.c, d.w_in, d.d, 0, rows, stream); });
-        step([&] { return launch_tc_wgrad(ex, g2, dw4, kws, d.n, 2 * d.c, 2 * d.k, d.s, d.d, q, stream, rows * 8); });
-        step([&] { return launch_sum_split_blocks(dw4, dw, d.k, d.c, d.s, stream); });
+        for (int ps = 0; ps < 2; ++ps) {
+            split_pass(ps);
+            step([&] { return launch_expand_rows(x2, C1D_DTYPE_BF16, ex, 2 * d.n * d.c, d.w_in, d.d, 0, rows, stream); });
+            step([&] { return launch_tc_wgrad(ex, g2, dw4[ps], kws, d.n, 2 * d.c, 2 * d.k, d.s, d.d, q, stream, rows * 8); });
+        }
+        step([&] { return launch_sum_split3(dw4[0], dw4[1], dw, d.k, d.c, d.s, stream); });
         return e;
     }
     if (dp.kind == DilPlan::kPhases) {
         const int64_t pitch = round8(std::max<int64_t>(d.w_in, q + 8 * (dp.sp - 1)));
-        uint16_t* xs = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * pitch));
-        float* dw4b = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * dp.sp));
+        uint16_t* xs[2] = {bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * pitch)),
+                           bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(2 * d.n * d.c * pitch))};
+        uint16_t* g2b = bump.take<uint16_t>(sizeof(uint16_t) * ng);  // pass B's dy split (pass A's stays in g2)
+        float* dw4b[2] = {bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * dp.sp)),
+                          bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * dp.sp))};
         float* dwb = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * dp.sp));
         size_t kb = 0;
         for (int64_t b = 0; b < dp.p; ++b)
             kb = std::max(kb, tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, ceil_div(d.s - b, dp.m), 8, q));
         void* kws = bump.take<char>(kb);
+        // both splits of dy once; x's two splits are re-shifted per phase
+        step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[0], stream); });
+        step([&] { return launch_split_channels(static_cast<const float*>(dy), g2b, d.n, d.k, q, 2, pat_g[1], stream); });
+        const uint16_t* gsrc[2] = {g2, g2b};
         for (int64_t b = 0; b < dp.p; ++b) {
             const int64_t sb = ceil_div(d.s - b, dp.m);
-            step([&] { return launch_shift_copies(x2, C1D_DTYPE_BF16, xs, d.n, 2 * d.c, d.w_in, 1, b * d.d, 0, pitch, stream); });
-            step([&] { return launch_tc_wgrad(xs, g2, dw4b, kws, d.n, 2 * d.c, 2 * d.k, sb, 8, q, stream, pitch); });
-            step([&] { return launch_sum_split_blocks(dw4b, dwb, d.k, d.c, sb, stream); });
+            for (int ps = 0; ps < 2; ++ps) {
+                step([&] {
+                    return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, pat_x[ps], stream);
+                });
+                step([&] { return launch_shift_copies(x2, C1D_DTYPE_BF16, xs[ps], d.n, 2 * d.c, d.w_in, 1, b * d.d, 0, pitch, stream); });
+                step([&] { return launch_tc_wgrad(xs[ps], gsrc[ps], dw4b[ps], kws, d.n, 2 * d.c, 2 * d.k, sb, 8, q, stream, pitch); });
+            }
+            step([&] { return launch_sum_split3(dw4b[0], dw4b[1], dwb, d.k, d.c, sb, stream); });
             step([&] { return launch_scatter_phase_wgrad(dwb, dw, d.k, d.c, d.s, dp.m, b, stream); });
         }
         return e;
     }
-    float* dw4 = bump.take<float>(4 * sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
+    float* dw4[2] = {bump.take<float>(4 * sizeof(float) * kcs), bump.take<float>(4 * sizeof(float) * kcs)};
     if (dp.kind == DilPlan::kPlanes) {
         uint16_t* px = bump.take<uint16_t>(sizeof(uint16_t) * nx);
         uint16_t* pg = bump.take<uint16_t>(sizeof(uint16_t) * ng);
         void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m));
-        step([&] { return launch_to_planes(x2, C1D_DTYPE_BF16, px, d.n, 2 * d.c, d.w_in, dp.m, stream); });
-        step([&] { return launch_to_planes(g2, C1D_DTYPE_BF16, pg, d.n, 2 * d.k, q, dp.m, stream); });
-        step([&] { return launch_tc_wgrad(px, pg, dw4, kws, d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m, stream); });
+        for (int ps = 0; ps < 2; ++ps) {
+            split_pass(ps);
+            step([&] { return launch_to_planes(x2, C1D_DTYPE_BF16, px, d.n, 2 * d.c, d.w_in, dp.m, stream); });
+            step([&] { return launch_to_planes(g2, C1D_DTYPE_BF16, pg, d.n, 2 * d.k, q, dp.m, stream); });
+            step([&] { return launch_tc_wgrad(px, pg, dw4[ps], kws, d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m, stream); });
+        }
     } else {
         void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, 8, q));
-        step([&] { return launch_tc_wgrad(x2, g2, dw4, kws, d.n, 2 * d.c, 2 * d.k, d.s, 8, q, stream); });
+        for (int ps = 0; ps < 2; ++ps) {
+            split_pass(ps);
+            step([&] { return launch_tc_wgrad(x2, g2, dw4[ps], kws, d.n, 2 * d.c, 2 * d.k, d.s, 8, q, stream); });
+        }
     }
-    step([&] { return launch_sum_split_blocks(dw4, dw, d.k, d.c, d.s, stream); });
+    step([&] { return launch_sum_split3(dw4[0], dw4[1], dw, d.k, d.c, d.s, stream); });
     return e;
 }
 
@@ -738,6 +837,7 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     int64_t q = 0;
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
+    const ExactAccumScope exact_scope(exact_for(*desc));
     const c1d_desc& d = *desc;
     if (d.n == 0) return C1D_OK;
     if (!in || !w_kcs || (!out && !glue)) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL tensor pointer");
@@ -752,6 +852,7 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     if (algo == C1D_ALGO_BF16X3) {
         // FP32 via split BF16 operands (split.cu), composed with the dilation plans
         const cudaError_t e = split_conv_any(d, pass, q, in, w_kcs, out, bump, stream);
+        if (bump.overflow) return workspace_overflow();
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (bf16x3)");
         return C1D_OK;
     }
@@ -762,11 +863,13 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     float* wg = bump.take<float>(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
     cudaError_t e = cudaSuccess;
     const bool use_xr = algo == C1D_ALGO_TCGEN05 && dp.kind == DilPlan::kPhases && xr_ok(g);
+    if (bump.overflow) return workspace_overflow();
     if (algo == C1D_ALGO_DIRECT || (dp.kind != DilPlan::kNative && !use_xr))
         e = launch_prep_weights(w_kcs, wg, d.k, d.c, d.s,
                                 pass == C1D_PASS_FORWARD ? kWeightsForward : kWeightsBackwardData, bf16, stream);
     if (e != cudaSuccess) return cuda_fail(e, "prep_weights");
     if (algo == C1D_ALGO_DIRECT) {
+        if (bump.overflow) return workspace_overflow();
         e = launch_direct_conv(in, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, wg, out, g, stream);
         if (e != cudaSuccess) return cuda_fail(e, "direct_conv");
         return C1D_OK;
@@ -776,9 +879,11 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         const ConvGeom gp = plane_geom(g, dp);
         uint16_t* pin = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * g.in_w));
         float* pout = bump.take<float>(sizeof(float) * static_cast<size_t>(gp.n * gp.out_ch * gp.out_w));
+        if (bump.overflow) return workspace_overflow();
         e = launch_to_planes(in, d.in_dtype, pin, g.n, g.in_ch, g.in_w, dp.m, stream);
         if (e != cudaSuccess) return cuda_fail(e, "to_planes");
         void* kws = bump.take<char>(tc_conv_workspace_bytes(gp));
+        if (bump.overflow) return workspace_overflow();
         e = launch_tc_conv(pin, wg, pout, gp, kws, stream);
         if (e == cudaSuccess) e = launch_from_planes(pout, out, g.n, g.out_ch, g.out_w, dp.m, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (planes)");
@@ -790,18 +895,22 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         const uint16_t* in_b = static_cast<const uint16_t*>(in);
         if (gi.in_stride) {
             uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * gi.in_stride));
+            if (bump.overflow) return workspace_overflow();
             e = launch_pad_rows(in, d.in_dtype, tmp, g.n * g.in_ch, g.in_w, gi.in_stride, stream);
             if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
             in_b = tmp;
         } else if (d.in_dtype == C1D_DTYPE_F32) {
             const int64_t count = g.n * g.in_ch * g.in_w;
             uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(count));
+            if (bump.overflow) return workspace_overflow();
             e = launch_round_bf16(static_cast<const float*>(in), tmp, count, stream);
             if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
             in_b = tmp;
         }
-        void* kws = bump.take<char>(tc_conv_workspace_bytes(gi));
-        e = launch_tc_conv(in_b, w_kcs, out, gi, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
+        const int64_t mc = glue ? 0 : xr_main_ch(gi);
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gi, mc));
+        if (bump.overflow) return workspace_overflow();
+        e = launch_tc_conv(in_b, w_kcs, out, gi, kws, stream, mc, pass == C1D_PASS_BACKWARD_DATA, glue);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (expanded rows, inline)");
         return C1D_OK;
     }
@@ -809,10 +918,13 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         // d < 8: expanded rows (E = 8-element rows at every d-column start), 16 taps per MMA
         const ConvGeom gx = xr_geom(g);
         uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(gx.n * gx.in_ch * gx.xr_rows));
+        if (bump.overflow) return workspace_overflow();
         e = launch_expand_rows(in, d.in_dtype, ex, g.n * g.in_ch, g.in_w, g.dil, g.in_off, gx.xr_rows, stream);
         if (e != cudaSuccess) return cuda_fail(e, "expand_rows");
-        void* kws = bump.take<char>(tc_conv_workspace_bytes(gx));
-        e = launch_tc_conv(ex, w_kcs, out, gx, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
+        const int64_t mc = glue ? 0 : xr_main_ch(gx);
+        void* kws = bump.take<char>(tc_conv_workspace_bytes(gx, mc));
+        if (bump.overflow) return workspace_overflow();
+        e = launch_tc_conv(ex, w_kcs, out, gx, kws, stream, mc, pass == C1D_PASS_BACKWARD_DATA, glue);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (expanded rows)");
         return C1D_OK;
     }
@@ -822,10 +934,12 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         const PhaseCopy pc = phase_copy(g);
         uint16_t* cp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(gp.n * gp.in_ch * gp.in_w));
         float* wph = bump.take<float>(sizeof(float) * static_cast<size_t>(gp.out_ch * gp.in_ch * dp.sp));
+        if (bump.overflow) return workspace_overflow();
         e = launch_shift_copies(in, d.in_dtype, cp, g.n, g.in_ch, g.in_w, dp.p, pc.base, d.d, gp.in_w, stream);
         if (e == cudaSuccess) e = launch_phase_split_weights(wg, wph, g.out_ch, g.in_ch, d.s, dp.m, dp.p, stream);
         if (e != cudaSuccess) return cuda_fail(e, "phase copies");
         void* kws = bump.take<char>(tc_conv_workspace_bytes(gp));
+        if (bump.overflow) return workspace_overflow();
         e = launch_tc_conv(cp, wph, out, gp, kws, stream, 0, false, glue);
         if (e != cudaSuccess) return cuda_fail(e, "tc_conv (phases)");
         return C1D_OK;
@@ -834,20 +948,23 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     const uint16_t* in_b = static_cast<const uint16_t*>(in);
     if (gq.in_stride) {  // unaligned row pitch: zero-padded bf16 copy (rounds FP32 storage too)
         uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(g.n * g.in_ch * gq.in_stride));
+        if (bump.overflow) return workspace_overflow();
         e = launch_pad_rows(in, d.in_dtype, tmp, g.n * g.in_ch, g.in_w, gq.in_stride, stream);
         if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
         in_b = tmp;
     } else if (d.in_dtype == C1D_DTYPE_F32) {
         const int64_t count = g.n * g.in_ch * g.in_w;
         uint16_t* tmp = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(count));
+        if (bump.overflow) return workspace_overflow();
         e = launch_round_bf16(static_cast<const float*>(in), tmp, count, stream);
         if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
         in_b = tmp;
     }
-    ConvGeom gk = gq;
-    if (!glue && native_direct(gq)) gk.xr_inline = true;  // carry-free direct accumulation (see native_direct)
-    void* kws = bump.take<char>(tc_conv_workspace_bytes(gk));
-    e = launch_tc_conv(in_b, w_kcs, out, gk, kws, stream, 0, pass == C1D_PASS_BACKWARD_DATA, glue);
+    // glued calls keep the carry mode; otherwise native_choice (carry / direct / two chains)
+    const ChainPlan cp = glue ? ChainPlan{gq, 0} : native_choice(gq);
+    void* kws = bump.take<char>(tc_conv_workspace_bytes(cp.g, cp.main_ch));
+    if (bump.overflow) return workspace_overflow();
+    e = launch_tc_conv(in_b, w_kcs, out, cp.g, kws, stream, cp.main_ch, pass == C1D_PASS_BACKWARD_DATA, glue);
     if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
     return C1D_OK;
 }
@@ -938,6 +1055,7 @@ c1d_status c1d_workspace_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes
     int64_t q = 0;
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
+    const ExactAccumScope exact_scope(exact_for(*desc));
     const c1d_algo a = resolve(*desc, pass, q);
     if (static_cast<int>(a) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     if (bytes) *bytes = workspace_for(*desc, pass, q, a);
@@ -964,6 +1082,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
     const c1d_desc& d = *desc;
+    const ExactAccumScope exact_scope(exact_for(d));
     if (!dw_kcs) return fail(C1D_ERR_INVALID_ARGUMENT, "NULL dw pointer");
     st = check_device();
     if (st != C1D_OK) return st;
@@ -982,11 +1101,13 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     cudaError_t e;
     if (algo == C1D_ALGO_BF16X3) {
         e = split_wgrad_run(d, q, x, dy, dw_kcs, bump, stream);
+        if (bump.overflow) return workspace_overflow();
         if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (bf16x3)");
         return C1D_OK;
     }
     if (algo == C1D_ALGO_DIRECT) {
         float* part = bump.take<float>(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
+        if (bump.overflow) return workspace_overflow();
         e = launch_direct_wgrad(x, dy, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, dw_kcs, part, d.n, d.c, d.k,
                                 d.s, d.d, q, stream);
         if (e != cudaSuccess) return cuda_fail(e, "direct_wgrad");
@@ -997,10 +1118,12 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         // d = 8m: both operands as chunk planes; the plane items sum into the same dW
         uint16_t* px = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
         uint16_t* pdy = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        if (bump.overflow) return workspace_overflow();
         e = launch_to_planes(x, d.in_dtype, px, d.n, d.c, d.w_in, dpl.m, stream);
         if (e == cudaSuccess) e = launch_to_planes(dy, d.in_dtype, pdy, d.n, d.k, q, dpl.m, stream);
         if (e != cudaSuccess) return cuda_fail(e, "to_planes");
         void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n * dpl.m, d.c, d.k, d.s, 8, q / dpl.m));
+        if (bump.overflow) return workspace_overflow();
         e = launch_tc_wgrad(px, pdy, dw_kcs, kws, d.n * dpl.m, d.c, d.k, d.s, 8, q / dpl.m, stream);
         if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (planes)");
         return C1D_OK;
@@ -1012,6 +1135,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         const uint16_t* g16 = static_cast<const uint16_t*>(dy);
         if (wpd.pad || d.in_dtype == C1D_DTYPE_F32) {
             uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad));
+            if (bump.overflow) return workspace_overflow();
             e = wpd.pad ? launch_pad_rows(dy, d.in_dtype, tg, d.n * d.k, q, wpd.q_pad, stream)
                         : launch_round_bf16(static_cast<const float*>(dy), tg, d.n * d.k * q, stream);
             if (e != cudaSuccess) return cuda_fail(e, "dy copy");
@@ -1023,20 +1147,24 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
             const uint16_t* x16 = static_cast<const uint16_t*>(x);
             if (xw != d.w_in || d.in_dtype == C1D_DTYPE_F32) {
                 uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * xw));
+                if (bump.overflow) return workspace_overflow();
                 e = launch_pad_rows(x, d.in_dtype, tx, d.n * d.c, d.w_in, xw, stream);
                 if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
                 x16 = tx;
             }
             void* kws = bump.take<char>(tc_wgrad_xin_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+            if (bump.overflow) return workspace_overflow();
             e = launch_tc_wgrad_xin(x16, xw, g16, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, wpd.q_pad, stream);
             if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (expanded rows, inline)");
             return C1D_OK;
         }
         const int64_t rows = xr_wgrad_rows(d, wpd.q_pad);
         uint16_t* ex = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * d.c * rows));
+        if (bump.overflow) return workspace_overflow();
         e = launch_expand_rows(x, d.in_dtype, ex, d.n * d.c, d.w_in, d.d, 0, rows, stream);
         if (e != cudaSuccess) return cuda_fail(e, "expand_rows");
         void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+        if (bump.overflow) return workspace_overflow();
         e = launch_tc_wgrad(ex, g16, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, wpd.q_pad, stream, rows * 8);
         if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (expanded rows)");
         return C1D_OK;
@@ -1046,6 +1174,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     if (wpd.pad) {  // zero-padded bf16 copies with 8-element pitches (rounds FP32 storage too)
         uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * wpd.x_pitch));
         uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad));
+        if (bump.overflow) return workspace_overflow();
         e = launch_pad_rows(x, d.in_dtype, tx, d.n * d.c, d.w_in, wpd.x_pitch, stream);
         if (e == cudaSuccess) e = launch_pad_rows(dy, d.in_dtype, tg, d.n * d.k, q, wpd.q_pad, stream);
         if (e != cudaSuccess) return cuda_fail(e, "pad_rows");
@@ -1054,6 +1183,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
     } else if (d.in_dtype == C1D_DTYPE_F32) {
         uint16_t* tx = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));
         uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * q));
+        if (bump.overflow) return workspace_overflow();
         e = launch_round_bf16(static_cast<const float*>(x), tx, d.n * d.c * d.w_in, stream);
         if (e == cudaSuccess) e = launch_round_bf16(static_cast<const float*>(dy), tg, d.n * d.k * q, stream);
         if (e != cudaSuccess) return cuda_fail(e, "round_bf16");
@@ -1073,6 +1203,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         void* kws = bump.take<char>(kbytes);
         for (int64_t b = 0; b < dp.p && e == cudaSuccess; ++b) {
             const int64_t sb = ceil_div(d.s - b, dp.m);
+            if (bump.overflow) return workspace_overflow();
             e = launch_shift_copies(x, d.in_dtype, xs, d.n, d.c, d.w_in, 1, b * d.d, 0, xp, stream);
             if (e == cudaSuccess) e = launch_tc_wgrad(xs, gb, dwb, kws, d.n, d.c, d.k, sb, 8, wpd.q_pad, stream, xp);
             if (e == cudaSuccess) e = launch_scatter_phase_wgrad(dwb, dw_kcs, d.k, d.c, d.s, dp.m, b, stream);
@@ -1081,6 +1212,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         return C1D_OK;
     }
     void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, 8, wpd.q_pad));
+    if (bump.overflow) return workspace_overflow();
     e = launch_tc_wgrad(xb, gb, dw_kcs, kws, d.n, d.c, d.k, d.s, 8, wpd.q_pad, stream, wpd.pad ? wpd.x_pitch : 0);
     if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad");
     return C1D_OK;
@@ -1136,6 +1268,7 @@ c1d_status c1d_glued_workspace_size(const c1d_desc* desc, c1d_pass pass, int64_t
     int64_t q = 0;
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
+    const ExactAccumScope exact_scope(exact_for(*desc));
     if (pass == C1D_PASS_BACKWARD_WEIGHT) return fail(C1D_ERR_INVALID_ARGUMENT, "glue applies to conv-shaped passes");
     const c1d_algo a = resolve(*desc, pass, q);
     if (static_cast<int>(a) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
@@ -1153,6 +1286,7 @@ c1d_status c1d_forward_glued(const c1d_desc* desc, const void* x, const float* w
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
     const c1d_desc& d = *desc;
+    const ExactAccumScope exact_scope(exact_for(d));
     if (!glue || glue->act_pad < 0) return fail(C1D_ERR_INVALID_ARGUMENT, "bad forward glue");
     if (d.n == 0) return C1D_OK;
     if (d.n * d.k > 65535) return fail(C1D_ERR_UNSUPPORTED, "glue supports N*K <= 65535 rows");
@@ -1195,6 +1329,7 @@ c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const f
     c1d_status st = validate(desc, &q);
     if (st != C1D_OK) return st;
     const c1d_desc& d = *desc;
+    const ExactAccumScope exact_scope(exact_for(d));
     if (!glue || glue->off < 0 || glue->q <= 0 || glue->off + glue->q > d.w_in)
         return fail(C1D_ERR_INVALID_ARGUMENT, "bad backward glue window");
     if (d.n == 0) {
@@ -1245,6 +1380,12 @@ c1d_status c1d_backward_data_glued(const c1d_desc* desc, const void* dy, const f
                                                     d.c, glue->q, glue->mask != nullptr, glue->gsum, glue->grad_pre,
                                                     glue->grad_pre_bf16, glue->bias_grad, part, stream);
     return e == cudaSuccess ? C1D_OK : cuda_fail(e, "layer_backward_prologue");
+}
+
+c1d_status c1d_release_workspace(c1d_stream_t stream) {
+    t_last_error.clear();
+    const cudaError_t e = release_internal_workspace(reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "release_workspace");
 }
 
 uint64_t c1d_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }

@@ -8,6 +8,18 @@ namespace c1d {
 
 // Count of kernels this library launched (c1d_launch_count()).
 void note_launch(int n = 1);
+void set_last_error(const char* msg);  // detail text for c1d_last_error_message()
+
+// Accumulation-chain mode of the calling host thread's current pass (set by the C ABI from the
+// desc: FP32 precision, or BF16 with C1D_FLAG_EXACT_ACCUM). When set, the tensor-core kernels cap
+// every FP32 accumulation chain at ~4096 products (segmented backward-weight chains, two-region
+// conv reductions); see c1d.h C1D_FLAG_EXACT_ACCUM.
+bool exact_accum();
+struct ExactAccumScope {
+    bool saved;
+    explicit ExactAccumScope(bool on);
+    ~ExactAccumScope();
+};
 
 // Generic "forward-shaped" convolution:
 //   out[n][o][x] = sum_i sum_s wg[o][i][s] * in[n][i][x + s*dil + in_off]   (0 outside [0,in_w))
@@ -173,6 +185,19 @@ cudaError_t launch_sum3(const float* hh, const float* hl, const float* lh, float
                         cudaStream_t stream);
 cudaError_t launch_sum_split_blocks(const float* dw4, float* dw, int64_t K, int64_t C, int64_t S,
                                     cudaStream_t stream);
+// split patterns: 2-bit fields per channel block (0 hi, 1 mid / two-level lo, 2 three-level lo)
+constexpr unsigned kSplitHL = 0x4u;      // [hi | lo] (two-level)
+// conv-shaped FP32 passes: six channel blocks of the three-level split, x' = [h m h l h m] against
+// w' = [h h m h l m]: the products hh (main chain), hm, mh, hl, lh, mm (weights >= 2^-16)
+constexpr int kSplitBlocks = 6;
+constexpr unsigned kSplitX = 0x484u;  // fields 0 1 0 2 0 1
+constexpr unsigned kSplitW = 0x610u;  // fields 0 0 1 0 2 1
+constexpr unsigned kSplitHM = 0x4u;      // [hi | mid] (three-level)
+constexpr unsigned kSplitHL3 = 0x8u;     // [hi | lo3]
+constexpr unsigned kSplitL3H = 0x2u;     // [lo3 | hi]
+cudaError_t launch_sum_split3(const float* a, const float* b, float* dw, int64_t K, int64_t C, int64_t S,
+                              cudaStream_t stream);
+cudaError_t launch_sum6(const float* t, float* dw, int64_t count, cudaStream_t stream);
 
 int num_sms();
 

@@ -38,7 +38,27 @@ constexpr uint32_t kTmemCols = 512;
 constexpr int kLoaderThreads = 128;  // v3: warps 2, 3, 6, 7 stream X into the ring
 constexpr int kW2MaxStages = 6;
 constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage (the default cap)
-constexpr uint32_t kW2SmemBudget = 222 * 1024;  // v3 ring + stages (227 KB max per CTA, minus static + alignment)  // v3: warps 4-7 load X before running the epilogue
+constexpr uint32_t kW2SmemBudget = 222 * 1024;  // v3 ring + stages (227 KB max per CTA, minus static + alignment)
+// v3 warps: 0 dY TMA, 1 MMA issue, 2/3/6/7 X loaders, 4/5/10/11 accumulator drains (TMEM lane
+// quarters 0-3), 8/9 idle
+constexpr int kW2Threads = 384;
+// Accumulation segments: the tensor core's FP32 accumulation into one TMEM accumulator loses
+// ~1.1e-9 (norm-relative) per accumulated product with a consistent sign, so a CTA's chain over its
+// whole (item, K-step) split (config 3: ~3.2k K-steps = 52k products per dW entry) drifts to ~6e-5.
+// The MMA chain restarts every `seg` K-steps per accumulator copy (the first segment of a CTA is
+// shortened by a CTA-dependent amount so the CTAs' drains do not all land at once). The drain
+// warps copy each finished segment out of TMEM into its own slot (plain coalesced stores) and
+// hand TMEM back to the MMA warp; the reduce sums the (CTA, segment) slots in a fixed order.
+// Measured alternatives: red.add into one partial ran at the L2 atomic-unit rate (~48 us per
+// drain at config 3); adding each slot into an L2-resident running partial between drains needs
+// ~6 TB/s of extra L2 traffic at seg = 256 and stalled the MMAs behind it.
+// 256 K-steps = 4096 products per chain: ~4e-6 at config 3 (vs ~6e-5 unsegmented).
+constexpr int kW2SegChain = 256;
+__device__ __forceinline__ int64_t w2_seg_len(int64_t seg, int nseg_done, int cta, int ks) {
+    if (nseg_done > 0) return seg;
+    const int64_t first = seg * (8 + (cta & 7)) / 16;  // 1/2 .. 15/16 of a segment
+    return ((first + ks - 1) / ks) * ks;
+}
 
 struct WPlan {
     int cp, t, kp;
@@ -453,6 +473,10 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
 struct W2Params {
     int64_t n_items, c, k, s, q, w_in;
     int64_t steps_per_item, total_steps;
+    int64_t seg;  // K-steps per accumulation segment (0: the whole split is one chain)
+    int64_t slot_elems;  // floats per slot: K x (the role's taps) x C
+    int max_segs;        // slots per CTA
+    int* nseg;           // [cta]: slots this CTA wrote
     W2Plan pl;
     const uint16_t* x;  // [n][c][w_in] bf16
     float* part;        // [cta][k][c][s]
@@ -569,11 +593,11 @@ __device__ __forceinline__ void w2_expand_d(int off, uint32_t rc, int p0, int np
 #undef W2X
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kW2Threads, 1)
     tc_wgrad2_kernel(const __grid_constant__ CUtensorMap ymap, const W2Params p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[kW2MaxStages], empty[kW2MaxStages];
-    __shared__ uint64_t acc_done;
+    __shared__ uint64_t acc_full, acc_empty;
     __shared__ uint32_t tmem_base_s;
 
     const W2Plan& pl = p.pl;
@@ -593,7 +617,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&full[s], 1 + kLoaderThreads);  // dY TMA (tx bytes) + every X loader thread
             mbar_init(&empty[s], 1);
         }
-        mbar_init(&acc_done, 1);
+        mbar_init(&acc_full, 1);
+        mbar_init(&acc_empty, 4);  // one arrival per drain warp
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base_s);
@@ -647,7 +672,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // plain core-matrix layout with K-chunks one box apart.
         const uint32_t b_sbo = pl.bq == 8 ? 128u : 16u * static_cast<uint32_t>(pl.bq);
         const uint32_t b_lbo = pl.bq == 8 ? pl.box_bytes : 16u;
-        long long tf_sum = 0, ti_sum = 0, tc_sum = 0;
+        long long tf_sum = 0, ti_sum = 0, tc_sum = 0, te_sum = 0;
         const long long tb = clock64();
         int stage = 0;
         uint32_t phase = 0;
@@ -674,7 +699,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int ks = 0; ks < 9; ++ks)
             wi.b_off[ks] = static_cast<uint32_t>(ks / wi.per_box) * (wi.b_box + static_cast<uint32_t>(wi.per_box - 1) * wi.b_k) +
                            static_cast<uint32_t>(ks % wi.per_box) * wi.b_k;
-        int kdone = 0;  // K-steps issued so far (accumulator copy rotation)
+        int kdone = 0;  // K-steps issued so far
+        int seg_base = 0;  // kdone at the start of the current accumulation segment
+        int nseg_mma = 0;
+        uint32_t eph = 0;
         // ring bookkeeping mirrors the loaders': a segment (item) starts a fresh window of
         // span + kch chunks at v_pos; each later stage appends kch chunks and the window start
         // moves by kch
@@ -696,6 +724,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     v_pos += pl.kch;
                 }
                 if (v_pos >= pl.ring) v_pos -= pl.ring;
+                if (p.seg > 0 && kdone - seg_base >= w2_seg_len(p.seg, nseg_mma, blockIdx.x, pl.ks)) {
+                    // segment boundary: hand the accumulators to the drain warps, restart the chain
+                    if (elect_one()) mma_commit(smem_u32(&acc_full));
+                    __syncwarp();
+                    const long long te = clock64();
+                    mbar_wait(smem_u32(&acc_empty), eph);
+                    te_sum += clock64() - te;
+                    eph ^= 1;
+                    tc_fence_after();
+                    seg_base = kdone;
+                    ++nseg_mma;
+                }
                 const long long tf = clock64();
                 mbar_wait(smem_u32(&full[stage]), phase);
                 tf_sum += clock64() - tf;
@@ -710,12 +750,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const long long ti = clock64();
                 if (elect_one()) {
                     const uint64_t a_st = desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
+                    const int k0 = kdone - seg_base;  // K-step within the segment (copy rotation, init)
                     switch (g_count) {
-                        case 1: w2_issue_stage<1>(wi, tmem, a_st, by0, kdone, nks, 1); break;
-                        case 2: w2_issue_stage<2>(wi, tmem, a_st, by0, kdone, nks, 2); break;
-                        case 3: w2_issue_stage<3>(wi, tmem, a_st, by0, kdone, nks, 3); break;
-                        case 4: w2_issue_stage<4>(wi, tmem, a_st, by0, kdone, nks, 4); break;
-                        default: w2_issue_stage<0>(wi, tmem, a_st, by0, kdone, nks, g_count);
+                        case 1: w2_issue_stage<1>(wi, tmem, a_st, by0, k0, nks, 1); break;
+                        case 2: w2_issue_stage<2>(wi, tmem, a_st, by0, k0, nks, 2); break;
+                        case 3: w2_issue_stage<3>(wi, tmem, a_st, by0, k0, nks, 3); break;
+                        case 4: w2_issue_stage<4>(wi, tmem, a_st, by0, k0, nks, 4); break;
+                        default: w2_issue_stage<0>(wi, tmem, a_st, by0, k0, nks, g_count);
                     }
                 }
                 kdone += nks;
@@ -732,16 +773,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             cur = seg_end;
         }
-        if (elect_one()) mma_commit(smem_u32(&acc_done));
+        if (elect_one()) mma_commit(smem_u32(&acc_full));  // the last segment
         __syncwarp();
         if (p.prof && lane == 0) {
             p.prof[blockIdx.x * 8 + 2] = tf_sum;
             p.prof[blockIdx.x * 8 + 3] = ti_sum;
             p.prof[blockIdx.x * 8 + 5] = tc_sum;
             p.prof[blockIdx.x * 8 + 4] = clock64() - tb;
+            p.prof[blockIdx.x * 8 + 6] = te_sum;
         }
     }
-    if ((warp == 2 || warp == 3 || warp >= 6) && pl.xin) {
+    if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl.xin) {
         // ---- X loaders, inline expanded rows: the natural columns of a stage's positions land in
         // one of two `raw` buffers (16-B cp.async pieces, issued one stage ahead), then the loaders
         // write the ring rows (position p = the 8 elements at column D*p), proxy fence, arrive
@@ -835,7 +877,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             cur_s = nxt_s;
             have = have_next;
         }
-    } else if (warp == 2 || warp == 3 || warp >= 6) {
+    } else if (warp == 2 || warp == 3 || warp == 6 || warp == 7) {
         // ---- X loaders (warps 2, 3, 6, 7: the sub-partitions of the TMA and MMA warps stay free
         // of their issue load): 16-byte cp.async pieces straight from the [n][c][w] rows into the
         // q-chunk-major ring. One warp instruction moves 8 channels x 4 chunks: 64 contiguous bytes
@@ -892,50 +934,95 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         cp_async_wait_group<0>();
     }
-    if (warp >= 4) {
-        // ---- epilogue: D rows (t, c) x columns (p', k) -> partial[cta][k][tap][c] (c fastest: a
-        // warp's 32 lanes are consecutive channels, so every store is coalesced)
-        const int quarter = warp - 4;
+    if (warp == 4 || warp == 5 || warp == 10 || warp == 11) {
+        // ---- drains: D rows (t, c) x columns (p', k) -> slot[cta][j][k][tap - tap0][c] (c fastest:
+        // a warp's 32 lanes are consecutive channels, so every store is one coalesced 128-B line)
+        const int quarter = warp & 3;
         const int row = quarter * 32 + lane;
         const int t = row / pl.cp, c = row % pl.cp;
-        const bool have = kb < ke;
-        if (have) {
-            mbar_wait_sleep(smem_u32(&acc_done), 0, 1000);
+        const int role_taps = pl.gpc * pl.taps_per_group;
+        const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
+        const int kshift = __ffs(pl.kpw) - 1;  // KPw is a power of two >= 16: a 16-column chunk is
+        const int64_t kstride = static_cast<int64_t>(role_taps) * p.c;  // one (copy, filter run)
+        long long td_sum = 0;
+        // store 16 drained columns starting at col0 of group g
+        auto put16 = [&](float* dst, int g, int col0, const uint32_t (&v)[16]) {
+            if (c >= p.c) return;
+            const int pp = col0 >> kshift, kk0 = col0 & (pl.kpw - 1);
+            const int tap = g * pl.taps_per_group + t + pl.t * (pl.p - 1 - pp);
+            if (tap0 + tap >= p.s || kk0 >= p.k) return;
+            float* base = dst + (static_cast<int64_t>(kk0) * role_taps + tap) * p.c + c;
+            const int kn = static_cast<int>(imin(16, p.k - kk0));
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+                if (j < kn) base[j * kstride] = __uint_as_float(v[j]);
+        };
+        auto drain = [&](int64_t seg_k, int jslot, uint32_t parity) {
+            float* dst = p.part + (static_cast<int64_t>(blockIdx.x) * p.max_segs + jslot) * p.slot_elems;
+            mbar_wait_sleep(smem_u32(&acc_full), parity, 128);
             tc_fence_after();
-        }
-        float* dst = p.part + static_cast<int64_t>(blockIdx.x) * p.k * p.c * p.s;
-        for (int g = 0; g < g_count; ++g) {
-            const int64_t sgrp = tap0 + static_cast<int64_t>(g) * pl.taps_per_group + t;
-            for (int cb = 0; cb < pl.n; cb += 16) {
-                uint32_t v[16];
-                if (have) {
-                    const uint32_t lane_base = tmem + (static_cast<uint32_t>(quarter * 32) << 16);
-                    tmem_ld16(lane_base + static_cast<uint32_t>(g * pl.n + cb), v);
+            const long long td = clock64();
+            // copies this segment wrote (a short segment leaves the rest stale); order 0 + 1 + ...
+            const int used = static_cast<int>(imin(pl.copies, seg_k));
+            for (int g = 0; g < g_count; ++g) {
+                int col0 = 0;
+                if (used == 1) {  // four TMEM loads in flight per wait
+                    for (; col0 + 64 <= pl.n; col0 += 64) {
+                        uint32_t v0[16], v1[16], v2[16], v3[16];
+                        const uint32_t a0 = lane_base + static_cast<uint32_t>(g * pl.n + col0);
+                        tmem_ld16(a0, v0);
+                        tmem_ld16(a0 + 16, v1);
+                        tmem_ld16(a0 + 32, v2);
+                        tmem_ld16(a0 + 48, v3);
+                        tmem_ld_wait();
+                        put16(dst, g, col0, v0);
+                        put16(dst, g, col0 + 16, v1);
+                        put16(dst, g, col0 + 32, v2);
+                        put16(dst, g, col0 + 48, v3);
+                    }
+                }
+                for (; col0 < pl.n; col0 += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(lane_base + static_cast<uint32_t>(g * pl.n + col0), v);
                     tmem_ld_wait();
-                    // copies this CTA actually wrote (a CTA with fewer K-steps than copies leaves
-                    // the rest uninitialised); fixed order: copy 0 + 1 + ...
-                    const int used = static_cast<int>(imin(pl.copies, ke - kb));
                     for (int r = 1; r < used; ++r) {
                         uint32_t u[16];
-                        tmem_ld16(lane_base + static_cast<uint32_t>((r * pl.gpc + g) * pl.n + cb), u);
+                        tmem_ld16(lane_base + static_cast<uint32_t>((r * pl.gpc + g) * pl.n + col0), u);
                         tmem_ld_wait();
 #pragma unroll
                         for (int j = 0; j < 16; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(u[j]));
                     }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = 0;
-                }
-                if (c < p.c) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int col = cb + j;
-                        const int pp = col / pl.kpw, kk = col % pl.kpw;
-                        const int64_t tap = sgrp + static_cast<int64_t>(pl.t) * (pl.p - 1 - pp);
-                        if (kk < p.k && tap < p.s) dst[(static_cast<int64_t>(kk) * p.s + tap) * p.c + c] = __uint_as_float(v[j]);
-                    }
+                    put16(dst, g, col0, v);
                 }
             }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&acc_empty));
+            td_sum += clock64() - td;
+        };
+        int nseg = 0;
+        if (kb < ke) {
+            // the MMA warp's segmentation, replayed
+            int64_t kd = 0, sb = 0;
+            for (int64_t cur = kb; cur < ke;) {
+                const int64_t item = cur / p.steps_per_item;
+                const int64_t seg_end = imin(ke, (item + 1) * p.steps_per_item);
+                for (int64_t st = cur; st < seg_end; st += pl.ks) {
+                    if (p.seg > 0 && kd - sb >= w2_seg_len(p.seg, nseg, blockIdx.x, pl.ks)) {
+                        drain(kd - sb, nseg, static_cast<uint32_t>(nseg & 1));
+                        ++nseg;
+                        sb = kd;
+                    }
+                    kd += imin(pl.ks, seg_end - st);
+                }
+                cur = seg_end;
+            }
+            drain(kd - sb, nseg, static_cast<uint32_t>(nseg & 1));
+            ++nseg;
+        }
+        if (warp == 4 && lane == 0) {
+            p.nseg[blockIdx.x] = nseg;  // 0: no work, no slots
+            if (p.prof) p.prof[blockIdx.x * 8 + 7] = td_sum;
         }
     }
     tc_fence_before();
@@ -944,31 +1031,54 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 2) tmem_dealloc<kTmemCols>(tmem);
 }
 
-// dw = sum over the role's CTAs (ascending) of part[cta][e], e = (k*S + s)*C + c in the partials'
-// (k, tap, channel) order (coalesced reads); the sum lands at dw[(k*C + c)*S + s] (KCS). A block
-// covers 64 outputs x 4 CTA quarters: each thread sums its quarter of the CTAs in order (all loads
-// in flight), then the four quarter sums are added in order (fixed shape, deterministic).
-__global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restrict__ part, float* __restrict__ dw,
-                                                            int64_t K, int64_t C, int64_t S, const W2Plan pl) {
+// dw = the fixed-order sum over the role's CTAs (ascending) and each CTA's segment slots (ascending)
+// of slot[cta][j][k][tap - tap0][c]; the sum lands at dw[(k*C + c)*S + s] (KCS). Entries are taken
+// in (k, s, c) order so a warp reads consecutive channels (coalesced). A block covers 64 outputs x
+// 4 CTA quarters: each thread sums its quarter in order (eight loads in flight), then the four
+// quarter sums are added in order (fixed shape, deterministic).
+__global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restrict__ part, const int* __restrict__ nseg,
+                                                            float* __restrict__ dw, int64_t K, int64_t C, int64_t S,
+                                                            int max_segs, int64_t slot_elems, const W2Plan pl) {
     __shared__ float red[4][64];
     pdl_trigger();
     pdl_wait();
     const int64_t count = K * C * S;
     const int64_t e = static_cast<int64_t>(blockIdx.x) * 64 + (threadIdx.x % 64);
     const int quarter = threadIdx.x / 64;
+    const int role_taps = pl.gpc * pl.taps_per_group;
     float v = 0.0f;
     if (e < count) {
-        const int64_t s = (e / C) % S;
-        const int role = static_cast<int>(s / (static_cast<int64_t>(pl.gpc) * pl.taps_per_group));
+        const int64_t c = e % C, s = (e / C) % S, k = e / (C * S);
+        const int role = static_cast<int>(s / role_taps);
+        const int64_t idx = (k * role_taps + (s - static_cast<int64_t>(role) * role_taps)) * C + c;
         const int b0 = pl.role_cta_begin[role], b1 = pl.role_cta_begin[role + 1];
         const int n = b1 - b0;
         const int lo = b0 + n * quarter / 4, hi = b0 + n * (quarter + 1) / 4;
-        float t[16];
+        if (max_segs == 1) {
+            float t[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) t[j] = (lo + j < hi) ? part[static_cast<int64_t>(lo + j) * count + e] : 0.0f;
+            for (int j = 0; j < 16; ++j)
+                t[j] = (lo + j < hi && __ldg(nseg + lo + j) > 0) ? __ldg(part + static_cast<int64_t>(lo + j) * slot_elems + idx)
+                                                                  : 0.0f;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v += t[j];
-        for (int b = lo + 16; b < hi; ++b) v += part[static_cast<int64_t>(b) * count + e];
+            for (int j = 0; j < 16; ++j)
+                if (lo + j < hi) v += t[j];
+            for (int b = lo + 16; b < hi; ++b)
+                if (__ldg(nseg + b) > 0) v += __ldg(part + static_cast<int64_t>(b) * slot_elems + idx);
+        } else {
+            for (int b = lo; b < hi; ++b) {
+                const int ns = __ldg(nseg + b);
+                const float* src = part + static_cast<int64_t>(b) * max_segs * slot_elems + idx;
+                for (int j = 0; j < ns; j += 8) {
+                    float t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) t[u] = j + u < ns ? __ldg(src + static_cast<int64_t>(j + u) * slot_elems) : 0.0f;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (j + u < ns) v += t[u];
+                }
+            }
+        }
     }
     red[quarter][threadIdx.x % 64] = v;
     __syncthreads();
@@ -995,6 +1105,36 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }  // namespace
 
 namespace {
+// Segment bookkeeping of a v3 launch (shared by the workspace sizing and the launch).
+struct W2Seg {
+    int64_t steps_per_item, total_steps, seg, slot_elems;
+    int max_segs;
+    size_t part_bytes, nseg_bytes;
+};
+W2Seg w2_segments(const W2Plan& pl, int64_t n, int64_t c, int64_t k, int64_t q) {
+    W2Seg r{};
+    // reduction columns q in [0, Q + (P-1)*Bq): copy p' reaches (P-1-p')*Bq columns back
+    r.steps_per_item = ceil_div(q + static_cast<int64_t>(pl.p - 1) * pl.bq, 16);
+    r.total_steps = n * r.steps_per_item;
+    static const int64_t seg_env = [] {  // C1D_W2_SEG: dev override of kW2SegChain (0 = off)
+        const char* e = getenv("C1D_W2_SEG");
+        return e ? static_cast<int64_t>(atoll(e)) : int64_t{-1};
+    }();
+    // segmented chains only in the exact-accumulation mode (FP32, or C1D_FLAG_EXACT_ACCUM)
+    const int64_t seg_chain = !exact_accum() ? 0 : (seg_env >= 0 ? seg_env : static_cast<int64_t>(kW2SegChain));
+    // segment length in K-steps: kW2SegChain per accumulator copy, rounded up to whole stages
+    r.seg = seg_chain > 0 ? ceil_div(seg_chain * pl.copies, pl.ks) * pl.ks : 0;
+    int64_t longest = 0;  // the longest CTA split (K-steps)
+    for (int ro = 0; ro < pl.roles; ++ro)
+        longest = std::max<int64_t>(longest, ceil_div(r.total_steps, pl.role_cta_begin[ro + 1] - pl.role_cta_begin[ro]));
+    // segments of >= seg K-steps after a first one of >= seg/2: at most (longest - seg/2)/seg + 2
+    r.max_segs = r.seg > 0 ? static_cast<int>(std::max<int64_t>(0, longest - r.seg / 2) / r.seg + 2) : 1;
+    r.slot_elems = k * c * static_cast<int64_t>(pl.gpc) * pl.taps_per_group;
+    r.part_bytes = (sizeof(float) * static_cast<size_t>(pl.grid) * r.max_segs * r.slot_elems + 255) & ~size_t{255};
+    r.nseg_bytes = sizeof(int) * static_cast<size_t>(pl.grid);
+    return r;
+}
+
 cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw_kcs, void* workspace, int64_t n,
                       int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, const W2Plan& pl, cudaStream_t stream,
                       int64_t x_w) {
@@ -1027,18 +1167,22 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
     wp.s = s;
     wp.q = q;
     wp.w_in = w_in;
-    // reduction columns q in [0, Q + (P-1)*Bq): copy p' reaches (P-1-p')*Bq columns back
-    wp.steps_per_item = ceil_div(q + static_cast<int64_t>(pl.p - 1) * pl.bq, 16);
-    wp.total_steps = n * wp.steps_per_item;
+    const W2Seg sg = w2_segments(pl, n, c, k, q);
+    wp.steps_per_item = sg.steps_per_item;
+    wp.total_steps = sg.total_steps;
+    wp.seg = sg.seg;
+    wp.slot_elems = sg.slot_elems;
+    wp.max_segs = sg.max_segs;
     wp.pl = pl;
     wp.x = x_bf16;
     wp.part = static_cast<float*>(workspace);
+    wp.nseg = reinterpret_cast<int*>(static_cast<char*>(workspace) + sg.part_bytes);
     static const bool profile = getenv("C1D_PROFILE") != nullptr;
     if (profile) {
         cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * pl.grid);
         cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * pl.grid);
     }
-    e = launch_pdl(tc_wgrad2_kernel, dim3(pl.grid), dim3(kThreads), pl.smem_bytes, stream, ymap, wp);
+    e = launch_pdl(tc_wgrad2_kernel, dim3(pl.grid), dim3(kW2Threads), pl.smem_bytes, stream, ymap, wp);
     note_launch();
     if (e != cudaSuccess) return e;
     if (profile) {
@@ -1048,8 +1192,8 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         for (int bb = 0; bb < pl.grid; ++bb)
             for (int i2 = 0; i2 < 8; ++i2) acc[i2] += static_cast<double>(h[bb * 8 + i2]) / pl.grid;
         fprintf(stderr, "[tc_wgrad3 prof] T=%d P=%d N=%d gpc=%d roles=%d ks=%d stages=%d span=%d ring=%d nbox=%d copies=%d xb=%d | "
-                "producer wait_empty %.0f / total %.0f | mma wait_full %.0f issue %.0f commit %.0f total %.0f\n",
-                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.span, pl.ring, pl.nbox, pl.copies, pl.xb, acc[0], acc[1], acc[2], acc[3], acc[5], acc[4]);
+                "producer wait_empty %.0f / total %.0f | mma wait_full %.0f issue %.0f commit %.0f wait_drain %.0f total %.0f | drain %.0f\n",
+                pl.t, pl.p, pl.n, pl.gpc, pl.roles, pl.ks, pl.stages, pl.span, pl.ring, pl.nbox, pl.copies, pl.xb, acc[0], acc[1], acc[2], acc[3], acc[5], acc[6], acc[4], acc[7]);
         for (int r = 0; r < pl.roles; ++r) {
             unsigned long long mx = 0, wf = 0;
             for (int bb = pl.role_cta_begin[r]; bb < pl.role_cta_begin[r + 1]; ++bb) {
@@ -1064,8 +1208,9 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
     const int64_t count = k * c * s;
     note_launch();
     return launch_pdl(wgrad2_reduce_kernel, dim3(static_cast<unsigned>(ceil_div(count, 64))), dim3(256), 0, stream,
-                      static_cast<const float*>(wp.part), dw_kcs, static_cast<int64_t>(k), static_cast<int64_t>(c),
-                      static_cast<int64_t>(s), pl);
+                      static_cast<const float*>(wp.part), static_cast<const int*>(wp.nseg), dw_kcs,
+                      static_cast<int64_t>(k), static_cast<int64_t>(c), static_cast<int64_t>(s), sg.max_segs,
+                      sg.slot_elems, pl);
 }
 }  // namespace
 
@@ -1077,8 +1222,10 @@ bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, i
 
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
     W2Plan p2;
-    if (make_w2plan(n, c, k, s, d, q, &p2))
-        return sizeof(float) * static_cast<size_t>(p2.grid) * static_cast<size_t>(k * c * s);
+    if (make_w2plan(n, c, k, s, d, q, &p2)) {
+        const W2Seg sg = w2_segments(p2, n, c, k, q);
+        return sg.part_bytes + sg.nseg_bytes;
+    }
     WPlan p;
     if (!make_wplan(n, c, k, s, d, q, &p)) return 0;
     return sizeof(float) * static_cast<size_t>(p.roles) * p.splits * static_cast<size_t>(k * c * s);
@@ -1092,7 +1239,8 @@ bool tc_wgrad_xin_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t 
 size_t tc_wgrad_xin_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
     W2Plan p2;
     if (!make_w2plan(n, c, k, s, d, q, &p2, true)) return 0;
-    return sizeof(float) * static_cast<size_t>(p2.grid) * static_cast<size_t>(k * c * s);
+    const W2Seg sg = w2_segments(p2, n, c, k, q);
+    return sg.part_bytes + sg.nseg_bytes;
 }
 
 cudaError_t launch_tc_wgrad_xin(const uint16_t* x_bf16, int64_t x_w, const uint16_t* dy_bf16, float* dw_kcs,

@@ -13,11 +13,16 @@ Mirrors the reference's layer/network code (proj/src/train.cpp) on device tensor
                    conv-ReLU, conv-ReLU, conv-ReLU with the block input added after the last ReLU
                    (the reference does not specify the 3-conv arrangement; this is the natural
                    generalisation of its one-conv block).
-* losses           mse_loss / bce_with_logits (train.cpp:106-135), means over the local batch.
+* losses           mse_loss + bce_with_logits (train.cpp:106-135), means over the local batch, in one
+                   device pass (c1d_mse_bce_loss) that writes both heads' gradients; torch
+                   float64 restatements (mse_loss, bce_with_logits) stay for checks.
 * `train_step`     forward, combined loss, backward; with a process group the gradients of every
                    layer (one flat bucket) are all-reduced and divided by the world size (the
                    local losses are means over local items).
-* `sgd_step`       p <- p - lr*g (train.cpp:137-141).
+* `sgd_step`       p <- p - lr*g (train.cpp:137-141) over the flat parameter / gradient buckets
+                   (c1d_sgd_update, one launch).
+* samplers         Poisson(2) inputs / targets and Bernoulli(0.1) labels (c1d_fill_poisson /
+                   c1d_fill_bernoulli) for BASELINE config 5; `auroc` (train.cpp:143-171).
 
 Fused glue (through the C ABI's glued passes): every layer's forward is ONE
 call, c1d_forward_glued, whose tcgen05 epilogue adds the bias, applies ReLU and the skip, writes
@@ -38,10 +43,10 @@ import ctypes as C
 import math
 
 import torch
-import torch.distributed as dist
 
 from . import _lib as L
 from . import conv as cv
+from . import parallel
 
 
 def _uniform(shape, limit, gen, device):
@@ -174,28 +179,47 @@ class ResidualNet:
     """BASELINE config 5: input layer, `blocks` residual blocks of `convs_per_block` convs, 2 heads."""
 
     def __init__(self, blocks=5, convs_per_block=3, hidden=15, taps=51, dilation=8,
-                 precision=cv.Precision.Bf16, seed=1, device="cuda"):
+                 precision=cv.Precision.Bf16, seed=1, device="cuda", precision_rule="all"):
+        """precision_rule "all": every conv but the 1-tap heads runs in `precision` (BASELINE config
+        5: BF16 with 15 channels, which the C ABI accepts). "reference": make_layer's rule
+        (train.cpp:233-239), BF16 only where the channel and filter counts are both even, so the
+        1-channel input layer stays FP32 (the layout the reference's DemoNet uses)."""
+        if precision_rule not in ("all", "reference"):
+            raise ValueError("precision_rule is 'all' or 'reference'")
         gen = torch.Generator(device=device).manual_seed(seed)
         self.device = device
-        self.input = ConvLayer(1, hidden, taps, dilation, precision, True, False, 1.0, gen, device)
-        self.blocks = [[ConvLayer(hidden, hidden, taps, dilation, precision, True, True, 0.3, gen, device)
+
+        def prec(cin, cout):
+            if precision_rule == "reference" and (cin % 2 or cout % 2):
+                return cv.Precision.Fp32
+            return precision
+
+        self.input = ConvLayer(1, hidden, taps, dilation, prec(1, hidden), True, False, 1.0, gen, device)
+        self.blocks = [[ConvLayer(hidden, hidden, taps, dilation, prec(hidden, hidden), True, True, 0.3, gen, device)
                         for _ in range(convs_per_block)] for _ in range(blocks)]
         self.reg_head = ConvLayer(hidden, 1, 1, 1, cv.Precision.Fp32, False, False, 0.1, gen, device)
         self.peak_head = ConvLayer(hidden, 1, 1, 1, cv.Precision.Fp32, False, False, 0.1, gen, device)
         # both 1-tap heads run as ONE 2-filter FP32 conv (each output channel is accumulated on its
         # own, so the values are the separate heads'): h is read once per pass
         self.heads = ConvLayer(hidden, 2, 1, 1, cv.Precision.Fp32, False, False, 0.1, gen, device)
-        # one flat gradient bucket (all dW and bias grads) for a single all-reduce per step
+        # one flat gradient bucket (all dW and bias grads) for a single all-reduce per step, and a
+        # parameter bucket in the same order (w then bias per layer, the reference's gather_params
+        # order, train.cpp:318-325) so the SGD update is one pass over two flat vectors
         layers = self.layers()
         n = sum(t.numel() for layer in layers for t in layer.gradients())
         self.grad_bucket = torch.zeros(n, device=device)
+        self.param_bucket = torch.zeros(n, device=device)
         off = 0
         for layer in layers:
-            views = []
-            for g in layer.gradients():
-                views.append(self.grad_bucket[off:off + g.numel()].view_as(g))
+            gviews, pviews = [], []
+            for g, prm in zip(layer.gradients(), layer.parameters()):
+                gviews.append(self.grad_bucket[off:off + g.numel()].view_as(g))
+                pv = self.param_bucket[off:off + prm.numel()].view_as(prm)
+                pv.copy_(prm)
+                pviews.append(pv)
                 off += g.numel()
-            layer.grad_w, layer.grad_b = views
+            layer.grad_w, layer.grad_b = gviews
+            layer.w, layer.b = pviews
         self._bufs = {}
 
     def pad(self) -> int:
@@ -280,9 +304,19 @@ class ResidualNet:
         skip gradient, ReLU mask, BF16 rounding and bias gradient happen in the conv epilogue."""
         h = self.h_last
         n, hidden, width = h.shape
-        heads = self.heads
-        g2 = self._buf("g.heads", (n, 2, width), torch.float32)
+        g2 = self.head_grad_buffer(n, width)
         torch.cat([grad_pred, grad_logits], dim=1, out=g2)
+        self.backward_heads(g2)
+
+    def head_grad_buffer(self, n: int, width: int) -> torch.Tensor:
+        """(N, 2, width) gradient of the two heads' outputs (channel 0 regression, 1 peak logits)."""
+        return self._buf("g.heads", (n, 2, width), torch.float32)
+
+    def backward_heads(self, g2: torch.Tensor) -> None:
+        """The backward pass from the heads' output gradient g2 = head_grad_buffer(...)."""
+        h = self.h_last
+        n, hidden, width = h.shape
+        heads = self.heads
         layer_backward_prologue(g2, 0, None, n, 2, width, relu=False, bias_grad=heads.grad_b)
         heads.backward_weight(g2)
         chain = [self.input] + [layer for blk in self.blocks for layer in blk]  # forward order
@@ -336,12 +370,91 @@ class ResidualNet:
         cv.conv1d_backward_data(gp, first.w, first.p, out=self._buf("dx.in", (n, 1, first.x_in.shape[2]),
                                                                      torch.float32))
 
+    def load_params(self, flat) -> None:
+        """Set every weight and bias from a flat vector in the reference's gather_params order
+        (train.cpp:318-325; layers() order, w then bias)."""
+        flat = torch.as_tensor(flat, dtype=torch.float32).reshape(-1)
+        if flat.numel() != self.param_bucket.numel():
+            raise cv.ShapeMismatch(f"flat parameter vector has {flat.numel()} values, the net {self.param_bucket.numel()}")
+        self.param_bucket.copy_(flat.to(self.param_bucket.device))
+
     def sgd_step(self, lr: float) -> None:
+        """p <- p - lr*g over the flat buckets (sgd_step, train.cpp:137-141): one fused launch."""
         if not lr > 0:
             raise ValueError("sgd_step needs a positive learning rate")
-        for layer in self.layers():
-            for p, g in zip(layer.parameters(), layer.gradients()):
-                p.sub_(lr * g)
+        sgd_update_(self.param_bucket, self.grad_bucket, lr)
+
+
+def sgd_update_(params: torch.Tensor, grads: torch.Tensor, lr: float) -> None:
+    """params <- params - lr*grads in place: c1d_sgd_update, one launch over the flat buckets with
+    the reference's float rounding (a multiply, then a subtract; train.cpp:137-141)."""
+    if params.shape != grads.shape or params.dtype != torch.float32 or not params.is_contiguous() \
+            or not grads.is_contiguous():
+        raise cv.ShapeMismatch("sgd_update_ needs two contiguous float32 tensors of one shape")
+    cv._check(L.lib().c1d_sgd_update(params.data_ptr(), grads.data_ptr(), params.numel(), lr,
+                                     torch.cuda.current_stream(params.device).cuda_stream))
+
+
+def fill_poisson(shape, lam: float, seed: int, device) -> torch.Tensor:
+    """Poisson(lam) counts as float32 (c1d_fill_poisson: Knuth's product of uniforms on a
+    per-element splitmix64 stream; the reference's Rng has no Poisson sampler)."""
+    out = torch.empty(shape, dtype=torch.float32, device=device)
+    cv._check(L.lib().c1d_fill_poisson(out.data_ptr(), out.numel(), lam, seed,
+                                       torch.cuda.current_stream(out.device).cuda_stream))
+    return out
+
+
+def fill_bernoulli(shape, p: float, seed: int, device) -> torch.Tensor:
+    """Bernoulli(p) 0/1 labels as float32 (c1d_fill_bernoulli, same per-element streams)."""
+    out = torch.empty(shape, dtype=torch.float32, device=device)
+    cv._check(L.lib().c1d_fill_bernoulli(out.data_ptr(), out.numel(), p, seed,
+                                         torch.cuda.current_stream(out.device).cuda_stream))
+    return out
+
+
+def sample_inputs(n: int, width: int, pad: int, seed: int, device):
+    """BASELINE config 5's synthetic batch: inputs ~ Poisson(2) zero-padded by `pad` columns per
+    side, regression targets ~ Poisson(2), peak labels ~ Bernoulli(0.1); three seeded streams."""
+    x = torch.zeros((n, 1, width + 2 * pad), dtype=torch.float32, device=device)
+    x[:, :, pad:pad + width] = fill_poisson((n, 1, width), 2.0, 3 * seed, device)
+    return x, fill_poisson((n, 1, width), 2.0, 3 * seed + 1, device), fill_bernoulli((n, 1, width), 0.1, 3 * seed + 2,
+                                                                                    device)
+
+
+_LOSS_WS = {}
+
+
+def mse_bce(pred: torch.Tensor, logits: torch.Tensor, target: torch.Tensor, labels: torch.Tensor,
+            bce_weight: float = 1.0, grad: torch.Tensor | None = None) -> torch.Tensor:
+    """mse_loss + bce_weight * bce_with_logits on the device (c1d_mse_bce_loss, one pass;
+    train.cpp:106-135). pred / logits are (N, 1, W) views sharing one item stride (e.g. channels 0
+    and 1 of the heads' (N, 2, W) output); grad, if given, is an (N, 2, W) buffer that receives
+    the regression gradient in channel 0 and bce_weight * the logit gradient in channel 1.
+    Returns a float64 device tensor [mse, bce, total]."""
+    n, _, width = pred.shape
+    stride = pred.stride(0)
+    if logits.stride(0) != stride or pred.stride(2) != 1 or logits.stride(2) != 1:
+        raise cv.ShapeMismatch("pred and logits must be unit-stride rows with one item stride")
+    tgt, lab = target.contiguous(), labels.contiguous()
+    if tgt.numel() != n * width or lab.numel() != n * width:
+        raise cv.ShapeMismatch("targets and labels must be (N, 1, W)")
+    dev = pred.device
+    key = (dev, torch.cuda.current_stream(dev).cuda_stream)
+    ws = _LOSS_WS.get(key)
+    if ws is None:
+        ws = torch.zeros(L.lib().c1d_loss_workspace_size(), dtype=torch.uint8, device=dev)
+        _LOSS_WS[key] = ws
+    out = torch.empty(3, dtype=torch.float64, device=dev)
+    gp = gl = None
+    gstride = 0
+    if grad is not None:
+        if tuple(grad.shape) != (n, 2, width) or not grad.is_contiguous():
+            raise cv.ShapeMismatch("grad must be a contiguous (N, 2, W) buffer")
+        gp, gl, gstride = grad.data_ptr(), grad.data_ptr() + 4 * width, 2 * width
+    cv._check(L.lib().c1d_mse_bce_loss(pred.data_ptr(), logits.data_ptr(), stride, tgt.data_ptr(), lab.data_ptr(), n,
+                                       width, bce_weight, gp, gl, gstride, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       torch.cuda.current_stream(dev).cuda_stream))
+    return out
 
 
 def mse_loss(pred: torch.Tensor, target: torch.Tensor):
@@ -359,16 +472,43 @@ def bce_with_logits(logits: torch.Tensor, mask: torch.Tensor):
     return value, ((torch.sigmoid(l) - m) / n).float()
 
 
-def train_step(net: ResidualNet, x_padded, target, labels, bce_weight: float = 1.0, group=None):
-    """One data-parallel training step on this rank's shard; returns the local loss (a tensor)."""
+def auroc(scores: torch.Tensor, labels: torch.Tensor) -> float:
+    """Area under the ROC curve by the rank statistic with ties averaged (auroc, train.cpp:143-171),
+    on the device: stable sort, tie groups as runs of equal scores, 1-based ranks i+1..j averaged
+    per group, U = sum of positive ranks - P(P+1)/2, AUROC = U / (P*N). NaN with one class."""
+    s = scores.reshape(-1).float()
+    pos_mask = labels.reshape(-1) > 0.5
+    n = s.numel()
+    order = torch.argsort(s, stable=True)
+    ss, ll = s[order], pos_mask[order].double()
+    _, counts = torch.unique_consecutive(ss, return_counts=True)
+    ends = torch.cumsum(counts, 0).double()
+    rank = 0.5 * (ends - counts.double() + 1 + ends)
+    group = torch.repeat_interleave(torch.arange(counts.numel(), device=s.device), counts)
+    pos_per_group = torch.zeros(counts.numel(), dtype=torch.float64, device=s.device).index_add_(0, group, ll)
+    pos = float(ll.sum())
+    neg = n - pos
+    if pos == 0.0 or neg == 0.0:
+        return float("nan")
+    u = float((rank * pos_per_group).sum()) - pos * (pos + 1.0) / 2.0
+    return u / (pos * neg)
+
+
+def forward_backward(net: ResidualNet, x_padded, target, labels, bce_weight: float = 1.0):
+    """The local part of a training step (train_step, train.cpp:327-353): forward, combined loss
+    mse + bce_weight*bce, full backward into net.grad_bucket. No collective, so it can be captured
+    in a CUDA graph. Returns the local loss (a device tensor)."""
     pred, logits = net.forward(x_padded)
-    mse, g_pred = mse_loss(pred, target)
-    bce, g_log = bce_with_logits(logits, labels)
-    loss = mse + bce_weight * bce
-    net.backward(g_pred, bce_weight * g_log)
-    if group is not None or (dist.is_available() and dist.is_initialized()):
-        world = dist.get_world_size(group)
-        if world > 1:
-            dist.all_reduce(net.grad_bucket, group=group)
-            net.grad_bucket.div_(world)
+    n, _, width = pred.shape
+    g2 = net.head_grad_buffer(n, width)
+    loss3 = mse_bce(pred, logits, target, labels, bce_weight, grad=g2)  # losses + both head gradients
+    net.backward_heads(g2)
+    return loss3[2]
+
+
+def train_step(net: ResidualNet, x_padded, target, labels, bce_weight: float = 1.0, group=None):
+    """One data-parallel training step on this rank's shard: forward_backward, then the bucket
+    all-reduce divided by the world size (parallel.allreduce_mean_). Returns the local loss."""
+    loss = forward_backward(net, x_padded, target, labels, bce_weight)
+    parallel.allreduce_mean_(net.grad_bucket, group)
     return loss

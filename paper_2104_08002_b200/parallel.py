@@ -1,10 +1,16 @@
-"""Data-parallel plumbing for the conv layer.
+"""Data-parallel plumbing; the product's only collective code.
 
 The batch shards exactly like the reference's `parallel_for_items` (proj/src/conv.cpp:15-31):
 contiguous item ranges, rank r owning items [n*r/world, n*(r+1)/world). Forward and
-backward-data need no communication; backward-weight produces a per-rank partial dW that one
-all-reduce (NCCL on B200, gloo in the CPU tests) sums — the multi-GPU form of the reference's
-ascending per-item reduction (conv.cpp:308-314).
+backward-data need no communication. Backward-weight produces a per-rank partial dW that one
+all-reduce sums: the multi-GPU form of the reference's ascending per-item reduction
+(conv.cpp:308-314). NCCL carries it on B200; the CPU tests run the same functions over gloo.
+
+Callers:
+* `bench.py` (layer workload, weak scaling): `allreduce_sum_(dW)` once per step.
+* `network.train_step` (config 5, strong scaling): `allreduce_mean_(grad_bucket)` once per step
+  over the flat bucket of every layer's dW and bias gradient; the losses are means over the local
+  items (train.cpp:110,125), so the global gradient is the sum over ranks divided by the world size.
 """
 from __future__ import annotations
 
@@ -19,11 +25,27 @@ def shard_range(n_items: int, rank: int, world: int) -> tuple[int, int]:
     return n_items * rank // world, n_items * (rank + 1) // world
 
 
-def allreduce_dw(dw: torch.Tensor, group=None) -> torch.Tensor:
-    """Sum the per-rank partial weight gradients in place (one collective per step)."""
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(dw, op=dist.ReduceOp.SUM, group=group)
-    return dw
+def world_size(group=None) -> int:
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_world_size(group)
+    return 1
+
+
+def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the per-rank partials in place (one collective); no-op on one process."""
+    if world_size(group) > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+    return t
+
+
+def allreduce_mean_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum over ranks, then divide by the world size, in place: the global-batch gradient from
+    per-rank gradients of local-mean losses."""
+    w = world_size(group)
+    if w > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        t.div_(w)
+    return t
 
 
 def data_parallel_backward_weight(grad_out: torch.Tensor, inp: torch.Tensor, params, group=None,
@@ -34,5 +56,4 @@ def data_parallel_backward_weight(grad_out: torch.Tensor, inp: torch.Tensor, par
     local partial (defaults to the B200 kernel through the C ABI)."""
     if wgrad is None:
         from .conv import conv1d_backward_weight as wgrad
-    dw = wgrad(grad_out, inp, params)
-    return allreduce_dw(dw, group)
+    return allreduce_sum_(wgrad(grad_out, inp, params), group)

@@ -30,7 +30,7 @@ def _t(a, dtype=torch.float32):
     return torch.from_numpy(np.ascontiguousarray(a)).to("cuda").to(dtype)
 
 
-def run_passes(x, w, dy, d, precision=cv.Precision.Fp32, algo="auto", bf16_storage=False):
+def run_passes(x, w, dy, d, precision=cv.Precision.Fp32, algo="auto", bf16_storage=False, exact=False):
     k, c, s = w.shape
     p = cv.ConvParams(c, k, s, d, precision)
     if bf16_storage:
@@ -38,9 +38,9 @@ def run_passes(x, w, dy, d, precision=cv.Precision.Fp32, algo="auto", bf16_stora
     else:
         xt, gt = _t(x), _t(dy)
     wt = _t(w)
-    y = cv.conv1d_forward(xt, cv.pack_weights_forward(wt), p, algo=algo)
-    dx = cv.conv1d_backward_data(gt, cv.pack_weights_backward(wt), p, algo=algo)
-    dw = cv.conv1d_backward_weight(gt, xt, p, algo=algo)
+    y = cv.conv1d_forward(xt, cv.pack_weights_forward(wt), p, algo=algo, exact=exact)
+    dx = cv.conv1d_backward_data(gt, cv.pack_weights_backward(wt), p, algo=algo, exact=exact)
+    dw = cv.conv1d_backward_weight(gt, xt, p, algo=algo, exact=exact)
     torch.cuda.synchronize()
     return y.cpu().numpy(), dx.cpu().numpy(), dw.cpu().numpy()
 
