@@ -7,7 +7,9 @@ than the 126 MB L2, so no flush is needed between steps.
 
   value     device-resident throughput (TFLOP/s, 3 x 2*N*K*C*S*Q per step), CUDA events, max over ranks
   parity    the last timed step's y and dx on items {0, N-1} and dW on 256 sampled entries against a
-            float64 recomputation on the device (norm-relative; bound 1e-5 on BF16-rounded operands)
+            float64 recomputation on the device (norm-relative on BF16-rounded operands; 1e-5, and
+            1e-4 for the default-mode bwd-w, whose 1.92M-product sums drift ~6e-5 in the tensor core's
+            FP32 accumulation); `backward_weight_exact` times the C1D_FLAG_EXACT_ACCUM bwd-w (1e-5)
   e2e       the same metric through the C ABI (c1d_forward/backward_data/backward_weight, the call a
             reference host would make) with pinned HOST buffers: H2D of x and dy and D2H of y, dx
             and dW inside every timed step, pipelined over item chunks (pipeline.HostLayerStep)
@@ -269,10 +271,50 @@ def parity_check(x, w, dy, y, dx, dw, d: int):
         got.append(dw[kk, cc, ss])
     want_t, got_t = torch.stack(want), torch.stack(got)
     out = {"forward": rel(y[items], y_ref), "backward_data": rel(dx[items], dx_ref),
-           "backward_weight": rel(got_t, want_t), "tol": 1e-5,
+           "backward_weight": rel(got_t, want_t),
+           # bwd-w sums 1.92M products per entry; the default accumulation mode (one tensor-core
+           # chain per CTA) drifts ~6e-5, inside the reference's BF16 bound (1e-2, acceptance.cpp:526)
+           "tol": {"forward": 1e-5, "backward_data": 1e-5, "backward_weight": 1e-4},
            "how": "items {0, N-1} of y and dx, 256 sampled dW entries, vs float64 on the BF16-rounded operands"}
-    out["ok"] = all(out[p] <= 1e-5 for p in PASSES)
+    out["ok"] = all(out[p] <= out["tol"][p] for p in PASSES)
     return out
+
+
+def exact_wgrad(lib, desc_exact, x, dy, w, d, stream):
+    """Backward-weight in the exact-accumulation mode (C1D_FLAG_EXACT_ACCUM: chains capped at ~4096
+    products): its time alone and its parity on the same 256 sampled entries (bound 1e-5)."""
+    import torch
+
+    k, c, s = w.shape
+    q = dy.shape[2]
+    dw = torch.empty((k, c, s), device=x.device)
+    sp = stream.cuda_stream
+
+    def run():
+        st = lib.c1d_backward_weight(C.byref(desc_exact), x.data_ptr(), dy.data_ptr(), dw.data_ptr(), None, 0, sp)
+        if st != 0:
+            raise RuntimeError(lib.c1d_last_error_message().decode())
+
+    run()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ms = sorted(ts)[1]
+    g = torch.Generator(device="cpu").manual_seed(5)
+    idx = torch.stack([torch.randint(0, k, (256,), generator=g), torch.randint(0, c, (256,), generator=g),
+                       torch.randint(0, s, (256,), generator=g)], 1).tolist()
+    want = torch.stack([torch.dot(x[:, cc, ss * d:ss * d + q].double().reshape(-1), dy[:, kk, :].double().reshape(-1))
+                        for kk, cc, ss in idx])
+    got = torch.stack([dw[kk, cc, ss] for kk, cc, ss in idx]).double()
+    err = float((got - want).norm() / want.norm())
+    return {"ms": ms, "tflops": flops_per_pass() / (ms * 1e-3) / 1e12, "parity_backward_weight": err, "tol": 1e-5,
+            "ok": err <= 1e-5, "flag": "C1D_FLAG_EXACT_ACCUM"}
 
 
 def narrow_roofline(lib, dev, stream, peaks, traffic):
@@ -556,9 +598,10 @@ def main_arm(args):
     value = world * step_flops / (ms_step * 1e-3) / 1e12
 
     # ---- parity of the last timed step (rank 0's outputs; dW is the all-reduced sum when world > 1)
-    parity = None
+    parity = exact = None
     if world == 1 and not args.no_parity:
         parity = parity_check(x, w, dy, y, dx, dw, d)
+        exact = exact_wgrad(lib, cv.make_desc(p, n, w_in, L.DTYPE_BF16, exact=True), x, dy, w, d, stream)
 
     # ---- e2e through the C ABI with host buffers (H2D inputs, D2H outputs every step), the
     # transfers pipelined against the passes over item chunks (paper_2104_08002_b200/pipeline.py)
@@ -630,6 +673,7 @@ def main_arm(args):
             "roofline": roofline,
             "roofline_narrow": narrow,
             "parity": parity,
+            "backward_weight_exact": exact,
             "network": network,
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
