@@ -286,6 +286,15 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst_saddr, const void* tmap
         "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(bar_saddr)
         : "memory");
 }
+// 4-D tiled TMA load (coordinates innermost-first).
+__device__ __forceinline__ void tma_load_4d(uint32_t dst_saddr, const void* tmap, int32_t c0, int32_t c1, int32_t c2,
+                                            int32_t c3, uint32_t bar_saddr) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], "
+        "[%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst_saddr),
+        "l"(tmap), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar_saddr)
+        : "memory");
+}
 // 3-D tiled TMA store shared -> global (bulk-group completion; out-of-bounds elements are dropped).
 __device__ __forceinline__ void tma_store_3d(const void* tmap, uint32_t src_saddr, int32_t c0, int32_t c1,
                                              int32_t c2) {

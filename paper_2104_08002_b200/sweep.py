@@ -33,7 +33,7 @@ from . import conv as cv
 
 CSV_HEADER = "N,C,K,S,d,Q,pass,seconds,flops,gflops,efficiency,meets_condition,threads"
 ROOFLINE_HEADER = ("N,C,K,S,d,Q,precision,pass,algo,seconds,tflops,bytes,arith_intensity,bound,"
-                   "roofline_seconds,roofline_frac")
+                   "roofline_seconds,roofline_frac,algo_roofline_frac")
 PASSES = ("forward", "backward_data", "backward_weight")
 
 
@@ -125,24 +125,50 @@ def algorithmic_bytes(pass_: str, n, c, k, s, d, q, in_bytes: int) -> int:
 
 
 def load_peaks(root: str | None = None) -> dict:
+    """MEASURED_PEAKS.json (driver-written: HBM, BF16) plus profiles/fp32_peaks.json (measured here by
+    tools/peaks_fp32.py: FFMA, TF32/FP32 cuBLAS)."""
     root = root or os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     try:
         with open(os.path.join(root, "MEASURED_PEAKS.json")) as f:
-            return json.load(f)
+            peaks = json.load(f)
     except OSError:
-        return {"bf16_tflops": 1590.0, "hbm_gbs": 7000.0}
+        peaks = {"bf16_tflops": 1590.0, "hbm_gbs": 7000.0}
+    try:
+        with open(os.path.join(root, "profiles", "fp32_peaks.json")) as f:
+            peaks.update(json.load(f))
+    except (OSError, ValueError):
+        pass
+    return peaks
 
 
-def compute_peak_flops(algo: str, peaks: dict) -> float:
-    """Compute roof of the kernel family a point ran on (FLOP/s of the credited 2NKCSQ work):
-    BF16 tensor cores at the measured dense peak; the FP32 split (bf16x3) issues 4 BF16 MMAs per
-    product; the FFMA direct kernels at the nominal 148 SM x 128 lanes x 2 x 1.965 GHz."""
+# BF16 products per credited FP32 product of the split paths (split.cu): six channel blocks for the
+# conv-shaped passes, two launches of four blocks for backward-weight
+SPLIT_PRODUCTS = {"forward": 6, "backward_data": 6, "backward_weight": 8}
+
+
+def ffma_peak_flops(peaks: dict) -> float:
+    """Measured FFMA roof (profiles/fp32_peaks.json), else the nominal 148 x 128 x 2 x 1.965 GHz."""
+    v = peaks.get("ffma_fp32_tflops")
+    return v * 1e12 if v else 148 * 128 * 2 * 1.965e9
+
+
+def fp32_peak_flops(peaks: dict) -> float:
+    """One fixed FP32 roof for every FP32 point, whatever algorithm ran it: the fastest FP32-exact
+    method this GPU offers, max(measured FFMA, BF16 peak / 6 for the six-product split)."""
+    return max(ffma_peak_flops(peaks), peaks.get("bf16_tflops", 1590.0) * 1e12 / 6.0)
+
+
+def compute_peak_flops(algo: str, peaks: dict, pass_: str = "forward") -> float:
+    """Roof of the kernel family a point ran on (FLOP/s of the credited 2NKCSQ work): BF16 tensor
+    cores at the measured dense peak; the FP32 split over its BF16 products per FP32 product; the
+    FFMA direct kernels at the measured FFMA peak. Reported beside the fixed roof as
+    algo_roofline_frac."""
     tc = peaks.get("bf16_tflops", 1590.0) * 1e12
     if algo == "tcgen05":
         return tc
     if algo == "bf16x3":
-        return tc / 4.0
-    return 148 * 128 * 2 * 1.965e9
+        return tc / SPLIT_PRODUCTS.get(pass_, 6)
+    return ffma_peak_flops(peaks)
 
 
 def _iter_shapes(cfg: SweepConfig):
@@ -268,12 +294,21 @@ def parse_csv(path: str) -> list:
 
 
 def roofline(rec: SweepRecord, peaks: dict) -> tuple[str, float, float]:
-    """(bound, roofline seconds, fraction achieved) for one record."""
-    t_c = rec.flops / compute_peak_flops(rec.algo, peaks)
+    """(bound, roofline seconds, fraction achieved) for one record against the fixed roof of its
+    precision: the BF16 tensor peak, or fp32_peak_flops for every FP32 point."""
+    roof = peaks.get("bf16_tflops", 1590.0) * 1e12 if rec.precision.lower().startswith("bf16") else fp32_peak_flops(peaks)
+    t_c = rec.flops / roof
     t_m = rec.bytes / (peaks.get("hbm_gbs", 7000.0) * 1e9)
     bound = "compute" if t_c >= t_m else "hbm"
     t = max(t_c, t_m)
     return bound, t, t / rec.seconds
+
+
+def algo_roofline_frac(rec: SweepRecord, peaks: dict) -> float:
+    """The same fraction against the roof of the algorithm that actually ran (compute_peak_flops)."""
+    t_c = rec.flops / compute_peak_flops(rec.algo, peaks, rec.pass_)
+    t_m = rec.bytes / (peaks.get("hbm_gbs", 7000.0) * 1e9)
+    return max(t_c, t_m) / rec.seconds
 
 
 def write_roofline_csv(records, path: str, peaks: dict | None = None) -> None:
@@ -283,7 +318,8 @@ def write_roofline_csv(records, path: str, peaks: dict | None = None) -> None:
         bound, t, frac = roofline(r, peaks)
         lines.append(",".join([_num(r.n), _num(r.c), _num(r.k), _num(r.s), _num(r.d), _num(r.q), r.precision,
                                r.pass_, r.algo, _num(r.seconds), _num(r.flops / r.seconds / 1e12), _num(r.bytes),
-                               _num(r.flops / max(r.bytes, 1)), bound, _num(t), _num(frac)]))
+                               _num(r.flops / max(r.bytes, 1)), bound, _num(t), _num(frac),
+                               _num(algo_roofline_frac(r, peaks))]))
     with open(path, "w", newline="\n") as f:
         f.write("\n".join(lines) + "\n")
 
