@@ -129,7 +129,8 @@ __global__ void sum_split3_kernel(const float* __restrict__ a, const float* __re
                                   int64_t K, int64_t C, int64_t S) {
     const int64_t total = K * C * S;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t s = e % S, c = (e / S) % C, k = e / (S * C);
+        const uint32_t eu = static_cast<uint32_t>(e), su = static_cast<uint32_t>(S), cu = static_cast<uint32_t>(C);
+        const int64_t s = eu % su, c = (eu / su) % cu, k = eu / (su * cu);  // K*C*S < 2^31
         auto at = [&](const float* t, int kb, int cb) { return t[((kb * K + k) * 2 * C + (cb * C + c)) * S + s]; };
         const float hh = at(a, 0, 0), hm = at(a, 0, 1), mh = at(a, 1, 0), mm = at(a, 1, 1);
         const float lh = at(b, 0, 0), ll = at(b, 0, 1), hl = at(b, 1, 1);

@@ -1020,8 +1020,16 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             drain(kd - sb, nseg, static_cast<uint32_t>(nseg & 1));
             ++nseg;
         }
+        if (kb >= ke && c < p.c) {  // no work: a zero slot 0 (the one-slot reduce reads every CTA's)
+            float* dst = p.part + static_cast<int64_t>(blockIdx.x) * p.max_segs * p.slot_elems;
+            for (int g = 0; g < g_count; ++g)
+                for (int col0 = 0; col0 < pl.n; col0 += 16) {
+                    const uint32_t z[16] = {0};
+                    put16(dst, g, col0, z);
+                }
+        }
         if (warp == 4 && lane == 0) {
-            p.nseg[blockIdx.x] = nseg;  // 0: no work, no slots
+            p.nseg[blockIdx.x] = nseg;  // 0: no work (slot 0 holds zeros)
             if (p.prof) p.prof[blockIdx.x * 8 + 7] = td_sum;
         }
     }
@@ -1042,33 +1050,38 @@ __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restr
     __shared__ float red[4][64];
     pdl_trigger();
     pdl_wait();
-    const int64_t count = K * C * S;
-    const int64_t e = static_cast<int64_t>(blockIdx.x) * 64 + (threadIdx.x % 64);
+    // 32-bit index math (K*C*S < 2^31): 64-bit divisions made this kernel issue-bound (~100 us at
+    // config 1's 148 CTA partials)
+    const uint32_t count = static_cast<uint32_t>(K * C * S);
+    const uint32_t cc = static_cast<uint32_t>(C), ss = static_cast<uint32_t>(S);
+    const uint32_t e = blockIdx.x * 64u + (threadIdx.x % 64u);
     const int quarter = threadIdx.x / 64;
-    const int role_taps = pl.gpc * pl.taps_per_group;
+    const uint32_t role_taps = static_cast<uint32_t>(pl.gpc * pl.taps_per_group);
     float v = 0.0f;
+    uint32_t c = 0, s = 0, k = 0;
     if (e < count) {
-        const int64_t c = e % C, s = (e / C) % S, k = e / (C * S);
-        const int role = static_cast<int>(s / role_taps);
-        const int64_t idx = (k * role_taps + (s - static_cast<int64_t>(role) * role_taps)) * C + c;
+        c = e % cc;
+        const uint32_t ks = e / cc;
+        s = ks % ss;
+        k = ks / ss;
+        const uint32_t role = s / role_taps;
+        const int64_t idx = static_cast<int64_t>((k * role_taps + (s - role * role_taps)) * cc + c);
         const int b0 = pl.role_cta_begin[role], b1 = pl.role_cta_begin[role + 1];
         const int n = b1 - b0;
         const int lo = b0 + n * quarter / 4, hi = b0 + n * (quarter + 1) / 4;
-        if (max_segs == 1) {
-            float t[16];
+        if (max_segs == 1) {  // one slot per CTA, always written (zeros for a CTA without work)
+            for (int bb = lo; bb < hi; bb += 16) {
+                float t[16];
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                t[j] = (lo + j < hi && __ldg(nseg + lo + j) > 0) ? __ldg(part + static_cast<int64_t>(lo + j) * slot_elems + idx)
-                                                                  : 0.0f;
+                for (int j = 0; j < 16; ++j) t[j] = bb + j < hi ? __ldg(part + static_cast<int64_t>(bb + j) * slot_elems + idx) : 0.0f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-                if (lo + j < hi) v += t[j];
-            for (int b = lo + 16; b < hi; ++b)
-                if (__ldg(nseg + b) > 0) v += __ldg(part + static_cast<int64_t>(b) * slot_elems + idx);
+                for (int j = 0; j < 16; ++j)
+                    if (bb + j < hi) v += t[j];
+            }
         } else {
-            for (int b = lo; b < hi; ++b) {
-                const int ns = __ldg(nseg + b);
-                const float* src = part + static_cast<int64_t>(b) * max_segs * slot_elems + idx;
+            for (int bb = lo; bb < hi; ++bb) {
+                const int ns = __ldg(nseg + bb);
+                const float* src = part + static_cast<int64_t>(bb) * max_segs * slot_elems + idx;
                 for (int j = 0; j < ns; j += 8) {
                     float t[8];
 #pragma unroll
@@ -1082,10 +1095,9 @@ __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restr
     }
     red[quarter][threadIdx.x % 64] = v;
     __syncthreads();
-    if (threadIdx.x < 64 && e < count) {
-        const int64_t c = e % C, s = (e / C) % S, k = e / (C * S);
-        dw[(k * C + c) * S + s] = ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
-    }
+    if (threadIdx.x < 64 && e < count)
+        dw[(static_cast<int64_t>(k) * C + c) * S + s] =
+            ((red[0][threadIdx.x] + red[1][threadIdx.x]) + red[2][threadIdx.x]) + red[3][threadIdx.x];
 }
 
 }  // namespace

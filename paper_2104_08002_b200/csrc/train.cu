@@ -59,13 +59,7 @@ __global__ void bernoulli_kernel(float* out, int64_t count, double p, uint64_t s
 }
 
 // ---- losses ---------------------------------------------------------------------------------
-// Stable forms of train.cpp:39-46.
-__device__ __forceinline__ double softplus(double x) { return x > 0.0 ? x + log1p(exp(-x)) : log1p(exp(x)); }
-__device__ __forceinline__ double sigmoid(double x) {
-    if (x >= 0.0) return 1.0 / (1.0 + exp(-x));
-    const double e = exp(x);
-    return e / (1.0 + e);
-}
+// Stable forms of train.cpp:39-46 (stable_softplus, stable_sigmoid), evaluated in double.
 
 constexpr int kLossThreads = 256;
 
@@ -84,16 +78,28 @@ __global__ void __launch_bounds__(kLossThreads) mse_bce_kernel(
     const int64_t per = (count + gridDim.x - 1) / gridDim.x;
     const int64_t b0 = blockIdx.x * per, b1 = min(count, b0 + per);
     double mse = 0.0, bce = 0.0;
-    for (int64_t e = b0 + threadIdx.x; e < b1; e += kLossThreads) {
-        const int64_t i = e / width, x = e - i * width;
+    // (item, column) of this thread's first element; then advanced without divisions
+    int64_t e = b0 + threadIdx.x;
+    int64_t i = e / width, x = e - i * width;
+    for (; e < b1; e += kLossThreads) {
         const double p = pred[i * in_stride + x], t = target[e];
         const double diff = p - t;
         mse += diff * diff;
         const double l = logits[i * in_stride + x], m = labels[e];
-        bce += softplus(l) - m * l;
+        // one exp serves both stable forms: t = exp(-|l|); softplus = max(l, 0) + log1p(t),
+        // sigmoid = l >= 0 ? 1/(1+t) : t/(1+t) -- the same operations the reference's branches do
+        const double tl = exp(-fabs(l));
+        bce += ((l > 0.0 ? l : 0.0) + log1p(tl)) - m * l;
         if (grad_pred) grad_pred[i * grad_stride + x] = static_cast<float>(2.0 * diff * inv);
-        if (grad_logits)
-            grad_logits[i * grad_stride + x] = __fmul_rn(bce_weight, static_cast<float>((sigmoid(l) - m) * inv));
+        if (grad_logits) {
+            const double sg = l >= 0.0 ? 1.0 / (1.0 + tl) : tl / (1.0 + tl);
+            grad_logits[i * grad_stride + x] = __fmul_rn(bce_weight, static_cast<float>((sg - m) * inv));
+        }
+        x += kLossThreads;
+        while (x >= width) {
+            x -= width;
+            ++i;
+        }
     }
     __shared__ double sm[2][kLossThreads];
     sm[0][threadIdx.x] = mse;
@@ -116,15 +122,28 @@ __global__ void __launch_bounds__(kLossThreads) mse_bce_kernel(
     __syncthreads();
     if (!last) return;
     __threadfence();
-    if (threadIdx.x == 0) {
-        double a = 0.0, b = 0.0;
-        for (unsigned int j = 0; j < gridDim.x; ++j) {
-            a += __ldcg(part + 2 * j);
-            b += __ldcg(part + 2 * j + 1);
+    // the last block sums the block partials: thread t takes partials t, t + 256, ... in order, then
+    // the same fixed tree as above (a fixed shape, so the loss is deterministic)
+    double a = 0.0, b = 0.0;
+    for (unsigned int j = threadIdx.x; j < gridDim.x; j += kLossThreads) {
+        a += __ldcg(part + 2 * j);
+        b += __ldcg(part + 2 * j + 1);
+    }
+    sm[0][threadIdx.x] = a;
+    sm[1][threadIdx.x] = b;
+    __syncthreads();
+    for (int h = kLossThreads / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) {
+            sm[0][threadIdx.x] += sm[0][threadIdx.x + h];
+            sm[1][threadIdx.x] += sm[1][threadIdx.x + h];
         }
-        loss3[0] = a * inv;
-        loss3[1] = b * inv;
-        loss3[2] = a * inv + static_cast<double>(bce_weight) * (b * inv);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        const double ta = sm[0][0], tb = sm[1][0];
+        loss3[0] = ta * inv;
+        loss3[1] = tb * inv;
+        loss3[2] = ta * inv + static_cast<double>(bce_weight) * (tb * inv);
         *ticket = 0;  // ready for the next call (and for CUDA-graph replays)
     }
 }
