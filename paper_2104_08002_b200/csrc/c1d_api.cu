@@ -394,6 +394,8 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         const DilPlan dp = dil_plan(d, q);
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {
+            // small problems at d < 8 (few taps per phase x channels) stay on the sliding-window FFMA
+            // kernel (direct.cu): faster there than the split's expanded rows
             if (split_wgrad_blocks(d))
                 return dp.kind != DilPlan::kPhases || d.algo == C1D_ALGO_BF16X3 || phases_pay_off(dp, d.c);
             if (dp.kind == DilPlan::kPlanes) return tc_wgrad_supported(d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m);
@@ -439,7 +441,7 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     const size_t wbytes = align_up(sizeof(float) * static_cast<size_t>(d.k * d.c * d.s));
     if (algo == C1D_ALGO_BF16X3) return split_workspace(d, pass, q);
     if (algo == C1D_ALGO_DIRECT) {
-        if (pass == C1D_PASS_BACKWARD_WEIGHT) return align_up(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
+        if (pass == C1D_PASS_BACKWARD_WEIGHT) return align_up(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, q));
         return wbytes;
     }
     // tensor-core paths: BF16 copies of FP32 inputs + kernel workspace
@@ -1106,7 +1108,7 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         return C1D_OK;
     }
     if (algo == C1D_ALGO_DIRECT) {
-        float* part = bump.take<float>(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, q));
+        float* part = bump.take<float>(direct_wgrad_workspace_bytes(d.n, d.c, d.k, d.s, d.d, q));
         if (bump.overflow) return workspace_overflow();
         e = launch_direct_wgrad(x, dy, d.in_dtype, bf16 && d.in_dtype == C1D_DTYPE_F32, dw_kcs, part, d.n, d.c, d.k,
                                 d.s, d.d, q, stream);

@@ -8,6 +8,7 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100.cuh"
 
 namespace c1d {
 
@@ -234,10 +235,32 @@ static int64_t wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t q) {
 
 static bool pointwise_wgrad_ok(int64_t n, int64_t c, int64_t k, int64_t s);
 
-size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t q) {
+// the sliding-window kernel (below) whenever its shared memory fits: the X window of one 256-column
+// chunk plus the (S-1)*d reach of all taps
+static size_t slide_smem(int d, int sg);
+static bool slide_wgrad_ok(int64_t c, int64_t k, int64_t s, int64_t d) {
+    (void)c;
+    (void)k;
+    return d <= 256 && slide_smem(static_cast<int>(d), static_cast<int>(std::min<int64_t>(s, 8))) <= 200 * 1024;
+}
+static int64_t slide_wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    const int64_t tiles = ceil_div(k, 16) * ceil_div(c, 16);
+    const int64_t units = n * ceil_div(q, 256);
+    // one full wave: resident blocks per SM by the register bound of the widest tap group (<= 4 taps:
+    // 3, else 2) and the shared-memory bound (227 KB, 1 KB reserved per block); at least 3 units per
+    // block so the copy of the next unit overlaps the current one
+    const int64_t widest = ceil_div(s, ceil_div(s, 8));
+    const int64_t by_smem = (227 * 1024) / (static_cast<int64_t>(slide_smem(static_cast<int>(d), static_cast<int>(widest))) + 1024);
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(widest <= 4 ? 3 : 2, by_smem));
+    const int64_t want = std::max<int64_t>(1, per_sm * num_sms() / tiles);
+    return std::max<int64_t>(1, std::min<int64_t>(want, units / 3));
+}
+
+size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
     if (pointwise_wgrad_ok(n, c, k, s)) return sizeof(float) * static_cast<size_t>(n * ceil_div(q, 1024) * k * c);
     if (k * c * s <= 16) return sizeof(float) * static_cast<size_t>(592 * k * c * s);
-    return sizeof(float) * static_cast<size_t>(wgrad_splits(n, c, k, q) * k * c * s);
+    return sizeof(float) * static_cast<size_t>(std::max(wgrad_splits(n, c, k, q), slide_wgrad_splits(n, c, k, s, d, q)) *
+                                               k * c * s);
 }
 
 template <typename TIn>
@@ -311,6 +334,231 @@ __global__ void __launch_bounds__(256) direct_wgrad_kernel(const TIn* __restrict
     }
 }
 
+// Sliding-window FFMA gradient (round 2; replaces direct_wgrad_kernel above, whose 32 x 32 tiles
+// left 3/4 of the lanes idle at C = K = 16 and re-staged the whole chunk per 8-tap group: 792 us at
+// C = K = 16, S = 9, d = 1). Block (k-tile of 16, c-tile of 16, split) with thread (kk, cc) owning
+// ONE (filter, channel) pair and up to 16 taps in registers. Per 8 columns of one dilation phase a
+// thread reads 8 dY values and 8 + sg - 1 X values (the window slides: X[c][x + s*d] for
+// consecutive phase columns shares sg - 1 values) for 8 * sg FMAs. Units are (item, 256-column
+// chunk), split contiguously over the grid; partials part[split][k][c][s], summed in ascending
+// split order by reduce_splits_kernel (deterministic).
+namespace {
+constexpr int kSWT = 16;     // filters / channels per block tile
+constexpr int kSWQ = 256;    // columns per unit
+constexpr int kSWG = 8;      // most taps per group (registers)
+}  // namespace
+// per-phase lengths (multiples of 4 floats, room for the 8-column read-ahead) and row pitches (an odd
+// number of 16-B chunks: 16-B reads of 8 consecutive rows hit 8 distinct chunk slots, one wavefront)
+__host__ __device__ inline int slide_lg(int d) { return ((kSWQ + d - 1) / d + 8 + 3) / 4 * 4; }
+__host__ __device__ inline int slide_lx(int d, int sg) { return ((kSWQ + d - 1) / d + 8 + sg - 1 + 3 + 3) / 4 * 4; }
+__host__ __device__ inline int slide_pitch(int words) { return (words + 3) / 8 * 8 + 4; }
+
+// Copies `count` columns of one row (the first `lim` from src, zeros after) into shared memory at
+// dst with cp.async: 16-B copies when src is 16-B aligned, else 8-B when 8-B aligned, else 4-B.
+// count is a multiple of 4. One warp per row.
+template <int V>
+__device__ __forceinline__ void slide_copy_row_v(uint32_t dst, const float* src, int lim, int count, int lane) {
+    for (int col = V * lane; col < count; col += 32 * V) {
+        const bool full = col + V <= lim;
+        if (full || col >= lim) {
+            if (V == 4) sm100::cp_async16_zfill(dst + 4u * col, full ? src + col : src, full);
+            else if (V == 2) sm100::cp_async8_zfill(dst + 4u * col, full ? src + col : src, full);
+            else sm100::cp_async4_zfill(dst + 4u * col, full ? src + col : src, full);
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e)
+                sm100::cp_async4_zfill(dst + 4u * (col + e), src + (col + e < lim ? col + e : 0), col + e < lim);
+        }
+    }
+}
+__device__ __forceinline__ void slide_copy_row(uint32_t dst, const float* src, int lim, int count, int lane) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    if ((a & 15) == 0) slide_copy_row_v<4>(dst, src, lim, count, lane);
+    else if ((a & 7) == 0) slide_copy_row_v<2>(dst, src, lim, count, lane);
+    else slide_copy_row_v<1>(dst, src, lim, count, lane);
+}
+
+// One launch per tap group [s0, s0 + SG) (SG taps in registers, a compile-time count). The chunk is
+// staged dilation-phase-major (column ph + d*i at [ph][i]) so a phase's columns are contiguous and
+// the inner loop reads 16-B vectors. FP32 input streams in through double-buffered cp.async copies
+// (the next unit lands while this one is computed); BF16 or rounded input is staged through
+// registers. Partial sums are written split-minor: part[(k*C + c)*S + s][split].
+template <typename TIn, int SG>
+__global__ void __launch_bounds__(256, SG <= 4 ? 3 : 2) wgrad_slide_kernel(const TIn* __restrict__ x, const TIn* __restrict__ dy,
+                                                          float* __restrict__ part, int64_t N, int64_t C, int64_t K,
+                                                          int64_t S, int64_t D, int64_t Q, int64_t splits, int lx,
+                                                          int round_in, int64_t s0) {
+    extern __shared__ float4 smem4[];
+    float* smem = reinterpret_cast<float*>(smem4);
+    const int d = static_cast<int>(D);
+    const int lg = slide_lg(d);           // per-phase dY length (multiple of 4)
+    const int gpitch = slide_pitch(d * lg), xpitch = slide_pitch(d * lx);
+    const int buf_words = kSWT * (gpitch + xpitch);  // one buffer: [16][gpitch] dY, then [16][xpitch] X
+    const bool async = sizeof(TIn) == 4 && round_in == 0;
+    const int tid = threadIdx.x, lane = tid % 32;
+    const int64_t k0 = static_cast<int64_t>(blockIdx.x) * kSWT, c0 = static_cast<int64_t>(blockIdx.y) * kSWT;
+    const int64_t split = blockIdx.z;
+    const int64_t chunks_per_item = ceil_div(Q, kSWQ);
+    const int64_t units = N * chunks_per_item;
+    const int64_t u_begin = units * split / splits, u_end = units * (split + 1) / splits;
+    const int64_t W = Q + (S - 1) * D;
+    const int span = d * lx;  // staged X columns (the window plus the read-ahead, phase-padded)
+    const int step_q = 32 / d, step_r = 32 % d;
+    const int ph_l = lane % d, i_l = lane / d;  // this lane's first column (lane = ph + d*i)
+
+    // stage unit u into buffer b: one warp per row (coalesced global reads); the shared-memory slot
+    // of column col = ph + d*i is stepped through (phase, index) without divisions
+    const uint32_t sbase = sm100::smem_u32(smem);
+    const int gstep = 4 * (step_r * lg + step_q), xstep = 4 * (step_r * lx + step_q);  // bytes per 32 columns
+    const int gwrap = 4 * (1 - d * lg), xwrap = 4 * (1 - d * lx);                      // phase wrap-around
+    auto stage = [&](int64_t u, int b) {
+        const int64_t n = u / chunks_per_item;
+        const int64_t q0 = (u % chunks_per_item) * kSWQ;
+        const uint32_t gsb = sbase + 4u * static_cast<uint32_t>(b * buf_words);
+        const uint32_t xsb = gsb + 4u * static_cast<uint32_t>(kSWT * gpitch);
+        for (int r = tid / 32; r < kSWT; r += 8) {
+            const int64_t k = k0 + r, c = c0 + r;
+            const bool kok = k < K, cok = c < C;
+            const TIn* grow = dy + (n * K + (kok ? k : 0)) * Q + q0;
+            const TIn* xrow = x + (n * C + (cok ? c : 0)) * W + q0 + s0 * D;
+            const int glim = kok ? static_cast<int>(std::min<int64_t>(kSWQ, Q - q0)) : 0;
+            const int xlim = cok ? static_cast<int>(std::min<int64_t>(span, W - q0 - s0 * D)) : 0;
+            if (async && d == 1) {  // phase-major = plain order: widest copies the row alignment allows
+                slide_copy_row(gsb + 4u * static_cast<uint32_t>(r * gpitch), reinterpret_cast<const float*>(grow),
+                               glim, lg, lane);
+                slide_copy_row(xsb + 4u * static_cast<uint32_t>(r * xpitch), reinterpret_cast<const float*>(xrow),
+                               xlim, span, lane);
+                continue;
+            }
+            uint32_t sd = gsb + 4u * static_cast<uint32_t>(r * gpitch + ph_l * lg + i_l);
+            float* grs = smem + b * buf_words + r * gpitch;
+            int ph = ph_l, i = i_l;
+            for (int col = lane; col < d * lg; col += 32) {
+                if (async) {
+                    sm100::cp_async4_zfill(sd, grow + (col < glim ? col : 0), col < glim);
+                } else {
+                    grs[ph * lg + i] = col < glim ? load_as_float(grow, col, round_in != 0) : 0.0f;
+                }
+                ph += step_r;
+                i += step_q;
+                sd += gstep;
+                if (ph >= d) ph -= d, ++i, sd += gwrap;
+            }
+            sd = xsb + 4u * static_cast<uint32_t>(r * xpitch + ph_l * lx + i_l);
+            float* xrs = smem + b * buf_words + kSWT * gpitch + r * xpitch;
+            ph = ph_l, i = i_l;
+            for (int col = lane; col < span; col += 32) {
+                if (async) {
+                    sm100::cp_async4_zfill(sd, xrow + (col < xlim ? col : 0), col < xlim);
+                } else {
+                    xrs[ph * lx + i] = col < xlim ? load_as_float(xrow, col, round_in != 0) : 0.0f;
+                }
+                ph += step_r;
+                i += step_q;
+                sd += xstep;
+                if (ph >= d) ph -= d, ++i, sd += xwrap;
+            }
+        }
+        if (async) sm100::cp_async_commit();
+    };
+
+    // register tile: filters {kp, kp+8} x channels {cp, cp+8} x SG taps; the four warp pairs (qtr)
+    // take every fourth 8-column block of the unit and are summed in a fixed order at the end
+    const int qtr = tid / 64, kp = (tid % 64) / 8, cp = tid % 8;
+    float acc[2][2][SG];
+#pragma unroll
+    for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int j = 0; j < SG; ++j) acc[f][h][j] = 0.0f;
+    if (u_begin < u_end) stage(u_begin, 0);
+    int b = 0;
+    for (int64_t u = u_begin; u < u_end; ++u, b ^= 1) {
+        if (u + 1 < u_end) {
+            stage(u + 1, b ^ 1);  // buffer b^1 was released by the barrier that ended unit u-1
+            if (async) sm100::cp_async_wait_group<1>();
+        } else if (async) {
+            sm100::cp_async_wait_group<0>();
+        }
+        __syncthreads();
+        const float* gb = smem + b * buf_words;
+        const float* xb = gb + kSWT * gpitch;
+        // phase by phase, 8 columns at a time: column ph + d*i; tap s of it is X column ph + d*(i + s)
+        int blk0 = 0;  // 8-column blocks before this phase
+        for (int ph = 0; ph < d; ++ph) {
+            const int cols = ph < kSWQ ? (kSWQ - 1 - ph) / d + 1 : 0;
+            const int nb = (cols + 7) / 8;
+            const float4* g0 = reinterpret_cast<const float4*>(gb + kp * gpitch + ph * lg);
+            const float4* g1 = reinterpret_cast<const float4*>(gb + (kp + 8) * gpitch + ph * lg);
+            const float4* x0 = reinterpret_cast<const float4*>(xb + cp * xpitch + ph * lx);
+            const float4* x1 = reinterpret_cast<const float4*>(xb + (cp + 8) * xpitch + ph * lx);
+            for (int t = (qtr - blk0) & 3; t < nb; t += 4) {
+                constexpr int NW = (8 + SG - 1 + 3) / 4;
+                float ga[8], gc[8], wa[4 * NW], wc[4 * NW];
+                *reinterpret_cast<float4*>(&ga[0]) = g0[2 * t];
+                *reinterpret_cast<float4*>(&ga[4]) = g0[2 * t + 1];
+                *reinterpret_cast<float4*>(&gc[0]) = g1[2 * t];
+                *reinterpret_cast<float4*>(&gc[4]) = g1[2 * t + 1];
+#pragma unroll
+                for (int v = 0; v < NW; ++v) {
+                    *reinterpret_cast<float4*>(&wa[4 * v]) = x0[2 * t + v];
+                    *reinterpret_cast<float4*>(&wc[4 * v]) = x1[2 * t + v];
+                }
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+#pragma unroll
+                    for (int s = 0; s < SG; ++s) {
+                        acc[0][0][s] = fmaf(ga[j], wa[j + s], acc[0][0][s]);
+                        acc[0][1][s] = fmaf(ga[j], wc[j + s], acc[0][1][s]);
+                        acc[1][0][s] = fmaf(gc[j], wa[j + s], acc[1][0][s]);
+                        acc[1][1][s] = fmaf(gc[j], wc[j + s], acc[1][1][s]);
+                    }
+            }
+            blk0 += nb;
+        }
+        __syncthreads();
+    }
+    // fixed-order sum of the four quarters through shared memory (all copies have landed)
+    float* red = smem;  // [16 filters][16 channels][SG]
+    for (int q = 0; q < 4; ++q) {
+        if (qtr == q) {
+#pragma unroll
+            for (int f = 0; f < 2; ++f)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int j = 0; j < SG; ++j) {
+                        float* r = red + ((kp + 8 * f) * kSWT + cp + 8 * h) * SG + j;
+                        *r = q == 0 ? acc[f][h][j] : *r + acc[f][h][j];
+                    }
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < kSWT * kSWT * SG; e += 256) {
+        const int64_t k = k0 + e / (kSWT * SG), c = c0 + (e / SG) % kSWT;
+        const int j = e % SG;
+        if (k < K && c < C) part[((k * C + c) * S + s0 + j) * splits + split] = red[e];
+    }
+}
+
+// Split-minor partials (part[e][split]): one warp per output, lane j sums splits j, j+32, ... in
+// ascending order, then a fixed butterfly adds the 32 lane sums (deterministic).
+__global__ void __launch_bounds__(256) reduce_splits_minor_kernel(const float* __restrict__ part,
+                                                                  float* __restrict__ out, int64_t count, int splits) {
+    const int lane = threadIdx.x % 32;
+    for (int64_t e = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) / 32; e < count;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x / 32) {
+        const float* p = part + e * splits;
+        float v = 0.0f;
+#pragma unroll 4
+        for (int sp = lane; sp < splits; sp += 32) v += p[sp];
+#pragma unroll
+        for (int o = 16; o > 0; o /= 2) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) out[e] = v;
+    }
+}
+
 __global__ void reduce_splits_kernel(const float* __restrict__ part, float* __restrict__ out, int64_t count,
                                      int64_t splits) {
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
@@ -318,6 +566,44 @@ __global__ void reduce_splits_kernel(const float* __restrict__ part, float* __re
         for (int64_t sp = 0; sp < splits; ++sp) v += part[sp * count + e];
         out[e] = v;
     }
+}
+
+// Many splits: 32 outputs per block, each of the 8 warps sums the splits congruent to it mod 8 (in
+// ascending order), then warp 0 adds the 8 partial sums in warp order — a fixed order, so the
+// result is deterministic.
+__global__ void __launch_bounds__(256) reduce_splits_wide_kernel(const float* __restrict__ part,
+                                                                 float* __restrict__ out, int64_t count, int splits) {
+    __shared__ float sums[8][33];
+    const int lane = threadIdx.x % 32, wp = threadIdx.x / 32;
+    for (int64_t e0 = static_cast<int64_t>(blockIdx.x) * 32; e0 < count; e0 += static_cast<int64_t>(gridDim.x) * 32) {
+        const int64_t e = e0 + lane;
+        float v = 0.0f;
+        if (e < count) {
+            const float* p = part + e;
+#pragma unroll 4
+            for (int sp = wp; sp < splits; sp += 8) v += p[static_cast<int64_t>(sp) * count];
+        }
+        sums[wp][lane] = v;
+        __syncthreads();
+        if (wp == 0 && e < count) {
+            float t = sums[0][lane];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) t += sums[w][lane];
+            out[e] = t;
+        }
+        __syncthreads();
+    }
+}
+
+static void launch_reduce_splits(const float* part, float* out, int64_t count, int64_t splits, cudaStream_t stream) {
+    if (splits >= 32) {
+        reduce_splits_wide_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 32), 4096)), 256, 0,
+                                    stream>>>(part, out, count, static_cast<int>(splits));
+    } else {
+        reduce_splits_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 2048)), 256, 0, stream>>>(
+            part, out, count, splits);
+    }
+    note_launch();
 }
 
 // Tiny gradients (K*C*S <= 16, e.g. the 1-filter, 1-tap heads of the config-5 network): each
@@ -464,6 +750,37 @@ static cudaError_t launch_pointwise_wgrad(const TIn* x, const TIn* dy, float* dw
     return cudaGetLastError();
 }
 
+static size_t slide_smem(int d, int sg) {  // two buffers
+    return 2 * sizeof(float) *
+           static_cast<size_t>(kSWT * slide_pitch(d * slide_lg(d)) + kSWT * slide_pitch(d * slide_lx(d, sg)));
+}
+
+template <typename TIn, int SG>
+static cudaError_t launch_slide_sg(dim3 grid, size_t smem, cudaStream_t stream, const TIn* x, const TIn* dy, float* part,
+                                   int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, int64_t splits,
+                                   int lx, int round_in, int64_t s0) {
+    cudaError_t e = cudaFuncSetAttribute(wgrad_slide_kernel<TIn, SG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    wgrad_slide_kernel<TIn, SG><<<grid, 256, smem, stream>>>(x, dy, part, n, c, k, s, d, q, splits, lx, round_in, s0);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <typename TIn>
+static cudaError_t launch_slide(int sg, dim3 grid, size_t smem, cudaStream_t stream, const TIn* x, const TIn* dy,
+                                float* part, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q,
+                                int64_t splits, int lx, int round_in, int64_t s0) {
+#define C1D_SLIDE(SGV) \
+    case SGV:          \
+        return launch_slide_sg<TIn, SGV>(grid, smem, stream, x, dy, part, n, c, k, s, d, q, splits, lx, round_in, s0)
+    switch (sg) {
+        C1D_SLIDE(1); C1D_SLIDE(2); C1D_SLIDE(3); C1D_SLIDE(4); C1D_SLIDE(5); C1D_SLIDE(6); C1D_SLIDE(7);
+        default: C1D_SLIDE(8);
+    }
+#undef C1D_SLIDE
+}
+
 cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, bool round_in, float* dw_kcs,
                                 float* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d,
                                 int64_t q, cudaStream_t stream) {
@@ -490,6 +807,32 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
         const int64_t count = k * c * s;
         // reuse reduce_splits_kernel: it expects part[split * count + e]
         reduce_splits_kernel<<<1, 32, 0, stream>>>(workspace, dw_kcs, count, kSmallBlocks);
+        note_launch();
+        return cudaGetLastError();
+    }
+    if (slide_wgrad_ok(c, k, s, d)) {
+        const int64_t splits = slide_wgrad_splits(n, c, k, s, d, q);
+        dim3 grid(static_cast<unsigned>(ceil_div(k, kSWT)), static_cast<unsigned>(ceil_div(c, kSWT)),
+                  static_cast<unsigned>(splits));
+        cudaError_t e = cudaSuccess;
+        // balanced tap groups of at most kSWG taps (S = 9 -> 5 + 4, not 8 + 1)
+        const int64_t groups = ceil_div(s, kSWG);
+        for (int64_t gi = 0, s0 = 0; gi < groups && e == cudaSuccess; ++gi) {
+            const int sg = static_cast<int>(s / groups + (gi < s % groups ? 1 : 0));
+            const int lx = slide_lx(static_cast<int>(d), sg);
+            const size_t smem = slide_smem(static_cast<int>(d), sg);
+            e = in_dtype == 0 ? launch_slide<float>(sg, grid, smem, stream, static_cast<const float*>(x),
+                                                    static_cast<const float*>(dy), workspace, n, c, k, s, d, q, splits,
+                                                    lx, round_in ? 1 : 0, s0)
+                              : launch_slide<uint16_t>(sg, grid, smem, stream, static_cast<const uint16_t*>(x),
+                                                       static_cast<const uint16_t*>(dy), workspace, n, c, k, s, d, q,
+                                                       splits, lx, 0, s0);
+            s0 += sg;
+        }
+        if (e != cudaSuccess) return e;
+        const int64_t count = k * c * s;
+        reduce_splits_minor_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 8), 4096)), 256, 0,
+                                     stream>>>(workspace, dw_kcs, count, static_cast<int>(splits));
         note_launch();
         return cudaGetLastError();
     }
@@ -526,9 +869,7 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const int64_t count = k * c * s;
-    reduce_splits_kernel<<<static_cast<unsigned>(std::min<int64_t>(ceil_div(count, 256), 2048)), 256, 0, stream>>>(
-        workspace, dw_kcs, count, splits);
-    note_launch();
+    launch_reduce_splits(workspace, dw_kcs, count, splits, stream);
     return cudaGetLastError();
 }
 

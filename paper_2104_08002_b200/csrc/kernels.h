@@ -51,7 +51,7 @@ cudaError_t launch_prep_weights(const float* w_kcs, float* out, int64_t K, int64
 cudaError_t launch_direct_conv(const void* in, int in_dtype, bool round_in, const float* wg, float* out,
                                const ConvGeom& g, cudaStream_t stream);
 
-size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t q);
+size_t direct_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, bool round_in, float* dw_kcs,
                                 float* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d,
                                 int64_t q, cudaStream_t stream);

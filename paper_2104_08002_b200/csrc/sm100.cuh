@@ -243,7 +243,11 @@ __device__ __forceinline__ void cp_async16_zfill(uint32_t dst_saddr, const void*
                  "r"(valid ? 16 : 0)
                  : "memory");
 }
-// 4-byte variant (L1-allocating .ca, the only mode for sizes below 16)
+// 8- and 4-byte variants (L1-allocating .ca, the only mode for sizes below 16)
+__device__ __forceinline__ void cp_async8_zfill(uint32_t dst_saddr, const void* src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst_saddr), "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async4_zfill(uint32_t dst_saddr, const void* src, bool valid) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst_saddr), "l"(src), "r"(valid ? 4 : 0)
                  : "memory");

@@ -54,6 +54,7 @@ class SweepConfig:
     seed: int = 20260822
     pairs: bool = False      # C = K (BASELINE config 4) instead of the C x K grid
     strict: bool = False     # reference skip_reason for odd BF16 dims
+    algo: str = "auto"       # "auto" or a forced c1d_algo ("direct", "tcgen05", "bf16x3")
 
 
 @dataclass
@@ -212,7 +213,7 @@ def run_sweep(cfg: SweepConfig, progress=None, device="cuda") -> SweepResult:
         w = (torch.rand((k, c, s), device=device, generator=g) * 2 - 1) * lim
         x = torch.randn((n, c, w_in), device=device, generator=g).to(dt)
         dy = torch.randn((n, k, q), device=device, generator=g).to(dt)
-        desc = cv.make_desc(p, n, w_in, L.DTYPE_BF16 if bf16 else L.DTYPE_F32)
+        desc = cv.make_desc(p, n, w_in, L.DTYPE_BF16 if bf16 else L.DTYPE_F32, algo=cfg.algo)
         sp = torch.cuda.current_stream().cuda_stream
         outs = {"forward": torch.empty((n, k, q), device=device),
                 "backward_data": torch.empty((n, c, w_in), device=device),
@@ -227,6 +228,9 @@ def run_sweep(cfg: SweepConfig, progress=None, device="cuda") -> SweepResult:
         }
         for ps in cfg.passes:
             fn = calls[ps]
+            if cfg.algo != "auto" and fn() != 0:  # the forced algorithm does not support this shape
+                res.skips.append((n, c, k, s, d, q, ps, f"algo {cfg.algo} unsupported"))
+                continue
             for _ in range(cfg.warmup):
                 cv._check(fn())
             ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * cfg.iterations)]
@@ -240,8 +244,8 @@ def run_sweep(cfg: SweepConfig, progress=None, device="cuda") -> SweepResult:
             rec = SweepRecord(n, c, k, s, d, q, ps, secs, flops, flops / secs / 1e9, efficiency(flops, secs, peak),
                               meets_condition(s, q, c, k), cfg.threads,
                               precision="bf16" if bf16 else "fp32",
-                              algo=cv.selected_algo(p, n, w_in, PASSES.index(ps),
-                                                    in_dtype=L.DTYPE_BF16 if bf16 else L.DTYPE_F32),
+                              algo=cfg.algo if cfg.algo != "auto" else cv.selected_algo(
+                                  p, n, w_in, PASSES.index(ps), in_dtype=L.DTYPE_BF16 if bf16 else L.DTYPE_F32),
                               bytes=algorithmic_bytes(ps, n, c, k, s, d, q, 2 if bf16 else 4))
             res.records.append(rec)
             if progress:
@@ -358,6 +362,8 @@ def main(argv=None) -> int:
     ap.add_argument("--precision", choices=["bf16", "fp32", "both"], default="both")
     ap.add_argument("--iterations", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--algo", choices=["auto", "direct", "tcgen05", "bf16x3"], default="auto",
+                    help="force one algorithm (shapes it does not support are skipped)")
     ap.add_argument("--out", default="sweep.csv", help="reference-schema CSV; <out>.roofline.csv has the extras")
     args = ap.parse_args(argv)
     precs = {"bf16": [cv.Precision.Bf16], "fp32": [cv.Precision.Fp32],
@@ -365,6 +371,7 @@ def main(argv=None) -> int:
     allrec = SweepResult()
     for prec in precs:
         cfg = config4(prec, args.iterations, args.warmup)
+        cfg.algo = args.algo
         r = run_sweep(cfg, progress=lambda rec: print(
             f"{rec.precision} C={rec.c} S={rec.s} d={rec.d} {rec.pass_:15s} {rec.algo:8s} "
             f"{rec.seconds * 1e6:10.1f} us {rec.gflops / 1e3:8.2f} TFLOP/s", flush=True))
