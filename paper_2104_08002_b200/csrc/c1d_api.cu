@@ -367,6 +367,34 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
 constexpr int64_t kMaxSplitTerms = 3300;
 bool split_wgrad_blocks(const c1d_desc& d);
 
+// FP32 crossover between the FFMA sliding-window kernels (direct.cu) and the BF16 operand split:
+// below these products per output column (C_in * S; max(C, K) * S for backward-weight) the FFMA
+// kernels are faster. Measured on the BASELINE config-4 sweep (N = 16, Q = 20000, C = K in
+// {16, 32, 64, 128}, S in {3, 9, 25, 51}): the split's per-call floor
+// (split / pack / reduce launches) dominates small problems, and its expanded-row and plane
+// plans (d != 8) cost more tensor-core work per product than the native d = 8 plan.
+int64_t ffma_fp32_limit(c1d_pass pass, int64_t dil, int64_t width) {
+    if (pass == C1D_PASS_BACKWARD_WEIGHT) {
+        switch (dil) {
+            case 1: return INT64_MAX;
+            case 2: return 1200;
+            case 4: return width <= 64 ? 450 : 300;
+            default: return 150;
+        }
+    }
+    switch (dil) {
+        case 1: return 1000;
+        case 2: return 450;
+        case 4: return 200;
+        case 8: return 150;
+        default: return 400;
+    }
+}
+bool ffma_beats_split(const c1d_desc& d, c1d_pass pass) {
+    const int64_t width = pass == C1D_PASS_FORWARD ? d.c : (pass == C1D_PASS_BACKWARD_DATA ? d.k : std::max(d.c, d.k));
+    return width * d.s <= ffma_fp32_limit(pass, d.d, width);
+}
+
 // Resolve AUTO.
 c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     const bool tc_ok = [&] {
@@ -391,6 +419,7 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     }();
     const bool split_ok = [&] {
         if (is_bf16(d) || d.in_dtype != C1D_DTYPE_F32) return false;
+        if (d.algo == C1D_ALGO_AUTO && ffma_beats_split(d, pass)) return false;
         const DilPlan dp = dil_plan(d, q);
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {

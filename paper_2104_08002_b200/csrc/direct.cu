@@ -12,6 +12,10 @@
 
 namespace c1d {
 
+// shared-memory row pitch for the sliding-window kernels: an odd number of 16-B chunks, so 16-B
+// reads of 8 consecutive rows hit 8 distinct chunk slots (one wavefront)
+__host__ __device__ inline int slide_pitch(int words) { return (words + 3) / 8 * 8 + 4; }
+
 // ------------------------------------------------------------------------------- weights
 __global__ void prep_weights_kernel(const float* __restrict__ w, float* __restrict__ out, int64_t K, int64_t C,
                                     int64_t S, int mode, int round) {
@@ -120,6 +124,259 @@ __global__ void __launch_bounds__(256) direct_conv_kernel(const TIn* __restrict_
     }
 }
 
+// ------------------------------------------------------------------------------- sliding window
+// Forward-shaped FFMA convolution, dilation-phase register windows. Block: persistent, walking
+// 16-output x 512-column tiles; 256 threads, thread (q4, cg) owns outputs {q4, q4+4, q4+8, q4+12}
+// and 8 columns of one dilation phase, x0 + ph + d*(i0 + i) (i < 8), so tap s of its columns is
+// the 8-wide window at phase index i0 + s: the staged input rows are dilation-phase-major (column
+// ph + d*i at [ph][i]) and the windows are 16-B vector reads, as are the 4 outputs' weights of a
+// tap ([c][s][quad][4]). Input channels stream in chunks of 8 (one warp per row) through a double
+// buffer (cp.async for FP32 input). Taps run in groups of SG (S itself for S <= 3, else 4 with the
+// tap count padded by zero weights). The output tile is assembled in shared memory and written
+// with coalesced stores.
+namespace {
+constexpr int kCT = 8;     // input channels per staged chunk
+constexpr int kCO = 16;    // outputs per block
+constexpr int kCQ = 512;   // columns per block
+}  // namespace
+__host__ __device__ inline int cslide_nbp(int d) { return ((kCQ + d - 1) / d + 7) / 8; }  // 8-blocks per phase
+__host__ __device__ inline int cslide_lx(int d, int sp) { return (8 * cslide_nbp(d) + sp - 1 + 3 + 3) / 4 * 4; }
+__host__ __device__ inline int cslide_sg(int s) { return s <= 3 ? s : 4; }
+__host__ __device__ inline int cslide_sp(int s) { return (s + cslide_sg(s) - 1) / cslide_sg(s) * cslide_sg(s); }
+static size_t cslide_smem(int d, int s) {
+    const int sp = cslide_sp(s);
+    const size_t buf = static_cast<size_t>(kCT * slide_pitch(d * cslide_lx(d, sp)) + kCT * sp * kCO);
+    return sizeof(float) * (2 * buf + kCO * kCQ);  // double buffer + output tile
+}
+static bool cslide_ok(const ConvGeom& g) {
+    return g.dil <= 64 && !g.xr_rows && !g.xr_inline && g.in_stride == 0 &&
+           g.n * ceil_div(g.out_w, kCQ) * ceil_div(g.out_ch, kCO) < (int64_t{1} << 31) &&
+           cslide_smem(static_cast<int>(g.dil), static_cast<int>(g.taps)) <= 200 * 1024;
+}
+
+// Copies columns [0, count) of one row into shared memory at dst with cp.async (zeros outside
+// [lo, hi)): 16-B copies when src is 16-B aligned, else 8-B, else 4-B. count % 4 == 0.
+// (`safe` is any valid address, named by the zero-byte copies.)
+template <int V>
+__device__ __forceinline__ void copy_row_v(uint32_t dst, const float* src, const float* safe, int lo, int hi,
+                                           int count, int lane) {
+    for (int col = V * lane; col < count; col += 32 * V) {
+        const bool full = col >= lo && col + V <= hi;
+        if (full || col + V <= lo || col >= hi) {
+            if (V == 4) sm100::cp_async16_zfill(dst + 4u * col, full ? src + col : safe, full);
+            else if (V == 2) sm100::cp_async8_zfill(dst + 4u * col, full ? src + col : safe, full);
+            else sm100::cp_async4_zfill(dst + 4u * col, full ? src + col : safe, full);
+        } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) {
+                const bool ok = col + e >= lo && col + e < hi;
+                sm100::cp_async4_zfill(dst + 4u * (col + e), ok ? src + col + e : safe, ok);
+            }
+        }
+    }
+}
+__device__ __forceinline__ void copy_row(uint32_t dst, const float* src, const float* safe, int lo, int hi,
+                                         int count, int lane) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(src);
+    if ((a & 15) == 0) copy_row_v<4>(dst, src, safe, lo, hi, count, lane);
+    else if ((a & 7) == 0) copy_row_v<2>(dst, src, safe, lo, hi, count, lane);
+    else copy_row_v<1>(dst, src, safe, lo, hi, count, lane);
+}
+
+template <typename TIn, int SG, int NB>
+__global__ void __launch_bounds__(256, 2) conv_slide_kernel(const TIn* __restrict__ in, const float* __restrict__ wg,
+                                                            float* __restrict__ out, ConvGeom g, int round_in) {
+    extern __shared__ float4 smem4[];
+    float* smem = reinterpret_cast<float*>(smem4);
+    const int d = static_cast<int>(g.dil), S = static_cast<int>(g.taps);
+    const int sp = cslide_sp(S), nbp = cslide_nbp(d), lx = cslide_lx(d, sp);
+    const int span = d * lx;  // staged input columns per row
+    const int xpitch = slide_pitch(span);
+    const int wwords = kCT * sp * kCO;
+    const int buf_words = kCT * xpitch + wwords;
+    float* tile = smem + 2 * buf_words;  // [16][512] output tile
+    const bool async = sizeof(TIn) == 4 && round_in == 0;
+    const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+    const int q4 = tid % 4, cg = tid / 4;  // outputs {q4, q4+4, q4+8, q4+12}, column group 0..63
+    const int64_t C = g.in_ch;
+    const int nchunks = static_cast<int>(ceil_div(C, kCT));
+    const int64_t tiles_x = ceil_div(g.out_w, kCQ), tiles_o = ceil_div(g.out_ch, kCO);
+    const int tiles = static_cast<int>(g.n * tiles_x * tiles_o);
+    const uint32_t sbase = sm100::smem_u32(smem);
+    const int step_q = 32 / d, step_r = 32 % d;
+    const int xstep = 4 * (step_r * lx + step_q), xwrap = 4 * (1 - d * lx);
+    // this block's work: tiles blockIdx.x, +gridDim.x, ... (output tiles fastest, so the blocks
+    // running together share their input columns in L2), each as nchunks channel chunks
+    // (32-bit tile decode once per tile: tiles < 2^31 by the launch check)
+    struct Tile { int64_t n, x0, o0; };
+    const int ntx = static_cast<int>(tiles_x), nto = static_cast<int>(tiles_o);
+    auto tile_of = [&](int t) {
+        const int ot = t % nto, rest = t / nto;
+        return Tile{rest / ntx, static_cast<int64_t>(rest % ntx) * kCQ, static_cast<int64_t>(ot) * kCO};
+    };
+
+    auto stage = [&](const Tile& tl, int chunk, int b) {
+        const int64_t pos0 = tl.x0 + g.in_off;  // input position of staged column 0
+        const int lo = static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(span, -pos0)));
+        const int64_t c = static_cast<int64_t>(chunk) * kCT + warp;  // one row per warp (kCT == 8 warps)
+        const bool cok = c < C;
+        const int hi = cok ? static_cast<int>(std::max<int64_t>(0, std::min<int64_t>(span, g.in_w - pos0))) : 0;
+        const uint32_t xb = sbase + 4u * static_cast<uint32_t>(b * buf_words + warp * xpitch);
+        const TIn* row = in + (tl.n * C + (cok ? c : 0)) * g.in_w;
+        if (async && d == 1) {
+            copy_row(xb, reinterpret_cast<const float*>(row) + pos0, reinterpret_cast<const float*>(row), lo, hi, span,
+                     lane);
+        } else {
+            float* xr = smem + b * buf_words + warp * xpitch;
+            int ph = lane % d, i = lane / d;
+            uint32_t sd = xb + 4u * static_cast<uint32_t>(ph * lx + i);
+            for (int col = lane; col < span; col += 32) {
+                const bool ok = col >= lo && col < hi;
+                if (async) {
+                    sm100::cp_async4_zfill(sd, reinterpret_cast<const float*>(row) + (ok ? pos0 + col : 0), ok);
+                } else {
+                    xr[ph * lx + i] = ok ? load_as_float(row, pos0 + col, round_in != 0) : 0.0f;
+                }
+                ph += step_r;
+                i += step_q;
+                sd += xstep;
+                if (ph >= d) ph -= d, ++i, sd += xwrap;
+            }
+        }
+        // weights [cc][s][quad][j] = wg[(o0 + quad + 4j, c0 + cc, s)], zero past the edges
+        const uint32_t wb = sbase + 4u * static_cast<uint32_t>(b * buf_words + kCT * xpitch);
+        const int64_t c0 = static_cast<int64_t>(chunk) * kCT;
+        for (int e = tid; e < wwords; e += 256) {
+            const int j = e & 3, qq = (e >> 2) & 3, rest = e >> 4;
+            const int s = rest % sp, cc = rest / sp;
+            const int64_t o = tl.o0 + qq + 4 * j, ci = c0 + cc;
+            const bool ok = o < g.out_ch && ci < C && s < S;
+            sm100::cp_async4_zfill(wb + 4u * e, wg + (ok ? (o * C + ci) * S + s : 0), ok);
+        }
+        sm100::cp_async_commit();
+    };
+
+    float acc[NB][4][8];
+#pragma unroll
+    for (int a = 0; a < NB; ++a)
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[a][h][i] = 0.0f;
+    // items = (tile, chunk) pairs in order; `cur` is being computed, `nxt` is being staged
+    int t_cur = blockIdx.x, chunk = 0;
+    Tile cur = tile_of(t_cur);
+    if (t_cur < tiles) stage(cur, 0, 0);
+    for (int b = 0; t_cur < tiles; b ^= 1) {
+        int t_nxt = t_cur, chunk_nxt = chunk + 1;
+        if (chunk_nxt == nchunks) chunk_nxt = 0, t_nxt += gridDim.x;
+        const Tile nxt = t_nxt != t_cur && t_nxt < tiles ? tile_of(t_nxt) : cur;
+        if (t_nxt < tiles) {
+            stage(nxt, chunk_nxt, b ^ 1);  // buffer b^1 was released by the barrier that ended the last item
+            sm100::cp_async_wait_group<1>();
+        } else {
+            sm100::cp_async_wait_group<0>();
+        }
+        __syncthreads();
+        const float* xs = smem + b * buf_words;
+        const float* ws = xs + kCT * xpitch;
+        const int cmax = static_cast<int>(std::min<int64_t>(kCT, C - static_cast<int64_t>(chunk) * kCT));
+#pragma unroll
+        for (int a = 0; a < NB; ++a) {
+            const int blk = cg + 64 * a;
+            if (blk >= d * nbp) break;
+            const int ph = blk / nbp, i0 = 8 * (blk % nbp);
+            for (int cc = 0; cc < cmax; ++cc) {
+                const float4* xq = reinterpret_cast<const float4*>(xs + cc * xpitch + ph * lx + i0);
+                const float4* wq = reinterpret_cast<const float4*>(ws + cc * sp * kCO) + q4;
+                for (int s0 = 0; s0 < sp; s0 += SG) {
+                    constexpr int NW = (8 + SG - 1 + 3) / 4;
+                    float win[4 * NW];
+#pragma unroll
+                    for (int v = 0; v < NW; ++v) *reinterpret_cast<float4*>(&win[4 * v]) = xq[s0 / 4 + v];
+#pragma unroll
+                    for (int jj = 0; jj < SG; ++jj) {
+                        const float4 w = wq[(s0 + jj) * 4];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            acc[a][0][i] = fmaf(w.x, win[i + jj], acc[a][0][i]);
+                            acc[a][1][i] = fmaf(w.y, win[i + jj], acc[a][1][i]);
+                            acc[a][2][i] = fmaf(w.z, win[i + jj], acc[a][2][i]);
+                            acc[a][3][i] = fmaf(w.w, win[i + jj], acc[a][3][i]);
+                        }
+                    }
+                }
+            }
+        }
+        if (chunk == nchunks - 1) {
+            // tile done: assemble the 16 x 512 outputs in shared memory, then coalesced stores
+#pragma unroll
+            for (int a = 0; a < NB; ++a) {
+                const int blk = cg + 64 * a;
+                if (blk >= d * nbp) break;
+                const int ph = blk / nbp, i0 = 8 * (blk % nbp);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int col = ph + d * (i0 + i);
+#pragma unroll
+                    for (int h = 0; h < 4; ++h) {
+                        if (col < kCQ) tile[(q4 + 4 * h) * kCQ + col] = acc[a][h][i];
+                        acc[a][h][i] = 0.0f;
+                    }
+                }
+            }
+            __syncthreads();
+            const int cols = static_cast<int>(std::min<int64_t>(kCQ, g.out_w - cur.x0));
+            for (int r = warp; r < kCO; r += 8) {
+                const int64_t o = cur.o0 + r;
+                if (o >= g.out_ch) break;
+                float* dst = out + (cur.n * g.out_ch + o) * g.out_w + cur.x0;
+                for (int col = lane; col < cols; col += 32) dst[col] = tile[r * kCQ + col];
+            }
+        }
+        __syncthreads();
+        t_cur = t_nxt, chunk = chunk_nxt, cur = nxt;
+    }
+}
+
+template <typename TIn, int SG>
+static cudaError_t launch_cslide_sg(const TIn* in, const float* wg, float* out, const ConvGeom& g, int round_in,
+                                    cudaStream_t stream) {
+    const int d = static_cast<int>(g.dil);
+    const size_t smem = cslide_smem(d, static_cast<int>(g.taps));
+    // persistent blocks: up to two per SM (the register bound), each walking its tiles' channel
+    // chunks through one double-buffered pipeline
+    const int64_t tiles = g.n * ceil_div(g.out_w, kCQ) * ceil_div(g.out_ch, kCO);
+    const int per_sm = static_cast<int>(std::max<size_t>(1, std::min<size_t>(2, (227 * 1024) / (smem + 1024))));
+    const dim3 grid(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(tiles, per_sm * num_sms()))));
+    const bool two = d * cslide_nbp(d) > 64;
+    cudaError_t e;
+    if (two) {
+        e = cudaFuncSetAttribute(conv_slide_kernel<TIn, SG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        conv_slide_kernel<TIn, SG, 2><<<grid, 256, smem, stream>>>(in, wg, out, g, round_in);
+    } else {
+        e = cudaFuncSetAttribute(conv_slide_kernel<TIn, SG, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        conv_slide_kernel<TIn, SG, 1><<<grid, 256, smem, stream>>>(in, wg, out, g, round_in);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <typename TIn>
+static cudaError_t launch_cslide(const TIn* in, const float* wg, float* out, const ConvGeom& g, int round_in,
+                                 cudaStream_t stream) {
+    switch (cslide_sg(static_cast<int>(g.taps))) {
+        case 1: return launch_cslide_sg<TIn, 1>(in, wg, out, g, round_in, stream);
+        case 2: return launch_cslide_sg<TIn, 2>(in, wg, out, g, round_in, stream);
+        case 3: return launch_cslide_sg<TIn, 3>(in, wg, out, g, round_in, stream);
+        default: return launch_cslide_sg<TIn, 4>(in, wg, out, g, round_in, stream);
+    }
+}
+
 // ------------------------------------------------------------------------------- 1-tap (pointwise)
 // S = 1: out[n][o][x] = sum_i W[o][i] in[n][i][x + off]. Memory-bound; each thread owns 4
 // consecutive columns for all (<= OMAX) outputs, the input is read exactly once. (The config-5
@@ -188,6 +445,10 @@ cudaError_t launch_direct_conv(const void* in, int in_dtype, bool round_in, cons
         if (in_dtype == 0) return launch_pointwise(static_cast<const float*>(in), wg, out, g, round_in ? 1 : 0, stream);
         return launch_pointwise(static_cast<const uint16_t*>(in), wg, out, g, 0, stream);
     }
+    if (cslide_ok(g)) {
+        if (in_dtype == 0) return launch_cslide(static_cast<const float*>(in), wg, out, g, round_in ? 1 : 0, stream);
+        return launch_cslide(static_cast<const uint16_t*>(in), wg, out, g, 0, stream);
+    }
     const int64_t span = kTX + (g.taps - 1) * g.dil;
     const size_t smem = sizeof(float) * static_cast<size_t>(kCC * span + kTO * kCC * g.taps);
     if (smem > 227 * 1024) return cudaErrorInvalidValue;
@@ -238,10 +499,9 @@ static bool pointwise_wgrad_ok(int64_t n, int64_t c, int64_t k, int64_t s);
 // the sliding-window kernel (below) whenever its shared memory fits: the X window of one 256-column
 // chunk plus the (S-1)*d reach of all taps
 static size_t slide_smem(int d, int sg);
-static bool slide_wgrad_ok(int64_t c, int64_t k, int64_t s, int64_t d) {
-    (void)c;
-    (void)k;
-    return d <= 256 && slide_smem(static_cast<int>(d), static_cast<int>(std::min<int64_t>(s, 8))) <= 200 * 1024;
+static bool slide_wgrad_ok(int64_t n, int64_t s, int64_t d, int64_t q) {
+    return d <= 256 && n * ceil_div(q, 256) < (int64_t{1} << 31) &&
+           slide_smem(static_cast<int>(d), static_cast<int>(std::min<int64_t>(s, 8))) <= 200 * 1024;
 }
 static int64_t slide_wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
     const int64_t tiles = ceil_div(k, 16) * ceil_div(c, 16);
@@ -351,7 +611,6 @@ constexpr int kSWG = 8;      // most taps per group (registers)
 // number of 16-B chunks: 16-B reads of 8 consecutive rows hit 8 distinct chunk slots, one wavefront)
 __host__ __device__ inline int slide_lg(int d) { return ((kSWQ + d - 1) / d + 8 + 3) / 4 * 4; }
 __host__ __device__ inline int slide_lx(int d, int sg) { return ((kSWQ + d - 1) / d + 8 + sg - 1 + 3 + 3) / 4 * 4; }
-__host__ __device__ inline int slide_pitch(int words) { return (words + 3) / 8 * 8 + 4; }
 
 // Copies `count` columns of one row (the first `lim` from src, zeros after) into shared memory at
 // dst with cp.async: 16-B copies when src is 16-B aligned, else 8-B when 8-B aligned, else 4-B.
@@ -412,8 +671,9 @@ __global__ void __launch_bounds__(256, SG <= 4 ? 3 : 2) wgrad_slide_kernel(const
     const int gstep = 4 * (step_r * lg + step_q), xstep = 4 * (step_r * lx + step_q);  // bytes per 32 columns
     const int gwrap = 4 * (1 - d * lg), xwrap = 4 * (1 - d * lx);                      // phase wrap-around
     auto stage = [&](int64_t u, int b) {
-        const int64_t n = u / chunks_per_item;
-        const int64_t q0 = (u % chunks_per_item) * kSWQ;
+        // (32-bit: units < 2^31 by slide_wgrad_ok)
+        const int64_t n = static_cast<int>(u) / static_cast<int>(chunks_per_item);
+        const int64_t q0 = static_cast<int64_t>(static_cast<int>(u) % static_cast<int>(chunks_per_item)) * kSWQ;
         const uint32_t gsb = sbase + 4u * static_cast<uint32_t>(b * buf_words);
         const uint32_t xsb = gsb + 4u * static_cast<uint32_t>(kSWT * gpitch);
         for (int r = tid / 32; r < kSWT; r += 8) {
@@ -810,7 +1070,7 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
         note_launch();
         return cudaGetLastError();
     }
-    if (slide_wgrad_ok(c, k, s, d)) {
+    if (slide_wgrad_ok(n, s, d, q)) {
         const int64_t splits = slide_wgrad_splits(n, c, k, s, d, q);
         dim3 grid(static_cast<unsigned>(ceil_div(k, kSWT)), static_cast<unsigned>(ceil_div(c, kSWT)),
                   static_cast<unsigned>(splits));
