@@ -498,10 +498,15 @@ static bool pointwise_wgrad_ok(int64_t n, int64_t c, int64_t k, int64_t s);
 
 // the sliding-window kernel (below) whenever its shared memory fits: the X window of one 256-column
 // chunk plus the (S-1)*d reach of all taps
+namespace {
+constexpr int kSWT = 16;     // filters / channels per block tile
+constexpr int kSWQ = 256;    // columns per unit
+constexpr int kSWG = 10;     // most taps per group (registers)
+}  // namespace
 static size_t slide_smem(int d, int sg);
 static bool slide_wgrad_ok(int64_t n, int64_t s, int64_t d, int64_t q) {
     return d <= 256 && n * ceil_div(q, 256) < (int64_t{1} << 31) &&
-           slide_smem(static_cast<int>(d), static_cast<int>(std::min<int64_t>(s, 8))) <= 200 * 1024;
+           slide_smem(static_cast<int>(d), static_cast<int>(std::min<int64_t>(s, kSWG))) <= 200 * 1024;
 }
 static int64_t slide_wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
     const int64_t tiles = ceil_div(k, 16) * ceil_div(c, 16);
@@ -509,7 +514,7 @@ static int64_t slide_wgrad_splits(int64_t n, int64_t c, int64_t k, int64_t s, in
     // one full wave: resident blocks per SM by the register bound of the widest tap group (<= 4 taps:
     // 3, else 2) and the shared-memory bound (227 KB, 1 KB reserved per block); at least 3 units per
     // block so the copy of the next unit overlaps the current one
-    const int64_t widest = ceil_div(s, ceil_div(s, 8));
+    const int64_t widest = ceil_div(s, ceil_div(s, kSWG));
     const int64_t by_smem = (227 * 1024) / (static_cast<int64_t>(slide_smem(static_cast<int>(d), static_cast<int>(widest))) + 1024);
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(widest <= 4 ? 3 : 2, by_smem));
     const int64_t want = std::max<int64_t>(1, per_sm * num_sms() / tiles);
@@ -602,11 +607,6 @@ __global__ void __launch_bounds__(256) direct_wgrad_kernel(const TIn* __restrict
 // consecutive phase columns shares sg - 1 values) for 8 * sg FMAs. Units are (item, 256-column
 // chunk), split contiguously over the grid; partials part[split][k][c][s], summed in ascending
 // split order by reduce_splits_kernel (deterministic).
-namespace {
-constexpr int kSWT = 16;     // filters / channels per block tile
-constexpr int kSWQ = 256;    // columns per unit
-constexpr int kSWG = 8;      // most taps per group (registers)
-}  // namespace
 // per-phase lengths (multiples of 4 floats, room for the 8-column read-ahead) and row pitches (an odd
 // number of 16-B chunks: 16-B reads of 8 consecutive rows hit 8 distinct chunk slots, one wavefront)
 __host__ __device__ inline int slide_lg(int d) { return ((kSWQ + d - 1) / d + 8 + 3) / 4 * 4; }
@@ -1036,7 +1036,8 @@ static cudaError_t launch_slide(int sg, dim3 grid, size_t smem, cudaStream_t str
         return launch_slide_sg<TIn, SGV>(grid, smem, stream, x, dy, part, n, c, k, s, d, q, splits, lx, round_in, s0)
     switch (sg) {
         C1D_SLIDE(1); C1D_SLIDE(2); C1D_SLIDE(3); C1D_SLIDE(4); C1D_SLIDE(5); C1D_SLIDE(6); C1D_SLIDE(7);
-        default: C1D_SLIDE(8);
+        C1D_SLIDE(8); C1D_SLIDE(9);
+        default: C1D_SLIDE(10);
     }
 #undef C1D_SLIDE
 }
@@ -1075,7 +1076,7 @@ cudaError_t launch_direct_wgrad(const void* x, const void* dy, int in_dtype, boo
         dim3 grid(static_cast<unsigned>(ceil_div(k, kSWT)), static_cast<unsigned>(ceil_div(c, kSWT)),
                   static_cast<unsigned>(splits));
         cudaError_t e = cudaSuccess;
-        // balanced tap groups of at most kSWG taps (S = 9 -> 5 + 4, not 8 + 1)
+        // balanced tap groups of at most kSWG taps (S = 25 -> 9 + 8 + 8)
         const int64_t groups = ceil_div(s, kSWG);
         for (int64_t gi = 0, s0 = 0; gi < groups && e == cudaSuccess; ++gi) {
             const int sg = static_cast<int>(s / groups + (gi < s % groups ? 1 : 0));
