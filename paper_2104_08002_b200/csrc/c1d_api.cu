@@ -296,6 +296,40 @@ bool xin_wgrad_preferred(const c1d_desc& d) { return d.c <= 32 || d.d == 1; }
 bool xr_wgrad_ok(const c1d_desc& d, int64_t q_pad) {
     return (d.d == 1 || d.d == 2 || d.d == 4) && tc_wgrad_v3_supported(d.n, d.c, d.k, d.s, d.d, q_pad);
 }
+// backward-weight on channel-octet streams (any d != 8 up to 64; tc_wgrad.cu W2Plan::xt): X relaid
+// once as XT[n][C/8][rows][8], every tap shift a descriptor offset: no expanded rows, no phase
+// copies, no chunk planes
+bool xt_wgrad_ok(const c1d_desc& d, int64_t q_pad) {
+    static const bool off = getenv("C1D_NO_XT") != nullptr;     // dev A/B switches
+    static const bool at_d8 = getenv("C1D_XT_D8") != nullptr;
+    // (d = 4 with <= 32 channels: the expanded-row loaders measured slightly faster, 31.5 vs 34.5 us
+    // at C = 16, S = 3)
+    if (off || (d.d == 8 && !at_d8) || (d.d == 4 && d.c <= 32) || d.d > 64) return false;
+    // d = 8m also runs as chunk planes at dilation 8; the octet streams win there only while the T
+    // tap copies stacked on M (T = 128 / CP) reach little: measured (config-4 sweep, d = 16) T = 1
+    // or T*d*S <= 600 (C = 32, S = 9: 47 vs 60 us; C = 32, S = 25: 114 vs 69 us)
+    if (d.d % 8 == 0) {
+        int64_t cp = 16;
+        while (cp < d.c) cp *= 2;
+        const int64_t t = 128 / cp;
+        if (t > 1 && t * d.d * d.s > 600) return false;
+    }
+    return d.n * ((d.c + 7) / 8) <= 65535 && tc_wgrad_xt_supported(d.n, d.c, d.k, d.s, d.d, q_pad);
+}
+// the FP32 split's backward-weight problem (2C channels x 2K filters, BF16) and whether it runs
+// as one octet-stream launch per split pass (else: the BF16 block passes, the phase / plane plans)
+c1d_desc split_wgrad_desc(const c1d_desc& d) {
+    c1d_desc d2 = d;
+    d2.c = 2 * d.c;
+    d2.k = 2 * d.k;
+    return d2;
+}
+bool split_wgrad_xt_ok(const c1d_desc& d, int64_t q) {
+    return d.c * 2 <= 128 && d.k * 2 <= 128 && q % 8 == 0 && xt_wgrad_ok(split_wgrad_desc(d), q);
+}
+int64_t xt_rows(const c1d_desc& d, int64_t q_pad) {
+    return std::max<int64_t>(d.w_in, q_pad + d.d * (d.s - 1)) + tc_wgrad_xt_pad_rows(d.n, d.c, d.k, d.s, d.d, q_pad);
+}
 // backward-weight: Q is padded to a multiple of 8 (zero dY columns add nothing) and x gets a
 // zero-padded pitch covering Q_pad + d(S-1) when either width is unaligned.
 struct WgradPad {
@@ -367,21 +401,16 @@ SplitConv split_conv_geom(const c1d_desc& d, c1d_pass pass, int64_t q, const Dil
 constexpr int64_t kMaxSplitTerms = 3300;
 bool split_wgrad_blocks(const c1d_desc& d);
 
-// FP32 crossover between the FFMA sliding-window kernels (direct.cu) and the BF16 operand split:
-// below these products per output column (C_in * S; max(C, K) * S for backward-weight) the FFMA
-// kernels are faster. Measured on the BASELINE config-4 sweep (N = 16, Q = 20000, C = K in
-// {16, 32, 64, 128}, S in {3, 9, 25, 51}): the split's per-call floor
-// (split / pack / reduce launches) dominates small problems, and its expanded-row and plane
-// plans (d != 8) cost more tensor-core work per product than the native d = 8 plan.
-int64_t ffma_fp32_limit(c1d_pass pass, int64_t dil, int64_t width) {
-    if (pass == C1D_PASS_BACKWARD_WEIGHT) {
-        switch (dil) {
-            case 1: return INT64_MAX;
-            case 2: return 1200;
-            case 4: return width <= 64 ? 450 : 300;
-            default: return 150;
-        }
-    }
+// FP32 crossover between the FFMA sliding-window kernels (direct.cu) and the BF16 operand split,
+// measured on the BASELINE config-4 sweep (N = 16, Q = 20000, C = K in {16, 32, 64, 128}, S in
+// {3, 9, 25, 51}; forced-algorithm sweeps): the split's per-call floor
+// (split / pack / sum launches) dominates small problems.
+//   forward / backward-data: FFMA while C_in * S is at most a per-dilation limit (the split's
+//   d != 8 plans spend more tensor-core work per product than the native one);
+//   backward-weight: FFMA while C * K * S (products per output column) is at most 24000 at
+//   d = 1, 2, 4 (the split runs on channel-octet streams there) and 3000 otherwise.
+int64_t ffma_fp32_limit(c1d_pass pass, int64_t dil) {
+    if (pass == C1D_PASS_BACKWARD_WEIGHT) return dil == 1 || dil == 2 || dil == 4 ? 24000 : 3000;
     switch (dil) {
         case 1: return 1000;
         case 2: return 450;
@@ -391,8 +420,9 @@ int64_t ffma_fp32_limit(c1d_pass pass, int64_t dil, int64_t width) {
     }
 }
 bool ffma_beats_split(const c1d_desc& d, c1d_pass pass) {
-    const int64_t width = pass == C1D_PASS_FORWARD ? d.c : (pass == C1D_PASS_BACKWARD_DATA ? d.k : std::max(d.c, d.k));
-    return width * d.s <= ffma_fp32_limit(pass, d.d, width);
+    if (pass == C1D_PASS_BACKWARD_WEIGHT) return d.c * d.k * d.s <= ffma_fp32_limit(pass, d.d);
+    const int64_t width = pass == C1D_PASS_FORWARD ? d.c : d.k;
+    return width * d.s <= ffma_fp32_limit(pass, d.d);
 }
 
 // Resolve AUTO.
@@ -400,6 +430,7 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
     const bool tc_ok = [&] {
         if (!is_bf16(d)) return false;
         const DilPlan dp = dil_plan(d, q);
+        if (pass == C1D_PASS_BACKWARD_WEIGHT && xt_wgrad_ok(d, wgrad_pad(d, q).q_pad)) return true;  // any d
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {
             const WgradPad wp = wgrad_pad(d, q);
@@ -421,6 +452,7 @@ c1d_algo resolve(const c1d_desc& d, c1d_pass pass, int64_t q) {
         if (is_bf16(d) || d.in_dtype != C1D_DTYPE_F32) return false;
         if (d.algo == C1D_ALGO_AUTO && ffma_beats_split(d, pass)) return false;
         const DilPlan dp = dil_plan(d, q);
+        if (pass == C1D_PASS_BACKWARD_WEIGHT && split_wgrad_xt_ok(d, q)) return true;  // any d
         if (dp.kind == DilPlan::kNone) return false;
         if (pass == C1D_PASS_BACKWARD_WEIGHT) {
             // small problems at d < 8 (few taps per phase x channels) stay on the sliding-window FFMA
@@ -476,6 +508,12 @@ size_t workspace_for(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo)
     // tensor-core paths: BF16 copies of FP32 inputs + kernel workspace
     const bool conv_in_f32 = d.in_dtype == C1D_DTYPE_F32;
     const DilPlan dp = dil_plan(d, q);
+    if (pass == C1D_PASS_BACKWARD_WEIGHT && xt_wgrad_ok(d, wgrad_pad(d, q).q_pad)) {
+        const WgradPad wpd = wgrad_pad(d, q);
+        return align_up(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad)) +
+               align_up(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * ((d.c + 7) / 8) * xt_rows(d, wpd.q_pad))) +
+               align_up(tc_wgrad_xt_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+    }
     if (pass == C1D_PASS_BACKWARD_WEIGHT && dp.kind == DilPlan::kPhases && xr_wgrad_ok(d, wgrad_pad(d, q).q_pad) &&
         xin_wgrad_preferred(d) && tc_wgrad_xin_supported(d.n, d.c, d.k, d.s, d.d, wgrad_pad(d, q).q_pad)) {
         const WgradPad wpd = wgrad_pad(d, q);
@@ -783,6 +821,21 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
         step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, pat_x[pass], stream); });
         step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[pass], stream); });
     };
+    const c1d_desc d2 = split_wgrad_desc(d);
+    if (split_wgrad_xt_ok(d, q)) {
+        // channel-octet streams of the split x, one launch per split pass
+        const int64_t rows = xt_rows(d2, q);
+        uint16_t* xt = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * ((d2.c + 7) / 8) * rows));
+        float* dw4[2] = {bump.take<float>(4 * sizeof(float) * kcs), bump.take<float>(4 * sizeof(float) * kcs)};
+        void* kws = bump.take<char>(tc_wgrad_xt_workspace_bytes(d.n, d2.c, d2.k, d.s, d.d, q));
+        for (int ps = 0; ps < 2; ++ps) {
+            split_pass(ps);
+            step([&] { return launch_to_octets(x2, C1D_DTYPE_BF16, xt, d.n, d2.c, d.w_in, rows, stream); });
+            step([&] { return launch_tc_wgrad_xt(xt, rows, g2, dw4[ps], kws, d.n, d2.c, d2.k, d.s, d.d, q, stream); });
+        }
+        step([&] { return launch_sum_split3(dw4[0], dw4[1], dw, d.k, d.c, d.s, stream); });
+        return e;
+    }
     if (dp.kind == DilPlan::kPhases && (d.d == 1 || d.d == 2 || d.d == 4) &&
         tc_wgrad_v3_supported(d.n, 2 * d.c, 2 * d.k, d.s, d.d, q)) {
         // expanded rows of the split x, one launch per split pass
@@ -1145,6 +1198,31 @@ c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, const void* 
         return C1D_OK;
     }
     const DilPlan dpl = dil_plan(d, q);
+    if (xt_wgrad_ok(d, wgrad_pad(d, q).q_pad)) {
+        const WgradPad wpd = wgrad_pad(d, q);
+        // the octet-stream plan needs no aligned x pitch: dY is copied only when Q itself is
+        // unaligned or stored as FP32
+        const uint16_t* g16 = static_cast<const uint16_t*>(dy);
+        if (q % 8 != 0 || d.in_dtype == C1D_DTYPE_F32) {
+            uint16_t* tg = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.k * wpd.q_pad));
+            if (bump.overflow) return workspace_overflow();
+            e = q % 8 != 0 ? launch_pad_rows(dy, d.in_dtype, tg, d.n * d.k, q, wpd.q_pad, stream)
+                           : launch_round_bf16(static_cast<const float*>(dy), tg, d.n * d.k * q, stream);
+            if (e != cudaSuccess) return cuda_fail(e, "dy copy");
+            g16 = tg;
+        }
+        // channel-octet streams of x (FP32 rounded on the way)
+        const int64_t rows = xt_rows(d, wpd.q_pad);
+        uint16_t* xt = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * ((d.c + 7) / 8) * rows));
+        if (bump.overflow) return workspace_overflow();
+        e = launch_to_octets(x, d.in_dtype, xt, d.n, d.c, d.w_in, rows, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "to_octets");
+        void* kws = bump.take<char>(tc_wgrad_xt_workspace_bytes(d.n, d.c, d.k, d.s, d.d, wpd.q_pad));
+        if (bump.overflow) return workspace_overflow();
+        e = launch_tc_wgrad_xt(xt, rows, g16, dw_kcs, kws, d.n, d.c, d.k, d.s, d.d, wpd.q_pad, stream);
+        if (e != cudaSuccess) return cuda_fail(e, "tc_wgrad (octet streams)");
+        return C1D_OK;
+    }
     if (dpl.kind == DilPlan::kPlanes) {
         // d = 8m: both operands as chunk planes; the plane items sum into the same dW
         uint16_t* px = bump.take<uint16_t>(sizeof(uint16_t) * static_cast<size_t>(d.n * d.c * d.w_in));

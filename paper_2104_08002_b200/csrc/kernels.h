@@ -140,6 +140,18 @@ size_t tc_wgrad_xin_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, 
 cudaError_t launch_tc_wgrad_xin(const uint16_t* x_bf16, int64_t x_w, const uint16_t* dy_bf16, float* dw_kcs,
                                 void* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q,
                                 cudaStream_t stream);
+// any d < 8 (1, 2, 4) on channel-octet streams XT[n][ceil(C/8)][rows][8] (launch_to_octets): every
+// tap shift is a descriptor offset (tc_wgrad.cu, W2Plan::xt); rows >= q + d*(s-1)
+bool tc_wgrad_xt_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+size_t tc_wgrad_xt_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+// zero rows XT needs past q + d*(s-1): a stage's TMA window may run that far past the last column
+int64_t tc_wgrad_xt_pad_rows(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
+cudaError_t launch_tc_wgrad_xt(const uint16_t* xt, int64_t rows, const uint16_t* dy_bf16, float* dw_kcs,
+                               void* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q,
+                               cudaStream_t stream);
+// XT[n][o][u][e] = bf16(in[n][8o + e][u]), u < rows (zero past C / w)
+cudaError_t launch_to_octets(const void* in, int in_dtype, uint16_t* out, int64_t n, int64_t c, int64_t w,
+                             int64_t rows, cudaStream_t stream);
 
 // relayout.cu: dilations other than 8 on the dilation-8 tensor-core kernels
 // (O, I, S) -> (O, P*I, S'), S' = ceil(S/m): out[o][b*I + i][t] = w[o][i][b + m*t] (0 past S), P = min(m, S)

@@ -127,20 +127,29 @@ __global__ void shift_copies_kernel(const TIn* __restrict__ in, TOut* __restrict
     }
 }
 
+// grid (column blocks of 1024, rows in y with a stride loop): 4 columns per thread, 32-bit
+// column math (a per-element 64-bit division made this HBM-trivial copy ALU-bound)
 template <typename TIn>
-__global__ void pad_rows_kernel(const TIn* __restrict__ in, uint16_t* __restrict__ out, int64_t rows, int64_t w,
-                                int64_t w_pad) {
-    const int64_t total = rows * w_pad;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = e % w_pad, r = e / w_pad;
-        uint16_t v = 0;
-        if (j < w) {
-            if constexpr (sizeof(TIn) == 4)
-                v = fp32_to_bf16_bits(reinterpret_cast<const float*>(in)[r * w + j]);
-            else
-                v = reinterpret_cast<const uint16_t*>(in)[r * w + j];
+__global__ void __launch_bounds__(256) pad_rows_kernel(const TIn* __restrict__ in, uint16_t* __restrict__ out,
+                                                       int64_t rows, int64_t w, int64_t w_pad) {
+    const int j0 = (blockIdx.x * 256 + threadIdx.x) * 4;
+    if (j0 >= w_pad) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const TIn* src = in + r * w;
+        uint16_t* dst = out + r * w_pad;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+            const int j = j0 + jj;
+            if (j >= w_pad) break;
+            uint16_t v = 0;
+            if (j < w) {
+                if constexpr (sizeof(TIn) == 4)
+                    v = fp32_to_bf16_bits(__ldg(reinterpret_cast<const float*>(src) + j));
+                else
+                    v = __ldg(reinterpret_cast<const uint16_t*>(src) + j);
+            }
+            dst[j] = v;
         }
-        out[e] = v;
     }
 }
 
@@ -175,7 +184,55 @@ __global__ void expand_rows_kernel(const TIn* __restrict__ in, uint4* __restrict
     }
 }
 
+// Channel-octet streams for tc_wgrad2's xt mode: out[n][o][u][0..7] = bf16(in[n][8o + e][u]) for
+// u < rows (zero for channels >= C or columns >= w). Thread u of a block reads column u of the
+// octet's 8 channel rows (each load instruction is coalesced along the row) and writes one 16-B
+// row (consecutive threads: consecutive rows).
+template <typename TIn>
+__global__ void __launch_bounds__(256) to_octets_kernel(const TIn* __restrict__ in, uint4* __restrict__ out,
+                                                        int64_t c, int64_t w, int64_t rows, int64_t octets) {
+    const int64_t no = blockIdx.y;  // n * octets + o
+    const int64_t n = no / octets, o = no % octets;
+    const int64_t u = static_cast<int64_t>(blockIdx.x) * 256 + threadIdx.x;
+    if (u >= rows) return;
+    uint16_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+        const int64_t ch = 8 * o + e;
+        uint16_t b = 0;
+        if (ch < c && u < w) {
+            const TIn* src = in + (n * c + ch) * w + u;
+            if constexpr (sizeof(TIn) == 4)
+                b = fp32_to_bf16_bits(__ldg(reinterpret_cast<const float*>(src)));
+            else
+                b = __ldg(reinterpret_cast<const uint16_t*>(src));
+        }
+        v[e] = b;
+    }
+    uint4 pk;
+    pk.x = v[0] | (static_cast<uint32_t>(v[1]) << 16);
+    pk.y = v[2] | (static_cast<uint32_t>(v[3]) << 16);
+    pk.z = v[4] | (static_cast<uint32_t>(v[5]) << 16);
+    pk.w = v[6] | (static_cast<uint32_t>(v[7]) << 16);
+    out[no * rows + u] = pk;
+}
+
 }  // namespace
+
+cudaError_t launch_to_octets(const void* in, int in_dtype, uint16_t* out, int64_t n, int64_t c, int64_t w,
+                             int64_t rows, cudaStream_t stream) {
+    const int64_t octets = (c + 7) / 8;
+    if (n * octets > 65535) return cudaErrorInvalidValue;
+    const dim3 grid(static_cast<unsigned>(ceil_div(rows, 256)), static_cast<unsigned>(n * octets));
+    if (in_dtype == 0)
+        to_octets_kernel<float><<<grid, 256, 0, stream>>>(static_cast<const float*>(in), reinterpret_cast<uint4*>(out), c,
+                                                          w, rows, octets);
+    else
+        to_octets_kernel<uint16_t><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(in),
+                                                             reinterpret_cast<uint4*>(out), c, w, rows, octets);
+    note_launch();
+    return cudaGetLastError();
+}
 
 cudaError_t launch_expand_rows(const void* in, int in_dtype, uint16_t* out, int64_t nc, int64_t w, int64_t d,
                                int64_t off, int64_t rows, cudaStream_t stream) {
@@ -213,12 +270,13 @@ cudaError_t launch_shift_copies_f32(const float* in, float* out, int64_t n, int6
 
 cudaError_t launch_pad_rows(const void* in, int in_dtype, uint16_t* out, int64_t rows, int64_t w, int64_t w_pad,
                             cudaStream_t stream) {
+    if (w_pad >= (int64_t{1} << 30)) return cudaErrorInvalidValue;
+    const dim3 grid(static_cast<unsigned>(ceil_div(w_pad, 1024)), static_cast<unsigned>(std::min<int64_t>(rows, 65535)));
+    if (rows == 0) return cudaSuccess;
     if (in_dtype == 0)
-        pad_rows_kernel<float><<<blocks_for(rows * w_pad), 256, 0, stream>>>(static_cast<const float*>(in), out, rows,
-                                                                             w, w_pad);
+        pad_rows_kernel<float><<<grid, 256, 0, stream>>>(static_cast<const float*>(in), out, rows, w, w_pad);
     else
-        pad_rows_kernel<uint16_t><<<blocks_for(rows * w_pad), 256, 0, stream>>>(static_cast<const uint16_t*>(in), out,
-                                                                                rows, w, w_pad);
+        pad_rows_kernel<uint16_t><<<grid, 256, 0, stream>>>(static_cast<const uint16_t*>(in), out, rows, w, w_pad);
     note_launch();
     return cudaGetLastError();
 }

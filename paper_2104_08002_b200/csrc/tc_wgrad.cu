@@ -362,16 +362,34 @@ struct W2Plan {
     // channel, 16-B cp.async pieces) and write the ring's rows themselves (no row tensor in HBM)
     int xin, raw_cols;
     uint32_t raw_bytes;
+    // Channel-octet streams (xt, d = 1, 2, 4): X arrives as XT[n][c/8][w][8] (launch_to_octets), 8
+    // channels x one column = one 16-B row. Each stage holds its own X window (no ring): 16
+    // streams (M groups) of xt_rows rows, stream j = t*(CP/8) + o = channel octet o of copy t,
+    // shifted by t*d columns (the T taps of a group stacked on M), each copy loaded by ONE 3-D TMA
+    // box (256 elements x xt_nb blocks x CP/8 octets, through an overlapping view whose block
+    // stride is 512 B) that lands the octets xt_rows*16 B apart. A is MN-major: K rows (columns)
+    // 16 B apart, K groups 128 B apart, M groups one stream apart, so ANY column shift is a
+    // start-address offset: tap group g of K-step k starts at row 16k + g*T*d. No expansion, no
+    // dY copies, and the loader warps stay idle.
+    int xt;
+    int xt_nb;                    // 256-element blocks per stream and stage (xt_rows = 32 * xt_nb)
+    uint32_t xt_x_bytes;          // X bytes per stage (16 streams)
+    uint32_t stream_bytes;        // xt: stream stride in a stage (xt_rows x 16 B)
+    uint32_t a_lbo, a_sbo, a_mn;  // A descriptor
+    uint32_t a_ks_bytes, a_g_bytes;  // A advance per K-step / per tap group
 };
 
-bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out, bool xin = false) {
+bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out, bool xin = false,
+                 bool xt = false, int gpc_cap = 8) {
     if (q % 8 != 0 || q < 16) return false;
-    if (d != 8 && d != 1 && d != 2 && d != 4) return false;
+    if (xt ? (d < 1 || d > 64) : (d != 8 && d != 1 && d != 2 && d != 4)) return false;
     if (xin && d == 8) return false;
+    if (xin && xt) return false;
     if (c > 128 || k > 128) return false;
     if (n * c >= (int64_t{1} << 31) || n * k >= (int64_t{1} << 31)) return false;
     W2Plan p{};
-    p.ph = static_cast<int>(8 / d);
+    p.xt = xt ? 1 : 0;
+    p.ph = xt ? 1 : static_cast<int>(8 / d);  // (xt: any d)
     p.cp = 16;
     while (p.cp < c) p.cp *= 2;
     p.t = 128 / p.cp;
@@ -380,14 +398,14 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     // dY copies (P > 1) shift by Bq = 8T columns, so their boxes are 8T columns wide; at T = 1 that is a
     // 16-B box, which TMA moves at ~16 B/clk (too slow to feed the MMAs: C = 128 ran 63% data-starved),
     // so T = 1 and the expanded rows run without copies and with wide dY boxes
-    p.p = (d == 8 && p.t > 1) ? std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t))) : 1;
+    p.p = (d == 8 && !xt && p.t > 1) ? std::min<int>(256 / p.kpw, static_cast<int>(ceil_div(s, p.t))) : 1;
     p.n = p.p * p.kpw;
     p.bq = 8 * p.t;  // with P = 1 re-chosen per stage size below (64 / 32 / 16 columns)
     if (p.bq > 64) return false;
     p.taps_per_group = p.t * p.p;
     p.groups_total = static_cast<int>(ceil_div(s, p.taps_per_group));
     p.gpc = std::max(1, static_cast<int>(kTmemCols) / p.n);
-    if (p.gpc > 8) p.gpc = 8;
+    if (p.gpc > gpc_cap) p.gpc = gpc_cap;
     if (p.n > static_cast<int>(kTmemCols)) return false;
     if (p.gpc > p.groups_total) p.gpc = p.groups_total;
     p.roles = static_cast<int>(ceil_div(p.groups_total, p.gpc));
@@ -421,8 +439,10 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     // Ring positions [0, xb) are mirrored past the end, xb = the furthest chunk one stage's MMAs
     // reach beyond the stage's first chunk, so a stage never wraps. Expanded rows take ph chunks
     // per 8 columns, so their stages shrink (fewer K-steps) until the ring fits.
-    p.chunk_bytes = static_cast<uint32_t>(p.cp * 16);
-    p.span = static_cast<int>(ceil_div(p.gpc * p.taps_per_group + p.t + p.ph, 4) * 4);
+    p.chunk_bytes = xt ? 16u : static_cast<uint32_t>(p.cp * 16);
+    // xt: a stage's window is its 16*ks rows plus the reach of the other tap groups, (gpc-1)*T*d
+    p.span = xt ? static_cast<int>(ceil_div(static_cast<int64_t>(p.gpc - 1) * p.t * d + 1, 4) * 4)
+                : static_cast<int>(ceil_div(p.gpc * p.taps_per_group + p.t + p.ph, 4) * 4);
     static const int max_stages = [] {  // C1D_W2_STAGES: dev override of the stage cap
         const char* e = getenv("C1D_W2_STAGES");
         const int v = e ? atoi(e) : kW2MaxStages;
@@ -444,19 +464,25 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         p.box_bytes = static_cast<uint32_t>(p.kpw * 2 * p.bq);
         p.ks = ks;
         p.stage_q = 16 * p.ks;
-        p.kch = 2 * p.ks * p.ph;
-        p.xb = 2 * p.ph * (p.ks - 1) + (p.gpc - 1) * p.taps_per_group + p.t + p.ph;
+        p.kch = xt ? 16 * p.ks : 2 * p.ks * p.ph;
+        p.xb = xt ? 0 : 2 * p.ph * (p.ks - 1) + (p.gpc - 1) * p.taps_per_group + p.t + p.ph;
         p.x_chunks = p.kch + p.span;
         p.nbox = p.stage_q / p.bq + p.p - 1 + (p.bq == 8 ? 1 : 0);
         p.y_bytes = (static_cast<uint32_t>(p.nbox) * p.box_bytes + 1023) & ~1023u;
         p.stage_bytes = p.y_bytes;
+        if (xt) {  // the stage's X window: 16 K-step rows x ks plus the other groups' reach
+            p.xt_nb = static_cast<int>(ceil_div(p.kch + p.span, 32));
+            p.stream_bytes = static_cast<uint32_t>(p.xt_nb) * 512u;
+            p.xt_x_bytes = 16u * p.stream_bytes;
+            p.stage_bytes = p.y_bytes + p.xt_x_bytes;
+        }
         p.xin = xin ? 1 : 0;
         p.raw_cols = xin ? static_cast<int>(ceil_div(static_cast<int64_t>(d) * (p.span + p.kch) + 40, 8) * 8) : 0;
         p.raw_bytes = xin ? ((static_cast<uint32_t>(p.cp * p.raw_cols * 2) + 1023) & ~1023u) : 0u;  // one of two
         for (int st = max_stages; st >= 3; --st) {
             p.stages = st;
-            p.ring = static_cast<int>(ceil_div(2 * p.span + st * p.kch, 4) * 4);
-            p.ring_bytes = ((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u;
+            p.ring = xt ? 0 : static_cast<int>(ceil_div(2 * p.span + st * p.kch, 4) * 4);
+            p.ring_bytes = xt ? 0u : (((static_cast<uint32_t>(p.ring + p.xb) * p.chunk_bytes) + 1023) & ~1023u);
             if (p.ring_bytes + static_cast<uint32_t>(st) * p.stage_bytes + 2 * p.raw_bytes <= kW2SmemBudget) {
                 ok = true;
                 break;
@@ -464,14 +490,38 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         }
     }
     if (!ok) return false;
+    if (xt && (p.stream_bytes >= (1u << 18) || p.xt_nb > 256)) return false;  // descriptor stride / box dims
+    if (xt) {
+        p.a_mn = 1;
+        p.a_lbo = 128;                // K groups (8 columns) are consecutive 128-B core matrices
+        p.a_sbo = p.stream_bytes;     // M groups (8 rows of D) are streams
+        p.a_ks_bytes = 16u * 16u;     // a K-step = 16 rows
+        p.a_g_bytes = static_cast<uint32_t>(p.t * d) * 16u;
+    } else {
+        p.a_mn = 0;
+        p.a_lbo = static_cast<uint32_t>(p.ph * p.cp * 16);
+        p.a_sbo = 128;
+        p.a_ks_bytes = 2u * static_cast<uint32_t>(p.ph) * p.chunk_bytes;
+        p.a_g_bytes = static_cast<uint32_t>(p.taps_per_group) * p.chunk_bytes;
+    }
     p.x_bytes = p.ring_bytes;
     p.smem_bytes = p.ring_bytes + static_cast<size_t>(p.stages) * p.stage_bytes + 2 * p.raw_bytes + 1024;
     *out = p;
     return true;
 }
 
+// xt plans: the widest tap-group count per CTA whose stage window (16 K-step rows plus the other
+// groups' reach, (gpc-1)*T*d rows) still leaves >= 3 pipeline stages; long reaches (large T*d)
+// trade roles (each re-reading X and dY) for window size
+bool make_w2plan_xt(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q, W2Plan* out) {
+    for (int cap = 8; cap >= 1; --cap)
+        if (make_w2plan(n, c, k, s, d, q, out, false, true, cap)) return true;
+    return false;
+}
+
 struct W2Params {
     int64_t n_items, c, k, s, q, w_in;
+    int64_t dil;
     int64_t steps_per_item, total_steps;
     int64_t seg;  // K-steps per accumulation segment (0: the whole split is one chain)
     int64_t slot_elems;  // floats per slot: K x (the role's taps) x C
@@ -594,7 +644,8 @@ __device__ __forceinline__ void w2_expand_d(int off, uint32_t rc, int p0, int np
 }
 
 __global__ void __launch_bounds__(kW2Threads, 1)
-    tc_wgrad2_kernel(const __grid_constant__ CUtensorMap ymap, const W2Params p) {
+    tc_wgrad2_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
+                     const W2Params p) {
     extern __shared__ uint8_t smem_raw[];
     __shared__ uint64_t full[kW2MaxStages], empty[kW2MaxStages];
     __shared__ uint64_t acc_full, acc_empty;
@@ -614,7 +665,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < pl.stages; ++s) {
-            mbar_init(&full[s], 1 + kLoaderThreads);  // dY TMA (tx bytes) + every X loader thread
+            mbar_init(&full[s], pl.xt ? 1 : 1 + kLoaderThreads);  // dY (+ xt: X) TMA tx bytes + every X loader thread
             mbar_init(&empty[s], 1);
         }
         mbar_init(&acc_full, 1);
@@ -634,6 +685,8 @@ __global__ void __launch_bounds__(kW2Threads, 1)
     if (warp == 0) {
         if (lane == 0) {
             prefetch_tmap(&ymap);
+            if (pl.xt) prefetch_tmap(&xmap);
+            const int octets = static_cast<int>((p.c + 7) / 8);
             long long tw_sum = 0;
             const long long tb = clock64();
             int stage = 0;
@@ -648,12 +701,21 @@ __global__ void __launch_bounds__(kW2Threads, 1)
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     tw_sum += clock64() - tw;
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.nbox) * pl.box_bytes);
+                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.nbox) * pl.box_bytes + (pl.xt ? pl.xt_x_bytes : 0u));
                     uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
                     for (int b = 0; b < pl.nbox; ++b)
                         tma_load_3d(smem_u32(sbase + static_cast<uint32_t>(b) * pl.box_bytes), &ymap,
                                     static_cast<int32_t>(q0 - back + static_cast<int64_t>(b) * pl.bq), 0,
                                     static_cast<int32_t>(item), fb);
+                    if (pl.xt) {
+                        // copy t: columns q0 + tap0*d + t*d .. of every octet, one box
+                        const int64_t col0 = q0 + static_cast<int64_t>(tap0) * p.dil;
+                        const uint32_t xs = smem_u32(sbase + pl.y_bytes);
+                        for (int t = 0; t < pl.t; ++t)
+                            tma_load_3d(xs + static_cast<uint32_t>(t * (pl.cp / 8)) * pl.stream_bytes, &xmap,
+                                        static_cast<int32_t>(8 * (col0 + static_cast<int64_t>(t) * p.dil)), 0,
+                                        static_cast<int32_t>(item * octets), fb);
+                    }
                     if (++stage == pl.stages) {
                         stage = 0;
                         phase ^= 1;
@@ -667,7 +729,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             }
         }
     } else if (warp == 1) {
-        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.n), kFmtBF16, 0, 0);
+        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.n), kFmtBF16, pl.a_mn, 0);
         // B (dY) descriptor: swizzled K-major rows of 2*Bq bytes (8-row atoms), or for Bq = 8 the
         // plain core-matrix layout with K-chunks one box apart.
         const uint32_t b_sbo = pl.bq == 8 ? 128u : 16u * static_cast<uint32_t>(pl.bq);
@@ -680,8 +742,8 @@ __global__ void __launch_bounds__(kW2Threads, 1)
         // 16/Bq K-steps (32 B each) per box
         W2Issue wi;
         wi.idesc = idesc;
-        wi.a_ks = (2u * static_cast<uint32_t>(pl.ph) * pl.chunk_bytes) >> 4;
-        wi.a_g = (static_cast<uint32_t>(pl.taps_per_group) * pl.chunk_bytes) >> 4;
+        wi.a_ks = pl.a_ks_bytes >> 4;
+        wi.a_g = pl.a_g_bytes >> 4;
         if (pl.bq == 8) {
             wi.per_box = 1;
             wi.b_box = (2u * pl.box_bytes) >> 4;
@@ -743,13 +805,15 @@ __global__ void __launch_bounds__(kW2Threads, 1)
                 uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
                 // A (X) of K-step ks, group g starts at chunk lo + 2ks + g*tpg: ring position
                 const int stage_pos = cur_pos;  // ring position of chunk `lo`
-                const uint64_t ax0 = make_smem_desc(smem_u32(smem), static_cast<uint32_t>(pl.ph * pl.cp * 16), 128, kLayoutNone);
+                const uint64_t ax0 = make_smem_desc(smem_u32(smem), pl.a_lbo, pl.a_sbo, kLayoutNone);
                 const uint64_t by0 = make_smem_desc(smem_u32(sbase), b_lbo, b_sbo, pl.swz);
                 // One elected lane issues the whole stage. The ring mirror keeps every address of
                 // the stage wrap-free, so a full stage is a straight-line run of MMAs.
                 const long long ti = clock64();
                 if (elect_one()) {
-                    const uint64_t a_st = desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
+                    // xt: the stage's own window (rows from its first column); else the ring
+                    const uint64_t a_st = pl.xt ? make_smem_desc(smem_u32(sbase + pl.y_bytes), pl.a_lbo, pl.a_sbo, kLayoutNone)
+                                                : desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
                     const int k0 = kdone - seg_base;  // K-step within the segment (copy rotation, init)
                     switch (g_count) {
                         case 1: w2_issue_stage<1>(wi, tmem, a_st, by0, k0, nks, 1); break;
@@ -783,7 +847,9 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             p.prof[blockIdx.x * 8 + 6] = te_sum;
         }
     }
-    if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl.xin) {
+    if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl.xt) {
+        // xt: the producer's TMA boxes bring X; nothing to load here
+    } else if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl.xin) {
         // ---- X loaders, inline expanded rows: the natural columns of a stage's positions land in
         // one of two `raw` buffers (16-B cp.async pieces, issued one stage ahead), then the loaders
         // write the ring rows (position p = the 8 elements at column D*p), proxy fence, arrive
@@ -1154,7 +1220,7 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
     if (!encode) return cudaErrorNotSupported;
     const int64_t w_in = x_w > 0 ? x_w : q + d * (s - 1);
     CUtensorMap ymap;
-    if ((reinterpret_cast<uintptr_t>(x_bf16) & 15u) || (w_in % 8)) return cudaErrorInvalidValue;
+    if ((reinterpret_cast<uintptr_t>(x_bf16) & 15u) || (!pl.xt && w_in % 8)) return cudaErrorInvalidValue;
     {
         const cuuint64_t dims[3] = {static_cast<cuuint64_t>(q), static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n)};
         const cuuint64_t strides[2] = {static_cast<cuuint64_t>(q) * 2, static_cast<cuuint64_t>(k * q) * 2};
@@ -1169,6 +1235,22 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
+    CUtensorMap xmap = ymap;  // unused unless xt
+    if (pl.xt) {
+        // XT[n][o][u][8] as (element e of the stream, 256-element block j, stream n*octets + o): element
+        // (e, j, r) at r*rows*16 + j*512 + e*2 -- an overlapping view, so a box of 256 x nb x CP/8 is
+        // nb*256 consecutive elements of CP/8 consecutive streams (OOB past the stream: zeros)
+        const int64_t octets = (c + 7) / 8;
+        const cuuint64_t dims[3] = {static_cast<cuuint64_t>(w_in) * 8, static_cast<cuuint64_t>(ceil_div(w_in * 8, 256)),
+                                    static_cast<cuuint64_t>(n * octets)};
+        const cuuint64_t strides[2] = {512, static_cast<cuuint64_t>(w_in) * 16};
+        const cuuint32_t box[3] = {256, static_cast<cuuint32_t>(pl.xt_nb), static_cast<cuuint32_t>(pl.cp / 8)};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        if (encode(&xmap, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<uint16_t*>(x_bf16), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
     cudaError_t e = cudaFuncSetAttribute(tc_wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
     if (e != cudaSuccess) return e;
@@ -1178,7 +1260,8 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
     wp.k = k;
     wp.s = s;
     wp.q = q;
-    wp.w_in = w_in;
+    wp.w_in = w_in;  // xt: rows per octet stream
+    wp.dil = d;
     const W2Seg sg = w2_segments(pl, n, c, k, q);
     wp.steps_per_item = sg.steps_per_item;
     wp.total_steps = sg.total_steps;
@@ -1194,7 +1277,7 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * pl.grid);
         cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * pl.grid);
     }
-    e = launch_pdl(tc_wgrad2_kernel, dim3(pl.grid), dim3(kW2Threads), pl.smem_bytes, stream, ymap, wp);
+    e = launch_pdl(tc_wgrad2_kernel, dim3(pl.grid), dim3(kW2Threads), pl.smem_bytes, stream, ymap, xmap, wp);
     note_launch();
     if (e != cudaSuccess) return e;
     if (profile) {
@@ -1261,6 +1344,32 @@ cudaError_t launch_tc_wgrad_xin(const uint16_t* x_bf16, int64_t x_w, const uint1
     W2Plan p2;
     if (!make_w2plan(n, c, k, s, d, q, &p2, true)) return cudaErrorNotSupported;
     return launch_v2(x_bf16, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream, x_w);
+}
+
+bool tc_wgrad_xt_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    return make_w2plan_xt(n, c, k, s, d, q, &p2);
+}
+
+int64_t tc_wgrad_xt_pad_rows(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    if (!make_w2plan_xt(n, c, k, s, d, q, &p2)) return 0;
+    return 32 * static_cast<int64_t>(p2.xt_nb) + 16;
+}
+
+size_t tc_wgrad_xt_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {
+    W2Plan p2;
+    if (!make_w2plan_xt(n, c, k, s, d, q, &p2)) return 0;
+    const W2Seg sg = w2_segments(p2, n, c, k, q);
+    return sg.part_bytes + sg.nseg_bytes;
+}
+
+cudaError_t launch_tc_wgrad_xt(const uint16_t* xt, int64_t rows, const uint16_t* dy_bf16, float* dw_kcs,
+                               void* workspace, int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q,
+                               cudaStream_t stream) {
+    W2Plan p2;
+    if (!make_w2plan_xt(n, c, k, s, d, q, &p2)) return cudaErrorNotSupported;
+    return launch_v2(xt, dy_bf16, dw_kcs, workspace, n, c, k, s, d, q, p2, stream, rows);
 }
 
 bool tc_wgrad_v3_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q) {

@@ -248,6 +248,33 @@ def test_other_dilations_on_tensor_cores(d, bf16_storage, q):
         assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} q={q} {name}")
 
 
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 6, 12, 16, 40])
+@pytest.mark.parametrize("c,k,s,q", [(15, 15, 51, 1500), (40, 24, 9, 997), (128, 96, 25, 1024)])
+def test_octet_stream_backward_weight(d, c, k, s, q):
+    """Backward-weight on channel-octet streams (tc_wgrad.cu W2Plan::xt: X relaid as XT[n][C/8][w][8],
+    every tap shift a descriptor offset), at dilations the other tensor-core plans cannot take
+    (3, 5, 6, 12, 40) and those they can; several tap groups / roles, ragged and unaligned widths.
+    BF16 vs the oracle on rounded operands, and the FP32 split (bf16x3) on the same streams vs the
+    naive FP32 oracle."""
+    rng = oracle.Rng(5000 + 10 * d + c)
+    n = 2
+    w_in = q + d * (s - 1)
+    x, dy = rng.fill_uniform((n, c, w_in)), rng.fill_uniform((n, k, q))
+    w = rng.fill_uniform((k, c, s))
+    want16 = oracle.naive_backward_weight(oracle.round_bf16(dy), oracle.round_bf16(x), s, d)
+    p16 = cv.ConvParams(c, k, s, d, cv.Precision.Bf16)
+    if d != 4 or c > 32:  # (d = 4 at <= 32 channels keeps the expanded-row loaders)
+        assert cv.selected_algo(p16, n, w_in, 2, in_dtype=0, algo="tcgen05") == "tcgen05", (d, c)
+    got = cv.conv1d_backward_weight(_t(dy), _t(x), p16, algo="tcgen05")
+    torch.cuda.synchronize()
+    assert_close(got.cpu().numpy(), want16, BF16_TOL_ROUNDED, f"bf16 d={d} c={c}")
+    if 2 * c <= 128 and 2 * k <= 128 and q % 8 == 0:
+        p32 = cv.ConvParams(c, k, s, d, cv.Precision.Fp32)
+        got = cv.conv1d_backward_weight(_t(dy), _t(x), p32, algo="bf16x3")
+        torch.cuda.synchronize()
+        assert_close(got.cpu().numpy(), oracle.naive_backward_weight(dy, x, s, d), FP32_TOL, f"fp32 d={d} c={c}")
+
+
 @pytest.mark.parametrize("d", [1, 2, 4])
 @pytest.mark.parametrize("c,k,s", [(15, 15, 51), (64, 64, 51), (96, 128, 25)])
 def test_expanded_rows_long_filters(d, c, k, s):
