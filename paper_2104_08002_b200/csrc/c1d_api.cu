@@ -304,16 +304,17 @@ bool xt_wgrad_ok(const c1d_desc& d, int64_t q_pad) {
     static const bool at_d8 = getenv("C1D_XT_D8") != nullptr;
     // (d = 4 with <= 32 channels: the expanded-row loaders measured slightly faster, 31.5 vs 34.5 us
     // at C = 16, S = 3)
-    if (off || (d.d == 8 && !at_d8) || (d.d == 4 && d.c <= 32) || d.d > 64) return false;
-    // d = 8m also runs as chunk planes at dilation 8; the octet streams win there only while the T
-    // tap copies stacked on M (T = 128 / CP) reach little: measured (config-4 sweep, d = 16) T = 1
-    // or T*d*S <= 600 (C = 32, S = 9: 47 vs 60 us; C = 32, S = 25: 114 vs 69 us)
-    if (d.d % 8 == 0) {
-        int64_t cp = 16;
-        while (cp < d.c) cp *= 2;
-        const int64_t t = 128 / cp;
-        if (t > 1 && t * d.d * d.s > 600) return false;
-    }
+    if (off || (d.d == 4 && d.c <= 32) || d.d > 64) return false;
+    int64_t cp = 16;
+    while (cp < d.c) cp *= 2;
+    const int64_t t = 128 / cp;  // tap copies stacked on M
+    // d = 8: the native plan (P dY copies, N = 256) wins except at T = 1 with long filters
+    // (C = K = 128, N = 16, Q = 20000: S = 51 475 vs 560 us, S = 25 276 vs 307, S = 9 158 vs 150)
+    if (d.d == 8 && !at_d8 && (t > 1 || d.s < 16)) return false;
+    // d = 8m also runs as chunk planes at dilation 8; the octet streams win there only while the
+    // copies reach little: measured (config-4 sweep, d = 16) T = 1 or T*d*S <= 600 (C = 32, S = 9:
+    // 47 vs 60 us; C = 32, S = 25: 114 vs 69 us)
+    if (d.d % 8 == 0 && d.d != 8 && t > 1 && t * d.d * d.s > 600) return false;
     return d.n * ((d.c + 7) / 8) <= 65535 && tc_wgrad_xt_supported(d.n, d.c, d.k, d.s, d.d, q_pad);
 }
 // the FP32 split's backward-weight problem (2C channels x 2K filters, BF16) and whether it runs

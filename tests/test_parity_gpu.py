@@ -248,7 +248,7 @@ def test_other_dilations_on_tensor_cores(d, bf16_storage, q):
         assert_close(g, wv, BF16_TOL_ROUNDED, f"d={d} q={q} {name}")
 
 
-@pytest.mark.parametrize("d", [1, 2, 3, 5, 6, 12, 16, 40])
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 6, 8, 12, 16, 40])
 @pytest.mark.parametrize("c,k,s,q", [(15, 15, 51, 1500), (40, 24, 9, 997), (128, 96, 25, 1024)])
 def test_octet_stream_backward_weight(d, c, k, s, q):
     """Backward-weight on channel-octet streams (tc_wgrad.cu W2Plan::xt: X relaid as XT[n][C/8][w][8],
@@ -256,6 +256,8 @@ def test_octet_stream_backward_weight(d, c, k, s, q):
     (3, 5, 6, 12, 40) and those they can; several tap groups / roles, ragged and unaligned widths.
     BF16 vs the oracle on rounded operands, and the FP32 split (bf16x3) on the same streams vs the
     naive FP32 oracle."""
+    if d % 8 == 0 and c <= 64:
+        pytest.skip("d = 8m at T > 1 tap copies with long reach runs as chunk planes (xt_wgrad_ok)")
     rng = oracle.Rng(5000 + 10 * d + c)
     n = 2
     w_in = q + d * (s - 1)
