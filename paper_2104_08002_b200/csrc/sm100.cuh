@@ -88,6 +88,23 @@ __device__ __forceinline__ void mma_bf16_ss_alastuse(uint32_t d_tmem, uint64_t a
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
+// Weight-stationary MMA (tcgen05.mma.ws, M <= 128, N in {64, 128, 256}): B is latched in collector
+// buffer b0 by ::fill and re-used by ::use / ::lastuse without another shared-memory read (their B
+// descriptor is ignored). tools/probe_ws.cu: same D as the regular MMA; N = 64 with the forward's
+// overlapped MN-major A runs at 40 cycles per MMA instead of 48 (the B re-read is gone).
+#define C1D_WS_MMA(NAME, COLL)                                                                              \
+    __device__ __forceinline__ void NAME(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,   \
+                                         uint32_t accumulate) {                                             \
+        asm volatile(                                                                                       \
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"                                              \
+            "tcgen05.mma.ws.cta_group::1.kind::f16" COLL " [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),          \
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));                                           \
+    }
+C1D_WS_MMA(mma_ws_fill, ".collector::b0::fill")
+C1D_WS_MMA(mma_ws_use, ".collector::b0::use")
+C1D_WS_MMA(mma_ws_lastuse, ".collector::b0::lastuse")
+#undef C1D_WS_MMA
+
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile(

@@ -43,6 +43,7 @@ namespace {
 using namespace sm100;
 
 __host__ __device__ __forceinline__ int64_t imin64(int64_t a, int64_t b) { return a < b ? a : b; }
+__host__ __device__ __forceinline__ int64_t imax64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 constexpr int kTileQ = 128;      // output columns per tile (MMA M)
 constexpr int kSegQ = 256;       // TMA box width in elements
@@ -100,6 +101,9 @@ struct Plan {
     // single-row boxes (each TMA box costs the producer ~100 cycles); only for windows inside
     // [0, in_w), since the view's bounds are checked per dimension (edge windows keep the 2-D boxes)
     int xbox3;
+    // Weight-stationary main MMAs (tcgen05.mma.ws, B latched in the collector across a channel's
+    // tiles): only where the main MMA is N = 64 (KP = 16 narrow layers; sm100.cuh mma_ws_*)
+    int ws;
 };
 
 constexpr uint32_t kWresMax = 64 * 1024;
@@ -254,6 +258,7 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     p.tx_stage_bytes = p.tail ? ((static_cast<uint32_t>(p.tail_chunks * p.cc * 16) + 1023) & ~1023u) : 0;
     p.tw_stage_bytes = p.tail ? static_cast<uint32_t>(p.kp * kTapsPerBlock * 2) : 0;
     plan_wres(g, &p, allow_wres);
+    p.ws = (p.tail ? p.g - 1 : p.g) * p.kp == 64 && getenv("C1D_NO_WS") == nullptr ? 1 : 0;
     const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.tx_stage_bytes + p.tw_stage_bytes;
     p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve - p.wres_bytes) / stage));
     if (p.stages < 2) return p.wres_bytes ? make_plan(g, pl, main_ch, reserve, false) : false;
@@ -659,6 +664,43 @@ __device__ __forceinline__ void expand_rows_d(uint32_t rc, uint32_t xc, int rows
     }
 }
 
+// The main MMAs of a stage: for each channel, its NT consecutive input tiles as one straight-line
+// run. Tile t reads A at +256 B per tile and accumulates at column dcol + t*KP; every descriptor and
+// column is an independent add from the channel base (a dependent uniform-register chain between
+// MMAs throttled the issuing thread to ~70 cycles per MMA). With ws, the channel's B block is
+// latched in the collector by its first MMA and re-used by the others (tcgen05.mma.ws).
+struct IssueArgs {
+    uint32_t dcol, kp, acc2;
+    uint64_t adesc, bdesc;
+    uint32_t idesc, a_chan_bytes, b_chan_bytes;
+    int ccn, c_split;  // channels of the stage; channels >= c_split accumulate at +acc2
+    int ws;
+};
+template <int NT>
+__device__ __forceinline__ void issue_channels(const IssueArgs& ia) {
+    uint64_t adesc = ia.adesc, bdesc = ia.bdesc;
+    for (int c = 0; c < ia.ccn; ++c) {
+        const uint32_t dcol = ia.dcol + (c >= ia.c_split ? ia.acc2 : 0u);
+        if (ia.ws && NT >= 2) {
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const uint64_t a = adesc + static_cast<uint64_t>(t * (kTileQ * 2 / 16));
+                const uint32_t d = dcol + static_cast<uint32_t>(t) * ia.kp;
+                if (t == 0) mma_ws_fill(d, a, bdesc, ia.idesc, 1);
+                else if (t == NT - 1) mma_ws_lastuse(d, a, bdesc, ia.idesc, 1);
+                else mma_ws_use(d, a, bdesc, ia.idesc, 1);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < NT; ++t)
+                mma_bf16_ss(dcol + static_cast<uint32_t>(t) * ia.kp, adesc + static_cast<uint64_t>(t * (kTileQ * 2 / 16)),
+                            bdesc, ia.idesc, 1);
+        }
+        adesc = desc_advance(adesc, ia.a_chan_bytes);
+        bdesc = desc_advance(bdesc, ia.b_chan_bytes);
+    }
+}
+
 // kMode: 0 plain FP32 store, 1 forward glue, 2 backward glue (p.glue.mode); kKPB (modes 1-2): 16-channel
 // blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
 // mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
@@ -916,6 +958,28 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                     const int tsplit = need_carry ? (su.tcur < G - 1 ? su.tcur : G - 1) : 0;
                     // main MMAs of input tiles [t0, t1) for every channel of the stage
                     auto issue_tiles = [&](int t0, int t1) {
+                        if constexpr (kKPB == 1) {
+                            // KP = 16 (own instantiation): straight-line runs per channel, B latched in
+                            // the collector (ws); the wider plans keep the loop below, which keeps
+                            // their kernels' code small (straight-line runs there cost config 3 ~4%)
+                            const uint64_t a_t0 = desc_advance(a0, static_cast<uint32_t>(t0 * kTileQ * 2));
+                            const uint32_t dchan = rtmem + main_slot + static_cast<uint32_t>(t0 * KP);
+                            const int c_split = static_cast<int>(imin64(ccn, imax64(0, p.main_ch - c0)));
+                            const IssueArgs ia{dchan, static_cast<uint32_t>(KP), pl.acc2, a_t0, b0, idesc,
+                                               static_cast<uint32_t>(pl.xw * 2), pl.b_chan_bytes, ccn, c_split, pl.ws};
+                            switch (t1 - t0) {
+                                case 1: issue_channels<1>(ia); break;
+                                case 2: issue_channels<2>(ia); break;
+                                case 3: issue_channels<3>(ia); break;
+                                case 4: issue_channels<4>(ia); break;
+                                case 5: issue_channels<5>(ia); break;
+                                case 6: issue_channels<6>(ia); break;
+                                case 7: issue_channels<7>(ia); break;
+                                case 8: issue_channels<8>(ia); break;
+                                default: break;
+                            }
+                            return;
+                        }
                         uint64_t bdesc = b0;
                         uint64_t achan = desc_advance(a0, static_cast<uint32_t>(t0 * kTileQ * 2));
                         for (int c = 0; c < ccn; ++c) {
@@ -1485,7 +1549,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
-    auto kernel = tc_conv_kernel<0, 0, 1>;
+    // KP = 16 plans get their own instantiation (kKPB = 1) with the straight-line narrow issue
+    auto kernel = pl.kp == 16 ? tc_conv_kernel<0, 1, 1> : tc_conv_kernel<0, 0, 1>;
     if (mode == 1)
         kernel = pl.kp == 16 ? (eg == 2 ? tc_conv_kernel<1, 1, 2> : tc_conv_kernel<1, 1, 1>)
                : (pl.kp == 32 ? (eg == 2 ? tc_conv_kernel<1, 2, 2> : tc_conv_kernel<1, 2, 1>) : tc_conv_kernel<1, 4, 1>);
