@@ -51,6 +51,27 @@ __device__ __forceinline__ float load_as_float<uint16_t>(const uint16_t* p, int6
     return bf16_bits_to_fp32(__ldg(p + i));
 }
 
+// Four consecutive elements p[i .. i+3] as floats with one vector load (i must be a multiple of 4
+// and p 16-B (float) / 8-B (bf16) aligned): the 1-tap kernels' HBM-bound streams.
+template <typename T>
+__device__ __forceinline__ void load4_as_float(const T* p, int64_t i, bool round, float (&v)[4]);
+template <>
+__device__ __forceinline__ void load4_as_float<float>(const float* p, int64_t i, bool round, float (&v)[4]) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p + i));
+    v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+    if (round)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = round_to_bf16(v[j]);
+}
+template <>
+__device__ __forceinline__ void load4_as_float<uint16_t>(const uint16_t* p, int64_t i, bool, float (&v)[4]) {
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p + i));
+    v[0] = bf16_bits_to_fp32(static_cast<uint16_t>(t.x & 0xffffu));
+    v[1] = bf16_bits_to_fp32(static_cast<uint16_t>(t.x >> 16));
+    v[2] = bf16_bits_to_fp32(static_cast<uint16_t>(t.y & 0xffffu));
+    v[3] = bf16_bits_to_fp32(static_cast<uint16_t>(t.y >> 16));
+}
+
 __host__ __device__ constexpr int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // ---- programmatic dependent launch (PDL) ------------------------------------------------------

@@ -388,7 +388,7 @@ template <typename TIn, int OMAX>
 __global__ void __launch_bounds__(kPwThreads) pointwise_conv_kernel(const TIn* __restrict__ in,
                                                                     const float* __restrict__ wg,
                                                                     float* __restrict__ out, ConvGeom g,
-                                                                    int round_in) {
+                                                                    int round_in, int vec) {
     const int64_t n = blockIdx.y;
     const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kPwCols + threadIdx.x * 4;
     if (x0 >= g.out_w) return;
@@ -402,8 +402,12 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_conv_kernel(const TIn* _
     for (int64_t i = 0; i < g.in_ch; ++i) {
         const int64_t base = (n * g.in_ch + i) * g.in_w + x0 + g.in_off;
         float v[4];
+        if (vec && cnt == 4) {
+            load4_as_float(in, base, round_in != 0, v);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = j < cnt ? load_as_float(in, base + j, round_in != 0) : 0.0f;
+            for (int j = 0; j < 4; ++j) v[j] = j < cnt ? load_as_float(in, base + j, round_in != 0) : 0.0f;
+        }
 #pragma unroll
         for (int o = 0; o < OMAX; ++o) {
             const float w = o < O ? __ldg(wg + static_cast<int64_t>(o) * g.in_ch + i) : 0.0f;
@@ -415,9 +419,13 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_conv_kernel(const TIn* _
     for (int o = 0; o < OMAX; ++o) {
         if (o >= O) continue;
         float* dst = out + (n * g.out_ch + o) * g.out_w + x0;
+        if (vec && cnt == 4) {
+            *reinterpret_cast<float4*>(dst) = make_float4(acc[o][0], acc[o][1], acc[o][2], acc[o][3]);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            if (j < cnt) dst[j] = acc[o][j];
+            for (int j = 0; j < 4; ++j)
+                if (j < cnt) dst[j] = acc[o][j];
+        }
     }
 }
 
@@ -425,16 +433,20 @@ template <typename TIn>
 static cudaError_t launch_pointwise(const TIn* in, const float* wg, float* out, const ConvGeom& g, int round_in,
                                     cudaStream_t stream) {
     const dim3 grid(static_cast<unsigned>(ceil_div(g.out_w, kPwCols)), static_cast<unsigned>(g.n));
+    // vector loads / stores: every row start 16-B (float) / 8-B (bf16) aligned
+    const uintptr_t al = sizeof(TIn) == 4 ? 15u : 7u;
+    const int vec = g.in_w % 4 == 0 && g.in_off % 4 == 0 && g.out_w % 4 == 0 && (reinterpret_cast<uintptr_t>(in) & al) == 0 &&
+                    (reinterpret_cast<uintptr_t>(out) & 15u) == 0;
     if (g.out_ch <= 1)
-        pointwise_conv_kernel<TIn, 1><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+        pointwise_conv_kernel<TIn, 1><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in, vec);
     else if (g.out_ch <= 2)
-        pointwise_conv_kernel<TIn, 2><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+        pointwise_conv_kernel<TIn, 2><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in, vec);
     else if (g.out_ch <= 4)
-        pointwise_conv_kernel<TIn, 4><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+        pointwise_conv_kernel<TIn, 4><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in, vec);
     else if (g.out_ch <= 8)
-        pointwise_conv_kernel<TIn, 8><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+        pointwise_conv_kernel<TIn, 8><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in, vec);
     else
-        pointwise_conv_kernel<TIn, 16><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in);
+        pointwise_conv_kernel<TIn, 16><<<grid, kPwThreads, 0, stream>>>(in, wg, out, g, round_in, vec);
     note_launch();
     return cudaGetLastError();
 }
@@ -919,7 +931,7 @@ template <typename TIn, int KMAX, int CMAX>
 __global__ void __launch_bounds__(kPwThreads) pointwise_wgrad_kernel(const TIn* __restrict__ x,
                                                                      const TIn* __restrict__ dy,
                                                                      float* __restrict__ part, int64_t C, int64_t K,
-                                                                     int64_t Q, int round_in) {
+                                                                     int64_t Q, int round_in, int vec) {
     __shared__ float red[kPwThreads / 32][KMAX * CMAX];
     const int64_t n = blockIdx.y;
     const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kPwCols + threadIdx.x * 4;
@@ -935,12 +947,17 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_wgrad_kernel(const TIn* 
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             gv[kk][j] = (kk < K && j < cnt) ? load_as_float(dy, (n * K + kk) * Q + x0 + j, round_in != 0) : 0.0f;
+    const bool v4 = vec && cnt == 4;
 #pragma unroll
     for (int cc = 0; cc < CMAX; ++cc) {
         if (cc >= C) break;
         float xv[4];
+        if (v4) {
+            load4_as_float(x, (n * C + cc) * Q + x0, round_in != 0, xv);
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) xv[j] = j < cnt ? load_as_float(x, (n * C + cc) * Q + x0 + j, round_in != 0) : 0.0f;
+            for (int j = 0; j < 4; ++j) xv[j] = j < cnt ? load_as_float(x, (n * C + cc) * Q + x0 + j, round_in != 0) : 0.0f;
+        }
 #pragma unroll
         for (int kk = 0; kk < KMAX; ++kk)
 #pragma unroll
@@ -995,12 +1012,14 @@ template <typename TIn>
 static cudaError_t launch_pointwise_wgrad(const TIn* x, const TIn* dy, float* dw, float* part, int64_t n, int64_t c,
                                           int64_t k, int64_t q, int round_in, cudaStream_t stream) {
     const dim3 grid(static_cast<unsigned>(ceil_div(q, kPwCols)), static_cast<unsigned>(n));
+    const uintptr_t al = sizeof(TIn) == 4 ? 15u : 7u;
+    const int vec = q % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & al) == 0;  // vector loads of x rows
     if (k <= 2 && c <= 16)
-        pointwise_wgrad_kernel<TIn, 2, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in);
+        pointwise_wgrad_kernel<TIn, 2, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in, vec);
     else if (c <= 16)
-        pointwise_wgrad_kernel<TIn, 4, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in);
+        pointwise_wgrad_kernel<TIn, 4, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in, vec);
     else
-        pointwise_wgrad_kernel<TIn, 4, 64><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in);
+        pointwise_wgrad_kernel<TIn, 4, 64><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in, vec);
     note_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

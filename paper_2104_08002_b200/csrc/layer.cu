@@ -48,9 +48,11 @@ __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __rest
                                                                   uint16_t* __restrict__ act_bf16, int64_t pad,
                                                                   uint32_t* __restrict__ mask, bool vec) {
     const int64_t row = blockIdx.y;
+    const int k32 = static_cast<int>(k), row32 = static_cast<int>(blockIdx.y);  // 32-bit (n*k <= 65535)
+    const int item = row32 / k32, ch = row32 - item * k32;
     const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
     const bool live = x0 < q;
-    const float b = bias ? bias[row % k] : 0.0f;
+    const float b = bias ? bias[ch] : 0.0f;
     float* pr = pre + row * q + x0;
     const int cnt = live ? static_cast<int>(q - x0 < kEltPerThread ? q - x0 : kEltPerThread) : 0;
     const bool v4 = vec && cnt == kEltPerThread;
@@ -77,9 +79,8 @@ __global__ void __launch_bounds__(kEltThreads) fwd_epilogue_kernel(float* __rest
     }
     if (!live) return;
     if (mask) {  // channel-block words (kernels.h): OR this row's bit into the 4 columns' words
-        const int64_t n = row / k, c = row % k;
-        uint32_t* wd = mask + (n * ((k + 15) / 16) + c / 16) * q + x0;
-        const uint32_t bit = 1u << (c % 16);
+        uint32_t* wd = mask + static_cast<int64_t>(item * ((k32 + 15) / 16) + ch / 16) * q + x0;
+        const uint32_t bit = 1u << (ch % 16);
         for (int j = 0; j < cnt; ++j)
             if (v[j] > 0.0f) atomicOr(wd + j, bit);
     }
@@ -111,6 +112,10 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
     const float* __restrict__ pw_w, int pw_k) {
     __shared__ float red[kEltThreads / 32];
     const int64_t row = blockIdx.y;
+    // (item, channel) of the row in 32-bit math (the launcher bounds n*k by 65535): 64-bit divisions
+    // per thread made this pass issue-bound (the heads' 1-tap backward: 298 us)
+    const int k32 = static_cast<int>(k), row32 = static_cast<int>(blockIdx.y);
+    const int item = row32 / k32, ch = row32 - item * k32;
     const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
     float gp[4] = {0.f, 0.f, 0.f, 0.f};
     if (x0 < q) {
@@ -121,12 +126,11 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
         if (pw_dy) {
             // gin = the 1-tap backward-data of pw_k filters computed here (the FP32 pointwise
             // conv's order: fmaf over the filters from 0), instead of read from a scratch tensor
-            const int64_t item = row / k, ch = row % k;
 #pragma unroll
             for (int j = 0; j < 4; ++j) g[j] = 0.0f;
             for (int f = 0; f < pw_k; ++f) {
                 const float wv = __ldg(pw_w + f * k + ch);
-                const float* src = pw_dy + (item * pw_k + f) * q + x0;
+                const float* src = pw_dy + static_cast<int64_t>(item * pw_k + f) * q + x0;
                 float dv[4];
                 if (v4) {  // q % 4 == 0 and 16-B aligned rows (launcher's vec flag)
                     const float4 t = __ldg(reinterpret_cast<const float4*>(src));
@@ -171,10 +175,10 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
                 if (relu && !mask && j < cnt) pr[j] = pre[row * q + x0 + j];
             }
         }
-        const float pb = (relu && pre_bias) ? pre_bias[row % k] : 0.0f;  // mask of pre + bias
+        const float pb = (relu && pre_bias) ? pre_bias[ch] : 0.0f;  // mask of pre + bias
         // or the forward's mask words: bit c % 16 of word (n, c / 16, x)
-        const uint32_t* mwd = mask ? mask + ((row / k) * ((k + 15) / 16) + (row % k) / 16) * q + x0 : nullptr;
-        const uint32_t mbit = 1u << ((row % k) % 16);
+        const uint32_t* mwd = mask ? mask + static_cast<int64_t>(item * ((k32 + 15) / 16) + ch / 16) * q + x0 : nullptr;
+        const uint32_t mbit = 1u << (ch % 16);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             g[j] += ad[j];
@@ -208,6 +212,88 @@ __global__ void __launch_bounds__(kEltThreads) bwd_prologue_kernel(
     }
 }
 
+// The 1-tap glued backward-data of a few-filter layer (the network's heads) for all k <= KMAX
+// channels of an item at once: block (bx, n) owns 1024 columns of item n, each thread 4 columns. The
+// PWK filter rows of dy and the channel-block mask word are loaded once per column instead of once
+// per channel row (bwd_prologue_kernel's one-row-per-block layout re-read them k times and spent its
+// time on per-row index math: 256 us at batch 64 against ~55 us of HBM writes). Same arithmetic in
+// the same order as bwd_prologue_kernel (fmaf over the filters from 0, + gadd, mask; the bias
+// partial of a (row, block) is the same fixed tree), so the outputs are bit-identical.
+// With pw_dy == nullptr the incoming gradient is read from gin (row pitch gin_w, offset gin_off)
+// instead: the same per-item layout for any k <= KMAX (e.g. the heads' own bias gradient).
+template <int KMAX, int PWK>
+__global__ void __launch_bounds__(kEltThreads) pw_bwd_prologue_kernel(
+    const float* __restrict__ gin, int64_t gin_w, int64_t gin_off,
+    const float* __restrict__ pw_dy, const float* __restrict__ pw_w, int pw_k, const float* __restrict__ gadd,
+    const uint32_t* __restrict__ mask, int k, int64_t q, float* __restrict__ gsum, float* __restrict__ grad_pre,
+    uint16_t* __restrict__ grad_pre_bf16, float* __restrict__ part) {
+    __shared__ float red[kEltThreads / 32][KMAX];
+    const int n = blockIdx.y;
+    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kEltPerBlock + threadIdx.x * kEltPerThread;
+    const bool live = x0 < q;  // q % 4 == 0: a live thread owns 4 valid columns
+    float dv[PWK][4];
+#pragma unroll
+    for (int f = 0; f < PWK; ++f) {
+        float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (pw_dy && live && f < pw_k) t = __ldg(reinterpret_cast<const float4*>(pw_dy + (static_cast<int64_t>(n) * pw_k + f) * q + x0));
+        dv[f][0] = t.x, dv[f][1] = t.y, dv[f][2] = t.z, dv[f][3] = t.w;
+    }
+    uint4 mw = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
+    if (mask && live) mw = __ldg(reinterpret_cast<const uint4*>(mask + static_cast<int64_t>(n) * q + x0));  // k <= 16: one word
+    const uint32_t mws[4] = {mw.x, mw.y, mw.z, mw.w};
+    float bs[KMAX];
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c) {
+        bs[c] = 0.0f;
+        if (c >= k) continue;
+        const int64_t row = static_cast<int64_t>(n) * k + c;
+        float g[4] = {0.f, 0.f, 0.f, 0.f}, ad[4] = {0.f, 0.f, 0.f, 0.f}, gp[4];
+        if (pw_dy) {
+#pragma unroll
+            for (int f = 0; f < PWK; ++f) {
+                if (f >= pw_k) break;
+                const float wv = __ldg(pw_w + f * k + c);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) g[j] = fmaf(wv, dv[f][j], g[j]);
+            }
+        }
+        if (!live) continue;
+        if (!pw_dy) {
+            const float4 t = __ldg(reinterpret_cast<const float4*>(gin + row * gin_w + gin_off + x0));
+            g[0] = t.x, g[1] = t.y, g[2] = t.z, g[3] = t.w;
+        }
+        if (gadd) {
+            const float4 t = *reinterpret_cast<const float4*>(gadd + row * q + x0);
+            ad[0] = t.x, ad[1] = t.y, ad[2] = t.z, ad[3] = t.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            g[j] += ad[j];
+            gp[j] = (mask && (mws[j] & (1u << c)) == 0) ? 0.0f : g[j];
+        }
+        if (gsum) *reinterpret_cast<float4*>(gsum + row * q + x0) = make_float4(g[0], g[1], g[2], g[3]);
+        if (grad_pre) *reinterpret_cast<float4*>(grad_pre + row * q + x0) = make_float4(gp[0], gp[1], gp[2], gp[3]);
+        if (grad_pre_bf16) store_bf16x4(grad_pre_bf16 + row * q + x0, gp, true);
+        bs[c] = ((gp[0] + gp[1]) + (gp[2] + gp[3]));
+    }
+    if (!part) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c) {
+        if (c >= k) break;
+        float t = bs[c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) red[warp][c] = t;
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {
+        float t = 0.0f;
+        for (int w = 0; w < kEltThreads / 32; ++w) t += red[w][threadIdx.x];
+        part[(static_cast<int64_t>(n) * k + threadIdx.x) * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 // bias_grad[c] = sum of part[(item*k + c) * nbx + bx] over items and blocks; one CTA per channel,
 // thread t sums the entries t, t+256, ... (items outer, blocks inner) in order, then a fixed tree.
 __global__ void __launch_bounds__(kEltThreads) bias_grad_reduce_kernel(const float* __restrict__ part,
@@ -217,9 +303,15 @@ __global__ void __launch_bounds__(kEltThreads) bias_grad_reduce_kernel(const flo
     const int64_t c = blockIdx.x;
     const int64_t total = n * nbx;
     float t = 0.0f;
+    // entries e = threadIdx.x, +256, ... in order; (i, b) = (e / nbx, e % nbx) advanced without divisions
+    int64_t i = threadIdx.x / nbx, b = threadIdx.x - (threadIdx.x / nbx) * nbx;
     for (int64_t e = threadIdx.x; e < total; e += kEltThreads) {
-        const int64_t i = e / nbx, b = e % nbx;
         t += part[(i * k + c) * nbx + b];
+        b += kEltThreads;
+        while (b >= nbx) {
+            b -= nbx;
+            ++i;
+        }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
@@ -268,6 +360,25 @@ cudaError_t launch_layer_bwd_prologue(const float* gin, int64_t gin_w, int64_t g
                      (!grad_pre || aligned16(grad_pre)) &&
                      (!grad_pre_bf16 || (reinterpret_cast<uintptr_t>(grad_pre_bf16) & 7u) == 0);
     const int64_t nbx = layer_bias_blocks(q);
+    // few channels per item (the heads): one block row per item, all channels per thread
+    if (vec && k <= 16 && (!pw_dy || pw_k <= 2) && (relu == 0 || mask != nullptr) && (pw_dy || gin) &&
+        (!mask || (reinterpret_cast<uintptr_t>(mask) & 15u) == 0) && n <= 65535) {
+        const dim3 g2(static_cast<unsigned>(nbx), static_cast<unsigned>(n));
+        const uint32_t* m = relu ? mask : nullptr;
+        float* pt = bias_grad ? part : nullptr;
+        if (pw_dy && pw_k == 2)
+            pw_bwd_prologue_kernel<16, 2><<<g2, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, pw_dy, pw_w, pw_k, gadd, m,
+                                                                          static_cast<int>(k), q, gsum, grad_pre,
+                                                                          grad_pre_bf16, pt);
+        else
+            pw_bwd_prologue_kernel<16, 1><<<g2, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, pw_dy, pw_w, pw_k, gadd, m,
+                                                                          static_cast<int>(k), q, gsum, grad_pre,
+                                                                          grad_pre_bf16, pt);
+        note_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess || !bias_grad) return e;
+        return launch_bias_grad_reduce(part, bias_grad, n, k, nbx, stream);
+    }
     const dim3 grid(static_cast<unsigned>(nbx), static_cast<unsigned>(n * k));
     bwd_prologue_kernel<<<grid, kEltThreads, 0, stream>>>(gin, gin_w, gin_off, gadd, pre, pre_bias, mask, k, q, relu, gsum,
                                                           grad_pre, grad_pre_bf16, bias_grad ? part : nullptr, vec,
