@@ -873,7 +873,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         // ------------------------------------------------------------------ MMA issuer
         // The whole warp walks the schedule (warp-uniform control flow keeps descriptors in
         // uniform registers); one elected lane issues each tcgen05 instruction.
-        long long t_full = 0, t_tmem = 0, t_full_first = -1, n_super = 0;
+        long long t_full = 0, t_tmem = 0, t_full_first = -1, n_super = 0, t_issue = 0;
         const long long t_begin = clock64();
         Cursor cur = make_cursor(p);
         int stage = 0;
@@ -995,8 +995,10 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                             achan = desc_advance(achan, static_cast<uint32_t>(pl.xw * 2));
                         }
                     };
+                    const long long ti0 = clock64();
                     if (elect_one()) issue_tiles(tsplit, su.tcur);
                     __syncwarp();
+                    t_issue += clock64() - ti0;
                     if (need_carry) {
                         const long long tc0 = clock64();
                         mbar_wait(smem_u32(&carry_full), cphase);
@@ -1004,8 +1006,10 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                         t_tmem += clock64() - tc0;
                         tc_fence_after();
                         need_carry = false;
+                        const long long ti1 = clock64();
                         if (elect_one()) issue_tiles(0, tsplit);
                         __syncwarp();
+                        t_issue += clock64() - ti1;
                     }
                     if (pl.tail && elect_one()) {
                         // A[m][k = r*cc + c] = x[c][q0 + m + 8r] (tap 16(G-1) + r): MN-major, K rows
@@ -1042,6 +1046,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             p.prof[blockIdx.x * kProfSlots + 4] = clock64() - t_begin;
             p.prof[blockIdx.x * kProfSlots + 12] = t_full_first;
             p.prof[blockIdx.x * kProfSlots + 13] = n_super;
+            p.prof[blockIdx.x * kProfSlots + 14] = t_issue;
         }
     } else if (warp == 2 || warp == 3) {
         // ------------------------------------------------------------------ E-row expanders
@@ -1613,7 +1618,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         cudaMemcpy(h.data(), kp.prof, h.size() * 8, cudaMemcpyDeviceToHost);
         double a[8] = {0}, mma_max = 0;
         unsigned long long t0 = ~0ull, t1 = 0, t1_min = ~0ull;
-        double mhz = 0, cta_us = 0, first = 0, nsup = 0;
+        double mhz = 0, cta_us = 0, first = 0, nsup = 0, issue = 0;
         for (int b = 0; b < grid; ++b) {
             for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[b * kProfSlots + i]) / grid;
             mma_max = std::max(mma_max, static_cast<double>(h[b * kProfSlots + 4]));
@@ -1625,9 +1630,10 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
             cta_us += dt * 1e-3 / grid;
             first += static_cast<double>(h[b * kProfSlots + 12]) / grid;
             nsup += static_cast<double>(h[b * kProfSlots + 13]) / grid;
+            issue += static_cast<double>(h[b * kProfSlots + 14]) / grid;
         }
-        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f (max %.0f) | epilogue store %.0f carry %.0f zero %.0f (cycles, CTA avg) | span %.1f us, first CTA done %.1f us, CTA avg %.1f us at %.0f MHz | mma waits in super-tile 1: %.0f, super-tiles %.1f\n",
-                a[0], a[1], a[2], a[3], a[4], mma_max, a[5], a[6], a[7], (t1 - t0) * 1e-3, (t1_min - t0) * 1e-3, cta_us, mhz, first, nsup);
+        fprintf(stderr, "[tc_conv prof] producer wait_empty %.0f / total %.0f | mma wait_full %.0f wait_slot %.0f total %.0f (max %.0f) | epilogue store %.0f carry %.0f zero %.0f (cycles, CTA avg) | span %.1f us, first CTA done %.1f us, CTA avg %.1f us at %.0f MHz | mma waits in super-tile 1: %.0f, super-tiles %.1f, issue %.0f\n",
+                a[0], a[1], a[2], a[3], a[4], mma_max, a[5], a[6], a[7], (t1 - t0) * 1e-3, (t1_min - t0) * 1e-3, cta_us, mhz, first, nsup, issue);
         cudaFree(kp.prof);
     }
     return cudaSuccess;

@@ -194,6 +194,120 @@ __global__ void __launch_bounds__(256, 1) ws_rate(int ksteps, long long* cyc, in
     if (threadIdx.x / 32 == 0) tmem_dealloc<512>(tmem_s);
 }
 
+// The forward kernel's narrow-layer MMA pattern (config 2): per super-tile, for each of 15
+// channels a run over tiles 3..7, then for each channel a run over tiles 0..2; A of (channel c,
+// tile t) at c*2560 + t*256 B, B of channel c at 64 KB + c*2048 B, D at region + 16*t (N = 64),
+// region alternating 0 / 256. WS: 1 = ws fill/use/lastuse runs, 0 = regular MMAs.
+template <int WS>
+__global__ void __launch_bounds__(256, 1) kpattern(int supers, long long* cyc, const uint8_t* gsrc, int bg_bytes) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_s;
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    for (int i = threadIdx.x; i < 96 * 1024 / 16; i += blockDim.x) reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x / 32 == 0) tmem_alloc<512>(&tmem_s);
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        fence_mbar_init();
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    __shared__ int done_k;
+    __shared__ uint64_t bgbar;
+    if (threadIdx.x == 0) {
+        done_k = 0;
+        mbar_init(&bgbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 32 && bg_bytes > 0) {
+        // background bulk copies (like the producer's TMA loads): bg_bytes per ~1000 cycles into
+        // [120 KB, 150 KB)
+        uint32_t ph = 0;
+        long long t_next = clock64();
+        int i = 0;
+        while (!*reinterpret_cast<volatile int*>(&done_k)) {
+            while (clock64() < t_next) {}
+            t_next += 1000;
+            mbar_arrive_expect_tx(smem_u32(&bgbar), static_cast<uint32_t>(bg_bytes));
+            bulk_g2s(smem_u32(smem + 120 * 1024), gsrc + (static_cast<size_t>(blockIdx.x * 64 + (i++ & 63)) << 15),
+                     static_cast<uint32_t>(bg_bytes), smem_u32(&bgbar));
+            mbar_wait(smem_u32(&bgbar), ph);
+            ph ^= 1;
+        }
+    }
+    if (threadIdx.x / 32 == 0 && elect_one()) {
+        const uint32_t tb = tmem_s;
+        const uint64_t a0 = make_smem_desc(smem_u32(smem), 128, 16, kLayoutNone);
+        const uint64_t b0 = make_smem_desc(smem_u32(smem + 64 * 1024), 128, 256, kLayoutNone);
+        const uint32_t idesc = make_idesc(128, 64, kFmtBF16, 1, 0);
+        const long long t0 = clock64();
+        for (int sidx = 0; sidx < supers; ++sidx) {
+            const uint32_t region = (sidx & 1) ? 256u : 0u;
+            for (int part = 0; part < 2; ++part) {
+                const int t0r = part == 0 ? 3 : 0;
+                for (int c = 0; c < 15; ++c) {
+                    const uint64_t ac = a0 + static_cast<uint64_t>((c * 2560 + t0r * 256) >> 4);
+                    const uint64_t bc = b0 + static_cast<uint64_t>((c * 2048) >> 4);
+                    const uint32_t dc = tb + region + 16u * t0r;
+                    if (part == 0) {
+#pragma unroll
+                        for (int t = 0; t < 5; ++t) {
+                            const uint64_t a = ac + static_cast<uint64_t>(t * 16);
+                            const uint32_t d = dc + 16u * t;
+                            if (!WS) mma_bf16_ss(d, a, bc, idesc, 1);
+                            else if (t == 0) ws_fill(d, a, bc, idesc, 1);
+                            else if (t == 4) ws_lastuse(d, a, bc, idesc, 1);
+                            else ws_use(d, a, bc, idesc, 1);
+                        }
+                    } else {
+#pragma unroll
+                        for (int t = 0; t < 3; ++t) {
+                            const uint64_t a = ac + static_cast<uint64_t>(t * 16);
+                            const uint32_t d = dc + 16u * t;
+                            if (!WS) mma_bf16_ss(d, a, bc, idesc, 1);
+                            else if (t == 0) ws_fill(d, a, bc, idesc, 1);
+                            else if (t == 2) ws_lastuse(d, a, bc, idesc, 1);
+                            else ws_use(d, a, bc, idesc, 1);
+                        }
+                    }
+                }
+            }
+        }
+        mma_commit(smem_u32(&bar));
+        mbar_wait(smem_u32(&bar), 0);
+        cyc[blockIdx.x] = clock64() - t0;
+        *reinterpret_cast<volatile int*>(&done_k) = 1;
+    }
+    __syncwarp();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (threadIdx.x / 32 == 0) tmem_dealloc<512>(tmem_s);
+}
+
+template <int WS>
+void run_kpattern(const char* name, long long* cyc, int bg_bytes = 0) {
+    static uint8_t* gsrc = nullptr;
+    if (!gsrc) {
+        CK(cudaMalloc(&gsrc, size_t(148) * 64 * 32768 + 65536));
+        CK(cudaMemset(gsrc, 0, size_t(148) * 64 * 32768 + 65536));
+    }
+    const int supers = 64;
+    CK(cudaFuncSetAttribute(kpattern<WS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+    for (int rep = 0; rep < 2; ++rep) {
+        kpattern<WS><<<148, 256, 160 * 1024>>>(supers, cyc, gsrc, bg_bytes);
+        CK(cudaDeviceSynchronize());
+    }
+    long long h[148];
+    CK(cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost));
+    long long mx = 0;
+    for (long long v : h) mx = v > mx ? v : mx;
+    printf("%-26s bg %5d B/kcyc: %6.1f cyc/MMA\n", name, bg_bytes, static_cast<double>(mx) / (supers * 120));
+}
+
 template <int MODE, int N, int GRP>
 void run_rate(const char* name, long long* cyc, int bg = 0) {
     const int ksteps = 8192;
@@ -281,6 +395,9 @@ int main() {
     // ---- part 2: rates
     long long* cyc;
     CK(cudaMalloc(&cyc, 148 * sizeof(long long)));
+    run_kpattern<0>("kernel pattern ss", cyc);
+    run_kpattern<1>("kernel pattern ws", cyc);
+    for (int bgb : {2048, 4096, 8192, 16384}) run_kpattern<1>("kernel pattern ws", cyc, bgb);
     run_rate<0, 64, 8>("ss N=64", cyc);
     run_rate<3, 64, 8>("ws plain N=64", cyc);
     run_rate<1, 64, 8>("ws discard N=64", cyc);
