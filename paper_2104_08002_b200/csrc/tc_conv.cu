@@ -369,10 +369,30 @@ __device__ __forceinline__ bool next_super(Cursor& c, int64_t J, int G, int T, S
     return true;
 }
 
+// This CTA's output tiles [b, e). Every item segment a CTA walks costs G-1 warm-up input tiles
+// before its first output, so the split is even over "virtual" tiles: each item is G-1 warm-up
+// tiles followed by its J output tiles, and a CTA whose range holds an item start gets G-1 fewer
+// outputs (an even split of the outputs alone left those CTAs ~6% behind at config 2).
+__device__ __forceinline__ void cta_tile_range(const KParams& p, int G, int64_t* b, int64_t* e) {
+    if (p.total_tiles < 2 * static_cast<int64_t>(gridDim.x)) {  // about one tile per CTA: plain split
+        *b = p.total_tiles * blockIdx.x / gridDim.x;
+        *e = p.total_tiles * (blockIdx.x + 1) / gridDim.x;
+        return;
+    }
+    const int64_t J = p.tiles_per_item, W = J + (G - 1);
+    const int64_t V = p.n_items * W;
+    auto real = [&](int64_t v) -> int64_t {
+        const int64_t n = v / W, r = v - n * W;
+        return n * J + (r > G - 1 ? r - (G - 1) : 0);
+    };
+    *b = real(V * blockIdx.x / gridDim.x);
+    *e = real(V * (blockIdx.x + 1) / gridDim.x);
+}
+
 __device__ __forceinline__ Cursor make_cursor(const KParams& p) {
     Cursor c{};
-    const int64_t b = p.total_tiles * blockIdx.x / gridDim.x;
-    const int64_t e = p.total_tiles * (blockIdx.x + 1) / gridDim.x;
+    int64_t b, e;
+    cta_tile_range(p, p.pl.xr ? 1 : p.pl.g, &b, &e);
     c.cur = b;
     c.end = e;
     c.valid = next_segment(c, p.tiles_per_item);
@@ -1126,8 +1146,9 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         // layer glue input prefetch: this warp's blocks are (tile, kbi) for the CTA's tiles [cta_b, cta_e)
         // in order (the super-tile walk emits every output tile once, in increasing order)
         constexpr int kB = kKPB > 0 ? kKPB : 1;
-        const int64_t cta_b = p.total_tiles * blockIdx.x / gridDim.x;
-        const int64_t cta_tiles = p.total_tiles * (blockIdx.x + 1) / gridDim.x - cta_b;
+        int64_t cta_b, cta_e;
+        cta_tile_range(p, G, &cta_b, &cta_e);
+        const int64_t cta_tiles = cta_e - cta_b;
         const int64_t nblk = (cta_tiles > egrp ? (cta_tiles - egrp + kEG - 1) / kEG : 0) * kB;  // this group's blocks
         const bool pf_on = kMode != 0 && (p.pf_rows | p.pf_mask) != 0;
         const uint32_t pf_base = smem_u32(smem) + p.pf_off + static_cast<uint32_t>(ew * kPfRing) * p.pf_slot_bytes;
