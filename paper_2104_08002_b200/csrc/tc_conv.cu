@@ -271,8 +271,8 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
 // Weight value (o, i, s) of the forward-shaped problem: from prepped (o, i, s) weights, or straight
 // from the caller's KCS weights for backward-data (o = c, i = k, taps reversed; tensor.cpp:23-41)
 // so the separate prep launch disappears. BF16 RNE happens in the packing (bf16.hpp:29-40).
-__device__ __forceinline__ float wval(const float* __restrict__ w, int bwd_raw, int64_t O, int64_t I, int64_t S,
-                                      int64_t o, int64_t i, int64_t s) {
+template <typename Ix>
+__device__ __forceinline__ float wval(const float* __restrict__ w, int bwd_raw, Ix O, Ix I, Ix S, Ix o, Ix i, Ix s) {
     return bwd_raw ? w[(i * O + o) * S + (S - 1 - s)] : w[(o * I + i) * S + s];
 }
 
@@ -282,39 +282,45 @@ __device__ __forceinline__ float wval(const float* __restrict__ w, int bwd_raw, 
 //        writes output slot t+b (column (t+b)*KP), because tap block g of tile p lands on tile p-g.
 //  tail: timg[kg][chunk h][row o][k], k = r*cc + c: tap 16(G-1) + r of channel h*cc + c, zero for
 //        k >= tail*cc or past C / K (the tail-tap MMAs, see Plan::tail).
+// Index type Ix: 32-bit when every element index fits (always, in practice): 64-bit divisions per
+// element made this launch ~7 us for images of ~15k elements.
+template <typename Ix>
 __global__ void pack_images_kernel(const float* __restrict__ w, int bwd_raw, uint16_t* __restrict__ img,
-                                   uint16_t* __restrict__ timg, int64_t out_ch, int64_t in_ch, int64_t taps, int kp,
-                                   int g, int kgroups, int cc, int tail, int64_t chunks) {
-    const int64_t ntot = static_cast<int64_t>(g) * kp;
-    const int64_t per_chan = ntot * kTapsPerBlock;
-    const int64_t main_total = static_cast<int64_t>(kgroups) * in_ch * per_chan;
-    const int64_t per_tail = static_cast<int64_t>(kp) * kTapsPerBlock;
-    const int64_t total = main_total + (tail ? static_cast<int64_t>(kgroups) * chunks * per_tail : 0);
+                                   uint16_t* __restrict__ timg, int64_t out_ch_, int64_t in_ch_, int64_t taps_, int kp,
+                                   int g, int kgroups, int cc, int tail, int64_t chunks_) {
+    const Ix out_ch = static_cast<Ix>(out_ch_), in_ch = static_cast<Ix>(in_ch_), taps = static_cast<Ix>(taps_);
+    const Ix chunks = static_cast<Ix>(chunks_);
+    const Ix ntot = static_cast<Ix>(g) * kp;
+    const Ix per_chan = ntot * kTapsPerBlock;
+    const Ix main_total = static_cast<Ix>(kgroups) * in_ch * per_chan;
+    const Ix per_tail = static_cast<Ix>(kp) * kTapsPerBlock;
+    const Ix total = main_total + (tail ? static_cast<Ix>(kgroups) * chunks * per_tail : 0);
     pdl_trigger();
     pdl_wait();
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    for (Ix e = static_cast<Ix>(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += static_cast<Ix>(gridDim.x) * blockDim.x) {
         if (e < main_total) {
-            const int64_t r = e % kTapsPerBlock;
-            const int64_t row = (e / kTapsPerBlock) % ntot;
-            const int64_t c = (e / per_chan) % in_ch;
-            const int64_t kg = e / (per_chan * in_ch);
-            const int64_t blk = row / kp, o = kg * kp + row % kp, s = (g - 1 - blk) * kTapsPerBlock + r;
+            const Ix r = e % kTapsPerBlock;
+            const Ix q16 = e / kTapsPerBlock;
+            const Ix row = q16 % ntot;
+            const Ix cq = q16 / ntot;  // kg * in_ch + c
+            const Ix c = cq % in_ch;
+            const Ix blk = row / kp, o = (cq / in_ch) * kp + row % kp, s = (g - 1 - blk) * kTapsPerBlock + r;
             float v = 0.0f;
             if (o < out_ch && s < taps) v = wval(w, bwd_raw, out_ch, in_ch, taps, o, c, s);
-            const int64_t off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
-            img[(kg * in_ch + c) * per_chan + off] = fp32_to_bf16_bits(v);
+            const Ix off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
+            img[static_cast<int64_t>(cq) * per_chan + off] = fp32_to_bf16_bits(v);
         } else {
-            const int64_t f = e - main_total;
-            const int64_t k = f % kTapsPerBlock;
-            const int64_t row = (f / kTapsPerBlock) % kp;
-            const int64_t h = (f / per_tail) % chunks;
-            const int64_t kg = f / (per_tail * chunks);
-            const int64_t rr = k / cc, c = h * cc + k % cc, o = kg * kp + row;
-            const int64_t s = static_cast<int64_t>(g - 1) * kTapsPerBlock + rr;
+            const Ix f = e - main_total;
+            const Ix k = f % kTapsPerBlock;
+            const Ix row = (f / kTapsPerBlock) % kp;
+            const Ix h = (f / per_tail) % chunks;
+            const Ix kg = f / (per_tail * chunks);
+            const Ix rr = k / cc, c = h * cc + k % cc, o = kg * kp + row;
+            const Ix s = static_cast<Ix>(g - 1) * kTapsPerBlock + rr;
             float v = 0.0f;
             if (rr < tail && c < in_ch && o < out_ch && s < taps) v = wval(w, bwd_raw, out_ch, in_ch, taps, o, c, s);
-            const int64_t off = (row / 8) * 128 + (k / 8) * 64 + (row % 8) * 8 + (k % 8);
-            timg[(kg * chunks + h) * per_tail + off] = fp32_to_bf16_bits(v);
+            const Ix off = (row / 8) * 128 + (k / 8) * 64 + (row % 8) * 8 + (k % 8);
+            timg[static_cast<int64_t>(kg * chunks + h) * per_tail + off] = fp32_to_bf16_bits(v);
         }
     }
 }
@@ -1517,9 +1523,16 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
                               (g.in_ch * pl.ntot + (pl.tail ? n_chunks * pl.kp : 0)) * kTapsPerBlock;
         const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
         note_launch();
-        cudaError_t e = launch_pdl(pack_images_kernel, dim3(blocks), dim3(256), 0, stream, wg, w_bwd_raw ? 1 : 0, img,
-                                   img_tail, static_cast<int64_t>(g.out_ch), static_cast<int64_t>(g.in_ch),
-                                   static_cast<int64_t>(g.taps), pl.kp, pl.g, pl.kgroups, pl.cc, pl.tail, n_chunks);
+        const bool i32 = total + 256 * 4096 < (int64_t{1} << 31) &&
+                         static_cast<int64_t>(g.out_ch) * g.in_ch * g.taps < (int64_t{1} << 31);
+        cudaError_t e = i32 ? launch_pdl(pack_images_kernel<int32_t>, dim3(blocks), dim3(256), 0, stream, wg,
+                                         w_bwd_raw ? 1 : 0, img, img_tail, static_cast<int64_t>(g.out_ch),
+                                         static_cast<int64_t>(g.in_ch), static_cast<int64_t>(g.taps), pl.kp, pl.g,
+                                         pl.kgroups, pl.cc, pl.tail, n_chunks)
+                            : launch_pdl(pack_images_kernel<int64_t>, dim3(blocks), dim3(256), 0, stream, wg,
+                                         w_bwd_raw ? 1 : 0, img, img_tail, static_cast<int64_t>(g.out_ch),
+                                         static_cast<int64_t>(g.in_ch), static_cast<int64_t>(g.taps), pl.kp, pl.g,
+                                         pl.kgroups, pl.cc, pl.tail, n_chunks);
         if (e != cudaSuccess) return e;
     }
     CUtensorMap tmap;
