@@ -37,6 +37,7 @@ constexpr int kMaxStages = 4;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kLoaderThreads = 128;  // v3: warps 2, 3, 6, 7 stream X into the ring
 constexpr int kW2MaxStages = 6;
+constexpr int kW2MaxGrid = 1024;  // CTAs of one launch (the reduce keeps their segment counts in shared memory)
 constexpr int kW2Ks = 8;  // v3: K-steps (16 columns) per pipeline stage (the default cap)
 constexpr uint32_t kW2SmemBudget = 222 * 1024;  // v3 ring + stages (227 KB max per CTA, minus static + alignment)
 // v3 warps: 0 dY TMA, 1 MMA issue, 2/3/6/7 X loaders, 4/5/10/11 accumulator drains (TMEM lane
@@ -425,6 +426,7 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
         assigned = end;
     }
     p.grid = assigned;
+    if (p.grid > kW2MaxGrid) return false;
     p.box_bytes = static_cast<uint32_t>(p.kpw * 2 * p.bq);
     // Accumulator copies: MMAs into one accumulator serialise on a ~128-cycle chain, so when a
     // K-step's MMAs (gpc x N/2 cycles) are shorter than that, consecutive K-steps rotate over R
@@ -1114,8 +1116,12 @@ __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restr
                                                             float* __restrict__ dw, int64_t K, int64_t C, int64_t S,
                                                             int max_segs, int64_t slot_elems, const W2Plan pl) {
     __shared__ float red[4][64];
+    __shared__ int ns_s[kW2MaxGrid];
     pdl_trigger();
     pdl_wait();
+    if (max_segs > 1)
+        for (int i = threadIdx.x; i < pl.grid; i += blockDim.x) ns_s[i] = __ldg(nseg + i);
+    __syncthreads();
     // 32-bit index math (K*C*S < 2^31): 64-bit divisions made this kernel issue-bound (~100 us at
     // config 1's 148 CTA partials)
     const uint32_t count = static_cast<uint32_t>(K * C * S);
@@ -1145,17 +1151,30 @@ __global__ void __launch_bounds__(256) wgrad2_reduce_kernel(const float* __restr
                     if (bb + j < hi) v += t[j];
             }
         } else {
-            for (int bb = lo; bb < hi; ++bb) {
-                const int ns = __ldg(nseg + bb);
-                const float* src = part + static_cast<int64_t>(bb) * max_segs * slot_elems + idx;
-                for (int j = 0; j < ns; j += 8) {
-                    float t[8];
+            // the (CTA, segment) slots in order, 16 loads in flight: the segment counts come from
+            // shared memory (a dependent global load of each CTA's count before its slots made this
+            // loop latency-bound: ~55 us at config 1 in FP32)
+            int bb = lo, j = 0;
+            while (bb < hi && ns_s[bb] == 0) ++bb;
+            while (bb < hi) {
+                float t[16];
+                int cnt = 0;
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) t[u] = j + u < ns ? __ldg(src + static_cast<int64_t>(j + u) * slot_elems) : 0.0f;
-#pragma unroll
-                    for (int u = 0; u < 8; ++u)
-                        if (j + u < ns) v += t[u];
+                for (int u = 0; u < 16; ++u) {
+                    t[u] = 0.0f;
+                    if (bb < hi) {
+                        t[u] = __ldg(part + (static_cast<int64_t>(bb) * max_segs + j) * slot_elems + idx);
+                        ++cnt;
+                        if (++j == ns_s[bb]) {
+                            j = 0;
+                            ++bb;
+                            while (bb < hi && ns_s[bb] == 0) ++bb;
+                        }
+                    }
                 }
+#pragma unroll
+                for (int u = 0; u < 16; ++u)
+                    if (u < cnt) v += t[u];
             }
         }
     }
