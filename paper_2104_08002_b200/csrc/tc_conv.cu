@@ -532,17 +532,27 @@ __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t 
         x[jj] = __uint_as_float(v[jj]) + bias16[jj];
         a[jj] = (relu && !(x[jj] > 0.0f)) ? 0.0f : x[jj];
     }
+    // mask word (bit jj = x[jj] > 0) from integer ops: with ReLU, a[jj] is +0 or x[jj] > 0 (NaN -> 0),
+    // so bit = (bits(a) != 0) = (bits(a) + 0x7fffffff) >> 31, accumulated MSB-first; the float
+    // compare form compiled to ~100 predicate-juggling instructions per block
+    uint32_t mword = 0;
+    if (gl.mask_out) {
+        if (relu) {
+#pragma unroll
+            for (int jj = 15; jj >= 0; --jj) mword = (mword << 1) | ((__float_as_uint(a[jj]) + 0x7fffffffu) >> 31);
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) mword |= (x[jj] > 0.0f ? 1u : 0u) << jj;
+        }
+    }
     if (gl.skip) {  // prefetched rows (zero outside the tensor)
         const uint32_t src = pf_slot + static_cast<uint32_t>(lane) * 4u;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) a[jj] += ld_shared_f32(src + jj * 128);
     }
     if (gl.mask_out) {  // one word per column and 16-channel block: bit jj = row k0 + jj
-        uint32_t m = 0;
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) m |= (x[jj] > 0.0f ? 1u : 0u) << jj;
         const int64_t kblocks = (p.out_ch + 15) >> 4;
-        if (qv && kvalid > 0) gl.mask_out[(n * kblocks + (k0 >> 4)) * out_w + q] = m;
+        if (qv && kvalid > 0) gl.mask_out[(n * kblocks + (k0 >> 4)) * out_w + q] = mword;
     }
     uint32_t pc[8];
     if (gl.act_bf16) pack_bf16_rows(a, pc);
