@@ -138,6 +138,7 @@ struct KParams {
     // glue inputs (skip / gadd rows, mask words) prefetched kPfRing blocks ahead with cp.async into
     // per-warp rings: pf_rows / pf_mask = slot has 16 x 32 fp32 rows / 32 mask words
     uint32_t pf_off, pf_slot_bytes, pf_rows, pf_mask;
+    uint32_t pf_vec;  // prefetch rows as 16-B pieces (width, column offset and base 16-B compatible)
 };
 
 bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve, bool allow_wres = true) {
@@ -480,7 +481,23 @@ __device__ __forceinline__ void glue_prefetch(const KParams& p, int64_t n, int64
     const int64_t k0 = p.k_begin + kbi * 16;
     const int kvalid = static_cast<int>(imin64(16, p.out_ch - k0));
     const int64_t row0 = n * p.out_ch + k0;
-    if (p.pf_rows) {
+    if (p.pf_rows && p.pf_vec) {
+        // 16-B pieces: lane copies columns 4*(lane%8) .. +3 of rows lane/8 + 4i (i < 4). The width
+        // and the block's first column are multiples of 4, so a piece is wholly inside or outside.
+        const float* base = gl.mode == 1 ? gl.skip : gl.gadd;
+        const int64_t w = gl.mode == 1 ? p.out_w : gl.g_q;
+        const int64_t c = (gl.mode == 1 ? x : x - gl.g_off) - lane + 4 * (lane & 7);
+        const bool cv = c >= 0 && c < w;
+        const int r0 = lane >> 3;
+        const float* src = base + (row0 + r0) * w + c;
+        const uint32_t dst = slot + static_cast<uint32_t>(r0 * 128 + (lane & 7) * 16);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const bool v = cv && r0 + 4 * i < kvalid;
+            cp_async16_zfill(dst + i * 512, v ? src : base, v);
+            src += 4 * w;
+        }
+    } else if (p.pf_rows) {
         const float* base = gl.mode == 1 ? gl.skip : gl.gadd;
         const int64_t w = gl.mode == 1 ? p.out_w : gl.g_q;
         const int64_t c = gl.mode == 1 ? x : x - gl.g_off;
@@ -1638,6 +1655,11 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     kp.pf_slot_bytes = pf_slot;
     kp.pf_rows = pf_rows;
     kp.pf_mask = pf_mask;
+    if (glue && pf_rows) {
+        const int64_t w = mode == 1 ? g.out_w : glue->g_q;
+        const float* rows = mode == 1 ? glue->skip : glue->gadd;
+        kp.pf_vec = w % 4 == 0 && (mode == 1 || glue->g_off % 4 == 0) && (reinterpret_cast<uintptr_t>(rows) & 15u) == 0;
+    }
     const int grid = static_cast<int>(std::min<int64_t>(num_sms(), kp.total_tiles));
     if (glue && glue->mode != 0) {
         kp.glue = *glue;
