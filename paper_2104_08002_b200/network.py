@@ -41,6 +41,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import torch
 
@@ -312,11 +313,41 @@ class ResidualNet:
         """(N, 2, width) gradient of the two heads' outputs (channel 0 regression, 1 peak logits)."""
         return self._buf("g.heads", (n, 2, width), torch.float32)
 
+    def _wgrad_stream(self, dev):
+        """Side stream for the backward-weight passes (None: run them in order on the current
+        stream; C1D_NET_SERIAL=1, a dev A/B switch)."""
+        if os.environ.get("C1D_NET_SERIAL"):
+            return None
+        if getattr(self, "_side", None) is None or self._side.device != dev:
+            self._side = torch.cuda.Stream(dev)
+        return self._side
+
     def backward_heads(self, g2: torch.Tensor) -> None:
-        """The backward pass from the heads' output gradient g2 = head_grad_buffer(...)."""
+        """The backward pass from the heads' output gradient g2 = head_grad_buffer(...).
+
+        Each layer's backward-weight (reads its pre-activation gradient gp and its forward input)
+        runs on a side stream, concurrently with that layer's glued backward-data (which writes the
+        other gp slot); the next backward-data, which overwrites this gp slot, waits for it. The
+        kernels and their inputs are the same as in order, so the results are bit-identical; the
+        overlap fills each pass's fill / drain tails and takes the wgrad reduce off the critical
+        path (it matters most at the small per-rank batches of data-parallel strong scaling)."""
         h = self.h_last
         n, hidden, width = h.shape
         heads = self.heads
+        main = torch.cuda.current_stream(g2.device)
+        side = self._wgrad_stream(g2.device)
+
+        def wgrad_async(layer, grad):
+            if side is None:
+                layer.backward_weight(grad)
+                return None
+            side.wait_stream(main)  # grad is ready
+            with torch.cuda.stream(side):
+                layer.backward_weight(grad)
+            ev = torch.cuda.Event()
+            ev.record(side)
+            return ev
+
         layer_backward_prologue(g2, 0, None, n, 2, width, relu=False, bias_grad=heads.grad_b)
         heads.backward_weight(g2)
         chain = [self.input] + [layer for blk in self.blocks for layer in blk]  # forward order
@@ -352,7 +383,7 @@ class ResidualNet:
         g_outs = {len(self.blocks) - 1: g_out} if self.blocks else {}
         for li in range(len(chain) - 1, 0, -1):
             layer, below = chain[li], chain[li - 1]
-            layer.backward_weight(gp)
+            wg_done = wgrad_async(layer, gp)
             slot ^= 1
             gp_next, kw = glue_out(below, slot)
             if li in first_of_block:
@@ -363,12 +394,16 @@ class ResidualNet:
                     g_outs[bi - 1] = self._buf(f"g.b{bi - 1}", (n, hidden, width), torch.float32)
                     kw["gsum"] = g_outs[bi - 1]
             layer.backward_data_into(gp, below, width, **kw)
+            if wg_done is not None:
+                main.wait_event(wg_done)  # the next backward-data overwrites the gp slot it reads
             gp = gp_next
         first = self.input
-        first.backward_weight(gp)
+        wg_done = wgrad_async(first, gp)
         # gradient w.r.t. the padded network input: computed as the reference does, then discarded
         cv.conv1d_backward_data(gp, first.w, first.p, out=self._buf("dx.in", (n, 1, first.x_in.shape[2]),
                                                                      torch.float32))
+        if wg_done is not None:
+            main.wait_event(wg_done)
 
     def load_params(self, flat) -> None:
         """Set every weight and bias from a flat vector in the reference's gather_params order
