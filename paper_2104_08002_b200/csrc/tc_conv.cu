@@ -348,10 +348,18 @@ struct Super {
 
 __device__ __forceinline__ bool next_segment(Cursor& c, int64_t J) {
     if (c.cur >= c.end) return false;
-    c.n = c.cur / J;
-    c.j0 = c.cur % J;
+    // 32-bit divisions when the tile indices fit (always, in practice): a 64-bit division is a
+    // ~70-instruction software routine on every warp role's path to its first tile
+    if (c.end < (int64_t{1} << 31) && J < (int64_t{1} << 31)) {
+        const uint32_t cur = static_cast<uint32_t>(c.cur), j = static_cast<uint32_t>(J);
+        c.n = cur / j;
+        c.j0 = cur - static_cast<uint32_t>(c.n) * j;
+    } else {
+        c.n = c.cur / J;
+        c.j0 = c.cur % J;
+    }
     const int64_t last = imin64(c.end, (c.n + 1) * J) - 1;
-    c.j1 = last % J;
+    c.j1 = last - c.n * J;
     c.cur = last + 1;
     c.i = c.j0;
     return true;
@@ -382,12 +390,23 @@ __device__ __forceinline__ bool next_super(Cursor& c, int64_t J, int G, int T, S
 // outputs (an even split of the outputs alone left those CTAs ~6% behind at config 2).
 __device__ __forceinline__ void cta_tile_range(const KParams& p, int G, int64_t* b, int64_t* e) {
     if (p.total_tiles < 2 * static_cast<int64_t>(gridDim.x)) {  // about one tile per CTA: plain split
-        *b = p.total_tiles * blockIdx.x / gridDim.x;
-        *e = p.total_tiles * (blockIdx.x + 1) / gridDim.x;
+        *b = static_cast<int64_t>(static_cast<uint32_t>(p.total_tiles) * blockIdx.x / gridDim.x);
+        *e = static_cast<int64_t>(static_cast<uint32_t>(p.total_tiles) * (blockIdx.x + 1) / gridDim.x);
         return;
     }
     const int64_t J = p.tiles_per_item, W = J + (G - 1);
     const int64_t V = p.n_items * W;
+    if (V * static_cast<int64_t>(gridDim.x) < (int64_t{1} << 31)) {  // 32-bit divisions
+        const uint32_t w = static_cast<uint32_t>(W), g1 = static_cast<uint32_t>(G - 1), j = static_cast<uint32_t>(J);
+        auto real32 = [&](uint32_t v) -> int64_t {
+            const uint32_t n = v / w, r = v - n * w;
+            return static_cast<int64_t>(n) * j + (r > g1 ? r - g1 : 0u);
+        };
+        const uint32_t v32 = static_cast<uint32_t>(V);
+        *b = real32(v32 * blockIdx.x / gridDim.x);
+        *e = real32(v32 * (blockIdx.x + 1) / gridDim.x);
+        return;
+    }
     auto real = [&](int64_t v) -> int64_t {
         const int64_t n = v / W, r = v - n * W;
         return n * J + (r > G - 1 ? r - (G - 1) : 0);
