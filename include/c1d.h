@@ -92,6 +92,13 @@ typedef enum c1d_pass { C1D_PASS_FORWARD = 0, C1D_PASS_BACKWARD_DATA = 1, C1D_PA
  * at config 3, at some cost in time (config-3 backward-weight ~+45%). FP32 precision always runs
  * this way. */
 #define C1D_FLAG_EXACT_ACCUM 0x2u
+/* The weight pointer of c1d_forward / c1d_backward_data (and the glued variants) is a weight image
+ * made by c1d_pack_weights for this desc and pass, not KCS weights. The call skips its own packing
+ * launch and loads the image while the previous kernel on the stream is still running, so the image
+ * must be complete before that kernel is launched (pack earlier than the kernel right before the
+ * call; c1d_pack_weights itself never lets its successor start early). Only plans with at most 32
+ * filters per group on the dilation-8 tensor-core path take images (c1d_packed_weights_size). */
+#define C1D_FLAG_PREPACKED_WEIGHTS 0x4u
 
 /* Mirrors conv1d::ConvParams (conv.hpp:18-25) plus the tensor sizes the reference reads from
  * its Tensor3D arguments. */
@@ -147,6 +154,14 @@ C1D_EXPORT c1d_status c1d_backward_weight(const c1d_desc* desc, const void* x, c
                                void* workspace, size_t workspace_bytes, c1d_stream_t stream);
 
 /* out[i] = bf16 bits of in[i], round-to-nearest-even, NaN -> quiet NaN (bf16.hpp:29-40). */
+/* Size of the weight image of (desc, pass) for C1D_FLAG_PREPACKED_WEIGHTS; C1D_ERR_UNSUPPORTED
+ * when that pass's plan packs its own weights. */
+C1D_EXPORT c1d_status c1d_packed_weights_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes);
+/* Pack `count` images in one launch (several when count > 32): image i from the KCS weights w[i] of
+ * descs[i] for passes[i] (C1D_PASS_FORWARD or C1D_PASS_BACKWARD_DATA; backward-data images are the
+ * transposed, tap-reversed filters, as c1d_backward_data packs them). */
+C1D_EXPORT c1d_status c1d_pack_weights(int count, const c1d_desc* descs, const int32_t* passes,
+                                       const float* const* w, void* const* images, c1d_stream_t stream);
 C1D_EXPORT c1d_status c1d_round_bf16(const float* in, uint16_t* out, int64_t count, c1d_stream_t stream);
 
 /* ---- Fused layer glue of the reference's ConvLayer (train.cpp:173-221) ----

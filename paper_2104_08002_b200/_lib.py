@@ -19,6 +19,7 @@ ALGO_AUTO, ALGO_DIRECT, ALGO_TCGEN05, ALGO_BF16X3 = 0, 1, 2, 3
 DTYPE_F32, DTYPE_BF16 = 0, 1
 FLAG_STRICT_BF16_DIMS = 0x1
 FLAG_EXACT_ACCUM = 0x2
+FLAG_PREPACKED_WEIGHTS = 0x4
 
 
 class Desc(C.Structure):
@@ -109,6 +110,10 @@ def lib() -> C.CDLL:
     L.c1d_backward_weight.argtypes = [P(Desc), C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t,
                                       C.c_void_p]
     L.c1d_backward_weight.restype = C.c_int
+    L.c1d_packed_weights_size.argtypes = [P(Desc), C.c_int, P(C.c_size_t)]
+    L.c1d_packed_weights_size.restype = C.c_int
+    L.c1d_pack_weights.argtypes = [C.c_int, P(Desc), P(C.c_int32), P(C.c_void_p), P(C.c_void_p), C.c_void_p]
+    L.c1d_pack_weights.restype = C.c_int
     L.c1d_round_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
     L.c1d_round_bf16.restype = C.c_int
     L.c1d_launch_count.restype = C.c_uint64

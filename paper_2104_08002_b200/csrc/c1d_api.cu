@@ -916,6 +916,15 @@ size_t split_workspace(const c1d_desc& d, c1d_pass pass, int64_t q) {
 // Conv-shaped pass (forward or backward-data).
 // glue (optional): layer glue fused into the tensor-core epilogue; only for glue_fusable() passes,
 // and `out` may then be NULL.
+// C1D_FLAG_PREPACKED_WEIGHTS: BF16 on the native dilation-8 tensor-core path, one accumulator
+// chain (the carry plan), and a plan whose image tc_conv_prepack_bytes describes
+bool prepack_ok(const c1d_desc& d, c1d_pass pass, int64_t q, c1d_algo algo) {
+    if (pass == C1D_PASS_BACKWARD_WEIGHT || algo != C1D_ALGO_TCGEN05 || !is_bf16(d)) return false;
+    if (dil_plan(d, q).kind != DilPlan::kNative) return false;
+    const ConvGeom g = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q));
+    return tc_conv_prepack_bytes(g) > 0;
+}
+
 c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const float* w_kcs, float* out,
                      void* ws, size_t ws_bytes, cudaStream_t stream, const LayerGlue* glue = nullptr) {
     t_last_error.clear();
@@ -931,6 +940,9 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
     const c1d_algo algo = resolve(d, pass, q);
     if (static_cast<int>(algo) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     const ConvGeom g = pass == C1D_PASS_FORWARD ? fwd_geom(d, q) : bwd_geom(d, q);
+    const bool prepacked = (d.flags & C1D_FLAG_PREPACKED_WEIGHTS) != 0;
+    if (prepacked && !prepack_ok(d, pass, q, algo))
+        return fail(C1D_ERR_UNSUPPORTED, "C1D_FLAG_PREPACKED_WEIGHTS: this pass's plan packs its own weights");
     Bump bump{};
     st = acquire_workspace(ws, ws_bytes, workspace_for(d, pass, q, algo), &bump, stream);
     if (st != C1D_OK) return st;
@@ -1046,10 +1058,11 @@ c1d_status conv_pass(const c1d_desc* desc, c1d_pass pass, const void* in, const 
         in_b = tmp;
     }
     // glued calls keep the carry mode; otherwise native_choice (carry / direct / two chains)
-    const ChainPlan cp = glue ? ChainPlan{gq, 0} : native_choice(gq);
+    const ChainPlan cp = glue || prepacked ? ChainPlan{gq, 0} : native_choice(gq);
     void* kws = bump.take<char>(tc_conv_workspace_bytes(cp.g, cp.main_ch));
     if (bump.overflow) return workspace_overflow();
-    e = launch_tc_conv(in_b, w_kcs, out, cp.g, kws, stream, cp.main_ch, pass == C1D_PASS_BACKWARD_DATA, glue);
+    e = launch_tc_conv(in_b, w_kcs, out, cp.g, kws, stream, cp.main_ch, pass == C1D_PASS_BACKWARD_DATA, glue,
+                       prepacked ? reinterpret_cast<const uint16_t*>(w_kcs) : nullptr);
     if (e != cudaSuccess) return cuda_fail(e, "tc_conv");
     return C1D_OK;
 }
@@ -1145,6 +1158,47 @@ c1d_status c1d_workspace_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes
     if (static_cast<int>(a) < 0) return fail(C1D_ERR_UNSUPPORTED, "requested algo cannot run this shape");
     if (bytes) *bytes = workspace_for(*desc, pass, q, a);
     return C1D_OK;
+}
+
+c1d_status c1d_packed_weights_size(const c1d_desc* desc, c1d_pass pass, size_t* bytes) {
+    t_last_error.clear();
+    int64_t q = 0;
+    c1d_status st = validate(desc, &q);
+    if (st != C1D_OK) return st;
+    const ExactAccumScope exact_scope(exact_for(*desc));
+    const c1d_algo a = resolve(*desc, pass, q);
+    if (static_cast<int>(a) < 0 || !prepack_ok(*desc, pass, q, a))
+        return fail(C1D_ERR_UNSUPPORTED, "this pass's plan packs its own weights");
+    if (bytes)
+        *bytes = tc_conv_prepack_bytes(pitched(pass == C1D_PASS_FORWARD ? fwd_geom(*desc, q) : bwd_geom(*desc, q)));
+    return C1D_OK;
+}
+
+c1d_status c1d_pack_weights(int count, const c1d_desc* descs, const int32_t* passes, const float* const* w,
+                            void* const* images, c1d_stream_t stream) {
+    t_last_error.clear();
+    if (count < 0 || (count > 0 && (!descs || !passes || !w || !images)))
+        return fail(C1D_ERR_INVALID_ARGUMENT, "bad c1d_pack_weights arguments");
+    if (count == 0) return C1D_OK;
+    c1d_status st = check_device();
+    if (st != C1D_OK) return st;
+    std::vector<ConvGeom> gs(static_cast<size_t>(count));
+    std::vector<int> raw(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+        const c1d_pass pass = static_cast<c1d_pass>(passes[i]);
+        int64_t q = 0;
+        st = validate(&descs[i], &q);
+        if (st != C1D_OK) return st;
+        const ExactAccumScope exact_scope(exact_for(descs[i]));
+        const c1d_algo a = resolve(descs[i], pass, q);
+        if (static_cast<int>(a) < 0 || !prepack_ok(descs[i], pass, q, a) || !w[i] || !images[i])
+            return fail(C1D_ERR_UNSUPPORTED, "c1d_pack_weights: job " + std::to_string(i) + " cannot take an image");
+        gs[static_cast<size_t>(i)] = pitched(pass == C1D_PASS_FORWARD ? fwd_geom(descs[i], q) : bwd_geom(descs[i], q));
+        raw[static_cast<size_t>(i)] = pass == C1D_PASS_BACKWARD_DATA ? 1 : 0;
+    }
+    const cudaError_t e = launch_pack_images_multi(count, gs.data(), w, raw.data(), images,
+                                                   reinterpret_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? C1D_OK : cuda_fail(e, "pack_weights");
 }
 
 c1d_status c1d_forward(const c1d_desc* desc, const void* x, const float* w_kcs, float* y, void* workspace,

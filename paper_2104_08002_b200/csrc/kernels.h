@@ -124,7 +124,12 @@ size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch = 0);
 // NULL); its bias-gradient partials need out_ch * num_sms() floats at glue->part.
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g,
                            void* workspace, cudaStream_t stream, int64_t main_ch = 0, bool w_bwd_raw = false,
-                           const LayerGlue* glue = nullptr);
+                           const LayerGlue* glue = nullptr, const uint16_t* prepacked = nullptr);
+// Bytes of a prepacked weight image for this geometry (0: the plan needs its own packing).
+size_t tc_conv_prepack_bytes(const ConvGeom& g);
+// Pack `count` weight images (fwd KCS, or raw layer weights with bwd_raw) in one or a few launches.
+cudaError_t launch_pack_images_multi(int count, const ConvGeom* gs, const float* const* w, const int* bwd_raw,
+                                     void* const* images, cudaStream_t stream);
 
 bool tc_wgrad_supported(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);
 size_t tc_wgrad_workspace_bytes(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t q);

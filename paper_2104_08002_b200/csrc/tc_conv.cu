@@ -128,6 +128,9 @@ struct KParams {
     int64_t main_ch;       // channels < main_ch -> region 0, others -> region acc2 (split FP32)
     float* out;
     unsigned long long* prof;  // optional per-CTA cycle counters (C1D_PROFILE=1), else nullptr
+    // resident image prepacked by the caller (c1d_pack_weights, written before the previous launch
+    // on the stream): its bulk load is issued before the PDL wait, overlapping the previous kernel
+    int early_w;
     LayerGlue glue;            // mode 0: plain FP32 store of `out`
     // glue outputs through shared-memory staging + TMA stores: slot bits 1 = fp32 A (pre / gsum),
     // 2 = fp32 B (act / gp), 4 = bf16 C (act_bf16 / gp_bf16); 0 = per-lane global stores
@@ -323,6 +326,39 @@ __global__ void pack_images_kernel(const float* __restrict__ w, int bwd_raw, uin
             const Ix off = (row / 8) * 128 + (k / 8) * 64 + (row % 8) * 8 + (k % 8);
             timg[static_cast<int64_t>(kg * chunks + h) * per_tail + off] = fp32_to_bf16_bits(v);
         }
+    }
+}
+
+// Several layers' main images in one launch (c1d_pack_weights): job j covers elements [begin_j,
+// begin_{j+1}) of the concatenated images; element layout as pack_images_kernel's main image.
+struct PackJob {
+    const float* w;
+    uint16_t* img;
+    int32_t bwd_raw, out_ch, in_ch, taps, kp, g, kgroups, pad_;
+    int64_t begin;
+};
+constexpr int kMaxPackJobs = 32;
+struct PackJobs {
+    PackJob j[kMaxPackJobs];
+    int32_t count, pad_;
+    int64_t total;
+};
+__global__ void pack_images_multi_kernel(const PackJobs jobs) {
+    for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < jobs.total;
+         e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int ji = 0;
+        while (ji + 1 < jobs.count && e >= jobs.j[ji + 1].begin) ++ji;
+        const PackJob& jb = jobs.j[ji];
+        const int32_t el = static_cast<int32_t>(e - jb.begin);  // < 2^31 (checked on the host)
+        const int32_t ntot = jb.g * jb.kp, per_chan = ntot * kTapsPerBlock;
+        const int32_t r = el % kTapsPerBlock, q16 = el / kTapsPerBlock;
+        const int32_t row = q16 % ntot, cq = q16 / ntot, c = cq % jb.in_ch;
+        const int32_t blk = row / jb.kp, o = (cq / jb.in_ch) * jb.kp + row % jb.kp;
+        const int32_t s = (jb.g - 1 - blk) * kTapsPerBlock + r;
+        float v = 0.0f;
+        if (o < jb.out_ch && s < jb.taps) v = wval<int32_t>(jb.w, jb.bwd_raw, jb.out_ch, jb.in_ch, jb.taps, o, c, s);
+        const int32_t off = (row / 8) * 128 + (r / 8) * 64 + (row % 8) * 8 + (r % 8);
+        jb.img[static_cast<int64_t>(cq) * per_chan + off] = fp32_to_bf16_bits(v);
     }
 }
 
@@ -823,7 +859,14 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    // PDL: everything above overlapped the previous kernel; global memory only from here on
+    if (p.early_w && threadIdx.x == 0) {
+        const uint32_t wbytes = static_cast<uint32_t>(p.in_ch) * pl.b_chan_bytes;
+        mbar_arrive_expect_tx(smem_u32(&wres_full), wbytes);
+        for (uint32_t o = 0; o < wbytes; o += 32768u)
+            bulk_g2s(wres_s + o, p.bimg + o / 2, wbytes - o < 32768u ? wbytes - o : 32768u, smem_u32(&wres_full));
+    }
+    // PDL: everything above overlapped the previous kernel; global memory only from here on (the
+    // prepacked weight image excepted: it was complete before the previous kernel was launched)
     pdl_trigger();
     pdl_wait();
     if (p.prof && threadIdx.x == 0) {
@@ -843,7 +886,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             uint32_t phase = 0;
             Super su;
             const uint32_t wchan = pl.wres_bytes ? 0u : pl.b_chan_bytes;  // weight bytes per channel and stage
-            if (pl.wres_bytes) {
+            if (pl.wres_bytes && !p.early_w) {
                 const uint32_t wbytes = static_cast<uint32_t>(p.in_ch) * pl.b_chan_bytes;
                 mbar_arrive_expect_tx(smem_u32(&wres_full), wbytes);
                 for (uint32_t o = 0; o < wbytes; o += 32768u)
@@ -1526,8 +1569,55 @@ size_t tc_conv_workspace_bytes(const ConvGeom& g, int64_t main_ch) {
     return static_cast<size_t>(pl.kgroups) * static_cast<size_t>(g.in_ch) * pl.b_chan_bytes + ((tail + 255) & ~size_t{255});
 }
 
+// Prepacked images (c1d_pack_weights): plans whose main image is the whole B operand (no tail
+// image, natural rows, one accumulator region); the layout depends only on (KP, G, filter groups, C).
+size_t tc_conv_prepack_bytes(const ConvGeom& g) {
+    Plan pl;
+    if (g.xr_rows > 0 || g.xr_inline || !make_plan(g, &pl)) return 0;
+    if (pl.tail || pl.kp > 32) return 0;
+    if (static_cast<int64_t>(pl.kgroups) * g.in_ch * pl.ntot * kTapsPerBlock >= (int64_t{1} << 31)) return 0;
+    if (g.out_ch * g.in_ch * g.taps >= (int64_t{1} << 31)) return 0;
+    return static_cast<size_t>(pl.kgroups) * static_cast<size_t>(g.in_ch) * pl.b_chan_bytes;
+}
+
+cudaError_t launch_pack_images_multi(int count, const ConvGeom* gs, const float* const* w, const int* bwd_raw,
+                                     void* const* images, cudaStream_t stream) {
+    for (int j0 = 0; j0 < count; j0 += kMaxPackJobs) {
+        PackJobs jobs{};
+        int64_t total = 0;
+        for (int j = j0; j < count && j - j0 < kMaxPackJobs; ++j) {
+            Plan pl;
+            if (!tc_conv_prepack_bytes(gs[j]) || !make_plan(gs[j], &pl)) return cudaErrorInvalidValue;
+            PackJob& jb = jobs.j[jobs.count++];
+            jb.w = w[j];
+            jb.img = static_cast<uint16_t*>(images[j]);
+            jb.bwd_raw = bwd_raw[j];
+            jb.out_ch = static_cast<int32_t>(gs[j].out_ch);
+            jb.in_ch = static_cast<int32_t>(gs[j].in_ch);
+            jb.taps = static_cast<int32_t>(gs[j].taps);
+            jb.kp = pl.kp;
+            jb.g = pl.g;
+            jb.kgroups = pl.kgroups;
+            jb.begin = total;
+            total += static_cast<int64_t>(pl.kgroups) * gs[j].in_ch * pl.ntot * kTapsPerBlock;
+        }
+        jobs.total = total;
+        const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
+        if (blocks > 0) {
+            // a plain launch (no PDL trigger): the next kernel starts after this one completes, so
+            // the images are complete before any conv that loads them early
+            pack_images_multi_kernel<<<blocks, 256, 0, stream>>>(jobs);
+            note_launch();
+            const cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out, const ConvGeom& g, void* workspace,
-                           cudaStream_t stream, int64_t main_ch, bool w_bwd_raw, const LayerGlue* glue) {
+                           cudaStream_t stream, int64_t main_ch, bool w_bwd_raw, const LayerGlue* glue,
+                           const uint16_t* prepacked) {
     auto encode = get_encode_fn();
     if (!encode) return cudaErrorNotSupported;
     GlueMaps gm;
@@ -1566,10 +1656,11 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
         pf_off = stg_off + stg_total;
         pl.smem_bytes = pf_off + pf_total + 1024;
     }
-    uint16_t* img = static_cast<uint16_t*>(workspace);
+    uint16_t* img = prepacked ? const_cast<uint16_t*>(prepacked) : static_cast<uint16_t*>(workspace);
     const int64_t n_chunks = ceil_div(g.in_ch, pl.cc);
     uint16_t* img_tail = img + static_cast<size_t>(pl.kgroups) * g.in_ch * (pl.b_chan_bytes / 2);
-    {
+    if (prepacked && (pl.tail || pl.xr || pl.kp > 32 || main_ch > 0)) return cudaErrorInvalidValue;
+    if (!prepacked) {
         const int64_t total = static_cast<int64_t>(pl.kgroups) *
                               (g.in_ch * pl.ntot + (pl.tail ? n_chunks * pl.kp : 0)) * kTapsPerBlock;
         const int blocks = static_cast<int>(std::min<int64_t>(ceil_div(total, 256), 4096));
@@ -1664,6 +1755,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     kp.main_ch = main_ch > 0 ? main_ch : g.in_ch;
     kp.pl = pl;
     kp.out = out;
+    kp.early_w = prepacked && pl.wres_bytes ? 1 : 0;
     kp.tma_slots = gm.slots;
     kp.stg_off = stg_off;
     kp.stg_bytes = gm.stg_bytes;

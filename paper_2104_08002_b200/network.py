@@ -90,25 +90,52 @@ def _desc_for(x: torch.Tensor, p: cv.ConvParams, w_in: int):
 
 
 def conv_forward_glued(x, w_kcs, p: cv.ConvParams, *, bias=None, skip=None, relu=True, pre=None, act=None,
-                       act_bf16=None, act_pad=0, mask=None):
+                       act_bf16=None, act_pad=0, mask=None, image=None):
     """c1d_forward_glued: conv + bias + ReLU (+ skip) in one call; the glue runs in the tcgen05 conv
-    epilogue where the shape allows it. mask: int32 mask_shape(N, K, Q) ReLU-mask words."""
+    epilogue where the shape allows it. mask: int32 mask_shape(N, K, Q) ReLU-mask words. image: a
+    weight image from pack_weights (C1D_FLAG_PREPACKED_WEIGHTS) used instead of w_kcs."""
     desc = _desc_for(x, p, x.shape[2])
+    if image is not None:
+        desc.flags |= L.FLAG_PREPACKED_WEIGHTS
     glue = L.FwdGlue(_ptr(bias), _ptr(skip), _ptr(pre), _ptr(act), _ptr(act_bf16), _ptr(mask), act_pad, int(relu), 0)
-    cv._check(L.lib().c1d_forward_glued(C.byref(desc), x.data_ptr(), w_kcs.data_ptr(), C.byref(glue), None, 0,
+    w = image if image is not None else w_kcs
+    cv._check(L.lib().c1d_forward_glued(C.byref(desc), x.data_ptr(), w.data_ptr(), C.byref(glue), None, 0,
                                         _stream()))
 
 
 def conv_backward_data_glued(dy, w_kcs, p: cv.ConvParams, off: int, q: int, *, gadd=None, mask=None, gsum=None,
-                             grad_pre=None, grad_pre_bf16=None, bias_grad=None):
+                             grad_pre=None, grad_pre_bf16=None, bias_grad=None, image=None):
     """c1d_backward_data_glued: backward-data, then the glue of the layer that owns columns
-    [off, off + q) of the input gradient (skip gradient, ReLU mask bits, BF16 rounding, bias grad)."""
+    [off, off + q) of the input gradient (skip gradient, ReLU mask bits, BF16 rounding, bias grad).
+    image: a backward-data weight image from pack_weights, used instead of w_kcs."""
     w_in = dy.shape[2] + p.dilation * (p.taps - 1)
     desc = _desc_for(dy, p, w_in)
+    if image is not None:
+        desc.flags |= L.FLAG_PREPACKED_WEIGHTS
     glue = L.BwdGlue(off, q, _ptr(gadd), _ptr(mask), _ptr(gsum), _ptr(grad_pre), _ptr(grad_pre_bf16),
                      _ptr(bias_grad))
-    cv._check(L.lib().c1d_backward_data_glued(C.byref(desc), dy.data_ptr(), w_kcs.data_ptr(), C.byref(glue), None,
+    w = image if image is not None else w_kcs
+    cv._check(L.lib().c1d_backward_data_glued(C.byref(desc), dy.data_ptr(), w.data_ptr(), C.byref(glue), None,
                                               0, _stream()))
+
+
+def packed_weights_bytes(p: cv.ConvParams, n: int, w_in: int, pass_: int) -> int:
+    """Bytes of the pass's weight image (c1d_packed_weights_size), 0 when its plan packs its own."""
+    b = C.c_size_t(0)
+    st = L.lib().c1d_packed_weights_size(C.byref(cv.make_desc(p, n, w_in, L.DTYPE_BF16)), pass_, C.byref(b))
+    return int(b.value) if st == 0 else 0
+
+
+def pack_weights(jobs) -> None:
+    """c1d_pack_weights: jobs = [(params, n, w_in, pass, w_kcs, image)], one launch per 32 images."""
+    if not jobs:
+        return
+    cnt = len(jobs)
+    descs = (L.Desc * cnt)(*[cv.make_desc(p, n, w_in, L.DTYPE_BF16) for p, n, w_in, _, _, _ in jobs])
+    passes = (C.c_int32 * cnt)(*[j[3] for j in jobs])
+    ws = (C.c_void_p * cnt)(*[j[4].data_ptr() for j in jobs])
+    imgs = (C.c_void_p * cnt)(*[j[5].data_ptr() for j in jobs])
+    cv._check(L.lib().c1d_pack_weights(cnt, descs, passes, ws, imgs, _stream()))
 
 
 def glue_is_fused(p: cv.ConvParams, n: int, w_in: int, pass_: int, in_dtype: int = L.DTYPE_BF16) -> bool:
@@ -137,13 +164,17 @@ class ConvLayer:
         self.grad_b = torch.zeros_like(self.b)
         self.x_in = None
         self.mask = None
+        self.img = {}  # pass -> weight image (C1D_FLAG_PREPACKED_WEIGHTS), refreshed by ResidualNet.forward
 
     @property
     def bf16(self) -> bool:
         return self.p.precision == cv.Precision.Bf16
 
     def out_width(self, x_in: torch.Tensor) -> int:
-        return x_in.shape[2] - self.p.dilation * (self.p.taps - 1)
+        return self.out_width_of(x_in.shape[2])
+
+    def out_width_of(self, w_in: int) -> int:
+        return w_in - self.p.dilation * (self.p.taps - 1)
 
     def forward(self, x_in: torch.Tensor, *, skip=None, act=None, act_bf16=None, act_pad=0, pre=None):
         """Glued forward (c1d_forward_glued): conv, bias, ReLU, skip, activation outputs."""
@@ -156,7 +187,7 @@ class ConvLayer:
                 self.mask = torch.empty(shape, dtype=torch.int32, device=x_in.device)
             mask = self.mask
         conv_forward_glued(x_in, self.w, self.p, bias=self.b, skip=skip, relu=self.relu, pre=pre, act=act,
-                           act_bf16=act_bf16, act_pad=act_pad, mask=mask)
+                           act_bf16=act_bf16, act_pad=act_pad, mask=mask, image=self.img.get(L.PASS_FORWARD))
 
     def backward_weight(self, grad_pre: torch.Tensor) -> None:
         cv.conv1d_backward_weight(grad_pre, self.x_in, self.p, out=self.grad_w)
@@ -167,7 +198,8 @@ class ConvLayer:
         the padded input gradient)."""
         conv_backward_data_glued(dy, self.w, self.p, self.pad, q,
                                  mask=target.mask if target is not None and target.relu else None,
-                                 bias_grad=target.grad_b if target is not None else None, **glue)
+                                 bias_grad=target.grad_b if target is not None else None,
+                                 image=self.img.get(L.PASS_BACKWARD_DATA), **glue)
 
     def parameters(self):
         return [self.w, self.b]
@@ -276,9 +308,36 @@ class ResidualNet:
         return nin
 
     # ---------------------------------------------------------------- forward / backward
+    def _pack_images(self, n: int, w_first: int) -> None:
+        """One c1d_pack_weights launch for the step: every BF16 conv's forward image and every body
+        conv's backward-data image (the weights changed at the last SGD step). The glued passes then
+        skip their own pack launches and load their images while the previous kernel runs."""
+        if os.environ.get("C1D_NET_NO_PREPACK"):  # dev A/B switch
+            for layer in self.layers():
+                layer.img = {}
+            return
+        jobs = []
+        width = self.input.out_width_of(w_first)
+        chain = [(self.input, w_first, False)] + [(layer, width + 2 * layer.pad, True)
+                                                  for blk in self.blocks for layer in blk]
+        for layer, w_in, bwd in chain:
+            if not layer.bf16:
+                continue
+            for pass_ in ((L.PASS_FORWARD, L.PASS_BACKWARD_DATA) if bwd else (L.PASS_FORWARD,)):
+                img = layer.img.get(pass_)
+                if img is None:
+                    nb = packed_weights_bytes(layer.p, n, w_in, pass_)
+                    if nb == 0:
+                        continue
+                    img = torch.empty(nb, dtype=torch.uint8, device=layer.w.device)
+                    layer.img[pass_] = img
+                jobs.append((layer.p, n, w_in, pass_, layer.w, img))
+        pack_weights(jobs)
+
     def forward(self, x_padded: torch.Tensor):
         n = x_padded.shape[0]
         first = self.input
+        self._pack_images(n, x_padded.shape[2])
         x0 = cv.round_bf16(x_padded) if first.bf16 else x_padded.float().contiguous()
         width = first.out_width(x0)
         h = self._buf("h.in", (n, first.p.filters, width), torch.float32)  # block input (skip source)
