@@ -71,8 +71,7 @@ constexpr int kLossThreads = 256;
 __global__ void __launch_bounds__(kLossThreads) mse_bce_kernel(
     const float* __restrict__ pred, const float* __restrict__ logits, int64_t in_stride,
     const float* __restrict__ target, const float* __restrict__ labels, int64_t n, int64_t width, float bce_weight,
-    float* __restrict__ grad_pred, float* __restrict__ grad_logits, int64_t grad_stride, double* __restrict__ part,
-    unsigned int* __restrict__ ticket, double* __restrict__ loss3) {
+    float* __restrict__ grad_pred, float* __restrict__ grad_logits, int64_t grad_stride, double* __restrict__ part) {
     const int64_t count = n * width;
     const double inv = 1.0 / static_cast<double>(count);
     const int64_t per = (count + gridDim.x - 1) / gridDim.x;
@@ -112,22 +111,24 @@ __global__ void __launch_bounds__(kLossThreads) mse_bce_kernel(
         }
         __syncthreads();
     }
-    __shared__ bool last;
     if (threadIdx.x == 0) {
         part[2 * blockIdx.x] = sm[0][0];
         part[2 * blockIdx.x + 1] = sm[1][0];
-        __threadfence();
-        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    // the last block sums the block partials: thread t takes partials t, t + 256, ... in order, then
-    // the same fixed tree as above (a fixed shape, so the loss is deterministic)
+}
+
+// The block partials summed in a fixed shape (thread t takes partials t, t + 256, ... in order, then
+// a tree), so the loss is deterministic. A second launch instead of a last-block ticket: the ticket
+// needed a per-call memset node, which cost ~14 us in the graph-replayed network step.
+__global__ void __launch_bounds__(kLossThreads) mse_bce_final_kernel(const double* __restrict__ part, int nblocks,
+                                                                     int64_t count, float bce_weight,
+                                                                     double* __restrict__ loss3) {
+    __shared__ double sm[2][kLossThreads];
+    const double inv = 1.0 / static_cast<double>(count);
     double a = 0.0, b = 0.0;
-    for (unsigned int j = threadIdx.x; j < gridDim.x; j += kLossThreads) {
-        a += __ldcg(part + 2 * j);
-        b += __ldcg(part + 2 * j + 1);
+    for (int j = threadIdx.x; j < nblocks; j += kLossThreads) {
+        a += part[2 * j];
+        b += part[2 * j + 1];
     }
     sm[0][threadIdx.x] = a;
     sm[1][threadIdx.x] = b;
@@ -144,7 +145,6 @@ __global__ void __launch_bounds__(kLossThreads) mse_bce_kernel(
         loss3[0] = ta * inv;
         loss3[1] = tb * inv;
         loss3[2] = ta * inv + static_cast<double>(bce_weight) * (tb * inv);
-        *ticket = 0;  // ready for the next call (and for CUDA-graph replays)
     }
 }
 
@@ -218,13 +218,11 @@ c1d_status c1d_mse_bce_loss(const float* pred, const float* logits, int64_t in_s
     const int64_t count = n * width;
     const int blocks = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(1024, (count + 4095) / 4096)));
     double* part = static_cast<double*>(workspace);
-    unsigned int* ticket = reinterpret_cast<unsigned int*>(static_cast<char*>(workspace) + 2 * sizeof(double) * 2 * 1024);
-    if (cudaMemsetAsync(ticket, 0, sizeof(unsigned int), reinterpret_cast<cudaStream_t>(stream)) != cudaSuccess)
-        return C1D_ERR_CUDA;
     mse_bce_kernel<<<blocks, kLossThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-        pred, logits, in_stride, target, labels, n, width, bce_weight, grad_pred, grad_logits, grad_stride, part, ticket,
-        loss3);
-    note_launch(1);
+        pred, logits, in_stride, target, labels, n, width, bce_weight, grad_pred, grad_logits, grad_stride, part);
+    mse_bce_final_kernel<<<1, kLossThreads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(part, blocks, count,
+                                                                                      bce_weight, loss3);
+    note_launch(2);
     return cudaGetLastError() == cudaSuccess ? C1D_OK : C1D_ERR_CUDA;
 }
 
