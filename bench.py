@@ -719,14 +719,14 @@ def spawn_ranks(n: int) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=20)  # the reference measure_kernel's 20 iterations (bench.hpp:31)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
     ap.add_argument("--no-narrow", action="store_true")
     ap.add_argument("--no-network", action="store_true")
-    ap.add_argument("--network-steps", type=int, default=50)
+    ap.add_argument("--network-steps", type=int, default=20)
     ap.add_argument("--workload", default="layer", choices=["layer", "network"])
     ap.add_argument("--e2e-chunks", type=int, default=8, help="item chunks of the pipelined host-buffer e2e step")
     ap.add_argument("--no-graph", action="store_true", help="network: launch the local step eagerly (no CUDA graph)")
