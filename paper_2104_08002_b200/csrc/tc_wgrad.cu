@@ -428,11 +428,18 @@ bool make_w2plan(int64_t n, int64_t c, int64_t k, int64_t s, int64_t d, int64_t 
     p.grid = assigned;
     if (p.grid > kW2MaxGrid) return false;
     p.box_bytes = static_cast<uint32_t>(p.kpw * 2 * p.bq);
-    // Accumulator copies: MMAs into one accumulator serialise on a ~128-cycle chain, so when a
-    // K-step's MMAs (gpc x N/2 cycles) are shorter than that, consecutive K-steps rotate over R
-    // copies (summed by the epilogue).
+    // Accumulator copies (consecutive K-steps rotating over R accumulators, summed by the drain) were
+    // added against a supposed ~128-cycle same-accumulator chain; that was the issuing thread, and
+    // with straight-line issue one accumulator runs as fast (C = K = 15, batch 64: copies 4 / 2 / 1
+    // = 106.5 / 105.5 / 104.5 us, the drain 9.2k -> 6.7k cycles), so the default is one copy.
+    static const int copies_cap = [] {  // C1D_W2_COPIES: dev override of the copy cap
+        const char* e = getenv("C1D_W2_COPIES");
+        const int v = e ? atoi(e) : 1;
+        return v == 1 || v == 2 || v == 4 ? v : 1;
+    }();
     p.copies = 1;
-    while (p.copies < 4 && p.gpc * p.n * p.copies < 256 && p.gpc * p.n * p.copies * 2 <= static_cast<int>(kTmemCols))
+    while (p.copies < copies_cap && p.gpc * p.n * p.copies < 256 &&
+           p.gpc * p.n * p.copies * 2 <= static_cast<int>(kTmemCols))
         p.copies *= 2;
     // X lives in a ring: every stage loads only its new chunks; the window's tap span is reused.
     // Safety (a stage slot is refilled only after that slot's MMAs completed):
