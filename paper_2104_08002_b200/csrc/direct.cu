@@ -927,6 +927,9 @@ __global__ void __launch_bounds__(256) small_wgrad_kernel(const TIn* __restrict_
 // dw[k][c] = sum_{n,x} dy[n][k][x] x[n][c][x]. Block (bx, n) owns 1024 columns of item n; each
 // thread keeps all K*C sums for its 4 columns, then a fixed-shape tree makes one partial per block
 // and output, and a block per output sums the partials in a fixed pattern (deterministic).
+// Each thread accumulates kPwGroups column groups of 4 (the block covers kPwGroups x 1024 columns)
+// before the K x C warp reductions, which cost more instructions than the loads of one group.
+constexpr int kPwGroups = 4;
 template <typename TIn, int KMAX, int CMAX>
 __global__ void __launch_bounds__(kPwThreads) pointwise_wgrad_kernel(const TIn* __restrict__ x,
                                                                      const TIn* __restrict__ dy,
@@ -934,34 +937,43 @@ __global__ void __launch_bounds__(kPwThreads) pointwise_wgrad_kernel(const TIn* 
                                                                      int64_t Q, int round_in, int vec) {
     __shared__ float red[kPwThreads / 32][KMAX * CMAX];
     const int64_t n = blockIdx.y;
-    const int64_t x0 = static_cast<int64_t>(blockIdx.x) * kPwCols + threadIdx.x * 4;
-    const int cnt = static_cast<int>(x0 < Q ? (Q - x0 < 4 ? Q - x0 : 4) : 0);
     float acc[KMAX][CMAX];
 #pragma unroll
     for (int kk = 0; kk < KMAX; ++kk)
 #pragma unroll
         for (int cc = 0; cc < CMAX; ++cc) acc[kk][cc] = 0.0f;
-    float gv[KMAX][4];
+    for (int grp = 0; grp < kPwGroups; ++grp) {
+        const int64_t x0 = (static_cast<int64_t>(blockIdx.x) * kPwGroups + grp) * kPwCols + threadIdx.x * 4;
+        const int cnt = static_cast<int>(x0 < Q ? (Q - x0 < 4 ? Q - x0 : 4) : 0);
+        if (cnt == 0) break;
+        const bool v4 = vec && cnt == 4;
+        float gv[KMAX][4];
 #pragma unroll
-    for (int kk = 0; kk < KMAX; ++kk)
+        for (int kk = 0; kk < KMAX; ++kk) {
+            if (v4 && kk < K) {
+                load4_as_float(dy, (n * K + kk) * Q + x0, round_in != 0, gv[kk]);
+            } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            gv[kk][j] = (kk < K && j < cnt) ? load_as_float(dy, (n * K + kk) * Q + x0 + j, round_in != 0) : 0.0f;
-    const bool v4 = vec && cnt == 4;
-#pragma unroll
-    for (int cc = 0; cc < CMAX; ++cc) {
-        if (cc >= C) break;
-        float xv[4];
-        if (v4) {
-            load4_as_float(x, (n * C + cc) * Q + x0, round_in != 0, xv);
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) xv[j] = j < cnt ? load_as_float(x, (n * C + cc) * Q + x0 + j, round_in != 0) : 0.0f;
+                for (int j = 0; j < 4; ++j)
+                    gv[kk][j] = (kk < K && j < cnt) ? load_as_float(dy, (n * K + kk) * Q + x0 + j, round_in != 0) : 0.0f;
+            }
         }
 #pragma unroll
-        for (int kk = 0; kk < KMAX; ++kk)
+        for (int cc = 0; cc < CMAX; ++cc) {
+            if (cc >= C) break;
+            float xv[4];
+            if (v4) {
+                load4_as_float(x, (n * C + cc) * Q + x0, round_in != 0, xv);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[kk][cc] = fmaf(gv[kk][j], xv[j], acc[kk][cc]);
+                for (int j = 0; j < 4; ++j)
+                    xv[j] = j < cnt ? load_as_float(x, (n * C + cc) * Q + x0 + j, round_in != 0) : 0.0f;
+            }
+#pragma unroll
+            for (int kk = 0; kk < KMAX; ++kk)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[kk][cc] = fmaf(gv[kk][j], xv[j], acc[kk][cc]);
+        }
     }
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
 #pragma unroll
@@ -1011,9 +1023,10 @@ static bool pointwise_wgrad_ok(int64_t n, int64_t c, int64_t k, int64_t s) {
 template <typename TIn>
 static cudaError_t launch_pointwise_wgrad(const TIn* x, const TIn* dy, float* dw, float* part, int64_t n, int64_t c,
                                           int64_t k, int64_t q, int round_in, cudaStream_t stream) {
-    const dim3 grid(static_cast<unsigned>(ceil_div(q, kPwCols)), static_cast<unsigned>(n));
+    const dim3 grid(static_cast<unsigned>(ceil_div(q, kPwCols * kPwGroups)), static_cast<unsigned>(n));
     const uintptr_t al = sizeof(TIn) == 4 ? 15u : 7u;
-    const int vec = q % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & al) == 0;  // vector loads of x rows
+    const int vec = q % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & al) == 0 &&
+                    (reinterpret_cast<uintptr_t>(dy) & al) == 0;  // vector loads of x and dy rows
     if (k <= 2 && c <= 16)
         pointwise_wgrad_kernel<TIn, 2, 16><<<grid, kPwThreads, 0, stream>>>(x, dy, part, c, k, q, round_in, vec);
     else if (c <= 16)
