@@ -491,12 +491,11 @@ __device__ __forceinline__ void st_shared_bf16_pair(uint32_t a, uint32_t pk) {
                  "r"(pk)
                  : "memory");
 }
-__device__ __forceinline__ void glue_tma_store(const KParams& p, uint32_t& sbuf, uint32_t wbase, int lane,
-                                               const float (&va)[16], const float (&vb)[16],
+__device__ __forceinline__ void glue_tma_store(const KParams& p, const uint32_t slots, uint32_t& sbuf, uint32_t wbase,
+                                               int lane, const float (&va)[16], const float (&vb)[16],
                                                const uint32_t (&pc)[8], const CUtensorMap* m0,
                                                const CUtensorMap* m1, const CUtensorMap* m2, int32_t col,
                                                int32_t col_c, int32_t row, int32_t item) {
-    const uint32_t slots = p.tma_slots;
     const uint32_t b = wbase + sbuf * p.stg_bytes;
     if (lane == 0) bulk_wait_read<1>();
     __syncwarp();
@@ -588,17 +587,34 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
 }
 
 // forward glue for rows k0 .. k0+15 of column q; bias16 = those rows' bias (0 past the channel count)
+// kFx: 0 = the glue's outputs from its runtime flags; 1-3 = the config-5 network's layer shapes with
+// the flags fixed at compile time (no per-block flag loads / branches in the issue-bound glue):
+//   1: bias, ReLU, mask, BF16 activation (TMA slot 4)       -- body layers
+//   2: + skip add and FP32 activation (slots 2 | 4)          -- block-output layers
+//   3: bias, ReLU, mask, FP32 + BF16 activation, no skip    -- the input layer
+template <int kFx>
+struct FwdFx {
+    static constexpr bool kRelu = true, kMask = true, kBf16 = true;
+    static constexpr bool kSkip = kFx == 2;
+    static constexpr uint32_t kSlots = kFx == 1 ? 4u : 6u;  // slot 2 = the FP32 activation (kFx 2, 3)
+};
+template <int kFx>
 __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t (&v)[16], int64_t n, int64_t q,
                                                int64_t k0, int lane, const float (&bias16)[16], uint32_t& sbuf,
                                                uint32_t wbase, const CUtensorMap* m0, const CUtensorMap* m1,
                                                const CUtensorMap* m2, uint32_t pf_slot) {
     const LayerGlue& gl = p.glue;
+    using F = FwdFx<kFx>;
     const int64_t out_w = p.out_w;
     const bool qv = q < out_w;
     const int kvalid = static_cast<int>(imin64(16, p.out_ch - k0));
     const int64_t row0 = n * p.out_ch + k0;
     float x[16], a[16];
-    const bool relu = gl.relu != 0;
+    const bool relu = kFx ? F::kRelu : gl.relu != 0;
+    const bool has_mask = kFx ? F::kMask : gl.mask_out != nullptr;
+    const bool has_skip = kFx ? F::kSkip : gl.skip != nullptr;
+    const bool has_bf16 = kFx ? F::kBf16 : gl.act_bf16 != nullptr;
+    const uint32_t slots = kFx ? F::kSlots : p.tma_slots;
 #pragma unroll
     for (int jj = 0; jj < 16; ++jj) {
         x[jj] = __uint_as_float(v[jj]) + bias16[jj];
@@ -608,7 +624,7 @@ __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t 
     // so bit = (bits(a) != 0) = (bits(a) + 0x7fffffff) >> 31, accumulated MSB-first; the float
     // compare form compiled to ~100 predicate-juggling instructions per block
     uint32_t mword = 0;
-    if (gl.mask_out) {
+    if (has_mask) {
         if (relu) {
 #pragma unroll
             for (int jj = 15; jj >= 0; --jj) mword = (mword << 1) | ((__float_as_uint(a[jj]) + 0x7fffffffu) >> 31);
@@ -617,19 +633,19 @@ __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t 
             for (int jj = 0; jj < 16; ++jj) mword |= (x[jj] > 0.0f ? 1u : 0u) << jj;
         }
     }
-    if (gl.skip) {  // prefetched rows (zero outside the tensor)
+    if (has_skip) {  // prefetched rows (zero outside the tensor)
         const uint32_t src = pf_slot + static_cast<uint32_t>(lane) * 4u;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) a[jj] += ld_shared_f32(src + jj * 128);
     }
-    if (gl.mask_out) {  // one word per column and 16-channel block: bit jj = row k0 + jj
+    if (has_mask) {  // one word per column and 16-channel block: bit jj = row k0 + jj
         const int64_t kblocks = (p.out_ch + 15) >> 4;
         if (qv && kvalid > 0) gl.mask_out[(n * kblocks + (k0 >> 4)) * out_w + q] = mword;
     }
     uint32_t pc[8];
-    if (gl.act_bf16) pack_bf16_rows(a, pc);
-    if (p.tma_slots) {
-        glue_tma_store(p, sbuf, wbase, lane, x, a, pc, m0, m1, m2, static_cast<int32_t>(q - lane),
+    if (has_bf16) pack_bf16_rows(a, pc);
+    if (slots) {
+        glue_tma_store(p, slots, sbuf, wbase, lane, x, a, pc, m0, m1, m2, static_cast<int32_t>(q - lane),
                        static_cast<int32_t>(gl.act_off + q - lane), static_cast<int32_t>(k0), static_cast<int32_t>(n));
         return;
     }
@@ -662,23 +678,32 @@ __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t 
 }
 
 // backward glue for rows k0 .. k0+15 of padded column x (the glued layer's column xi = x - g_off)
+// kFx: 0 = runtime flags; 1 = ReLU mask + BF16 gradient + bias gradient, per-lane stores (body
+// layers); 2 = 1 + skip gradient added (gadd) and the sum stored (gsum) (block-input layers)
+template <int kFx>
 __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t (&v)[16], int64_t n, int64_t x,
                                                 int64_t k0, int lane, float (&bs)[16], uint32_t& sbuf,
                                                 uint32_t wbase, const CUtensorMap* m0, const CUtensorMap* m1,
                                                 const CUtensorMap* m2, uint32_t pf_slot) {
     const LayerGlue& gl = p.glue;
+    const bool has_mask = kFx ? true : gl.mask_in != nullptr;
+    const bool has_gadd = kFx ? kFx == 2 : gl.gadd != nullptr;
+    const bool has_gsum = kFx ? kFx == 2 : gl.gsum != nullptr;
+    const bool has_gp = kFx ? false : gl.gp != nullptr;
+    const bool has_gpb = kFx ? true : gl.gp_bf16 != nullptr;
+    const uint32_t slots = kFx ? 0u : p.tma_slots;
     const int64_t gq = gl.g_q;
     const int64_t xi = x - gl.g_off;
     const bool xv = xi >= 0 && xi < gq;
     const int kvalid = static_cast<int>(imin64(16, p.out_ch - k0));
     const int64_t row0 = n * p.out_ch + k0;
     // ReLU mask: this column's word for the 16-row block (prefetched; bit jj = row k0 + jj)
-    const uint32_t mword = gl.mask_in ? ld_shared_u32(pf_slot + (p.pf_rows ? 2048u : 0u) + static_cast<uint32_t>(lane) * 4u)
-                                      : 0xffffu;
+    const uint32_t mword = has_mask ? ld_shared_u32(pf_slot + (has_gadd ? 2048u : 0u) + static_cast<uint32_t>(lane) * 4u)
+                                    : 0xffffu;
     float g[16];
 #pragma unroll
     for (int jj = 0; jj < 16; ++jj) g[jj] = __uint_as_float(v[jj]);
-    if (gl.gadd) {  // prefetched rows (zero outside the window)
+    if (has_gadd) {  // prefetched rows (zero outside the window)
         const uint32_t src = pf_slot + static_cast<uint32_t>(lane) * 4u;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) g[jj] += ld_shared_f32(src + jj * 128);
@@ -692,18 +717,18 @@ __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t
             if (jj < kvalid) bs[jj] += gp[jj];
     }
     uint32_t pc[8];
-    if (gl.gp_bf16) pack_bf16_rows(gp, pc);
+    if (has_gpb) pack_bf16_rows(gp, pc);
     // TMA stores need a non-negative start column: the warp straddling the glued window's left
     // edge (once per item) takes the per-lane path
     const int64_t col = xi - lane;
-    if (p.tma_slots && col >= 0) {
-        glue_tma_store(p, sbuf, wbase, lane, g, gp, pc, m0, m1, m2, static_cast<int32_t>(col),
+    if (slots && col >= 0) {
+        glue_tma_store(p, slots, sbuf, wbase, lane, g, gp, pc, m0, m1, m2, static_cast<int32_t>(col),
                        static_cast<int32_t>(col), static_cast<int32_t>(k0), static_cast<int32_t>(n));
         return;
     }
     if (!xv) return;
     const int64_t e = row0 * gq + xi;
-    if (gl.gsum) {
+    if (has_gsum) {
         float* d = gl.gsum + e;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
@@ -711,7 +736,7 @@ __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t
             d += gq;
         }
     }
-    if (gl.gp) {
+    if (has_gp) {
         float* d = gl.gp + e;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
@@ -719,7 +744,7 @@ __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t
             d += gq;
         }
     }
-    if (gl.gp_bf16) {
+    if (has_gpb) {
         uint16_t* d = gl.gp_bf16 + e;
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
@@ -813,7 +838,7 @@ __device__ __forceinline__ void issue_channels(const IssueArgs& ia) {
 // blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
 // mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
 // and TMA warps, and an all-modes kernel (~30k instructions) ran the epilogue 6x slower.
-template <int kMode, int kKPB, int kEG = 1>
+template <int kMode, int kKPB, int kEG = 1, int kFx = 0>
 __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
                    const __grid_constant__ CUtensorMap om0, const __grid_constant__ CUtensorMap om1,
@@ -1376,7 +1401,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                             for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(v2[jj]));
                         }
                         const uint32_t slot = pf_take();
-                        glue_forward16(p, v, su.n, q, p.k_begin + kbi * 16, lane, bias_r[kbi], sbuf, wbase, &om0,
+                        glue_forward16<kFx>(p, v, su.n, q, p.k_begin + kbi * 16, lane, bias_r[kbi], sbuf, wbase, &om0,
                                        &om1, &om2, slot);
                     }
                 }
@@ -1398,7 +1423,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                             for (int jj = 0; jj < 16; ++jj) v[jj] = __float_as_uint(__uint_as_float(v[jj]) + __uint_as_float(v2[jj]));
                         }
                         const uint32_t slot = pf_take();
-                        glue_backward16(p, v, su.n, q, p.k_begin + kbi * 16, lane, bsum[kbi], sbuf, wbase, &om0,
+                        glue_backward16<kFx>(p, v, su.n, q, p.k_begin + kbi * 16, lane, bsum[kbi], sbuf, wbase, &om0,
                                         &om1, &om2, slot);
                     }
                 }
@@ -1738,6 +1763,20 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     if (mode == 2)
         kernel = pl.kp == 16 ? (eg == 2 ? tc_conv_kernel<2, 1, 2> : tc_conv_kernel<2, 1, 1>)
                : (pl.kp == 32 ? (eg == 2 ? tc_conv_kernel<2, 2, 2> : tc_conv_kernel<2, 2, 1>) : tc_conv_kernel<2, 4, 1>);
+    // the network's layer shapes with their glue flags fixed at compile time (glue_forward16 /
+    // glue_backward16 kFx): narrow filter blocks, two epilogue groups
+    static const bool no_fx = getenv("C1D_NO_GLUE_FX") != nullptr;  // dev A/B switch
+    if (mode != 0 && pl.kp == 16 && eg == 2 && !no_fx) {
+        const LayerGlue& gl = *glue;
+        if (mode == 1 && gl.relu && gl.mask_out && gl.act_bf16 && !gl.pre) {
+            if (!gl.skip && !gl.act && gm.slots == 4u) kernel = tc_conv_kernel<1, 1, 2, 1>;
+            else if (gl.skip && gl.act && gm.slots == 6u) kernel = tc_conv_kernel<1, 1, 2, 2>;
+            else if (!gl.skip && gl.act && gm.slots == 6u) kernel = tc_conv_kernel<1, 1, 2, 3>;
+        } else if (mode == 2 && gl.mask_in && gl.gp_bf16 && !gl.gp && gm.slots == 0u) {
+            if (!gl.gadd && !gl.gsum) kernel = tc_conv_kernel<2, 1, 2, 1>;
+            else if (gl.gadd && gl.gsum) kernel = tc_conv_kernel<2, 1, 2, 2>;
+        }
+    }
     const int threads = 128 + 128 * eg;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
