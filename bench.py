@@ -456,6 +456,7 @@ def measure_network(world, rank, local, dev, steps, warmup, use_graph=True):
     e1.record(stream)
     torch.cuda.synchronize()
     launches = lib.c1d_launch_count() - l0
+    loss_timed = float(loss)  # the graph's loss buffer is overwritten by the e2e replays below
     if launches_per_local is not None:  # graph replays launch without the host counter
         launches = launches_per_local * steps
     barrier(world)
@@ -517,7 +518,7 @@ def measure_network(world, rank, local, dev, steps, warmup, use_graph=True):
                    "global_batch": global_batch, "per_gpu_batch": per, "width": width,
                    "parallelism": f"dp{world} (one all-reduce of the 173,162-float gradient bucket per step)",
                    "flops_per_step": flops_job, "params": net.num_parameters()},
-        "loss": float(loss),
+        "loss": loss_timed,
         "e2e": {"value": flops_job / (te * 1e-3) / 1e12, "unit": "TFLOP/s",
                 "h2d_bytes_per_step": (hx.numel() + ht.numel() + hl.numel()) * 4, "d2h_bytes_per_step": 8,
                 "ms_per_step": te,

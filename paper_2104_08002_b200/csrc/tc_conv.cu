@@ -592,11 +592,12 @@ __device__ __forceinline__ uint32_t ld_shared_u32(uint32_t a) {
 //   1: bias, ReLU, mask, BF16 activation (TMA slot 4)       -- body layers
 //   2: + skip add and FP32 activation (slots 2 | 4)          -- block-output layers
 //   3: bias, ReLU, mask, FP32 + BF16 activation, no skip    -- the input layer
+//   4: bias, ReLU, mask, skip, FP32 activation only         -- the last block's output (heads input)
 template <int kFx>
 struct FwdFx {
-    static constexpr bool kRelu = true, kMask = true, kBf16 = true;
-    static constexpr bool kSkip = kFx == 2;
-    static constexpr uint32_t kSlots = kFx == 1 ? 4u : 6u;  // slot 2 = the FP32 activation (kFx 2, 3)
+    static constexpr bool kRelu = true, kMask = true, kBf16 = kFx != 4;
+    static constexpr bool kSkip = kFx == 2 || kFx == 4;
+    static constexpr uint32_t kSlots = kFx == 1 ? 4u : (kFx == 4 ? 2u : 6u);  // slot 2: the FP32 activation
 };
 template <int kFx>
 __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t (&v)[16], int64_t n, int64_t q,
@@ -679,7 +680,8 @@ __device__ __forceinline__ void glue_forward16(const KParams& p, const uint32_t 
 
 // backward glue for rows k0 .. k0+15 of padded column x (the glued layer's column xi = x - g_off)
 // kFx: 0 = runtime flags; 1 = ReLU mask + BF16 gradient + bias gradient, per-lane stores (body
-// layers); 2 = 1 + skip gradient added (gadd) and the sum stored (gsum) (block-input layers)
+// layers); 2 = 1 + skip gradient added (gadd) and the sum stored (gsum) (block-input layers);
+// 3 = 1 + gadd without gsum (the first block's input layer)
 template <int kFx>
 __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t (&v)[16], int64_t n, int64_t x,
                                                 int64_t k0, int lane, float (&bs)[16], uint32_t& sbuf,
@@ -687,7 +689,7 @@ __device__ __forceinline__ void glue_backward16(const KParams& p, const uint32_t
                                                 const CUtensorMap* m2, uint32_t pf_slot) {
     const LayerGlue& gl = p.glue;
     const bool has_mask = kFx ? true : gl.mask_in != nullptr;
-    const bool has_gadd = kFx ? kFx == 2 : gl.gadd != nullptr;
+    const bool has_gadd = kFx ? kFx >= 2 : gl.gadd != nullptr;
     const bool has_gsum = kFx ? kFx == 2 : gl.gsum != nullptr;
     const bool has_gp = kFx ? false : gl.gp != nullptr;
     const bool has_gpb = kFx ? true : gl.gp_bf16 != nullptr;
@@ -1772,9 +1774,13 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
             if (!gl.skip && !gl.act && gm.slots == 4u) kernel = tc_conv_kernel<1, 1, 2, 1>;
             else if (gl.skip && gl.act && gm.slots == 6u) kernel = tc_conv_kernel<1, 1, 2, 2>;
             else if (!gl.skip && gl.act && gm.slots == 6u) kernel = tc_conv_kernel<1, 1, 2, 3>;
+        } else if (mode == 1 && gl.relu && gl.mask_out && !gl.act_bf16 && !gl.pre && gl.skip && gl.act &&
+                   gm.slots == 2u) {
+            kernel = tc_conv_kernel<1, 1, 2, 4>;
         } else if (mode == 2 && gl.mask_in && gl.gp_bf16 && !gl.gp && gm.slots == 0u) {
             if (!gl.gadd && !gl.gsum) kernel = tc_conv_kernel<2, 1, 2, 1>;
             else if (gl.gadd && gl.gsum) kernel = tc_conv_kernel<2, 1, 2, 2>;
+            else if (gl.gadd && !gl.gsum) kernel = tc_conv_kernel<2, 1, 2, 3>;
         }
     }
     const int threads = 128 + 128 * eg;
