@@ -822,6 +822,17 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
         step([&] { return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, pat_x[pass], stream); });
         step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[pass], stream); });
     };
+    // both split passes' operands from one read of x and one of dy (pass 1's into x2b / g2b)
+    auto split_both = [&](uint16_t* x2b, uint16_t* g2b) {
+        step([&] {
+            return launch_split_channels(static_cast<const float*>(x), x2, d.n, d.c, d.w_in, 2, pat_x[0], stream, 0, 0,
+                                         x2b, pat_x[1]);
+        });
+        step([&] {
+            return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[0], stream, 0, 0, g2b,
+                                         pat_g[1]);
+        });
+    };
     const c1d_desc d2 = split_wgrad_desc(d);
     if (split_wgrad_xt_ok(d, q)) {
         // channel-octet streams of the split x, one launch per split pass
@@ -829,10 +840,14 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
         uint16_t* xt = bump.take<uint16_t>(sizeof(uint16_t) * 8 * static_cast<size_t>(d.n * ((d2.c + 7) / 8) * rows));
         float* dw4[2] = {bump.take<float>(4 * sizeof(float) * kcs), bump.take<float>(4 * sizeof(float) * kcs)};
         void* kws = bump.take<char>(tc_wgrad_xt_workspace_bytes(d.n, d2.c, d2.k, d.s, d.d, q));
+        uint16_t* x2b = bump.take<uint16_t>(sizeof(uint16_t) * nx);
+        uint16_t* g2b = bump.take<uint16_t>(sizeof(uint16_t) * ng);
+        split_both(x2b, g2b);
+        const uint16_t* xsrc[2] = {x2, x2b};
+        const uint16_t* gsrc[2] = {g2, g2b};
         for (int ps = 0; ps < 2; ++ps) {
-            split_pass(ps);
-            step([&] { return launch_to_octets(x2, C1D_DTYPE_BF16, xt, d.n, d2.c, d.w_in, rows, stream); });
-            step([&] { return launch_tc_wgrad_xt(xt, rows, g2, dw4[ps], kws, d.n, d2.c, d2.k, d.s, d.d, q, stream); });
+            step([&] { return launch_to_octets(xsrc[ps], C1D_DTYPE_BF16, xt, d.n, d2.c, d.w_in, rows, stream); });
+            step([&] { return launch_tc_wgrad_xt(xt, rows, gsrc[ps], dw4[ps], kws, d.n, d2.c, d2.k, d.s, d.d, q, stream); });
         }
         step([&] { return launch_sum_split3(dw4[0], dw4[1], dw, d.k, d.c, d.s, stream); });
         return e;
@@ -865,8 +880,10 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
             kb = std::max(kb, tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, ceil_div(d.s - b, dp.m), 8, q));
         void* kws = bump.take<char>(kb);
         // both splits of dy once; x's two splits are re-shifted per phase
-        step([&] { return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[0], stream); });
-        step([&] { return launch_split_channels(static_cast<const float*>(dy), g2b, d.n, d.k, q, 2, pat_g[1], stream); });
+        step([&] {
+            return launch_split_channels(static_cast<const float*>(dy), g2, d.n, d.k, q, 2, pat_g[0], stream, 0, 0, g2b,
+                                         pat_g[1]);
+        });
         const uint16_t* gsrc[2] = {g2, g2b};
         for (int64_t b = 0; b < dp.p; ++b) {
             const int64_t sb = ceil_div(d.s - b, dp.m);
@@ -894,11 +911,14 @@ cudaError_t split_wgrad_run(const c1d_desc& d, int64_t q, const void* x, const v
             step([&] { return launch_tc_wgrad(px, pg, dw4[ps], kws, d.n * dp.m, 2 * d.c, 2 * d.k, d.s, 8, q / dp.m, stream); });
         }
     } else {
+        uint16_t* x2b = bump.take<uint16_t>(sizeof(uint16_t) * nx);
+        uint16_t* g2b = bump.take<uint16_t>(sizeof(uint16_t) * ng);
         void* kws = bump.take<char>(tc_wgrad_workspace_bytes(d.n, 2 * d.c, 2 * d.k, d.s, 8, q));
-        for (int ps = 0; ps < 2; ++ps) {
-            split_pass(ps);
-            step([&] { return launch_tc_wgrad(x2, g2, dw4[ps], kws, d.n, 2 * d.c, 2 * d.k, d.s, 8, q, stream); });
-        }
+        split_both(x2b, g2b);
+        const uint16_t* xsrc[2] = {x2, x2b};
+        const uint16_t* gsrc[2] = {g2, g2b};
+        for (int ps = 0; ps < 2; ++ps)
+            step([&] { return launch_tc_wgrad(xsrc[ps], gsrc[ps], dw4[ps], kws, d.n, 2 * d.c, 2 * d.k, d.s, 8, q, stream); });
     }
     step([&] { return launch_sum_split3(dw4[0], dw4[1], dw, d.k, d.c, d.s, stream); });
     return e;

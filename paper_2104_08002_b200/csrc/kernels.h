@@ -194,7 +194,7 @@ int64_t tc_conv_xr_rows(const ConvGeom& g);
 // item (a channel subset of a wider tensor), default c * w
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
                                   unsigned pattern, cudaStream_t stream, int64_t w_pitch = 0,
-                                  int64_t in_item_stride = 0);
+                                  int64_t in_item_stride = 0, uint16_t* out2 = nullptr, unsigned pattern2 = 0);
 cudaError_t launch_add_into(float* out, const float* add, int64_t count, cudaStream_t stream);
 cudaError_t launch_split_weights(const float* w, float* out, int64_t K, int64_t C, int64_t S, int kr, int cr,
                                  unsigned sel, cudaStream_t stream);

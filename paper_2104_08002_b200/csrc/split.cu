@@ -34,9 +34,11 @@ namespace c1d {
 // split) for b < R. One row (item, channel) per blockIdx.y step; each thread splits 8 consecutive
 // columns and writes them as one 16-B store per block when wp is a multiple of 8 (output rows then
 // 16-B aligned); rows whose input start is 16-B aligned read two float4s.
+// out2 / pattern2 (optional): a second set of `reps` levels from the same read (the FP32 backward-
+// weight's two split passes take different level patterns of the same x and dy)
 __global__ void split_channels_kernel(const float* __restrict__ in, uint16_t* __restrict__ out, int64_t n,
                                       int64_t c, int64_t w, int reps, unsigned pattern, int64_t wp,
-                                      int64_t in_item) {
+                                      int64_t in_item, uint16_t* __restrict__ out2, unsigned pattern2) {
     for (int64_t row = blockIdx.y; row < n * c; row += gridDim.y) {
         const int64_t item = row / c, ch = row - item * c;
         const float* src = in + item * in_item + ch * w;
@@ -69,16 +71,20 @@ __global__ void split_channels_kernel(const float* __restrict__ in, uint16_t* __
                 part[1][j] = static_cast<uint32_t>(m[0]) | (static_cast<uint32_t>(m[1]) << 16);
                 part[2][j] = static_cast<uint32_t>(l[0]) | (static_cast<uint32_t>(l[1]) << 16);
             }
-            for (int r = 0; r < reps; ++r) {
-                const unsigned sel = (pattern >> (2 * r)) & 3u;
-                const uint32_t* pv = part[sel > 2 ? 2 : sel];
-                uint16_t* dst = out + ((item * reps + r) * c + ch) * wp + x0;
-                if (vout) {
-                    *reinterpret_cast<uint4*>(dst) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
-                } else {  // unpadded odd-width rows: element stores
+            for (int set = 0; set < (out2 ? 2 : 1); ++set) {
+                uint16_t* const ob = set ? out2 : out;
+                const unsigned pat = set ? pattern2 : pattern;
+                for (int r = 0; r < reps; ++r) {
+                    const unsigned sel = (pat >> (2 * r)) & 3u;
+                    const uint32_t* pv = part[sel > 2 ? 2 : sel];
+                    uint16_t* dst = ob + ((item * reps + r) * c + ch) * wp + x0;
+                    if (vout && (!out2 || (reinterpret_cast<uintptr_t>(out2) & 15u) == 0)) {
+                        *reinterpret_cast<uint4*>(dst) = make_uint4(pv[0], pv[1], pv[2], pv[3]);
+                    } else {  // unpadded odd-width rows: element stores
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        if (x0 + j < wp) dst[j] = static_cast<uint16_t>(pv[j / 2] >> (16 * (j % 2)));
+                        for (int j = 0; j < 8; ++j)
+                            if (x0 + j < wp) dst[j] = static_cast<uint16_t>(pv[j / 2] >> (16 * (j % 2)));
+                    }
                 }
             }
         }
@@ -158,13 +164,14 @@ static unsigned blocks_for(int64_t total) {
 }
 
 cudaError_t launch_split_channels(const float* in, uint16_t* out, int64_t n, int64_t c, int64_t w, int reps,
-                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch, int64_t in_item_stride) {
+                                  unsigned pattern, cudaStream_t stream, int64_t w_pitch, int64_t in_item_stride,
+                                  uint16_t* out2, unsigned pattern2) {
     const int64_t wp = w_pitch > 0 ? w_pitch : w;
     const int64_t si = in_item_stride > 0 ? in_item_stride : c * w;
     const int64_t rows = n * c;
     const unsigned gx = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(wp, 8 * 256), 64)));
     const unsigned gy = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(rows, 65535)));
-    split_channels_kernel<<<dim3(gx, gy), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp, si);
+    split_channels_kernel<<<dim3(gx, gy), 256, 0, stream>>>(in, out, n, c, w, reps, pattern, wp, si, out2, pattern2);
     note_launch();
     return cudaGetLastError();
 }
