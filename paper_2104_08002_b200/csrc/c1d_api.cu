@@ -246,7 +246,7 @@ bool xr_inline_ok(const ConvGeom& g) {
 // input (measured, N = 16, Q = 20000: C = K = 128, S = 51 fwd 558 -> 499 us, S = 9 292 -> 181 us;
 // at K <= 64 the carry mode's N = 192-256 MMAs win: config 3 638 vs 938 us)
 bool native_direct(const ConvGeom& g, int64_t main_ch = 0) {
-    if (getenv("C1D_D8_CARRY") != nullptr) return false;  // dev A/B switch
+    if (dev_switch(DevSwitch::kD8Carry)) return false;  // dev A/B switch
     if (g.out_ch <= 64 && main_ch == 0) return false;
     // split FP32 (two TMEM regions): only when the carry mode would run tiny super-tiles (FP32
     // config 1, C = K = 15, keeps 8 tiles per super-tile in the carry mode: 99 vs 144 us)

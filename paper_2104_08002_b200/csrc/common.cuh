@@ -89,6 +89,16 @@ inline bool pdl_enabled() {
     return on;
 }
 
+// Dev A/B switches read by the planners: each environment variable is read once per process (the
+// planners run on every call, and getenv walks the environment).
+enum class DevSwitch { kNoWres, kNoDbuf, kNoTail, kNoWs, kD8Carry, kCount };
+inline bool dev_switch(DevSwitch s) {
+    static const bool on[static_cast<int>(DevSwitch::kCount)] = {
+        getenv("C1D_NO_WRES") != nullptr, getenv("C1D_NO_DBUF") != nullptr, getenv("C1D_NO_TAIL") != nullptr,
+        getenv("C1D_NO_WS") != nullptr, getenv("C1D_D8_CARRY") != nullptr};
+    return on[static_cast<int>(s)];
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                        Args&&... args) {

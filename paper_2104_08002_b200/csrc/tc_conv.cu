@@ -110,7 +110,7 @@ constexpr uint32_t kWresMax = 64 * 1024;
 
 // Resident-weight decision for a plan whose b_chan_bytes / cc are set (stages are sized afterwards)
 inline bool want_wres(const ConvGeom& g, uint32_t b_chan_bytes, bool allow) {
-    return allow && static_cast<uint64_t>(g.in_ch) * b_chan_bytes <= kWresMax && getenv("C1D_NO_WRES") == nullptr;
+    return allow && static_cast<uint64_t>(g.in_ch) * b_chan_bytes <= kWresMax && !dev_switch(DevSwitch::kNoWres);
 }
 inline void plan_wres(const ConvGeom& g, Plan* p, bool allow) {
     const uint64_t img = static_cast<uint64_t>(g.in_ch) * p->b_chan_bytes;
@@ -160,7 +160,7 @@ bool make_plan_xr(const ConvGeom& g, Plan* pl, int64_t main_ch, uint32_t reserve
     p.ntot = p.g * p.kp;
     if (p.ntot > 1024) return false;
     p.t = std::min(8, 256 / p.kp);  // no carry: T slots per 256-column region, double-buffered
-    p.dbuf = getenv("C1D_NO_DBUF") == nullptr && p.kp <= 64 ? 1 : 0;
+    p.dbuf = !dev_switch(DevSwitch::kNoDbuf) && p.kp <= 64 ? 1 : 0;
     if (!p.dbuf) p.t = std::min(8, p.r);
     p.acc2 = 0;
     if (main_ch > 0) {  // split FP32: the second 256-column region holds the correction terms
@@ -230,7 +230,7 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     if (two_regions) {  // two accumulator regions of 256 columns each
         p.t = std::min(p.t, 256 / p.kp - (p.g - 1));
         p.acc2 = 256;
-    } else if (std::min(8, 256 / p.kp - (p.g - 1)) >= 4 && getenv("C1D_NO_DBUF") == nullptr) {
+    } else if (std::min(8, 256 / p.kp - (p.g - 1)) >= 4 && !dev_switch(DevSwitch::kNoDbuf)) {
         p.t = std::min(8, 256 / p.kp - (p.g - 1));
         p.dbuf = 1;
     }
@@ -252,7 +252,7 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     {
         const int tail = static_cast<int>(g.taps - static_cast<int64_t>(kTapsPerBlock) * (p.g - 1));
         if (p.g >= 2 && p.kp == 64 && (p.g - 1) * p.kp >= 128 && tail * p.cc <= kTapsPerBlock &&
-            (!two_regions || main_ch % p.cc == 0) && getenv("C1D_NO_TAIL") == nullptr) {
+            (!two_regions || main_ch % p.cc == 0) && !dev_switch(DevSwitch::kNoTail)) {
             p.tail = tail;
             p.tail_chunks = 16 * p.t + static_cast<int>(ceil_div(kTapsPerBlock, p.cc));
         }
@@ -262,7 +262,7 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     p.tx_stage_bytes = p.tail ? ((static_cast<uint32_t>(p.tail_chunks * p.cc * 16) + 1023) & ~1023u) : 0;
     p.tw_stage_bytes = p.tail ? static_cast<uint32_t>(p.kp * kTapsPerBlock * 2) : 0;
     plan_wres(g, &p, allow_wres);
-    p.ws = (p.tail ? p.g - 1 : p.g) * p.kp == 64 && getenv("C1D_NO_WS") == nullptr ? 1 : 0;
+    p.ws = (p.tail ? p.g - 1 : p.g) * p.kp == 64 && !dev_switch(DevSwitch::kNoWs) ? 1 : 0;
     const uint32_t stage = p.x_stage_bytes + p.w_stage_bytes + p.tx_stage_bytes + p.tw_stage_bytes;
     p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve - p.wres_bytes) / stage));
     if (p.stages < 2) return p.wres_bytes ? make_plan(g, pl, main_ch, reserve, false) : false;
