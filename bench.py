@@ -339,12 +339,25 @@ def narrow_roofline(lib, dev, stream, peaks, traffic):
                          dw=torch.empty((k, c, s), device=dev)))
     w = (torch.rand((k, c, s), device=dev, generator=g) * 2 - 1) * (6.0 / (c * s)) ** 0.5
     sp = stream.cuda_stream
+    # weight images packed before the clock, as the reference's measure_kernel packs (bench.cpp:184-203)
+    wd, wp, images = {}, {}, []
+    for name, pi in (("forward", L.PASS_FORWARD), ("backward_data", L.PASS_BACKWARD_DATA)):
+        wd[name], wp[name] = cv.make_desc(p, n, w_in, L.DTYPE_BF16), w.data_ptr()
+        nbytes = C.c_size_t(0)
+        if lib.c1d_packed_weights_size(C.byref(wd[name]), pi, C.byref(nbytes)) == 0 and nbytes.value:
+            img = torch.empty(nbytes.value, dtype=torch.uint8, device=dev)
+            if lib.c1d_pack_weights(1, C.byref(wd[name]), (C.c_int32 * 1)(pi), (C.c_void_p * 1)(w.data_ptr()),
+                                    (C.c_void_p * 1)(img.data_ptr()), sp) != 0:
+                raise RuntimeError(lib.c1d_last_error_message().decode())
+            wd[name].flags |= L.FLAG_PREPACKED_WEIGHTS
+            wp[name] = img.data_ptr()
+            images.append(img)
 
     def call(name, b):
         if name == "forward":
-            st = lib.c1d_forward(C.byref(desc), b["x"].data_ptr(), w.data_ptr(), b["y"].data_ptr(), None, 0, sp)
+            st = lib.c1d_forward(C.byref(wd[name]), b["x"].data_ptr(), wp[name], b["y"].data_ptr(), None, 0, sp)
         elif name == "backward_data":
-            st = lib.c1d_backward_data(C.byref(desc), b["dy"].data_ptr(), w.data_ptr(), b["dx"].data_ptr(), None, 0, sp)
+            st = lib.c1d_backward_data(C.byref(wd[name]), b["dy"].data_ptr(), wp[name], b["dx"].data_ptr(), None, 0, sp)
         else:
             st = lib.c1d_backward_weight(C.byref(desc), b["x"].data_ptr(), b["dy"].data_ptr(), b["dw"].data_ptr(),
                                          None, 0, sp)
@@ -379,6 +392,8 @@ def narrow_roofline(lib, dev, stream, peaks, traffic):
                      "frac": max(t_hbm, t_tc) / t, "traffic": traffic.get(f"cfg2_{name}")}
     out["peaks"] = {"hbm_gbs": hbm, "bf16_tflops": tensor, "source": "MEASURED_PEAKS.json (burst)"}
     out["config"] = "BASELINE config 2: N=16 C=K=15 S=51 d=8 W_in=60400, bf16 storage; 4 rotating buffer sets > L2"
+    out["weights"] = ("prepacked images (c1d_pack_weights before the clock, like the reference's measure_kernel)"
+                      if images else "KCS, packed inside every call")
     return out
 
 

@@ -23,8 +23,9 @@ y = torch.empty((n, k, q), device="cuda")
 dx = torch.empty((n, c, w_in), device="cuda")
 dw = torch.empty((k, c, s), device="cuda")
 wb = cv.pack_weights_backward(w)
+wf = w if os.environ.get("KCS") else cv.pack_weights_forward(w)  # KCS=1: pack inside every call
 flush = torch.empty(64 * 1024 * 1024, device="cuda")
-fn = {"fwd": lambda: cv.conv1d_forward(x, w, p, out=y), "bwd_d": lambda: cv.conv1d_backward_data(dy, wb, p, out=dx),
+fn = {"fwd": lambda: cv.conv1d_forward(x, wf, p, out=y), "bwd_d": lambda: cv.conv1d_backward_data(dy, wb, p, out=dx),
       "bwd_w": lambda: cv.conv1d_backward_weight(dy, x, p, out=dw)}
 flops = cv.conv_flops(p, n, q)
 for name in passes:
