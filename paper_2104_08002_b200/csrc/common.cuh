@@ -91,11 +91,11 @@ inline bool pdl_enabled() {
 
 // Dev A/B switches read by the planners: each environment variable is read once per process (the
 // planners run on every call, and getenv walks the environment).
-enum class DevSwitch { kNoWres, kNoDbuf, kNoTail, kNoWs, kD8Carry, kCount };
+enum class DevSwitch { kNoWres, kNoDbuf, kNoTail, kNoWs, kD8Carry, kNoStagger, kCount };
 inline bool dev_switch(DevSwitch s) {
     static const bool on[static_cast<int>(DevSwitch::kCount)] = {
         getenv("C1D_NO_WRES") != nullptr, getenv("C1D_NO_DBUF") != nullptr, getenv("C1D_NO_TAIL") != nullptr,
-        getenv("C1D_NO_WS") != nullptr, getenv("C1D_D8_CARRY") != nullptr};
+        getenv("C1D_NO_WS") != nullptr, getenv("C1D_D8_CARRY") != nullptr, getenv("C1D_NO_STAGGER") != nullptr};
     return on[static_cast<int>(s)];
 }
 

@@ -49,6 +49,7 @@ constexpr int kTileQ = 128;      // output columns per tile (MMA M)
 constexpr int kSegQ = 256;       // TMA box width in elements
 constexpr int kTapsPerBlock = 16;
 constexpr int kMaxStages = 6;
+constexpr int kMaxStagger = 2;  // trailing chunks of a super-tile issued tile-major (Plan::stagger)
 
 constexpr int kPfRing = 4;  // layer glue: input blocks in flight per epilogue warp
 constexpr uint32_t kTmemCols = 512;
@@ -104,6 +105,13 @@ struct Plan {
     // Weight-stationary main MMAs (tcgen05.mma.ws, B latched in the collector across a channel's
     // tiles): only where the main MMA is N = 64 (KP = 16 narrow layers; sm100.cuh mma_ws_*)
     int ws;
+    // Staggered finish (single-buffered carry plans, KP >= 32): the last `stagger` channel chunks of a
+    // super-tile are issued tile by tile, each tile committing its own barrier, so the epilogue stores
+    // output tile t while the MMAs of tiles t+1.. still run (with all 512 TMEM columns in one
+    // super-tile nothing else overlaps the stores). Each accumulator sees its chunks in the same order.
+    // The count does not depend on the stage count (every plan has >= 2 stages), so a glued pass,
+    // whose epilogue staging leaves fewer stages, accumulates in the same order as the plain pass.
+    int stagger;
 };
 
 constexpr uint32_t kWresMax = 64 * 1024;
@@ -267,6 +275,9 @@ bool make_plan(const ConvGeom& g, Plan* pl, int64_t main_ch = 0, uint32_t reserv
     p.stages = static_cast<int>(std::min<uint32_t>(kMaxStages, (200 * 1024 - reserve - p.wres_bytes) / stage));
     if (p.stages < 2) return p.wres_bytes ? make_plan(g, pl, main_ch, reserve, false) : false;
     p.smem_bytes = p.wres_bytes + static_cast<size_t>(p.stages) * stage + 1024;
+    p.stagger = (!p.dbuf && p.kp >= 32 && !dev_switch(DevSwitch::kNoStagger))
+                    ? static_cast<int>(std::min<int64_t>(std::min(kMaxStagger, p.stages), ceil_div(g.in_ch, p.cc)))
+                    : 0;
     *pl = p;
     return true;
 }
@@ -851,6 +862,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     // double-buffered TMEM: tmem_empty / tmem_empty2 release region 0 / 1 (stores done, non-carry
     // slots zeroed); carry_full publishes the G-1 carried slots of the next super-tile
     __shared__ uint64_t tmem_full, tmem_empty, tmem_empty2, carry_full, wres_full;
+    __shared__ uint64_t tile_full[8];  // staggered finish: output slot t of the super-tile is complete
     __shared__ uint32_t tmem_base_s;
     __shared__ float bias_red[8 * 64];  // layer glue: per-epilogue-warp bias-gradient sums
 
@@ -879,6 +891,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         mbar_init(&tmem_empty2, 4);
         mbar_init(&carry_full, 4);
         mbar_init(&wres_full, 1);
+        for (int t = 0; t < 8; ++t) mbar_init(&tile_full[t], 1);
         fence_mbar_init();
     }
     if (warp == 2) tmem_alloc<kTmemCols>(&tmem_base_s);
@@ -1051,6 +1064,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             bool need_carry = pl.dbuf && G > 1 && !first_super;
             first_super = false;
             const uint32_t rtmem = tmem + region;
+            int sg_stage[kMaxStagger] = {0, 0};
             for (int ch = 0; ch < n_chunks; ++ch) {
                 const int c0 = ch * pl.cc;
                 const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - c0));
@@ -1058,6 +1072,16 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                 mbar_wait(smem_u32(&stage_full[stage]), phase);
                 t_full += clock64() - tf0;
                 tc_fence_after();
+                if constexpr (kKPB != 1) {
+                    if (ch >= n_chunks - pl.stagger) {  // staggered finish: issued tile-major below
+                        sg_stage[ch - (n_chunks - pl.stagger)] = stage;
+                        if (++stage == pl.stages) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
+                }
                 const uint32_t xs = smem_u32(xs_base + static_cast<size_t>(stage) * pl.x_stage_bytes);
                 const uint32_t wsm = pl.wres_bytes ? wres_s + static_cast<uint32_t>(c0) * pl.b_chan_bytes
                                                    : smem_u32(ws_base + static_cast<size_t>(stage) * pl.w_stage_bytes);
@@ -1176,7 +1200,48 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                     phase ^= 1;
                 }
             }
-            if (elect_one()) mma_commit(smem_u32(&tmem_full));
+            bool staggered = false;
+            if constexpr (kKPB != 1) {
+                if (pl.stagger) {
+                    // the deferred chunks, tile by tile: slot t is complete after tile t (input tile t
+                    // is the last to write it), so each tile commits its own barrier
+                    staggered = true;
+                    const long long ti0 = clock64();
+                    if (elect_one()) {
+                        for (int t = 0; t < su.tcur; ++t) {
+                            for (int i = 0; i < pl.stagger; ++i) {
+                                const int c0 = (n_chunks - pl.stagger + i) * pl.cc;
+                                const int ccn = static_cast<int>(imin64(pl.cc, p.in_ch - c0));
+                                const size_t st = static_cast<size_t>(sg_stage[i]);
+                                const uint32_t wsm = pl.wres_bytes ? wres_s + static_cast<uint32_t>(c0) * pl.b_chan_bytes
+                                                                   : smem_u32(ws_base + st * pl.w_stage_bytes);
+                                uint64_t adesc = desc_advance(make_smem_desc(smem_u32(xs_base + st * pl.x_stage_bytes), 128, 16, kLayoutNone),
+                                                              static_cast<uint32_t>(t * kTileQ * 2));
+                                uint64_t bdesc = make_smem_desc(wsm + main_brow, 128, 256, kLayoutNone);
+                                for (int c = 0; c < ccn; ++c) {
+                                    mma_bf16_ss(rtmem + ((c0 + c >= p.main_ch) ? pl.acc2 : 0u) + main_slot + static_cast<uint32_t>(t * KP),
+                                                adesc, bdesc, idesc, 1);
+                                    bdesc = desc_advance(bdesc, pl.b_chan_bytes);
+                                    adesc = desc_advance(adesc, static_cast<uint32_t>(pl.xw * 2));
+                                }
+                                if (pl.tail) {
+                                    const uint32_t tx = smem_u32(tx_base + st * pl.tx_stage_bytes);
+                                    const uint32_t tw = smem_u32(tw_base + st * pl.tw_stage_bytes);
+                                    mma_bf16_ss(rtmem + ((c0 >= p.main_ch) ? pl.acc2 : 0u) + static_cast<uint32_t>(t * KP),
+                                                desc_advance(make_smem_desc(tx, 128, static_cast<uint32_t>(pl.cc * 16), kLayoutNone),
+                                                             static_cast<uint32_t>(t * 16 * pl.cc * 16)),
+                                                make_smem_desc(tw, 128, 256, kLayoutNone), idesc_tail, 1);
+                                }
+                            }
+                            mma_commit(smem_u32(&tile_full[t]));
+                        }
+                        for (int i = 0; i < pl.stagger; ++i) mma_commit(smem_u32(&stage_empty[sg_stage[i]]));
+                    }
+                    __syncwarp();
+                    t_issue += clock64() - ti0;
+                }
+            }
+            if (!staggered && elect_one()) mma_commit(smem_u32(&tmem_full));
             __syncwarp();
             if (pl.dbuf) region ^= 256u;
             if (t_full_first < 0) t_full_first = t_full + t_tmem;
@@ -1375,10 +1440,20 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(region ? &tmem_empty2 : &tmem_empty));
         };
+        uint32_t tfph = 0;  // staggered finish: parity bit of each tile_full barrier
+        auto tile_wait = [&](int j) {
+            if (kKPB != 1 && pl.stagger) {
+                mbar_wait_sleep(smem_u32(&tile_full[j]), (tfph >> j) & 1u, 64);
+                tfph ^= 1u << j;
+                tc_fence_after();
+            }
+        };
         while (next_super(cur, J, G, T, &su)) {
-            mbar_wait_sleep(smem_u32(&tmem_full), tphase, 256);
-            tphase ^= 1;
-            tc_fence_after();
+            if (kKPB == 1 || !pl.stagger) {
+                mbar_wait_sleep(smem_u32(&tmem_full), tphase, 256);
+                tphase ^= 1;
+                tc_fence_after();
+            }
             const long long e0 = clock64();
             if (pl.dbuf && egrp == 0) carry_out(su);  // the next super-tile's carry-dependent tiles may start
             const long long e1 = clock64();
@@ -1387,6 +1462,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
             float* const out_item = p.out + su.n * p.out_ch * out_w;
             if constexpr (kMode == 1) {  // fused forward glue instead of the plain store
                 for (int j = 0; j < su.tcur; ++j) {
+                    tile_wait(j);
                     const int64_t o = su.i0 - (G - 1) + j;
                     if (o < su.j0 || o > su.j1 || !mine(su.n, o)) continue;
                     const int64_t q = o * kTileQ + quarter * 32 + lane;
@@ -1409,6 +1485,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                 }
             } else if constexpr (kMode == 2) {  // fused backward glue
                 for (int j = 0; j < su.tcur; ++j) {
+                    tile_wait(j);
                     const int64_t o = su.i0 - (G - 1) + j;
                     if (o < su.j0 || o > su.j1 || !mine(su.n, o)) continue;
                     const int64_t q = o * kTileQ + quarter * 32 + lane;
@@ -1431,6 +1508,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
                 }
             } else
             for (int j = 0; j < su.tcur; ++j) {
+                tile_wait(j);
                 const int64_t o = su.i0 - (G - 1) + j;
                 if (o < su.j0 || o > su.j1 || !mine(su.n, o)) continue;  // phantom (warm-up / beyond the segment)
                 const int64_t q = o * kTileQ + quarter * 32 + lane;
