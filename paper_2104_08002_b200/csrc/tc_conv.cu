@@ -1390,20 +1390,31 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         // them at a segment end) and zero dst's remaining used slots: dst is then ready
         auto prepare = [&](uint32_t src, uint32_t dst, const Super& s2) {
             for (uint32_t reg = 0; reg <= pl.acc2; reg += (pl.acc2 ? pl.acc2 : 1u)) {
-                for (int j = 0; j < G - 1; ++j) {
-                    for (int kb = 0; kb < KP; kb += 16) {
-                        uint32_t v[16];
-                        if (!s2.last_in_segment) {
-                            tmem_ld16(lane_base + src + reg + static_cast<uint32_t>((s2.tcur + j) * KP + kb), v);
-                            tmem_ld_wait();
-                            tmem_st16(lane_base + dst + reg + static_cast<uint32_t>(j * KP + kb), v);
-                        } else if (dst != src) {
-                            tmem_st16(lane_base + dst + reg + static_cast<uint32_t>(j * KP + kb), z);
-                        }
+                // the carried run (G-1 slots) is contiguous in both places; two 16-column loads in
+                // flight per round trip (the MMA warp waits for this pass)
+                const uint32_t run = static_cast<uint32_t>((G - 1) * KP);
+                const uint32_t from = lane_base + src + reg + static_cast<uint32_t>(s2.tcur * KP);
+                const uint32_t to = lane_base + dst + reg;
+                if (!s2.last_in_segment) {
+                    uint32_t col = 0;
+                    for (; col + 32 <= run; col += 32) {
+                        uint32_t va[16], vb[16];
+                        tmem_ld16(from + col, va);
+                        tmem_ld16(from + col + 16, vb);
+                        tmem_ld_wait();
+                        tmem_st16(to + col, va);
+                        tmem_st16(to + col + 16, vb);
                     }
+                    for (; col < run; col += 16) {
+                        uint32_t v[16];
+                        tmem_ld16(from + col, v);
+                        tmem_ld_wait();
+                        tmem_st16(to + col, v);
+                    }
+                } else if (dst != src) {
+                    for (uint32_t col = 0; col < run; col += 16) tmem_st16(to + col, z);
                 }
-                for (uint32_t col = static_cast<uint32_t>((G - 1) * KP); col < used_cols; col += 16)
-                    tmem_st16(lane_base + dst + reg + col, z);
+                for (uint32_t col = run; col < used_cols; col += 16) tmem_st16(lane_base + dst + reg + col, z);
             }
             tmem_st_wait();
             tc_fence_before();
