@@ -851,7 +851,10 @@ __device__ __forceinline__ void issue_channels(const IssueArgs& ia) {
 // blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
 // mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
 // and TMA warps, and an all-modes kernel (~30k instructions) ran the epilogue 6x slower.
-template <int kMode, int kKPB, int kEG = 1, int kFx = 0>
+// kLean: the plan is a natural-row, single-buffered carry plan with streamed weights and one
+// accumulator region (config 3); those plan fields are compile-time constants there, which drops the
+// other paths' code from the three roles' hot loops (they share the instruction cache).
+template <int kMode, int kKPB, int kEG = 1, int kFx = 0, int kLean = 0>
 __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
                    const __grid_constant__ CUtensorMap om0, const __grid_constant__ CUtensorMap om1,
@@ -866,7 +869,15 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     __shared__ uint32_t tmem_base_s;
     __shared__ float bias_red[8 * 64];  // layer glue: per-epilogue-warp bias-gradient sums
 
-    const Plan& pl = p.pl;
+    Plan plv = p.pl;
+    if constexpr (kLean) {
+        plv.xr = plv.xin = plv.dbuf = plv.ws = 0;
+        plv.wres_bytes = 0;
+        plv.acc2 = 0;
+        plv.raw_segs = plv.rows_alloc = plv.n_box = plv.box_rows = 0;
+        plv.raw_stage_bytes = 0;
+    }
+    const Plan& pl = plv;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     const uint32_t wres_s = smem_u32(smem);  // resident weights (pl.wres_bytes), then the stages
@@ -1872,6 +1883,9 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
             else if (gl.gadd && !gl.gsum) kernel = tc_conv_kernel<2, 1, 2, 3>;
         }
     }
+    static const bool no_lean = getenv("C1D_NO_LEAN") != nullptr;  // dev A/B switch
+    if (mode == 0 && pl.kp != 16 && !pl.xr && !pl.xin && !pl.dbuf && !pl.ws && !pl.wres_bytes && !pl.acc2 && !no_lean)
+        kernel = tc_conv_kernel<0, 0, 1, 0, 1>;
     const int threads = 128 + 128 * eg;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
