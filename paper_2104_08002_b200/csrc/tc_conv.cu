@@ -851,9 +851,11 @@ __device__ __forceinline__ void issue_channels(const IssueArgs& ia) {
 // blocks per filter group (KP/16), so the per-lane bias values / bias-gradient sums live in registers. One instantiation per
 // mode keeps each kernel's code small: the epilogue warps share the instruction cache with the MMA
 // and TMA warps, and an all-modes kernel (~30k instructions) ran the epilogue 6x slower.
-// kLean: the plan is a natural-row, single-buffered carry plan with streamed weights and one
-// accumulator region (config 3); those plan fields are compile-time constants there, which drops the
-// other paths' code from the three roles' hot loops (they share the instruction cache).
+// kLean 1: the plan is a natural-row, single-buffered carry plan with streamed weights and one
+// accumulator region (config 3); kLean 2 and the fixed-flag glue kernels (kFx): a natural-row,
+// double-buffered, one-region plan (config 2, the network's layers). Those plan fields are
+// compile-time constants there, which drops the other paths' code from the three roles' hot loops
+// (they share the instruction cache).
 template <int kMode, int kKPB, int kEG = 1, int kFx = 0, int kLean = 0>
 __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     tc_conv_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap tmap_tail,
@@ -870,12 +872,21 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
     __shared__ float bias_red[8 * 64];  // layer glue: per-epilogue-warp bias-gradient sums
 
     Plan plv = p.pl;
-    if constexpr (kLean) {
+    if constexpr (kLean == 1) {
         plv.xr = plv.xin = plv.dbuf = plv.ws = 0;
         plv.wres_bytes = 0;
         plv.acc2 = 0;
         plv.raw_segs = plv.rows_alloc = plv.n_box = plv.box_rows = 0;
         plv.raw_stage_bytes = 0;
+    }
+    if constexpr (kFx != 0 || kLean == 2) {
+        // the fixed-flag glue kernels (the network's narrow layers) only take natural-row,
+        // double-buffered, one-region plans (launch_tc_conv checks)
+        plv.xr = plv.xin = plv.tail = plv.stagger = 0;
+        plv.dbuf = 1;
+        plv.acc2 = 0;
+        plv.raw_segs = plv.rows_alloc = plv.n_box = plv.box_rows = 0;
+        plv.raw_stage_bytes = plv.tx_stage_bytes = plv.tw_stage_bytes = 0;
     }
     const Plan& pl = plv;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -1868,7 +1879,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     // the network's layer shapes with their glue flags fixed at compile time (glue_forward16 /
     // glue_backward16 kFx): narrow filter blocks, two epilogue groups
     static const bool no_fx = getenv("C1D_NO_GLUE_FX") != nullptr;  // dev A/B switch
-    if (mode != 0 && pl.kp == 16 && eg == 2 && !no_fx) {
+    if (mode != 0 && pl.kp == 16 && eg == 2 && !no_fx && !pl.xr && !pl.xin && pl.dbuf && !pl.acc2 && !pl.tail &&
+        !pl.stagger) {
         const LayerGlue& gl = *glue;
         if (mode == 1 && gl.relu && gl.mask_out && gl.act_bf16 && !gl.pre) {
             if (!gl.skip && !gl.act && gm.slots == 4u) kernel = tc_conv_kernel<1, 1, 2, 1>;
@@ -1886,6 +1898,9 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     static const bool no_lean = getenv("C1D_NO_LEAN") != nullptr;  // dev A/B switch
     if (mode == 0 && pl.kp != 16 && !pl.xr && !pl.xin && !pl.dbuf && !pl.ws && !pl.wres_bytes && !pl.acc2 && !no_lean)
         kernel = tc_conv_kernel<0, 0, 1, 0, 1>;
+    // kLean 2: the plain KP = 16 kernel on a natural-row, double-buffered, one-region plan (config 2)
+    if (mode == 0 && pl.kp == 16 && !pl.xr && !pl.xin && pl.dbuf && !pl.acc2 && !pl.tail && !pl.stagger && !no_lean)
+        kernel = tc_conv_kernel<0, 1, 1, 0, 2>;
     const int threads = 128 + 128 * eg;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
