@@ -652,6 +652,7 @@ __device__ __forceinline__ void w2_expand_d(int off, uint32_t rc, int p0, int np
 #undef W2X
 }
 
+template <int kLean>
 __global__ void __launch_bounds__(kW2Threads, 1)
     tc_wgrad2_kernel(const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap xmap,
                      const W2Params p) {
@@ -661,6 +662,11 @@ __global__ void __launch_bounds__(kW2Threads, 1)
     __shared__ uint32_t tmem_base_s;
 
     const W2Plan& pl = p.pl;
+    // kLean: the dilation-8 natural ring plan (no channel-octet streams, no inline expansion, one
+    // accumulator copy); folding those plan fields drops the other feeds' code from the hot loops
+    const int pl_xt = kLean ? 0 : pl.xt, pl_xin = kLean ? 0 : pl.xin, pl_ph = kLean ? 1 : pl.ph;
+    const int pl_copies = kLean ? 1 : pl.copies, pl_raw_cols = kLean ? 0 : pl.raw_cols;
+    const uint32_t pl_a_mn = kLean ? 0u : pl.a_mn, pl_raw_bytes = kLean ? 0u : pl.raw_bytes;
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     int role = 0;
@@ -674,7 +680,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < pl.stages; ++s) {
-            mbar_init(&full[s], pl.xt ? 1 : 1 + kLoaderThreads);  // dY (+ xt: X) TMA tx bytes + every X loader thread
+            mbar_init(&full[s], pl_xt ? 1 : 1 + kLoaderThreads);  // dY (+ xt: X) TMA tx bytes + every X loader thread
             mbar_init(&empty[s], 1);
         }
         mbar_init(&acc_full, 1);
@@ -694,7 +700,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
     if (warp == 0) {
         if (lane == 0) {
             prefetch_tmap(&ymap);
-            if (pl.xt) prefetch_tmap(&xmap);
+            if (pl_xt) prefetch_tmap(&xmap);
             const int octets = static_cast<int>((p.c + 7) / 8);
             long long tw_sum = 0;
             const long long tb = clock64();
@@ -710,13 +716,13 @@ __global__ void __launch_bounds__(kW2Threads, 1)
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
                     tw_sum += clock64() - tw;
                     const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.nbox) * pl.box_bytes + (pl.xt ? pl.xt_x_bytes : 0u));
+                    mbar_arrive_expect_tx(fb, static_cast<uint32_t>(pl.nbox) * pl.box_bytes + (pl_xt ? pl.xt_x_bytes : 0u));
                     uint8_t* sbase = smem + pl.ring_bytes + static_cast<size_t>(stage) * pl.stage_bytes;
                     for (int b = 0; b < pl.nbox; ++b)
                         tma_load_3d(smem_u32(sbase + static_cast<uint32_t>(b) * pl.box_bytes), &ymap,
                                     static_cast<int32_t>(q0 - back + static_cast<int64_t>(b) * pl.bq), 0,
                                     static_cast<int32_t>(item), fb);
-                    if (pl.xt) {
+                    if (pl_xt) {
                         // copy t: columns q0 + tap0*d + t*d .. of every octet, one box
                         const int64_t col0 = q0 + static_cast<int64_t>(tap0) * p.dil;
                         const uint32_t xs = smem_u32(sbase + pl.y_bytes);
@@ -738,7 +744,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             }
         }
     } else if (warp == 1) {
-        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.n), kFmtBF16, pl.a_mn, 0);
+        const uint32_t idesc = make_idesc(128, static_cast<uint32_t>(pl.n), kFmtBF16, pl_a_mn, 0);
         // B (dY) descriptor: swizzled K-major rows of 2*Bq bytes (8-row atoms), or for Bq = 8 the
         // plain core-matrix layout with K-chunks one box apart.
         const uint32_t b_sbo = pl.bq == 8 ? 128u : 16u * static_cast<uint32_t>(pl.bq);
@@ -763,9 +769,9 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             wi.b_box = (pl.box_bytes - static_cast<uint32_t>(wi.per_box - 1) * 32u) >> 4;
         }
         wi.copy_stride = static_cast<uint32_t>(pl.gpc * pl.n);
-        wi.cmask = static_cast<uint32_t>(pl.copies - 1);
+        wi.cmask = static_cast<uint32_t>(pl_copies - 1);
         wi.n = pl.n;
-        wi.copies = pl.copies;
+        wi.copies = pl_copies;
 #pragma unroll
         for (int ks = 0; ks < 9; ++ks)
             wi.b_off[ks] = static_cast<uint32_t>(ks / wi.per_box) * (wi.b_box + static_cast<uint32_t>(wi.per_box - 1) * wi.b_k) +
@@ -821,7 +827,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
                 const long long ti = clock64();
                 if (elect_one()) {
                     // xt: the stage's own window (rows from its first column); else the ring
-                    const uint64_t a_st = pl.xt ? make_smem_desc(smem_u32(sbase + pl.y_bytes), pl.a_lbo, pl.a_sbo, kLayoutNone)
+                    const uint64_t a_st = pl_xt ? make_smem_desc(smem_u32(sbase + pl.y_bytes), pl.a_lbo, pl.a_sbo, kLayoutNone)
                                                 : desc_advance(ax0, static_cast<uint32_t>(stage_pos) * pl.chunk_bytes);
                     const int k0 = kdone - seg_base;  // K-step within the segment (copy rotation, init)
                     switch (g_count) {
@@ -856,19 +862,19 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             p.prof[blockIdx.x * 8 + 6] = te_sum;
         }
     }
-    if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl.xt) {
+    if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl_xt) {
         // xt: the producer's TMA boxes bring X; nothing to load here
-    } else if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl.xin) {
+    } else if ((warp == 2 || warp == 3 || warp == 6 || warp == 7) && pl_xin) {
         // ---- X loaders, inline expanded rows: the natural columns of a stage's positions land in
         // one of two `raw` buffers (16-B cp.async pieces, issued one stage ahead), then the loaders
         // write the ring rows (position p = the 8 elements at column D*p), proxy fence, arrive
         const int lt = (warp < 4 ? warp - 2 : warp - 4) * 32 + lane;  // 0..127
-        const int d = 8 / pl.ph;
+        const int d = 8 / pl_ph;
         const int cshift = __ffs(pl.cp) - 1;
         const uint32_t ring_s = smem_u32(smem);
         const uint32_t raw_s0 = ring_s + pl.ring_bytes + static_cast<uint32_t>(pl.stages) * pl.stage_bytes;
         const uint32_t mirror_bytes = static_cast<uint32_t>(pl.ring) * pl.chunk_bytes;
-        const int pieces_per_c = pl.raw_cols / 8;
+        const int pieces_per_c = pl_raw_cols / 8;
         const int rg = d == 4 ? 4 : 8;
         // the loaders' stage sequence: (item, first position, positions) per stage
         struct XStage {
@@ -889,7 +895,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             const int64_t item = it_st / p.steps_per_item;
             const int64_t q0 = (it_st - item * p.steps_per_item) * 16;
             xs->item = item;
-            xs->first = it_seg_first ? q0 * pl.ph / 8 + tap0 : it_next;
+            xs->first = it_seg_first ? q0 * pl_ph / 8 + tap0 : it_next;
             xs->n = it_seg_first ? pl.span + pl.kch : pl.kch;
             it_seg_first = false;
             it_next = xs->first + xs->n;
@@ -903,7 +909,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
                 const int c = i & (pl.cp - 1), j = i >> cshift;
                 const int64_t col = col0 + 8 * j;
                 const bool valid = c < p.c && col < p.w_in;
-                cp_async16_zfill(raw_s + static_cast<uint32_t>((c * pl.raw_cols + 8 * j) * 2),
+                cp_async16_zfill(raw_s + static_cast<uint32_t>((c * pl_raw_cols + 8 * j) * 2),
                                  valid ? xi + static_cast<int64_t>(c) * p.w_in + col : p.x, valid);
             }
             cp_async_commit();
@@ -918,20 +924,20 @@ __global__ void __launch_bounds__(kW2Threads, 1)
         int v_pos = 0;
         while (have) {
             const bool have_next = next_stage(&nxt_s);
-            if (have_next) load_raw(nxt_s, raw_s0 + static_cast<uint32_t>(rb ^ 1) * pl.raw_bytes);
+            if (have_next) load_raw(nxt_s, raw_s0 + static_cast<uint32_t>(rb ^ 1) * pl_raw_bytes);
             mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
             if (have_next)
                 cp_async_wait_group<1>();  // this stage's raw has landed (the next one may be in flight)
             else
                 cp_async_wait_group<0>();
             asm volatile("bar.sync 3, 128;" ::: "memory");
-            const uint32_t raw_s = raw_s0 + static_cast<uint32_t>(rb) * pl.raw_bytes;
+            const uint32_t raw_s = raw_s0 + static_cast<uint32_t>(rb) * pl_raw_bytes;
             const int64_t cfirst = static_cast<int64_t>(d) * cur_s.first;
             const int off = static_cast<int>(cfirst & 7);
             const int ngroups = (cur_s.n + rg - 1) / rg;
             for (int i = lt; i < pl.cp * ngroups; i += kLoaderThreads) {
                 const int c = i & (pl.cp - 1), g = i >> cshift;
-                const uint32_t rc = raw_s + static_cast<uint32_t>(c * pl.raw_cols * 2);
+                const uint32_t rc = raw_s + static_cast<uint32_t>(c * pl_raw_cols * 2);
                 if (d == 1)
                     w2_expand_d<1>(off, rc, g * rg, cur_s.n, ring_s, v_pos, pl.ring, pl.xb, pl.chunk_bytes, mirror_bytes, c);
                 else if (d == 2)
@@ -978,7 +984,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             for (int64_t st = cur; st < seg_end; st += pl.ks) {
                 const int64_t q0 = (st - item * p.steps_per_item) * 16;
                 mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-                const int64_t first_chunk = seg_first ? q0 * pl.ph / 8 + tap0 : next_chunk;
+                const int64_t first_chunk = seg_first ? q0 * pl_ph / 8 + tap0 : next_chunk;
                 const int nchunks = seg_first ? pl.span + pl.kch : pl.kch;
                 seg_first = false;
                 next_chunk = first_chunk + nchunks;
@@ -1038,7 +1044,7 @@ __global__ void __launch_bounds__(kW2Threads, 1)
             tc_fence_after();
             const long long td = clock64();
             // copies this segment wrote (a short segment leaves the rest stale); order 0 + 1 + ...
-            const int used = static_cast<int>(imin(pl.copies, seg_k));
+            const int used = static_cast<int>(imin(pl_copies, seg_k));
             for (int g = 0; g < g_count; ++g) {
                 int col0 = 0;
                 if (used == 1) {  // four TMEM loads in flight per wait
@@ -1277,7 +1283,10 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
     }
-    cudaError_t e = cudaFuncSetAttribute(tc_wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    static const bool no_lean = getenv("C1D_NO_LEAN") != nullptr;  // dev A/B switch
+    auto kernel = (!pl.xt && !pl.xin && pl.ph == 1 && pl.copies == 1 && !pl.a_mn && !no_lean) ? tc_wgrad2_kernel<1>
+                                                                                              : tc_wgrad2_kernel<0>;
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(pl.smem_bytes));
     if (e != cudaSuccess) return e;
     W2Params wp{};
@@ -1303,7 +1312,7 @@ cudaError_t launch_v2(const uint16_t* x_bf16, const uint16_t* dy_bf16, float* dw
         cudaMalloc(&wp.prof, sizeof(unsigned long long) * 8 * pl.grid);
         cudaMemset(wp.prof, 0, sizeof(unsigned long long) * 8 * pl.grid);
     }
-    e = launch_pdl(tc_wgrad2_kernel, dim3(pl.grid), dim3(kW2Threads), pl.smem_bytes, stream, ymap, xmap, wp);
+    e = launch_pdl(kernel, dim3(pl.grid), dim3(kW2Threads), pl.smem_bytes, stream, ymap, xmap, wp);
     note_launch();
     if (e != cudaSuccess) return e;
     if (profile) {
