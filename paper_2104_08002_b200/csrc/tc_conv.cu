@@ -853,7 +853,8 @@ __device__ __forceinline__ void issue_channels(const IssueArgs& ia) {
 // and TMA warps, and an all-modes kernel (~30k instructions) ran the epilogue 6x slower.
 // kLean 1: the plan is a natural-row, single-buffered carry plan with streamed weights and one
 // accumulator region (config 3); kLean 2 and the fixed-flag glue kernels (kFx): a natural-row,
-// double-buffered, one-region plan (config 2, the network's layers). Those plan fields are
+// double-buffered, one-region plan with weight-stationary N = 64 MMAs (config 2, the network's
+// layers). Those plan fields are
 // compile-time constants there, which drops the other paths' code from the three roles' hot loops
 // (they share the instruction cache).
 template <int kMode, int kKPB, int kEG = 1, int kFx = 0, int kLean = 0>
@@ -883,7 +884,7 @@ __global__ void __launch_bounds__(128 + 128 * kEG, 1)
         // the fixed-flag glue kernels (the network's narrow layers) only take natural-row,
         // double-buffered, one-region plans (launch_tc_conv checks)
         plv.xr = plv.xin = plv.tail = plv.stagger = 0;
-        plv.dbuf = 1;
+        plv.dbuf = plv.ws = 1;
         plv.acc2 = 0;
         plv.raw_segs = plv.rows_alloc = plv.n_box = plv.box_rows = 0;
         plv.raw_stage_bytes = plv.tx_stage_bytes = plv.tw_stage_bytes = 0;
@@ -1880,7 +1881,7 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     // glue_backward16 kFx): narrow filter blocks, two epilogue groups
     static const bool no_fx = getenv("C1D_NO_GLUE_FX") != nullptr;  // dev A/B switch
     if (mode != 0 && pl.kp == 16 && eg == 2 && !no_fx && !pl.xr && !pl.xin && pl.dbuf && !pl.acc2 && !pl.tail &&
-        !pl.stagger) {
+        !pl.stagger && pl.ws) {
         const LayerGlue& gl = *glue;
         if (mode == 1 && gl.relu && gl.mask_out && gl.act_bf16 && !gl.pre) {
             if (!gl.skip && !gl.act && gm.slots == 4u) kernel = tc_conv_kernel<1, 1, 2, 1>;
@@ -1899,7 +1900,8 @@ cudaError_t launch_tc_conv(const uint16_t* in_bf16, const float* wg, float* out,
     if (mode == 0 && pl.kp != 16 && !pl.xr && !pl.xin && !pl.dbuf && !pl.ws && !pl.wres_bytes && !pl.acc2 && !no_lean)
         kernel = tc_conv_kernel<0, 0, 1, 0, 1>;
     // kLean 2: the plain KP = 16 kernel on a natural-row, double-buffered, one-region plan (config 2)
-    if (mode == 0 && pl.kp == 16 && !pl.xr && !pl.xin && pl.dbuf && !pl.acc2 && !pl.tail && !pl.stagger && !no_lean)
+    if (mode == 0 && pl.kp == 16 && !pl.xr && !pl.xin && pl.dbuf && !pl.acc2 && !pl.tail && !pl.stagger && pl.ws &&
+        !no_lean)
         kernel = tc_conv_kernel<0, 1, 1, 0, 2>;
     const int threads = 128 + 128 * eg;
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
