@@ -169,12 +169,15 @@ def _weights_kcs(w, p: ConvParams, want: WeightLayout) -> torch.Tensor:
             raise ShapeMismatch(f"packed weights are S={w.s} K={w.k} C={w.c}, conv params say "
                                 f"S={p.taps} K={p.filters} C={p.channels}")
         # the natural KCS copy is cached on the PackedWeights object and rebuilt whenever its data
-        # tensor is replaced or modified in place (torch bumps the tensor's version counter)
-        key = (w.data.data_ptr(), w.data._version, w.data.device)
+        # tensor is replaced (another tensor object: the cache holds the one it was built from, so
+        # its memory cannot be recycled into a look-alike) or modified in place (torch bumps the
+        # tensor's version counter); the device weight images of _weights_arg go with it
+        data = w.data
         cached = w.__dict__.get("_kcs")
-        if cached is None or cached[0] != key:
-            cached = (key, _dev_f32(unpack_weights(w)))
+        if cached is None or cached[2] is not data or cached[0] != data._version:
+            cached = (data._version, _dev_f32(unpack_weights(w)), data)
             w.__dict__["_kcs"] = cached
+            w.__dict__["_images"] = {}
         w = cached[1]
     if tuple(w.shape) != (p.filters, p.channels, p.taps):
         raise ShapeMismatch(f"weights are {tuple(w.shape)}, conv params say K={p.filters} C={p.channels} S={p.taps}")
@@ -191,11 +194,11 @@ def _weights_arg(w, p: ConvParams, want: WeightLayout, desc: L.Desc, pass_: int)
     wk = _weights_kcs(w, p, want)
     if not isinstance(w, PackedWeights):
         return wk
-    key = (w.__dict__["_kcs"][0], desc.n, desc.c, desc.k, desc.s, desc.d, desc.w_in, desc.precision, desc.in_dtype,
-           desc.algo, desc.flags, desc.block_w, pass_)
-    images = w.__dict__.setdefault("_images", {})
+    key = (desc.n, desc.c, desc.k, desc.s, desc.d, desc.w_in, desc.precision, desc.in_dtype, desc.algo, desc.flags,
+           desc.block_w, pass_)
+    images = w.__dict__["_images"]  # reset by _weights_kcs whenever the data changes
     if key not in images:
-        if len(images) >= 16:  # another data version or many shapes: start over
+        if len(images) >= 16:  # many shapes: start over
             images.clear()
         nbytes = C.c_size_t(0)
         img = None

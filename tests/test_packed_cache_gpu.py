@@ -65,3 +65,18 @@ def test_packed_weights_carry_the_device_image(layout, shape):
     assert (images[0] is not None) == (packed_weights_bytes(p, n, w_in, pi) > 0)
     assert torch.equal(packed_out, run(w))
     assert torch.equal(run(pw), packed_out) and len(pw.__dict__["_images"]) == 1
+
+
+def test_packed_weight_cache_survives_recycled_memory():
+    """Replacing the data tensor by a new one that lands on the freed tensor's address (same pointer,
+    same version counter) must still rebuild the cached copy and image."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    c, k, s, d, q, n = 15, 15, 51, 8, 1000, 1
+    p = cv.ConvParams(c, k, s, d, cv.Precision.Bf16)
+    x = cv.round_bf16(torch.randn((n, c, q + d * (s - 1)), device="cuda", generator=g))
+    w = torch.randn((k, c, s), device="cuda", generator=g) * 0.05
+    pw = cv.pack_weights_forward(w)
+    first = cv.conv1d_forward(x, pw, p)
+    for scale in (2.0, 4.0, 8.0):
+        pw.data = (scale * w).permute(2, 0, 1).contiguous()  # the previous tensor is freed here
+        assert torch.equal(cv.conv1d_forward(x, pw, p), scale * first)
